@@ -1,0 +1,219 @@
+"""Canonical device arithmetic ("devmath"), restated in numpy.
+
+TEST INFRASTRUCTURE ONLY.  Nothing in the product package imports this
+module; only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg
+may use it, and only as the checker.
+
+The reference (pkg/src/lfps) computes with numpy's pairwise sums, BLAS ddot
+and libm exp.  Those orders are machine-specific, so a GPU cannot reproduce
+them bit for bit.  The B200 kernels instead follow the fixed orders defined
+here; every function below is the exact IEEE-754 op sequence the CUDA code
+performs (`paper_2506_15704_b200/csrc/canon.cuh`), so GPU results can be
+compared with this oracle bit for bit.  The reference's own tests pin these
+quantities to tolerances only (moments 1e-12: pkg/tests/test_core.py:145-154,
+thresholds 1e-9: pkg/tests/test_tables.py:258-273), and tests/ check that the
+devmath oracle and the reference-arithmetic oracle select identical index
+sets on the golden trajectories.
+
+Definitions (DESIGN.md §3 "Canonical arithmetic"):
+
+* ``table_sum``   -- chunks of 512 elements; lane l of a warp accumulates
+  x[c*512 + e*32 + l] for e = 0..15 in order from 0.0, the 32 lane sums fold
+  halves (16, 8, 4, 2, 1); chunk partials then reduce by a pairwise tree
+  (zero-padded to a power of two).  Used for the table moments
+  (tables.py:127-140).
+* ``gdot``        -- fp64 dot: lane l (of 32) accumulates j = l, l+32, ...
+  in order, then folds 16..1.  Gate logits, head stats (gate.py:77-98).
+* ``sdot32``      -- fp32 probe score: 16 lanes each own d/16 contiguous
+  elements, sequential fused accumulate (exact: bf16*bf16 products are exact
+  in fp32), fold 8, 4, 2, 1, then IEEE division by fp32(sqrt(d))
+  (numerics.py:33-49, engine.py:169).
+* ``cexp``        -- fp64 exp from +,-,*,rint and an exact power-of-two
+  scale; arguments below -708 give 0.
+* ``block_sum``   -- 256 threads: thread t accumulates e[t + 256 i] in order,
+  warps fold 16..1, the 8 warp sums fold 4, 2, 1.  Update softmax
+  (engine.py:184, numerics.py:52-66).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+TABLE_CHUNK = 512  # elements per warp chunk in table_sum
+TABLE_LANES = 32
+BLOCK_THREADS = 256
+
+# fdlibm split of ln 2: LN2_HI has 21 trailing zero bits so k*LN2_HI is exact.
+LN2_HI = 6.93147180369123816490e-01
+LN2_LO = 1.90821492927058770002e-10
+INV_LN2 = 1.44269504088896338700e+00
+EXP_LOW = -708.0
+# Taylor coefficients 1/i!, i = 0..13, rounded to double.
+EXP_COEF = tuple(1.0 / math.factorial(i) for i in range(14))
+
+
+def _fold_halves(v: np.ndarray) -> np.ndarray:
+    """Butterfly fold over the last axis (length a power of two):
+    v[i] + v[i + h] for h = len/2, ..., 1.  Equals __shfl_xor reduction."""
+    while v.shape[-1] > 1:
+        h = v.shape[-1] // 2
+        v = v[..., :h] + v[..., h:]
+    return v[..., 0]
+
+
+def _pairwise_tree(p: np.ndarray) -> float:
+    """Adjacent-pair tree over a 1-D array zero-padded to a power of two."""
+    n = p.shape[0]
+    if n == 0:
+        return 0.0
+    size = 1
+    while size < n:
+        size *= 2
+    buf = np.zeros(size, dtype=np.float64)
+    buf[:n] = p
+    while buf.shape[0] > 1:
+        buf = buf[0::2] + buf[1::2]
+    return float(buf[0])
+
+
+def table_chunk_partials(x: np.ndarray) -> np.ndarray:
+    """Per-chunk partial sums of ``x`` (fp64, any length)."""
+    x = np.asarray(x, dtype=np.float64)
+    n = x.shape[0]
+    nch = max(1, -(-n // TABLE_CHUNK))
+    buf = np.zeros(nch * TABLE_CHUNK, dtype=np.float64)
+    buf[:n] = x
+    buf = buf.reshape(nch, TABLE_CHUNK // TABLE_LANES, TABLE_LANES)
+    acc = np.zeros((nch, TABLE_LANES), dtype=np.float64)
+    for e in range(TABLE_CHUNK // TABLE_LANES):
+        acc = acc + buf[:, e, :]
+    return _fold_halves(acc)
+
+
+def table_sum(x: np.ndarray) -> float:
+    """Canonical sum used by the table-moment kernel."""
+    return _pairwise_tree(table_chunk_partials(x))
+
+
+def table_moments(x: np.ndarray) -> tuple[float, float, float]:
+    """(mean_p, sum c^2, sum c^4) of a phys table view, canonical order.
+
+    Restates ScoreTablePair._phys_moments (tables.py:127-140): two passes,
+    mean first, then centred powers; only the summation order differs."""
+    x = np.asarray(x, dtype=np.float64)
+    m = x.shape[0]
+    mean = table_sum(x) / m
+    c = x - mean
+    c2 = c * c
+    return mean, table_sum(c2), table_sum(c2 * c2)
+
+
+def gdot(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """Canonical fp64 dot over the last axis (broadcasting).
+
+    Lane l accumulates products a[j]*b[j] for j = l (mod 32) in increasing j
+    (separate multiply and add; no fused op), then lanes fold 16..1."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    a, b = np.broadcast_arrays(a, b)
+    d = a.shape[-1]
+    steps = -(-d // 32)
+    pad = steps * 32 - d
+    if pad:
+        widths = [(0, 0)] * (a.ndim - 1) + [(0, pad)]
+        a = np.pad(a, widths)
+        b = np.pad(b, widths)
+    a = a.reshape(a.shape[:-1] + (steps, 32))
+    b = b.reshape(b.shape[:-1] + (steps, 32))
+    acc = np.zeros(a.shape[:-2] + (32,), dtype=np.float64)
+    for e in range(steps):
+        acc = acc + a[..., e, :] * b[..., e, :]
+    return _fold_halves(acc)
+
+
+def sdot32(keys: np.ndarray, q: np.ndarray, rsd: np.float32) -> np.ndarray:
+    """Canonical fp32 probe score (keys[..., d] . q) / fp32(sqrt d).
+
+    ``keys`` and ``q`` hold bf16-representable values.  Each of 16 lanes owns
+    d/16 contiguous elements and accumulates k*q (exact in fp32) in order;
+    the lane sums fold 8, 4, 2, 1; the result is divided (IEEE) by rsd."""
+    keys = np.asarray(keys, dtype=np.float32)
+    q = np.asarray(q, dtype=np.float32)
+    d = keys.shape[-1]
+    assert d % 16 == 0, "score kernels require d % 16 == 0"
+    per = d // 16
+    prod = (keys * q).reshape(keys.shape[:-1] + (16, per))
+    acc = np.zeros(keys.shape[:-1] + (16,), dtype=np.float32)
+    for e in range(per):
+        acc = acc + prod[..., e]
+    dot = _fold_halves(acc)
+    return (dot / np.float32(rsd)).astype(np.float32)
+
+
+def rsd_f32(d: int) -> np.float32:
+    """fp32 sqrt(d) constant handed to the score kernels."""
+    return np.float32(math.sqrt(d))
+
+
+def cexp(x) -> np.ndarray:
+    """Canonical fp64 exp (accurate to ~1 ulp), elementwise.
+
+    k = rint(x / ln2); r = (x - k*LN2_HI) - k*LN2_LO; Horner Taylor degree 13
+    on r; times 2^k.  Arguments below -708 return 0.0."""
+    x = np.asarray(x, dtype=np.float64)
+    k = np.rint(x * INV_LN2)
+    r = (x - k * LN2_HI) - k * LN2_LO
+    p = np.full_like(x, EXP_COEF[13])
+    for i in range(12, -1, -1):
+        p = p * r + EXP_COEF[i]
+    out = np.ldexp(p, k.astype(np.int64))
+    return np.where(x < EXP_LOW, 0.0, out)
+
+
+def block_sum(e: np.ndarray) -> float:
+    """Canonical 256-thread block reduction of a 1-D fp64 array."""
+    e = np.asarray(e, dtype=np.float64)
+    n = e.shape[0]
+    rows = max(1, -(-n // BLOCK_THREADS))
+    buf = np.zeros(rows * BLOCK_THREADS, dtype=np.float64)
+    buf[:n] = e
+    buf = buf.reshape(rows, BLOCK_THREADS)
+    acc = np.zeros(BLOCK_THREADS, dtype=np.float64)
+    for i in range(rows):
+        acc = acc + buf[i]
+    warp = _fold_halves(acc.reshape(BLOCK_THREADS // 32, 32))
+    return float(_fold_halves(warp))
+
+
+def softmax_update(z: np.ndarray) -> np.ndarray:
+    """Canonical fp64 softmax over the selected scores (engine.py:184)."""
+    z = np.asarray(z, dtype=np.float64)
+    e = cexp(z - z.max())
+    return e / block_sum(e)
+
+
+def seq_sum(x) -> float:
+    """Left-to-right fp64 sum from 0.0 (gate terms, gate.py:108-109)."""
+    acc = 0.0
+    for v in np.asarray(x, dtype=np.float64).tolist():
+        acc = acc + v
+    return acc
+
+
+def stats_sum_rows(x: np.ndarray) -> np.ndarray:
+    """Column sums of an (n, d) matrix, rows accumulated in order.
+
+    This is numpy's own axis-0 reduction order, so K-bar / V-bar match the
+    reference's keys_ns.mean(axis=0) bit for bit (gate.py:71-72)."""
+    x = np.asarray(x, dtype=np.float64)
+    acc = np.zeros(x.shape[1], dtype=np.float64)
+    for i in range(x.shape[0]):
+        acc = acc + x[i]
+    return acc
+
+
+def chunked_sum(x: np.ndarray) -> float:
+    """Canonical long 1-D sum (head-stats logits): same as table_sum."""
+    return table_sum(x)
