@@ -1,0 +1,188 @@
+/*
+ * lfps_b200.h -- C-ABI of the B200-native LFPS decode-step library
+ * (liblfps_b200.so, sm_100a).
+ *
+ * The reference (arXiv 2506.15704, pkg/src/lfps) is a pure Python/numpy
+ * package with no FFI: its drop-in surface is the Python functions
+ *   prefill_bootstrap  engine.py:67-94
+ *   decode_step        engine.py:97-201   (Algorithm 1, one head, one step)
+ *   run_session        engine.py:204-219
+ *   exact_topk_step    bench.py:73-80     (the exact comparison path)
+ * re-exported by __init__.py:13-58.  These entry points are what those
+ * functions become for a batch of (request, q-head) sessions on one GPU; the
+ * Python package paper_2506_15704_b200 binds them with ctypes
+ * (paper_2506_15704_b200/_lib.py) and mirrors the reference names on top.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Every pointer in lfps_state /
+ *    lfps_workspace is a DEVICE pointer owned by the caller; the library
+ *    never allocates.  `stream` is a cudaStream_t passed as void*.
+ *  - Return 0 on success or a negative LFPS_E_* code; lfps_last_error()
+ *    returns a thread-local message for the last failure.  All argument
+ *    validation happens on the host before any launch, so a rejected call
+ *    leaves the state untouched (engine.py:111-120 "all computation before
+ *    mutation").
+ *  - Data-dependent failures the reference raises on (non-finite logits,
+ *    gate.py:104-113; weights not summing to 1, tables.py:161-163; kappa == 0,
+ *    the ZeroDivisionError of tables.py:315) are detected on the device: the
+ *    step then commits NO state for any session (tables, KV rows and n_ctx
+ *    unchanged) and sets err[0]; per-session codes are in err[1 + s].
+ *  - Session index s = b * Hq + qh, q-head qh reads KV head qh / G (GQA).
+ */
+#ifndef LFPS_B200_H
+#define LFPS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define LFPS_API __attribute__((visibility("default")))
+#else
+#define LFPS_API
+#endif
+
+#define LFPS_ABI_VERSION 1
+
+#define LFPS_OK 0
+#define LFPS_E_INVALID -1   /* bad argument (shape, range, capacity) */
+#define LFPS_E_CUDA -2      /* CUDA runtime error */
+#define LFPS_E_UNSUPPORTED -3
+
+/* per-session device error codes (err[1 + s]) */
+#define LFPS_ERR_NONFINITE_LOGITS 1   /* gate.py:104-106 */
+#define LFPS_ERR_NONFINITE_RHO 2      /* gate.py:112-113 */
+#define LFPS_ERR_KAPPA_ZERO 3         /* tables.py:314-315 ZeroDivisionError */
+#define LFPS_ERR_WEIGHT_SUM 4         /* tables.py:161-163 */
+#define LFPS_ERR_PREFILL_SUM 5        /* engine.py:84-86 */
+#define LFPS_ERR_ZERO_QUERY 6         /* gate.py:61-63 zero-norm prefill query */
+
+/* Problem dimensions of one layer. */
+typedef struct lfps_dims {
+  int32_t batch;     /* B requests */
+  int32_t kv_heads;  /* Hkv */
+  int32_t group;     /* G query heads per KV head (Hq = Hkv * G) */
+  int32_t d;         /* head dimension, multiple of 16, <= 256 */
+  int32_t n_max;     /* KV rows allocated per (request, KV head) */
+  int32_t m_cap;     /* vertical-table slots per session (even); the slash
+                        ring holds m_cap + 2 slots */
+} lfps_dims;
+
+/* LfpsConfig (config.py:11-42) plus the per-call budget. */
+typedef struct lfps_params {
+  double r;            /* decay */
+  double epsilon;      /* gate threshold */
+  double a;            /* threshold scale */
+  double k_fraction;   /* Top-k budget fraction, (0, 1] */
+  double sqrt_d;       /* math.sqrt(d) */
+  float sqrt_d_f32;    /* fp32(sqrt(d)) used by the fp32 score dot */
+  int32_t s;           /* prefill steps seeding the tables */
+  int32_t sink_count;  /* S, <= 31 */
+  int32_t local_window;/* L, <= 64 */
+  int32_t bypass_mode; /* 0 = sink_average, 1 = mean_only */
+  int32_t exhaustive;  /* exhaustive_fallback */
+  int32_t n_offsets;   /* distinct expansion offsets, <= 16 */
+  int32_t offsets[16]; /* each in [-31, 31] */
+} lfps_params;
+
+/* Persistent per-layer state (caller-owned device buffers). */
+typedef struct lfps_state {
+  void* k_cache;          /* bf16 [B, Hkv, n_max, d] */
+  void* v_cache;          /* bf16 [B, Hkv, n_max, d] */
+  int32_t* n_ctx;         /* [B] rows currently in the cache (incl. sinks) */
+  double* ver;            /* [NS, m_cap] vertical phys table */
+  double* sla;            /* [NS, m_cap + 2] slash phys ring */
+  double* scale;          /* [NS] lazy decay scale */
+  int32_t* sla_base;      /* [NS] ring slot of logical index 0 */
+  int64_t* clamp_count;   /* [NS] cumulative clamp counter */
+  double* mean_key;       /* [B * Hkv, d] prior K-bar (gate.py:71) */
+  double* mean_value;     /* [B * Hkv, d] prior V-bar (gate.py:72) */
+  double* sigma_hat_sq;   /* [NS] prior sigma^2 / |q|^2 (gate.py:67-73) */
+} lfps_state;
+
+/* Offsets (bytes) of every region inside one workspace buffer. */
+typedef struct lfps_ws_layout {
+  size_t total_bytes;
+  size_t rho;         /* f64 [NS] sink share */
+  size_t bypass;      /* i32 [NS] 1 if gated */
+  size_t err;         /* i32 [1 + NS] err[0] = any, err[1+s] per session */
+  size_t out;         /* f32 [NS, d] attention output */
+  size_t thr;         /* f64 [NS, 2, 4] tau, mean, degenerate, kappa per table */
+  size_t counts;      /* i32 [NS, 8] |c0| |c1| |probe| c0_dropped k |c2| clamps spare */
+  size_t bits;        /* u32 [NS, 2 tables, 2 kinds, words] */
+  size_t probe_idx;   /* i32 [NS, list_cap] absolute indices, ascending */
+  size_t probe_score; /* f32 [NS, list_cap] */
+  size_t c2_idx;      /* i32 [NS, list_cap] */
+  size_t c2_score;    /* f32 [NS, list_cap] */
+  size_t scratch;     /* f64 [NS, list_cap] bootstrap scratch */
+  int32_t words;      /* bitmap words per (session, table, kind) */
+  int32_t list_cap;   /* capacity of each per-session list */
+} lfps_ws_layout;
+
+typedef struct lfps_workspace {
+  void* base;         /* device buffer of layout.total_bytes */
+  size_t bytes;
+} lfps_workspace;
+
+LFPS_API int lfps_abi_version(void);
+LFPS_API const char* lfps_last_error(void);
+
+/* Workspace layout for these dimensions. */
+LFPS_API int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out);
+
+/* Seed the tracker tables of sessions [s_begin, s_begin + count) from their
+ * trailing prefill weights (Eq. 4; init_tables, tables.py:247-281).
+ * weights: f32 device [count, p.s, m0] with m0 = n_ctx[b] - S of each
+ * session's request; rows must sum to 1 within 1e-4 (engine.py:84-86). */
+LFPS_API int lfps_bootstrap_tables(const lfps_dims* dims, const lfps_params* p,
+                          const lfps_state* st, const lfps_workspace* ws,
+                          const float* weights, int32_t s_begin, int32_t count,
+                          int32_t m0, void* stream);
+
+/* Freeze the gate priors of every session from the prefill rows
+ * (compute_head_stats, gate.py:51-74).  last_query: bf16 device [NS, d]. */
+LFPS_API int lfps_bootstrap_stats(const lfps_dims* dims, const lfps_params* p,
+                         const lfps_state* st, const lfps_workspace* ws,
+                         const void* last_query, void* stream);
+
+/* One LFPS decode step for all B * Hq sessions (decode_step,
+ * engine.py:97-201): gate, thresholds, candidates, fp32 probe scoring,
+ * Top-k, joint sink+selection attention, table update, then KV append of
+ * k_new / v_new and n_ctx += 1.
+ * q: bf16 [B, Hq, d]; k_new, v_new: bf16 [B, Hkv, d]; all device.
+ * n_host: the caller's host copy of n_ctx [B] (used for validation and
+ * launch sizing; must match the device copy).  Results land in the
+ * workspace (out, counts, c2 lists, rho, bypass, err). */
+LFPS_API int lfps_decode_step(const lfps_dims* dims, const lfps_params* p,
+                     const lfps_state* st, const lfps_workspace* ws,
+                     const void* q, const void* k_new, const void* v_new,
+                     const int32_t* n_host, void* stream);
+
+/* Exact full-scan Top-k comparison path (exact_topk_step, bench.py:73-80)
+ * over the pre-append rows of every session: fp32 scores of all non-sink
+ * rows, Top-k with lower-index ties, joint sink+selection output.  Read-only
+ * on the state; results in ws (c2 lists = the exact set, out). */
+LFPS_API int lfps_exact_topk_step(const lfps_dims* dims, const lfps_params* p,
+                         const lfps_state* st, const lfps_workspace* ws,
+                         const void* q, const int32_t* n_host, void* stream);
+
+/* Overlap ratio eta per session (overlap_ratio, attention.py:116-124):
+ * |sel ∩ exact| / |exact| for two ascending index lists per session.
+ * List s starts at sel + s * list_stride; its length is
+ * sel_cnt[s * cnt_stride] (same for exact).  eta: f64 [NS]. */
+LFPS_API int lfps_overlap(const lfps_dims* dims, const int32_t* sel, const int32_t* sel_cnt,
+                 const int32_t* exact, const int32_t* exact_cnt, int32_t list_stride,
+                 int32_t cnt_stride, double* eta, void* stream);
+
+/* Number of kernels lfps_decode_step / lfps_exact_topk_step launch. */
+LFPS_API int lfps_decode_launches(void);
+LFPS_API int lfps_exact_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LFPS_B200_H */

@@ -1,1 +1,33 @@
-"""placeholder"""
+"""B200-native LFPS sparse-index prediction for decode-step attention
+(arXiv 2506.15704), drop-in for the reference package ``lfps``
+(pkg/src/lfps/__init__.py:13-58).
+
+The decode path runs in hand-written sm_100a kernels (csrc/, built into
+lib/liblfps_b200.so) behind a C-ABI (include/lfps_b200.h); this package is
+the host side.  ``BatchedSession`` is the batched GPU API; the reference's
+per-head entry points (``prefill_bootstrap``, ``decode_step``,
+``run_session``) are kept with the same names, arguments and errors in
+``compat``.
+"""
+
+from .config import LfpsConfig
+from .errors import (BadMagicError, ChecksumError, DeviceError, LayoutError, LfpsError,
+                     SessionRunError, TraceFormatError, TruncatedFileError,
+                     UnsupportedVersionError)
+
+__version__ = "0.1.0"
+
+
+_LAZY = {"BatchedSession": "session", "BatchedStepResult": "session"}
+
+
+def __getattr__(name):
+    # device-backed names load lazily so that importing the package (configs,
+    # errors, the C-ABI loader) works on machines without a GPU
+    import importlib
+    if name.startswith("__") or name in ("session", "compat", "workload", "_lib"):
+        raise AttributeError(name)
+    mod = importlib.import_module(__name__ + "." + _LAZY.get(name, "compat"))
+    if hasattr(mod, name):
+        return getattr(mod, name)
+    raise AttributeError(name)

@@ -1,0 +1,123 @@
+"""ctypes binding of liblfps_b200.so (include/lfps_b200.h).
+
+The library is built in-tree (paper_2506_15704_b200/lib/liblfps_b200.so, by
+``__graft_entry__.build()`` or ``make -C paper_2506_15704_b200/csrc``).  There
+is no CPU fallback: if the library is missing or no CUDA device is visible,
+every entry point raises ``DeviceError``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import DeviceError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "liblfps_b200.so")
+ABI_VERSION = 1
+
+# per-session device error codes (include/lfps_b200.h)
+ERR_NAMES = {
+    1: "non-finite logits in sparsity estimate",
+    2: "non-finite sparsity ratio",
+    3: "float division by zero (kappa == 0 in compute_thresholds)",
+    4: "selection weights must sum to 1",
+    5: "each prefill weight vector must sum to 1 over its non-sink range",
+    6: "zero-norm prefill query",
+}
+
+EXPORTS = ("lfps_abi_version", "lfps_last_error", "lfps_workspace_layout",
+           "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step",
+           "lfps_exact_topk_step", "lfps_overlap", "lfps_decode_launches",
+           "lfps_exact_launches")
+
+
+class Dims(C.Structure):
+    _fields_ = [("batch", C.c_int32), ("kv_heads", C.c_int32), ("group", C.c_int32),
+                ("d", C.c_int32), ("n_max", C.c_int32), ("m_cap", C.c_int32)]
+
+
+class Params(C.Structure):
+    _fields_ = [("r", C.c_double), ("epsilon", C.c_double), ("a", C.c_double),
+                ("k_fraction", C.c_double), ("sqrt_d", C.c_double), ("sqrt_d_f32", C.c_float),
+                ("s", C.c_int32), ("sink_count", C.c_int32), ("local_window", C.c_int32),
+                ("bypass_mode", C.c_int32), ("exhaustive", C.c_int32),
+                ("n_offsets", C.c_int32), ("offsets", C.c_int32 * 16)]
+
+
+class State(C.Structure):
+    _fields_ = [("k_cache", C.c_void_p), ("v_cache", C.c_void_p), ("n_ctx", C.c_void_p),
+                ("ver", C.c_void_p), ("sla", C.c_void_p), ("scale", C.c_void_p),
+                ("sla_base", C.c_void_p), ("clamp_count", C.c_void_p),
+                ("mean_key", C.c_void_p), ("mean_value", C.c_void_p),
+                ("sigma_hat_sq", C.c_void_p)]
+
+
+class WsLayout(C.Structure):
+    _fields_ = [("total_bytes", C.c_size_t), ("rho", C.c_size_t), ("bypass", C.c_size_t),
+                ("err", C.c_size_t), ("out", C.c_size_t), ("thr", C.c_size_t),
+                ("counts", C.c_size_t), ("bits", C.c_size_t), ("probe_idx", C.c_size_t),
+                ("probe_score", C.c_size_t), ("c2_idx", C.c_size_t), ("c2_score", C.c_size_t),
+                ("scratch", C.c_size_t), ("words", C.c_int32), ("list_cap", C.c_int32)]
+
+
+class Workspace(C.Structure):
+    _fields_ = [("base", C.c_void_p), ("bytes", C.c_size_t)]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def _declare(lib):
+    P = C.POINTER
+    lib.lfps_abi_version.restype = C.c_int
+    lib.lfps_last_error.restype = C.c_char_p
+    lib.lfps_workspace_layout.argtypes = [P(Dims), P(WsLayout)]
+    lib.lfps_bootstrap_tables.argtypes = [P(Dims), P(Params), P(State), P(Workspace), C.c_void_p,
+                                          C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
+    lib.lfps_bootstrap_stats.argtypes = [P(Dims), P(Params), P(State), P(Workspace), C.c_void_p,
+                                         C.c_void_p]
+    lib.lfps_decode_step.argtypes = [P(Dims), P(Params), P(State), P(Workspace), C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.lfps_exact_topk_step.argtypes = [P(Dims), P(Params), P(State), P(Workspace), C.c_void_p,
+                                         C.c_void_p, C.c_void_p]
+    lib.lfps_overlap.argtypes = [P(Dims), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
+    for name in ("lfps_workspace_layout", "lfps_bootstrap_tables", "lfps_bootstrap_stats",
+                 "lfps_decode_step", "lfps_exact_topk_step", "lfps_overlap",
+                 "lfps_decode_launches", "lfps_exact_launches"):
+        getattr(lib, name).restype = C.c_int
+
+
+def load_library(path: str = LIB_PATH):
+    """Load (once) and return the CDLL; raises DeviceError if absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise DeviceError(
+                f"{path} is not built: run __graft_entry__.build() or "
+                "make -C paper_2506_15704_b200/csrc (there is no CPU fallback)")
+        lib = C.CDLL(path)
+        _declare(lib)
+        if lib.lfps_abi_version() != ABI_VERSION:
+            raise DeviceError(f"ABI mismatch: library {lib.lfps_abi_version()} != {ABI_VERSION}")
+        _lib = lib
+        return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load_library().lfps_last_error().decode(errors="replace")
+        if rc == -1:
+            raise ValueError(f"{what}: {msg}")
+        raise DeviceError(f"{what} failed ({rc}): {msg}")
+
+
+def workspace_layout(dims: Dims) -> WsLayout:
+    lay = WsLayout()
+    check(load_library().lfps_workspace_layout(C.byref(dims), C.byref(lay)), "workspace_layout")
+    return lay

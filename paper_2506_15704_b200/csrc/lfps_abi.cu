@@ -1,0 +1,279 @@
+// lfps_abi.cu -- extern "C" entry points of liblfps_b200.so (include/lfps_b200.h).
+//
+// Host-side validation mirrors the reference's preconditions
+// (engine.py:111-120, gate.py:89-90, tables.py:303-304, config.py:44-66) and
+// runs before any launch; the launch sequence of one decode step follows
+// Algorithm 1 (engine.py:97-201).
+#include <cstdio>
+#include <cstdarg>
+#include <cstring>
+#include <cmath>
+
+#include "common.cuh"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(LFPS_E_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+constexpr int kMaxSliceElems = 11776;   // k_scan.cu kMaxSlice rounded to 512
+constexpr int kMaxM = 16 * kMaxSliceElems;
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int check_dims(const lfps_dims* d) {
+  if (!d) return fail(LFPS_E_INVALID, "dims is NULL");
+  if (d->batch < 1 || d->kv_heads < 1) return fail(LFPS_E_INVALID, "batch and kv_heads must be >= 1");
+  if (!(d->group == 1 || d->group == 2 || d->group == 4 || d->group == 8))
+    return fail(LFPS_E_UNSUPPORTED, "group (q heads per KV head) must be 1, 2, 4 or 8, got %d", d->group);
+  if (!(d->d == 32 || d->d == 64 || d->d == 128 || d->d == 256))
+    return fail(LFPS_E_UNSUPPORTED, "head dimension must be 32, 64, 128 or 256, got %d", d->d);
+  if (d->m_cap < 2 || (d->m_cap & 1)) return fail(LFPS_E_INVALID, "m_cap must be even and >= 2");
+  if (d->n_max < 2) return fail(LFPS_E_INVALID, "n_max must be >= 2");
+  if ((long long)d->batch * d->kv_heads * d->group * 2 > 65535)
+    return fail(LFPS_E_UNSUPPORTED, "too many sessions for one launch (B*Hq <= 32767)");
+  return LFPS_OK;
+}
+
+int check_params(const lfps_params* p, const lfps_dims* d) {
+  if (!p) return fail(LFPS_E_INVALID, "params is NULL");
+  if (!(p->r >= 0.0 && p->r < 1.0)) return fail(LFPS_E_INVALID, "r must be in [0, 1), got %g", p->r);
+  if (!(p->epsilon > 0.0 && p->epsilon <= 1.0))
+    return fail(LFPS_E_INVALID, "epsilon must be in (0, 1], got %g", p->epsilon);
+  if (!(p->a > 0.0)) return fail(LFPS_E_INVALID, "a must be > 0, got %g", p->a);
+  if (!(p->k_fraction > 0.0 && p->k_fraction <= 1.0))
+    return fail(LFPS_E_INVALID, "k_fraction must be in (0, 1], got %g", p->k_fraction);
+  if (p->s < 1) return fail(LFPS_E_INVALID, "s must be >= 1");
+  if (p->sink_count < 1 || p->sink_count > 31)
+    return fail(LFPS_E_UNSUPPORTED, "sink_count must be in [1, 31], got %d", p->sink_count);
+  if (p->local_window < 1 || p->local_window > 64)
+    return fail(LFPS_E_UNSUPPORTED, "local_window must be in [1, 64], got %d", p->local_window);
+  if (p->bypass_mode != 0 && p->bypass_mode != 1) return fail(LFPS_E_INVALID, "bad bypass_mode");
+  if (p->n_offsets < 1 || p->n_offsets > 16) return fail(LFPS_E_UNSUPPORTED, "1..16 offsets supported");
+  bool zero = false;
+  for (int i = 0; i < p->n_offsets; ++i) {
+    if (p->offsets[i] < -31 || p->offsets[i] > 31)
+      return fail(LFPS_E_UNSUPPORTED, "expansion offsets must lie in [-31, 31]");
+    zero |= p->offsets[i] == 0;
+  }
+  if (!zero) return fail(LFPS_E_INVALID, "expansion_offsets must contain 0");
+  if (std::fabs(p->sqrt_d - std::sqrt((double)d->d)) > 0.0)
+    return fail(LFPS_E_INVALID, "sqrt_d must equal sqrt(d)");
+  return LFPS_OK;
+}
+
+int layout(const lfps_dims* d, lfps_ws_layout* L) {
+  const size_t NS = (size_t)d->batch * d->kv_heads * d->group;
+  const size_t cap = (size_t)d->m_cap;
+  memset(L, 0, sizeof(*L));
+  L->list_cap = d->m_cap;
+  L->words = (int)((cap + kMaxSliceElems + 31) / 32);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { const size_t at = o; o = align_up(o + bytes, 256); return at; };
+  L->rho = take(NS * 8);
+  L->bypass = take(NS * 4);
+  L->err = take((NS + 1) * 4);
+  L->out = take(NS * d->d * 4);
+  L->thr = take(NS * 8 * 8);
+  L->counts = take(NS * lfps::CNT_N * 4);
+  L->bits = take(NS * 4 * (size_t)L->words * 4);
+  L->probe_idx = take(NS * cap * 4);
+  L->probe_score = take(NS * cap * 4);
+  L->c2_idx = take(NS * cap * 4);
+  L->c2_score = take(NS * cap * 4);
+  // bootstrap scratch (f64 logits) aliases probe_idx + probe_score
+  L->scratch = L->probe_idx;
+  L->total_bytes = o;
+  return LFPS_OK;
+}
+
+int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
+             const lfps_workspace* ws, lfps::Ctx* c) {
+  int rc = check_dims(d);
+  if (rc) return rc;
+  rc = check_params(p, d);
+  if (rc) return rc;
+  if (!st || !ws || !ws->base) return fail(LFPS_E_INVALID, "state/workspace is NULL");
+  lfps_ws_layout L;
+  layout(d, &L);
+  if (ws->bytes < L.total_bytes)
+    return fail(LFPS_E_INVALID, "workspace too small: %zu < %zu bytes", ws->bytes, L.total_bytes);
+  memset(c, 0, sizeof(*c));
+  c->B = d->batch; c->Hkv = d->kv_heads; c->G = d->group; c->Hq = d->kv_heads * d->group;
+  c->NS = c->B * c->Hq; c->d = d->d; c->n_max = d->n_max; c->m_cap = d->m_cap;
+  c->ring_cap = d->m_cap + 2; c->words = L.words; c->list_cap = L.list_cap;
+  c->r = p->r; c->eps = p->epsilon; c->a = p->a; c->frac = p->k_fraction; c->sqrt_d = p->sqrt_d;
+  c->sqrt_d_f32 = p->sqrt_d_f32; c->s = p->s; c->S = p->sink_count; c->L = p->local_window;
+  c->bypass_mode = p->bypass_mode; c->exhaustive = p->exhaustive; c->n_off = p->n_offsets;
+  for (int i = 0; i < 16; ++i) c->off[i] = i < p->n_offsets ? p->offsets[i] : 0;
+  c->K = static_cast<const __nv_bfloat16*>(st->k_cache);
+  c->V = static_cast<const __nv_bfloat16*>(st->v_cache);
+  c->Kw = static_cast<__nv_bfloat16*>(st->k_cache);
+  c->Vw = static_cast<__nv_bfloat16*>(st->v_cache);
+  c->n_ctx = st->n_ctx; c->ver = st->ver; c->sla = st->sla; c->scale = st->scale;
+  c->sla_base = st->sla_base; c->clamp_count = reinterpret_cast<long long*>(st->clamp_count);
+  c->mean_key = st->mean_key; c->mean_value = st->mean_value; c->sigma = st->sigma_hat_sq;
+  if (!c->K || !c->V || !c->n_ctx || !c->ver || !c->sla || !c->scale || !c->sla_base ||
+      !c->clamp_count || !c->mean_key || !c->mean_value || !c->sigma)
+    return fail(LFPS_E_INVALID, "a state pointer is NULL");
+  char* base = static_cast<char*>(ws->base);
+  c->rho = reinterpret_cast<double*>(base + L.rho);
+  c->bypass = reinterpret_cast<int*>(base + L.bypass);
+  c->err = reinterpret_cast<int*>(base + L.err);
+  c->out = reinterpret_cast<float*>(base + L.out);
+  c->thr = reinterpret_cast<double*>(base + L.thr);
+  c->counts = reinterpret_cast<int*>(base + L.counts);
+  c->bits = reinterpret_cast<uint32_t*>(base + L.bits);
+  c->probe_idx = reinterpret_cast<int*>(base + L.probe_idx);
+  c->probe_score = reinterpret_cast<float*>(base + L.probe_score);
+  c->c2_idx = reinterpret_cast<int*>(base + L.c2_idx);
+  c->c2_score = reinterpret_cast<float*>(base + L.c2_score);
+  c->scratch = reinterpret_cast<double*>(base + L.scratch);
+  return LFPS_OK;
+}
+
+// decode preconditions on the host copy of n (engine.py:114-120, gate.py:89-90)
+int check_context(const lfps::Ctx& c, const int32_t* n_host, bool append, int* m_max) {
+  if (!n_host) return fail(LFPS_E_INVALID, "n_host is NULL");
+  int mm = 0;
+  for (int b = 0; b < c.B; ++b) {
+    const int n = n_host[b];
+    if (n <= c.S + c.L)
+      return fail(LFPS_E_INVALID, "request %d: context %d shorter than sink_count + local_window", b, n);
+    const int m = n - c.S;
+    if (append && n >= c.n_max)
+      return fail(LFPS_E_INVALID, "request %d: KV cache full (n=%d, n_max=%d)", b, n, c.n_max);
+    if (m + 2 > c.m_cap)
+      return fail(LFPS_E_INVALID, "request %d: tables full (m=%d, m_cap=%d)", b, m, c.m_cap);
+    if (m > kMaxM) return fail(LFPS_E_UNSUPPORTED, "context %d exceeds the scan limit", n);
+    if (m > mm) mm = m;
+  }
+  *m_max = mm;
+  return LFPS_OK;
+}
+
+#define LAUNCH(x)                                         \
+  do {                                                    \
+    cudaError_t e_ = (x);                                 \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #x);      \
+  } while (0)
+
+}  // namespace
+
+extern "C" {
+
+int lfps_abi_version(void) { return LFPS_ABI_VERSION; }
+
+const char* lfps_last_error(void) { return g_err; }
+
+int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out) {
+  int rc = check_dims(dims);
+  if (rc) return rc;
+  if (!out) return fail(LFPS_E_INVALID, "out is NULL");
+  return layout(dims, out);
+}
+
+int lfps_decode_launches(void) { return 10; }
+int lfps_exact_launches(void) { return 4; }
+
+int lfps_bootstrap_tables(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
+                          const lfps_workspace* ws, const float* weights, int32_t s_begin,
+                          int32_t count, int32_t m0, void* stream) {
+  lfps::Ctx c;
+  int rc = make_ctx(dims, p, st, ws, &c);
+  if (rc) return rc;
+  if (!weights) return fail(LFPS_E_INVALID, "weights is NULL");
+  if (s_begin < 0 || count < 1 || s_begin + count > c.NS)
+    return fail(LFPS_E_INVALID, "session range [%d, %d) outside [0, %d)", s_begin, s_begin + count, c.NS);
+  if (m0 < 1) return fail(LFPS_E_INVALID, "prefill weight vectors are empty");
+  if (m0 + 2 > c.m_cap) return fail(LFPS_E_INVALID, "m0=%d does not fit m_cap=%d", m0, c.m_cap);
+  if (count > 65535 || c.s > 65535) return fail(LFPS_E_UNSUPPORTED, "too many sessions per call");
+  cudaStream_t sm = static_cast<cudaStream_t>(stream);
+  LAUNCH(lfps::launch_boot_tables(c, weights, s_begin, count, m0, sm));
+  return LFPS_OK;
+}
+
+int lfps_bootstrap_stats(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
+                         const lfps_workspace* ws, const void* last_query, void* stream) {
+  lfps::Ctx c;
+  int rc = make_ctx(dims, p, st, ws, &c);
+  if (rc) return rc;
+  if (!last_query) return fail(LFPS_E_INVALID, "last_query is NULL");
+  cudaStream_t sm = static_cast<cudaStream_t>(stream);
+  LAUNCH(lfps::launch_boot_stats(c, static_cast<const __nv_bfloat16*>(last_query), c.m_cap, sm));
+  return LFPS_OK;
+}
+
+int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
+                     const lfps_workspace* ws, const void* q, const void* k_new,
+                     const void* v_new, const int32_t* n_host, void* stream) {
+  lfps::Ctx c;
+  int rc = make_ctx(dims, p, st, ws, &c);
+  if (rc) return rc;
+  if (!q || !k_new || !v_new) return fail(LFPS_E_INVALID, "q/k_new/v_new is NULL");
+  int m_max = 0;
+  rc = check_context(c, n_host, true, &m_max);
+  if (rc) return rc;
+  cudaStream_t sm = static_cast<cudaStream_t>(stream);
+  const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
+  LAUNCH(lfps::launch_clear_err(c, sm));
+  LAUNCH(lfps::launch_gate(c, qb, sm));
+  LAUNCH(lfps::launch_scan(c, m_max, sm));
+  LAUNCH(lfps::launch_probe(c, sm));
+  LAUNCH(lfps::launch_score(c, qb, m_max, sm));
+  LAUNCH(lfps::launch_topk(c, -1, sm));
+  LAUNCH(lfps::launch_attend(c, qb, 0, sm));
+  LAUNCH(lfps::launch_update(c, sm));
+  LAUNCH(lfps::launch_append(c, static_cast<const __nv_bfloat16*>(k_new),
+                             static_cast<const __nv_bfloat16*>(v_new), sm));
+  LAUNCH(lfps::launch_commit(c, sm));
+  return LFPS_OK;
+}
+
+int lfps_exact_topk_step(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
+                         const lfps_workspace* ws, const void* q, const int32_t* n_host,
+                         void* stream) {
+  lfps::Ctx c;
+  int rc = make_ctx(dims, p, st, ws, &c);
+  if (rc) return rc;
+  if (!q) return fail(LFPS_E_INVALID, "q is NULL");
+  int m_max = 0;
+  rc = check_context(c, n_host, false, &m_max);
+  if (rc) return rc;
+  cudaStream_t sm = static_cast<cudaStream_t>(stream);
+  const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
+  LAUNCH(lfps::launch_clear_err(c, sm));
+  LAUNCH(lfps::launch_exact_score(c, qb, m_max, sm));
+  LAUNCH(lfps::launch_topk(c, c.S, sm));
+  LAUNCH(lfps::launch_attend(c, qb, 1, sm));
+  return LFPS_OK;
+}
+
+int lfps_overlap(const lfps_dims* dims, const int32_t* sel, const int32_t* sel_cnt,
+                 const int32_t* exact, const int32_t* exact_cnt, int32_t list_stride,
+                 int32_t cnt_stride, double* eta, void* stream) {
+  int rc = check_dims(dims);
+  if (rc) return rc;
+  if (!sel || !sel_cnt || !exact || !exact_cnt || !eta) return fail(LFPS_E_INVALID, "NULL argument");
+  if (list_stride < 1 || cnt_stride < 1) return fail(LFPS_E_INVALID, "bad strides");
+  lfps::Ctx c;
+  memset(&c, 0, sizeof(c));
+  c.B = dims->batch; c.Hkv = dims->kv_heads; c.G = dims->group;
+  c.Hq = c.Hkv * c.G; c.NS = c.B * c.Hq;
+  LAUNCH(lfps::launch_overlap(c, sel, sel_cnt, exact, exact_cnt, list_stride, cnt_stride, eta,
+                              static_cast<cudaStream_t>(stream)));
+  return LFPS_OK;
+}
+
+}  // extern "C"

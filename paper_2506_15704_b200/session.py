@@ -1,0 +1,287 @@
+"""BatchedSession: device-resident LFPS state for B requests x Hq query heads.
+
+This is the B200 form of the reference's per-head ``HeadSession``
+(engine.py:38-47): one object owns, for one attention layer,
+
+* the bf16 KV cache [B, Hkv, n_max, d] shared by each KV head's G query
+  heads (GQA; the reference's sessions each own a private fp64 KvStore),
+* every (request, q-head) session's fp64 tracker tables (vertical table and
+  slash ring), lazy scale, ring base and clamp counter,
+* the frozen gate priors (K-bar, V-bar per KV head, sigma^2 per q-head),
+* one workspace of per-step scratch and results.
+
+All arithmetic runs in liblfps_b200.so (csrc/); this module only allocates
+device memory with torch and passes raw pointers across the C-ABI.  Torch is
+plumbing here, not the product: no torch op touches the decode path.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .config import LfpsConfig
+from .errors import DeviceError, LfpsError
+
+CNT_C0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP = range(7)
+
+
+def make_params(cfg: LfpsConfig, k_fraction: float) -> _lib.Params:
+    err = cfg.device_limits_error()
+    if err:
+        raise ValueError(err)
+    p = _lib.Params()
+    p.r, p.epsilon, p.a = cfg.r, cfg.epsilon, cfg.a
+    p.k_fraction = float(k_fraction)
+    p.sqrt_d = math.sqrt(cfg.d)
+    p.sqrt_d_f32 = float(torch.tensor(math.sqrt(cfg.d), dtype=torch.float32))
+    p.s, p.sink_count, p.local_window = cfg.s, cfg.sink_count, cfg.local_window
+    p.bypass_mode = 1 if cfg.bypass_mode == "mean_only" else 0
+    p.exhaustive = 1 if cfg.exhaustive_fallback else 0
+    offs = sorted(set(cfg.expansion_offsets))
+    p.n_offsets = len(offs)
+    for i, o in enumerate(offs):
+        p.offsets[i] = o
+    return p
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+@dataclass
+class BatchedStepResult:
+    """Device views of one step's results (valid until the next step)."""
+
+    output: torch.Tensor       # f32 [B, Hq, d]
+    rho: torch.Tensor          # f64 [B, Hq]
+    bypassed: torch.Tensor     # i32 [B, Hq]
+    counts: torch.Tensor       # i32 [B, Hq, 8]: c0 c1 probe c0_dropped k c2 clamps -
+    c2_idx: torch.Tensor       # i32 [B, Hq, list_cap] (first counts[..., 5] valid)
+    c2_score: torch.Tensor     # f32 [B, Hq, list_cap]
+    err: torch.Tensor          # i32 [1 + B*Hq]
+
+
+class BatchedSession:
+    """Device state of one layer for B requests (see module docstring)."""
+
+    def __init__(self, cfg: LfpsConfig, batch: int, kv_heads: int, group: int, n_max: int,
+                 m_cap: int | None = None, device: torch.device | str | None = None):
+        if device is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        device = torch.device(device)
+        if device.type != "cuda":
+            raise DeviceError("BatchedSession needs a CUDA device (no CPU fallback)")
+        if device.index is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = device
+        err = cfg.device_limits_error()
+        if err:
+            raise ValueError(err)
+        self.lib = _lib.load_library()
+        self.cfg = cfg
+        self.B, self.Hkv, self.G = batch, kv_heads, group
+        self.Hq = kv_heads * group
+        self.NS = batch * self.Hq
+        self.d = cfg.d
+        self.n_max = int(n_max)
+        m_cap = int(m_cap if m_cap is not None else n_max - cfg.sink_count + 2)
+        m_cap += m_cap & 1
+        self.m_cap = m_cap
+        self.dims = _lib.Dims(batch, kv_heads, group, cfg.d, self.n_max, m_cap)
+        self.layout = _lib.workspace_layout(self.dims)
+        dev = self.device
+        f64, i32 = torch.float64, torch.int32
+        self.k_cache = torch.zeros(batch, kv_heads, self.n_max, cfg.d, dtype=torch.bfloat16,
+                                   device=dev)
+        self.v_cache = torch.zeros_like(self.k_cache)
+        self.n_ctx = torch.zeros(batch, dtype=i32, device=dev)
+        self.n_host = [0] * batch
+        self.ver = torch.zeros(self.NS, m_cap, dtype=f64, device=dev)
+        self.sla = torch.zeros(self.NS, m_cap + 2, dtype=f64, device=dev)
+        self.scale = torch.ones(self.NS, dtype=f64, device=dev)
+        self.sla_base = torch.zeros(self.NS, dtype=i32, device=dev)
+        self.clamp_count = torch.zeros(self.NS, dtype=torch.int64, device=dev)
+        self.mean_key = torch.zeros(batch * kv_heads, cfg.d, dtype=f64, device=dev)
+        self.mean_value = torch.zeros_like(self.mean_key)
+        self.sigma_hat_sq = torch.zeros(self.NS, dtype=f64, device=dev)
+        self.ws_buf = torch.zeros(self.layout.total_bytes, dtype=torch.uint8, device=dev)
+        self.state = _lib.State(_ptr(self.k_cache), _ptr(self.v_cache), _ptr(self.n_ctx),
+                                _ptr(self.ver), _ptr(self.sla), _ptr(self.scale),
+                                _ptr(self.sla_base), _ptr(self.clamp_count),
+                                _ptr(self.mean_key), _ptr(self.mean_value),
+                                _ptr(self.sigma_hat_sq))
+        self.ws = _lib.Workspace(_ptr(self.ws_buf), self.layout.total_bytes)
+        self._views()
+        self.step_count = 0
+
+    # -- workspace views ----------------------------------------------------
+    def _region(self, off: int, dtype, shape):
+        nbytes = torch.empty((), dtype=dtype).element_size()
+        count = 1
+        for s in shape:
+            count *= s
+        return self.ws_buf[off: off + count * nbytes].view(dtype).view(*shape)
+
+    def _views(self):
+        L, NS, B, Hq = self.layout, self.NS, self.B, self.Hq
+        cap = L.list_cap
+        self.rho = self._region(L.rho, torch.float64, (B, Hq))
+        self.bypass = self._region(L.bypass, torch.int32, (B, Hq))
+        self.err = self._region(L.err, torch.int32, (NS + 1,))
+        self.out = self._region(L.out, torch.float32, (B, Hq, self.d))
+        self.thr = self._region(L.thr, torch.float64, (B, Hq, 2, 4))
+        self.counts = self._region(L.counts, torch.int32, (B, Hq, 8))
+        self.bits = self._region(L.bits, torch.int32, (NS, 2, 2, L.words))
+        self.probe_idx = self._region(L.probe_idx, torch.int32, (B, Hq, cap))
+        self.probe_score = self._region(L.probe_score, torch.float32, (B, Hq, cap))
+        self.c2_idx = self._region(L.c2_idx, torch.int32, (B, Hq, cap))
+        self.c2_score = self._region(L.c2_score, torch.float32, (B, Hq, cap))
+
+    def _stream(self):
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _params(self, k_fraction: float = 1.0) -> _lib.Params:
+        return make_params(self.cfg, k_fraction)
+
+    # -- bootstrap ----------------------------------------------------------
+    def load_prefill(self, b: int, keys: torch.Tensor, values: torch.Tensor):
+        """Copy request b's prefill rows (bf16 [Hkv, n0, d]) into the cache."""
+        n0 = keys.shape[1]
+        if n0 >= self.n_max:
+            raise ValueError("prefill longer than the KV cache")
+        if n0 <= self.cfg.sink_count + self.cfg.s:
+            raise ValueError(
+                f"prefill needs more than sink_count + s = {self.cfg.sink_count + self.cfg.s} rows")
+        self.k_cache[b, :, :n0].copy_(keys)
+        self.v_cache[b, :, :n0].copy_(values)
+        self.n_host[b] = n0
+        self.n_ctx[b] = n0
+
+    def bootstrap_tables(self, s_begin: int, weights: torch.Tensor):
+        """Eq. 4 seeding for sessions [s_begin, s_begin + count); weights
+        f32 [count, s, m0] on the device (init_tables, tables.py:247-281)."""
+        weights = weights.to(self.device, torch.float32).contiguous()
+        count, s, m0 = weights.shape
+        if s != self.cfg.s:
+            raise ValueError(f"expected {self.cfg.s} prefill weight vectors, got {s}")
+        _lib.check(self.lib.lfps_bootstrap_tables(
+            C.byref(self.dims), C.byref(self._params()), C.byref(self.state), C.byref(self.ws),
+            C.c_void_p(weights.data_ptr()), s_begin, count, m0, self._stream()),
+            "bootstrap_tables")
+
+    def bootstrap_stats(self, last_query: torch.Tensor):
+        """Freeze the gate priors (compute_head_stats, gate.py:51-74);
+        last_query bf16 [B, Hq, d]."""
+        lq = last_query.to(self.device, torch.bfloat16).contiguous()
+        _lib.check(self.lib.lfps_bootstrap_stats(
+            C.byref(self.dims), C.byref(self._params()), C.byref(self.state), C.byref(self.ws),
+            C.c_void_p(lq.data_ptr()), self._stream()), "bootstrap_stats")
+
+    def clear_errors(self):
+        self.err.zero_()
+
+    def check_errors(self, what: str = "step"):
+        """Raise the reference's exception for the first failed session."""
+        err = self.err.cpu()
+        if int(err[0]) == 0:
+            return
+        codes = err[1:]
+        bad = torch.nonzero(codes).flatten()
+        s = int(bad[0]) if bad.numel() else -1
+        code = int(codes[s]) if s >= 0 else 0
+        msg = _lib.ERR_NAMES.get(code, f"device error {code}")
+        if code == 3:
+            raise ZeroDivisionError(f"{what}: session {s}: {msg}")
+        raise ValueError(f"{what}: session {s}: {msg}")
+
+    # -- decode ---------------------------------------------------------------
+    def decode_step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,
+                    k_fraction: float, check: bool = False) -> BatchedStepResult:
+        """One LFPS decode step for all sessions (engine.py:97-201).
+
+        q bf16 [B, Hq, d]; k_new, v_new bf16 [B, Hkv, d] (device).  On a
+        data error no state is committed; ``check=True`` synchronises and
+        raises it."""
+        if not 0.0 < k_fraction <= 1.0:
+            raise ValueError(f"k_fraction must be in (0, 1], got {k_fraction}")
+        for name, t, shape in (("q", q, (self.B, self.Hq, self.d)),
+                               ("new_key", k_new, (self.B, self.Hkv, self.d)),
+                               ("new_value", v_new, (self.B, self.Hkv, self.d))):
+            if tuple(t.shape) != shape:
+                raise ValueError(f"{name} must have shape {shape}, got {tuple(t.shape)}")
+            if t.dtype != torch.bfloat16 or t.device != self.device or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous bf16 tensor on {self.device}")
+        n_host = (C.c_int32 * self.B)(*self.n_host)
+        _lib.check(self.lib.lfps_decode_step(
+            C.byref(self.dims), C.byref(self._params(k_fraction)), C.byref(self.state),
+            C.byref(self.ws), C.c_void_p(q.data_ptr()), C.c_void_p(k_new.data_ptr()),
+            C.c_void_p(v_new.data_ptr()), n_host, self._stream()), "decode_step")
+        if check:
+            torch.cuda.current_stream(self.device).synchronize()
+            self.check_errors("decode_step")
+        self.n_host = [n + 1 for n in self.n_host]
+        self.step_count += 1
+        return self.result()
+
+    def rollback_host_count(self):
+        """Undo the host mirror advance after a step that committed nothing."""
+        self.n_host = [n - 1 for n in self.n_host]
+        self.step_count -= 1
+
+    def result(self) -> BatchedStepResult:
+        return BatchedStepResult(output=self.out, rho=self.rho, bypassed=self.bypass,
+                                 counts=self.counts, c2_idx=self.c2_idx,
+                                 c2_score=self.c2_score, err=self.err)
+
+    def exact_topk_step(self, q: torch.Tensor, k_fraction: float) -> BatchedStepResult:
+        """Exact full-scan Top-k over the current rows (bench.py:73-80);
+        read-only on the tracker state.  Results reuse the workspace."""
+        if not 0.0 < k_fraction <= 1.0:
+            raise ValueError(f"k_fraction must be in (0, 1], got {k_fraction}")
+        if tuple(q.shape) != (self.B, self.Hq, self.d) or q.dtype != torch.bfloat16:
+            raise ValueError("q must be bf16 [B, Hq, d]")
+        n_host = (C.c_int32 * self.B)(*self.n_host)
+        _lib.check(self.lib.lfps_exact_topk_step(
+            C.byref(self.dims), C.byref(self._params(k_fraction)), C.byref(self.state),
+            C.byref(self.ws), C.c_void_p(q.contiguous().data_ptr()), n_host, self._stream()),
+            "exact_topk_step")
+        return self.result()
+
+    def overlap(self, sel_idx: torch.Tensor, sel_counts: torch.Tensor,
+                exact_idx: torch.Tensor, exact_counts: torch.Tensor) -> torch.Tensor:
+        """eta per session (overlap_ratio, attention.py:116-124) for two
+        [B, Hq, cap] index lists with [B, Hq, 8]-strided counts (slot 5)."""
+        eta = torch.empty(self.B, self.Hq, dtype=torch.float64, device=self.device)
+        cap = sel_idx.shape[-1]
+        if exact_idx.shape[-1] != cap:
+            raise ValueError("lists must share a capacity")
+        _lib.check(self.lib.lfps_overlap(
+            C.byref(self.dims), C.c_void_p(sel_idx.data_ptr()),
+            C.c_void_p(sel_counts.data_ptr() + 4 * CNT_C2), C.c_void_p(exact_idx.data_ptr()),
+            C.c_void_p(exact_counts.data_ptr() + 4 * CNT_C2), cap, sel_counts.shape[-1],
+            C.c_void_p(eta.data_ptr()), self._stream()), "overlap")
+        return eta
+
+    # -- host snapshots (tests, diagnostics) ---------------------------------
+    def session_tables(self, s: int):
+        """(ver phys [m], sla phys [m] in logical order, scale) of session s."""
+        b = s // self.Hq
+        m = self.n_host[b] - self.cfg.sink_count
+        base = int(self.sla_base[s])
+        C_ = self.m_cap + 2
+        slots = (base + torch.arange(m, device=self.device)) % C_
+        return (self.ver[s, :m].cpu().numpy(), self.sla[s][slots].cpu().numpy(),
+                float(self.scale[s]))
+
+    def c2_list(self, b: int, qh: int):
+        k = int(self.counts[b, qh, CNT_C2])
+        return self.c2_idx[b, qh, :k].cpu().numpy()
+
+    def probe_list(self, b: int, qh: int):
+        p = int(self.counts[b, qh, CNT_PROBE])
+        return self.probe_idx[b, qh, :p].cpu().numpy()

@@ -1,0 +1,94 @@
+"""Drive the device path and the devmath oracle side by side (GPU tests)."""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import lfps_oracle as lo
+from paper_2506_15704_b200.session import (CNT_C0, CNT_C1, CNT_C2, CNT_CLAMP, CNT_DROP,
+                                           CNT_K, CNT_PROBE, BatchedSession)
+
+
+def bf16(x) -> torch.Tensor:
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32)).to(torch.bfloat16)
+
+
+class Pair:
+    """One unit-batch on the GPU plus its oracle mirror.
+
+    keys/values: f32 (bf16 values) [B, Hkv, n_total, d]; weights f32
+    [B, Hkv, G, s, n0 - S]; finals [B, Hkv, G, d]."""
+
+    def __init__(self, cfg, keys, values, weights, finals, n0, n_max=None, m_cap=None):
+        B, Hkv, _, d = keys.shape
+        G = weights.shape[2]
+        self.cfg, self.B, self.Hkv, self.G, self.d, self.n0 = cfg, B, Hkv, G, d, n0
+        self.sess = BatchedSession(cfg, B, Hkv, G, n_max=n_max or keys.shape[2] + 8,
+                                   m_cap=m_cap, device="cuda")
+        for b in range(B):
+            self.sess.load_prefill(b, bf16(keys[b, :, :n0]).cuda(), bf16(values[b, :, :n0]).cuda())
+        w = torch.as_tensor(np.ascontiguousarray(weights, dtype=np.float32))
+        self.sess.bootstrap_tables(0, w.reshape(B * Hkv * G, cfg.s, n0 - cfg.sink_count).cuda())
+        self.sess.bootstrap_stats(bf16(finals.reshape(B, Hkv * G, d)).cuda())
+        torch.cuda.synchronize()
+        self.sess.check_errors("bootstrap")
+        self.units = []
+        for b in range(B):
+            for h in range(Hkv):
+                kv, trs, prs = lo.bootstrap_unit(keys[b, h, :n0], values[b, h, :n0],
+                                                 weights[b, h], finals[b, h], cfg, lo.DevArith)
+                self.units.append((kv, trs, prs))
+
+    def step(self, q, k_new, v_new, frac):
+        """q [B, Hkv, G, d]; k_new/v_new [B, Hkv, d] (f32 bf16-valued)."""
+        B, Hkv, G, d = self.B, self.Hkv, self.G, self.d
+        res = self.sess.decode_step(bf16(q.reshape(B, Hkv * G, d)).cuda(),
+                                    bf16(k_new).cuda(), bf16(v_new).cuda(), frac, check=True)
+        outs = []
+        for b in range(B):
+            for h in range(Hkv):
+                kv, trs, prs = self.units[b * Hkv + h]
+                outs.append(lo.unit_step(kv, trs, prs, q[b, h], k_new[b, h], v_new[b, h], frac,
+                                         self.cfg, lo.DevArith, "fp32"))
+        return res, outs
+
+    def compare_step(self, res, outs, out_tol=1e-5, tables=True):
+        """Assert bit-exact sets/scalars/tables and toleranced outputs."""
+        counts = res.counts.cpu().numpy()
+        rho = res.rho.cpu().numpy()
+        byp = res.bypassed.cpu().numpy()
+        out = res.output.cpu().numpy()
+        G = self.G
+        worst = 0.0
+        for u, unit_outs in enumerate(outs):
+            b, h = divmod(u, self.Hkv)
+            for g, o in enumerate(unit_outs):
+                qh = h * G + g
+                s = b * self.Hkv * G + qh
+                tag = f"b{b} qh{qh}"
+                assert bool(byp[b, qh]) == o.bypassed, tag
+                assert rho[b, qh] == o.rho, (tag, rho[b, qh], o.rho)
+                if not o.bypassed:
+                    c = counts[b, qh]
+                    assert c[CNT_C0] == o.c0.size, (tag, "c0", c[CNT_C0], o.c0.size)
+                    assert c[CNT_C1] == o.c1.size, (tag, "c1")
+                    assert c[CNT_PROBE] == o.probe.size, (tag, "probe", c[CNT_PROBE], o.probe.size)
+                    assert c[CNT_DROP] == o.c0_dropped, (tag, "drop")
+                    assert c[CNT_K] == o.budget_k, (tag, "k")
+                    assert c[CNT_C2] == o.c2.size, (tag, "c2")
+                    assert c[CNT_CLAMP] == o.clamps, (tag, "clamps")
+                    np.testing.assert_array_equal(self.sess.probe_list(b, qh), o.probe, err_msg=tag)
+                    np.testing.assert_array_equal(self.sess.c2_list(b, qh), o.c2, err_msg=tag)
+                ref = o.output
+                err = np.linalg.norm(out[b, qh] - ref) / max(np.linalg.norm(ref), 1e-12)
+                worst = max(worst, err)
+                assert err <= out_tol, (tag, err)
+                if tables:
+                    kv, trs, prs = self.units[u]
+                    tr = trs[g]
+                    ver, sla, sc = self.sess.session_tables(s)
+                    assert sc == tr.scale, (tag, sc, tr.scale)
+                    np.testing.assert_array_equal(ver, tr.ver_view(), err_msg=tag + " ver")
+                    np.testing.assert_array_equal(sla, tr.sla_view(), err_msg=tag + " sla")
+        return worst
