@@ -177,6 +177,18 @@ LFPS_API int lfps_overlap(const lfps_dims* dims, const int32_t* sel, const int32
                  const int32_t* exact, const int32_t* exact_cnt, int32_t list_stride,
                  int32_t cnt_stride, double* eta, void* stream);
 
+/* Per-kernel CUDA-event timing.  While enabled, every kernel the entry
+ * points launch is bracketed by events on its stream (do not enable during
+ * CUDA-graph capture).  lfps_profile_collect waits for the events, sums the
+ * durations per kernel name into out[0, *n_out) and clears the record. */
+typedef struct lfps_kernel_time {
+  char name[32];
+  int32_t launches;
+  double total_ms;
+} lfps_kernel_time;
+LFPS_API int lfps_profile_enable(int on);
+LFPS_API int lfps_profile_collect(lfps_kernel_time* out, int32_t cap, int32_t* n_out);
+
 /* Number of kernels lfps_decode_step / lfps_exact_topk_step launch. */
 LFPS_API int lfps_decode_launches(void);
 LFPS_API int lfps_exact_launches(void);

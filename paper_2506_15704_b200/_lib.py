@@ -30,7 +30,7 @@ ERR_NAMES = {
 EXPORTS = ("lfps_abi_version", "lfps_last_error", "lfps_workspace_layout",
            "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step",
            "lfps_exact_topk_step", "lfps_overlap", "lfps_decode_launches",
-           "lfps_exact_launches")
+           "lfps_exact_launches", "lfps_profile_enable", "lfps_profile_collect")
 
 
 class Dims(C.Structure):
@@ -62,6 +62,10 @@ class WsLayout(C.Structure):
                 ("scratch", C.c_size_t), ("words", C.c_int32), ("list_cap", C.c_int32)]
 
 
+class KernelTime(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int32), ("total_ms", C.c_double)]
+
+
 class Workspace(C.Structure):
     _fields_ = [("base", C.c_void_p), ("bytes", C.c_size_t)]
 
@@ -85,8 +89,10 @@ def _declare(lib):
                                          C.c_void_p, C.c_void_p]
     lib.lfps_overlap.argtypes = [P(Dims), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
-    for name in ("lfps_workspace_layout", "lfps_bootstrap_tables", "lfps_bootstrap_stats",
-                 "lfps_decode_step", "lfps_exact_topk_step", "lfps_overlap",
+    lib.lfps_profile_enable.argtypes = [C.c_int]
+    lib.lfps_profile_collect.argtypes = [P(KernelTime), C.c_int32, P(C.c_int32)]
+    for name in ("lfps_profile_enable", "lfps_profile_collect", "lfps_workspace_layout",
+                 "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step", "lfps_exact_topk_step", "lfps_overlap",
                  "lfps_decode_launches", "lfps_exact_launches"):
         getattr(lib, name).restype = C.c_int
 
@@ -121,3 +127,15 @@ def workspace_layout(dims: Dims) -> WsLayout:
     lay = WsLayout()
     check(load_library().lfps_workspace_layout(C.byref(dims), C.byref(lay)), "workspace_layout")
     return lay
+
+
+def profile_enable(on: bool) -> None:
+    check(load_library().lfps_profile_enable(1 if on else 0), "profile_enable")
+
+
+def profile_collect() -> dict:
+    """{kernel name: (launches, total_ms)} since the last collect."""
+    buf = (KernelTime * 64)()
+    n = C.c_int32(0)
+    check(load_library().lfps_profile_collect(buf, 64, C.byref(n)), "profile_collect")
+    return {buf[i].name.decode(): (buf[i].launches, buf[i].total_ms) for i in range(n.value)}

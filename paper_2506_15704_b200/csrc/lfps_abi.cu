@@ -8,6 +8,9 @@
 #include <cstdarg>
 #include <cstring>
 #include <cmath>
+#include <mutex>
+#include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -169,6 +172,43 @@ int check_context(const lfps::Ctx& c, const int32_t* n_host, bool append, int* m
     if (e_ != cudaSuccess) return cuda_fail(e_, #x);      \
   } while (0)
 
+// ---- optional per-kernel CUDA-event timing (lfps_profile_*) ----------------
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_pool;
+
+cudaEvent_t prof_event() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// launch `x` on stream `sm`, bracketed by events when profiling is on
+#define LAUNCH_P(name, sm, x)                                      \
+  do {                                                             \
+    cudaEvent_t a_ = nullptr;                                      \
+    if (g_prof_on) {                                               \
+      a_ = prof_event();                                           \
+      cudaEventRecord(a_, sm);                                     \
+    }                                                              \
+    LAUNCH(x);                                                     \
+    if (g_prof_on) {                                               \
+      cudaEvent_t b_ = prof_event();                               \
+      cudaEventRecord(b_, sm);                                     \
+      g_prof.push_back({name, a_, b_});                            \
+    }                                                              \
+  } while (0)
+
 }  // namespace
 
 extern "C" {
@@ -185,6 +225,39 @@ int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out) {
 }
 
 int lfps_decode_launches(void) { return 10; }
+
+int lfps_profile_enable(int on) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_on = on != 0;
+  return LFPS_OK;
+}
+
+int lfps_profile_collect(lfps_kernel_time* out, int32_t cap, int32_t* n_out) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  if (!out || !n_out || cap < 1) return fail(LFPS_E_INVALID, "bad profile buffer");
+  int n = 0;
+  for (const ProfRec& r : g_prof) {
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    int k = 0;
+    while (k < n && strncmp(out[k].name, r.name, sizeof(out[k].name)) != 0) ++k;
+    if (k == n) {
+      if (n == cap) continue;
+      memset(&out[n], 0, sizeof(out[n]));
+      strncpy(out[n].name, r.name, sizeof(out[n].name) - 1);
+      ++n;
+    }
+    out[k].launches += 1;
+    out[k].total_ms += ms;
+    g_pool.push_back(r.a);
+    g_pool.push_back(r.b);
+  }
+  g_prof.clear();
+  *n_out = n;
+  return LFPS_OK;
+}
 int lfps_exact_launches(void) { return 4; }
 
 int lfps_bootstrap_tables(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
@@ -227,17 +300,17 @@ int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_sta
   if (rc) return rc;
   cudaStream_t sm = static_cast<cudaStream_t>(stream);
   const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
-  LAUNCH(lfps::launch_clear_err(c, sm));
-  LAUNCH(lfps::launch_gate(c, qb, sm));
-  LAUNCH(lfps::launch_scan(c, m_max, sm));
-  LAUNCH(lfps::launch_probe(c, sm));
-  LAUNCH(lfps::launch_score(c, qb, m_max, sm));
-  LAUNCH(lfps::launch_topk(c, -1, sm));
-  LAUNCH(lfps::launch_attend(c, qb, 0, sm));
-  LAUNCH(lfps::launch_update(c, sm));
-  LAUNCH(lfps::launch_append(c, static_cast<const __nv_bfloat16*>(k_new),
+  LAUNCH_P("clear_err", sm, lfps::launch_clear_err(c, sm));
+  LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
+  LAUNCH_P("scan", sm, lfps::launch_scan(c, m_max, sm));
+  LAUNCH_P("probe", sm, lfps::launch_probe(c, sm));
+  LAUNCH_P("score", sm, lfps::launch_score(c, qb, m_max, sm));
+  LAUNCH_P("topk", sm, lfps::launch_topk(c, -1, sm));
+  LAUNCH_P("attend", sm, lfps::launch_attend(c, qb, 0, sm));
+  LAUNCH_P("update", sm, lfps::launch_update(c, sm));
+  LAUNCH_P("append", sm, lfps::launch_append(c, static_cast<const __nv_bfloat16*>(k_new),
                              static_cast<const __nv_bfloat16*>(v_new), sm));
-  LAUNCH(lfps::launch_commit(c, sm));
+  LAUNCH_P("commit", sm, lfps::launch_commit(c, sm));
   return LFPS_OK;
 }
 
@@ -253,10 +326,10 @@ int lfps_exact_topk_step(const lfps_dims* dims, const lfps_params* p, const lfps
   if (rc) return rc;
   cudaStream_t sm = static_cast<cudaStream_t>(stream);
   const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
-  LAUNCH(lfps::launch_clear_err(c, sm));
-  LAUNCH(lfps::launch_exact_score(c, qb, m_max, sm));
-  LAUNCH(lfps::launch_topk(c, c.S, sm));
-  LAUNCH(lfps::launch_attend(c, qb, 1, sm));
+  LAUNCH_P("clear_err", sm, lfps::launch_clear_err(c, sm));
+  LAUNCH_P("exact_score", sm, lfps::launch_exact_score(c, qb, m_max, sm));
+  LAUNCH_P("exact_topk", sm, lfps::launch_topk(c, c.S, sm));
+  LAUNCH_P("exact_attend", sm, lfps::launch_attend(c, qb, 1, sm));
   return LFPS_OK;
 }
 

@@ -162,6 +162,20 @@ class BatchedSession:
         self.n_host[b] = n0
         self.n_ctx[b] = n0
 
+    def load_unit(self, b: int, h: int, keys: torch.Tensor, values: torch.Tensor):
+        """Copy one (request, KV-head) unit's prefill rows (bf16 [n0, d]);
+        every unit of a request must be loaded with the same n0."""
+        n0 = keys.shape[0]
+        if n0 >= self.n_max:
+            raise ValueError("prefill longer than the KV cache")
+        if n0 <= self.cfg.sink_count + self.cfg.s:
+            raise ValueError(
+                f"prefill needs more than sink_count + s = {self.cfg.sink_count + self.cfg.s} rows")
+        self.k_cache[b, h, :n0].copy_(keys)
+        self.v_cache[b, h, :n0].copy_(values)
+        self.n_host[b] = n0
+        self.n_ctx[b] = n0
+
     def bootstrap_tables(self, s_begin: int, weights: torch.Tensor):
         """Eq. 4 seeding for sessions [s_begin, s_begin + count); weights
         f32 [count, s, m0] on the device (init_tables, tables.py:247-281)."""

@@ -194,3 +194,42 @@ def prefill_weights(keys_bf16: torch.Tensor, prefill_q_bf16: torch.Tensor, sink:
 def bf16_to_f64(x: torch.Tensor):
     """Host fp64 numpy copy of a bf16 tensor (exact upcast)."""
     return x.detach().to("cpu", torch.float64).numpy()
+
+
+@dataclass
+class StepStream:
+    """Per-step decode inputs for a whole batch, resident on the device."""
+
+    q: torch.Tensor       # bf16 [T, B, Hq, d]
+    k_new: torch.Tensor   # bf16 [T, B, Hkv, d]
+    v_new: torch.Tensor   # bf16 [T, B, Hkv, d]
+
+
+def populate(session, spec: GqaSpec, progress=None) -> StepStream:
+    """Fill a BatchedSession with the spec's synthetic prefill (KV rows,
+    Eq. 4 tables, gate priors) and return the decode-step inputs.  Runs
+    unit by unit on the session's device so 128k x 64 fits in memory."""
+    dev = session.device
+    B, Hkv, G, d = spec.batch, spec.kv_heads, spec.group, spec.d
+    n0, T = spec.n_prefill, spec.steps
+    q = torch.empty(T, B, Hkv * G, d, dtype=torch.bfloat16, device=dev)
+    kn = torch.empty(T, B, Hkv, d, dtype=torch.bfloat16, device=dev)
+    vn = torch.empty(T, B, Hkv, d, dtype=torch.bfloat16, device=dev)
+    finals = torch.empty(B, Hkv * G, d, dtype=torch.bfloat16, device=dev)
+    for b in range(B):
+        for h in range(Hkv):
+            u = gen_unit(spec, b, h, device=dev)
+            session.load_unit(b, h, u.keys[:n0], u.values[:n0])
+            s0 = b * Hkv * G + h * G
+            session.bootstrap_tables(s0, u.weights)
+            q[:, b, h * G:(h + 1) * G] = u.queries.transpose(0, 1)
+            kn[:, b, h] = u.keys[n0:n0 + T]
+            vn[:, b, h] = u.values[n0:n0 + T]
+            finals[b, h * G:(h + 1) * G] = u.final_query
+            del u
+        if progress:
+            progress(b)
+    session.bootstrap_stats(finals)
+    torch.cuda.synchronize(dev)
+    session.check_errors("bootstrap")
+    return StepStream(q=q, k_new=kn, v_new=vn)
