@@ -17,11 +17,11 @@ sets on the golden trajectories.
 
 Definitions (DESIGN.md §3 "Canonical arithmetic"):
 
-* ``table_sum``   -- chunks of 512 elements; lane l of a warp accumulates
-  x[c*512 + e*32 + l] for e = 0..15 in order from 0.0, the 32 lane sums fold
-  halves (16, 8, 4, 2, 1); chunk partials then reduce by a pairwise tree
-  (zero-padded to a power of two).  Used for the table moments
-  (tables.py:127-140).
+* ``table_sum``   -- chunks of 512 elements; lane l of a warp holds
+  x[c*512 + e*32 + l], e = 0..15, and reduces them by an adjacent-pair tree
+  over e, the 32 lane sums fold halves (16, 8, 4, 2, 1); chunk partials then
+  reduce by a pairwise tree (zero-padded to a power of two).  Used for the
+  table moments (tables.py:127-140) and the head-stats variance.
 * ``gdot``        -- fp64 dot: lane l (of 32) accumulates j = l, l+32, ...
   in order, then folds 16..1.  Gate logits, head stats (gate.py:77-98).
 * ``sdot32``      -- fp32 probe score: 16 lanes each own d/16 contiguous
@@ -86,10 +86,9 @@ def table_chunk_partials(x: np.ndarray) -> np.ndarray:
     buf = np.zeros(nch * TABLE_CHUNK, dtype=np.float64)
     buf[:n] = x
     buf = buf.reshape(nch, TABLE_CHUNK // TABLE_LANES, TABLE_LANES)
-    acc = np.zeros((nch, TABLE_LANES), dtype=np.float64)
-    for e in range(TABLE_CHUNK // TABLE_LANES):
-        acc = acc + buf[:, e, :]
-    return _fold_halves(acc)
+    while buf.shape[1] > 1:                 # per-lane adjacent-pair tree over e
+        buf = buf[:, 0::2, :] + buf[:, 1::2, :]
+    return _fold_halves(buf[:, 0, :])
 
 
 def table_sum(x: np.ndarray) -> float:

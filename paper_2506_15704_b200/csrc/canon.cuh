@@ -53,6 +53,17 @@ __device__ __forceinline__ double warp_fold(double v) {
   return v;
 }
 
+// Adjacent-pair tree over 16 lane-resident values (devmath.table_sum):
+// ((v0+v1)+(v2+v3)) + ... ; depth 4 instead of a 16-long dependent chain.
+__device__ __forceinline__ double lane_tree16(double* v) {
+#pragma unroll
+  for (int h = 1; h < 16; h <<= 1) {
+#pragma unroll
+    for (int k = 0; k < 16; k += 2 * h) v[k] = cadd(v[k], v[k + h]);
+  }
+  return v[0];
+}
+
 // Fold within 16-lane halves: h = 8..1 (fp32, score dots).
 __device__ __forceinline__ float half_fold(float v) {
 #pragma unroll

@@ -84,5 +84,6 @@ cudaError_t launch_overlap(const Ctx& c, const int* sel, const int* sel_cnt, con
                            const int* ex_cnt, int list_stride, int cnt_stride, double* eta,
                            cudaStream_t st);
 cudaError_t launch_clear_err(const Ctx& c, cudaStream_t st);
+cudaError_t launch_scan_experiment(const Ctx& c, int m_max, int mode, int slice, cudaStream_t st);
 
 }  // namespace lfps

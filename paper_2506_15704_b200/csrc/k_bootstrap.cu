@@ -130,16 +130,18 @@ __device__ double block_table_sum(const double* x, int cnt, double mu, double* p
   for (int i = threadIdx.x; i < n2; i += blockDim.x) parts[i] = 0.0;
   __syncthreads();
   for (int ch = warp; ch < nch; ch += blockDim.x >> 5) {
-    double acc = 0.0;
+    double v[16];
+#pragma unroll
     for (int e = 0; e < 16; ++e) {
       const int i = ch * 512 + e * 32 + lane;
+      v[e] = 0.0;
       if (i < cnt) {
-        double v = x[i];
-        if (CENTRED) { v = csub(v, mu); v = cmul(v, v); }
-        acc = cadd(acc, v);
+        double t = x[i];
+        if (CENTRED) { t = csub(t, mu); t = cmul(t, t); }
+        v[e] = t;
       }
     }
-    acc = warp_fold(acc);
+    double acc = warp_fold(lane_tree16(v));
     if (lane == 0) parts[ch] = acc;
   }
   __syncthreads();

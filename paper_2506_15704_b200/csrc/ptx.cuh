@@ -59,15 +59,17 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  // try_wait suspends the warp in hardware until the phase completes or the
+  // hint (ns) expires, so waiting warps do not steal issue slots by polling
   const uint32_t a = smem_u32(bar);
   uint32_t done = 0;
   while (!done) {
     asm volatile(
         "{\n .reg .pred p;\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
         " selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(done)
-        : "r"(a), "r"(phase)
+        : "r"(a), "r"(phase), "r"(1000000u)
         : "memory");
   }
 }
@@ -76,6 +78,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// Asynchronous remote stores into a peer CTA's shared memory that complete
+// `bytes` of transaction count on the peer's mbarrier (both addresses are
+// shared::cluster addresses from map_rank).
+__device__ __forceinline__ void st_async_f64(uint32_t caddr, double v, uint32_t cbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(caddr),
+               "d"(v), "r"(cbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v2f64(uint32_t caddr, double a, double b, uint32_t cbar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(caddr),
+      "d"(a), "d"(b), "r"(cbar)
+      : "memory");
 }
 // Bulk prefetch of [src, src + bytes) into L2 (16-byte aligned, bytes % 16 == 0).
 __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
