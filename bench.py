@@ -352,7 +352,7 @@ def run_ours(args, world, rank, local):
 
     # ---- roofline of the dominant kernel (tracker-table scan) ----
     peak, peak_src = measured_peaks()
-    scan_launches, scan_ms = kt.get("scan", (0, 0.0))
+    scan_launches, scan_ms = kt.get("tables", (0, 0.0))
     scan_avg_ms = scan_ms / max(1, scan_launches)
     active = ns_local - bypass
     scan_bytes = active * 2 * 8 * m_avg                       # both fp64 tables, read once
@@ -449,7 +449,7 @@ def run_ours(args, world, rank, local):
                    "sharding": "requests across ranks, no collective on the decode path",
                    "l2": "inputs larger than L2: 4.3 GB of fp64 tables read per step"},
         "gpu_launches": args.steps * _lib.load_library().lfps_decode_launches(),
-        "roofline": {"bound": "hbm", "kernel": "scan_kernel (tracker moments + thresholds)",
+        "roofline": {"bound": "hbm", "kernel": "table stage: stats + thresholds (+fallback) kernels",
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
                      "algorithmic_bytes_per_launch": scan_bytes,

@@ -40,8 +40,8 @@ int main(int argc, char** argv) {
   std::vector<int> n(c.B, m + 4); cudaMemcpy(c.n_ctx, n.data(), c.B * 4, cudaMemcpyHostToDevice);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   const double bytes = (double)NS * 2 * 8 * m;
-  int slices[] = {0, 9216, 11264};
-  for (int mode = 0; mode < 3; ++mode) {
+  int slices[] = {0, 12288, 4096};
+  for (int mode = 0; mode < 1; ++mode) {
     for (int si = 0; si < 3; ++si) {
       cudaError_t e = launch_scan_experiment(c, m, mode, slices[si], 0);
       if (e != cudaSuccess) { printf("mode %d slice %d: %s\n", mode, slices[si], cudaGetErrorString(e)); cudaGetLastError(); continue; }
@@ -64,7 +64,7 @@ int main(int argc, char** argv) {
   cudaMemcpy(tr.data(), c.scratch, tr.size() * 8, cudaMemcpyDeviceToHost);
   unsigned long long t0 = tr[0];
   for (int r = 0; r < 16; ++r) t0 = (tr[r * 16 * 12] && tr[r * 16 * 12] < t0) ? tr[r * 16 * 12] : t0;
-  printf("trace (us rel. start): rank item: start copies_issued pass1 r1_recv pass2 r2_recv pass3 end | lead_r1 lead_r2\n");
+  printf("trace (us): rank item: start stats sent lead_done - - bits_prev - | lead_gathered\n");
   for (int it = 0; it < 6; ++it)
     for (int r = 0; r < 16; r += 5) {
       const unsigned long long* t = &tr[((size_t)r * 16 + it) * 12];

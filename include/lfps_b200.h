@@ -112,12 +112,22 @@ typedef struct lfps_ws_layout {
   size_t out;         /* f32 [NS, d] attention output */
   size_t thr;         /* f64 [NS, 2, 4] tau, mean, degenerate, kappa per table */
   size_t counts;      /* i32 [NS, 8] |c0| |c1| |probe| c0_dropped k |c2| clamps spare */
-  size_t bits;        /* u32 [NS, 2 tables, 2 kinds, words] */
+  size_t bits;        /* u32 [NS, 2 tables, words] C0 bitmaps of fallback items */
   size_t probe_idx;   /* i32 [NS, list_cap] absolute indices, ascending */
   size_t probe_score; /* f32 [NS, list_cap] */
   size_t c2_idx;      /* i32 [NS, list_cap] */
   size_t c2_score;    /* f32 [NS, list_cap] */
   size_t scratch;     /* f64 [NS, list_cap] bootstrap scratch */
+  size_t cstat;       /* f64 [2 NS, 512, 4] chunk moments */
+  size_t cidx;        /* i32 [2 NS, capture_cap] captured slots */
+  size_t cval;        /* f64 [2 NS, capture_cap] captured phys values */
+  size_t ncap;        /* i32 [2 NS] */
+  size_t itemf;       /* f64 [2 NS, 4] tau/scale, mean/scale, degenerate */
+  size_t bound;       /* f64 [2 NS] capture bound, persists across steps */
+  size_t fb;          /* i32 [2 NS] fallback taken */
+  size_t fblist;      /* i32 [2 NS] */
+  size_t nfb;         /* i32 [1] */
+  int32_t capture_cap;
   int32_t words;      /* bitmap words per (session, table, kind) */
   int32_t list_cap;   /* capacity of each per-session list */
 } lfps_ws_layout;

@@ -21,7 +21,13 @@ Definitions (DESIGN.md §3 "Canonical arithmetic"):
   x[c*512 + e*32 + l], e = 0..15, and reduces them by an adjacent-pair tree
   over e, the 32 lane sums fold halves (16, 8, 4, 2, 1); chunk partials then
   reduce by a pairwise tree (zero-padded to a power of two).  Used for the
-  table moments (tables.py:127-140) and the head-stats variance.
+  head-stats variance.
+* ``table_moments`` -- single read of the table: per 512-slot chunk the
+  chunk mean (table_sum order / count) and the chunk's centred power sums
+  M2, M3, M4 (same lane/fold order), then a pairwise tree of exact
+  pairwise-update merges (Chan et al.; Pebay 2008) over the chunks.  Same
+  quantities as the reference's two-pass _phys_moments (tables.py:127-140),
+  different rounding; the golden tests pin identical selections.
 * ``gdot``        -- fp64 dot: lane l (of 32) accumulates j = l, l+32, ...
   in order, then folds 16..1.  Gate logits, head stats (gate.py:77-98).
 * ``sdot32``      -- fp32 probe score: 16 lanes each own d/16 contiguous
@@ -96,17 +102,74 @@ def table_sum(x: np.ndarray) -> float:
     return _pairwise_tree(table_chunk_partials(x))
 
 
-def table_moments(x: np.ndarray) -> tuple[float, float, float]:
-    """(mean_p, sum c^2, sum c^4) of a phys table view, canonical order.
+def _lane_tree(buf: np.ndarray) -> np.ndarray:
+    """[nch, 16, 32] -> per-chunk fold of per-lane adjacent-pair trees."""
+    while buf.shape[1] > 1:
+        buf = buf[:, 0::2, :] + buf[:, 1::2, :]
+    return _fold_halves(buf[:, 0, :])
 
-    Restates ScoreTablePair._phys_moments (tables.py:127-140): two passes,
-    mean first, then centred powers; only the summation order differs."""
+
+def chunk_moments(x: np.ndarray):
+    """Per-chunk (count, mean, M2, M3, M4) of a table, device order."""
     x = np.asarray(x, dtype=np.float64)
-    m = x.shape[0]
-    mean = table_sum(x) / m
-    c = x - mean
-    c2 = c * c
-    return mean, table_sum(c2), table_sum(c2 * c2)
+    n = x.shape[0]
+    nch = max(1, -(-n // TABLE_CHUNK))
+    buf = np.zeros(nch * TABLE_CHUNK, dtype=np.float64)
+    buf[:n] = x
+    valid = np.zeros(nch * TABLE_CHUNK, dtype=bool)
+    valid[:n] = True
+    shape = (nch, TABLE_CHUNK // TABLE_LANES, TABLE_LANES)
+    buf = buf.reshape(shape)
+    valid = valid.reshape(shape)
+    cnt = np.minimum(np.maximum(n - np.arange(nch) * TABLE_CHUNK, 0), TABLE_CHUNK).astype(np.float64)
+    mu = _lane_tree(buf) / cnt
+    d = np.where(valid, buf - mu[:, None, None], 0.0)
+    d2 = d * d
+    d3 = d2 * d
+    d4 = d2 * d2
+    return cnt, mu, _lane_tree(d2), _lane_tree(d3), _lane_tree(d4)
+
+
+def merge_moments(a, b):
+    """Exact pairwise update of (n, mean, M2, M3, M4), device op order.
+
+    Arrays broadcast; an empty side (n == 0) returns the other unchanged."""
+    na, ma, a2, a3, a4 = a
+    nb, mb, b2, b3, b4 = b
+    with np.errstate(invalid="ignore", divide="ignore"):
+        n = na + nb
+        delta = mb - ma
+        dn = delta / n
+        dn2 = dn * dn
+        t = ((delta * dn) * na) * nb
+        mean = ma + nb * dn
+        m2 = (a2 + b2) + t
+        m3 = ((a3 + b3) + (t * dn) * (na - nb)) + (3.0 * dn) * (na * b2 - nb * a2)
+        m4 = (((a4 + b4) + (t * dn2) * ((na * na - na * nb) + nb * nb))
+              + (6.0 * dn2) * ((na * na) * b2 + (nb * nb) * a2)) + (4.0 * dn) * (na * b3 - nb * a3)
+    out = []
+    for merged, av, bv in zip((n, mean, m2, m3, m4), a, b):
+        merged = np.where(nb == 0, av, merged)
+        merged = np.where(na == 0, bv, merged)
+        out.append(merged)
+    return tuple(out)
+
+
+def table_moments(x: np.ndarray) -> tuple[float, float, float]:
+    """(mean_p, sum c^2, sum c^4) of a phys table view in ONE read.
+
+    Restates ScoreTablePair._phys_moments (tables.py:127-140) as chunk
+    moments merged by a pairwise tree over the chunks (zero-count padding to
+    a power of two)."""
+    st = chunk_moments(x)
+    nch = st[0].shape[0]
+    size = 1
+    while size < nch:
+        size *= 2
+    st = [np.concatenate([v, np.zeros(size - nch)]) for v in st]
+    while st[0].shape[0] > 1:
+        st = list(merge_moments(tuple(v[0::2] for v in st), tuple(v[1::2] for v in st)))
+    return float(st[1][0]), float(st[2][0]), float(st[4][0])
 
 
 def gdot(a: np.ndarray, b: np.ndarray) -> np.ndarray:

@@ -59,7 +59,11 @@ class WsLayout(C.Structure):
                 ("err", C.c_size_t), ("out", C.c_size_t), ("thr", C.c_size_t),
                 ("counts", C.c_size_t), ("bits", C.c_size_t), ("probe_idx", C.c_size_t),
                 ("probe_score", C.c_size_t), ("c2_idx", C.c_size_t), ("c2_score", C.c_size_t),
-                ("scratch", C.c_size_t), ("words", C.c_int32), ("list_cap", C.c_int32)]
+                ("scratch", C.c_size_t), ("cstat", C.c_size_t), ("cidx", C.c_size_t),
+                ("cval", C.c_size_t), ("ncap", C.c_size_t), ("itemf", C.c_size_t),
+                ("bound", C.c_size_t), ("fb", C.c_size_t), ("fblist", C.c_size_t),
+                ("nfb", C.c_size_t), ("capture_cap", C.c_int32), ("words", C.c_int32),
+                ("list_cap", C.c_int32)]
 
 
 class KernelTime(C.Structure):

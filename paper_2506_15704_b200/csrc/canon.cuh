@@ -16,6 +16,15 @@ __device__ __forceinline__ double csub(double a, double b) { return __dsub_rn(a,
 __device__ __forceinline__ double cmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double cdiv(double a, double b) { return __ddiv_rn(a, b); }
 
+// a / n for a count n > 0: when n is a power of two the quotient is the
+// exact product a * 2^-k (same correctly rounded value as the division, far
+// cheaper than the division sequence); otherwise a true IEEE division.
+__device__ __forceinline__ double cdiv_count(double a, double n) {
+  const long long b = __double_as_longlong(n);
+  if ((b & 0x000FFFFFFFFFFFFFll) == 0) return __dmul_rn(a, __longlong_as_double(0x7FE0000000000000ll - b));
+  return __ddiv_rn(a, n);
+}
+
 // Constants as exact bit patterns (equal to the Python doubles in
 // oracle/devmath.py: LN2_HI/LN2_LO fdlibm split, 1/ln2, 1.0/math.factorial(i)).
 __device__ __forceinline__ double dbits(unsigned long long b) { return __longlong_as_double((long long)b); }

@@ -11,6 +11,20 @@
 
 namespace lfps {
 
+// Table-stage scratch (k_tables.cu, k_probe.cu).
+struct TablesWs {
+  double* cstat;   // [2 NS][512][4] chunk moments
+  int* cidx;       // [2 NS][cap] captured slot indices (logical)
+  double* cval;    // [2 NS][cap] captured phys values
+  int* ncap;       // [2 NS] capture counts
+  int cap;
+  double* itemf;   // [2 NS][4] thr0 = tau/scale, thrf = mean/scale, degenerate
+  double* bound;   // [2 NS] capture bound for the next step (persists across steps)
+  int* fb;         // [2 NS] item took the fallback (C0 bitmap in bits)
+  int* fblist;     // [2 NS] queued fallback items
+  int* nfb;        // [1]
+};
+
 // Flattened per-launch view of dims + state + workspace (passed by value).
 struct Ctx {
   // dims
@@ -49,6 +63,7 @@ struct Ctx {
   int* c2_idx;
   float* c2_score;
   double* scratch;
+  TablesWs tb;
 };
 
 enum { CNT_C0 = 0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_SPARE, CNT_N };
@@ -67,8 +82,8 @@ __device__ __forceinline__ void set_err(const Ctx& c, int s, int code) {
 
 // ---- host-side launch wrappers (defined in the k_*.cu files) -------------
 cudaError_t launch_gate(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
-cudaError_t launch_scan(const Ctx& c, int m_max, cudaStream_t st);
-cudaError_t launch_probe(const Ctx& c, cudaStream_t st);
+cudaError_t launch_tables(const Ctx& c, int m_max, cudaStream_t st);
+cudaError_t launch_probe(const Ctx& c, int m_max, cudaStream_t st);
 cudaError_t launch_score(const Ctx& c, const __nv_bfloat16* q, int max_list, cudaStream_t st);
 cudaError_t launch_topk(const Ctx& c, int implicit_base, cudaStream_t st);
 cudaError_t launch_attend(const Ctx& c, const __nv_bfloat16* q, int exact_mode, cudaStream_t st);
@@ -84,6 +99,5 @@ cudaError_t launch_overlap(const Ctx& c, const int* sel, const int* sel_cnt, con
                            const int* ex_cnt, int list_stride, int cnt_stride, double* eta,
                            cudaStream_t st);
 cudaError_t launch_clear_err(const Ctx& c, cudaStream_t st);
-cudaError_t launch_scan_experiment(const Ctx& c, int m_max, int mode, int slice, cudaStream_t st);
 
 }  // namespace lfps

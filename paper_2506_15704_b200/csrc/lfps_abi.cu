@@ -30,8 +30,7 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(LFPS_E_CUDA, "%s: %s", where, cudaGetErrorString(e));
 }
 
-constexpr int kMaxSliceElems = 11776;   // k_scan.cu kMaxSlice rounded to 512
-constexpr int kMaxM = 16 * kMaxSliceElems;
+constexpr int kMaxM = 262144;           // k_tables.cu: <= 512 chunks of 512 slots
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -76,12 +75,16 @@ int check_params(const lfps_params* p, const lfps_dims* d) {
   return LFPS_OK;
 }
 
+constexpr int kCaptureCap = 8192;       // captured slots per (session, table) per step
+constexpr int kChunkLeaves = 512;       // k_tables.cu kLeaves
+
 int layout(const lfps_dims* d, lfps_ws_layout* L) {
   const size_t NS = (size_t)d->batch * d->kv_heads * d->group;
+  const size_t NI = 2 * NS;
   const size_t cap = (size_t)d->m_cap;
   memset(L, 0, sizeof(*L));
   L->list_cap = d->m_cap;
-  L->words = (int)((cap + kMaxSliceElems + 31) / 32);
+  L->words = (int)((cap + 511) / 512 * 16);   // whole 512-slot chunks
   size_t o = 0;
   auto take = [&](size_t bytes) { const size_t at = o; o = align_up(o + bytes, 256); return at; };
   L->rho = take(NS * 8);
@@ -90,13 +93,23 @@ int layout(const lfps_dims* d, lfps_ws_layout* L) {
   L->out = take(NS * d->d * 4);
   L->thr = take(NS * 8 * 8);
   L->counts = take(NS * lfps::CNT_N * 4);
-  L->bits = take(NS * 4 * (size_t)L->words * 4);
+  L->bits = take(NI * (size_t)L->words * 4);
   L->probe_idx = take(NS * cap * 4);
   L->probe_score = take(NS * cap * 4);
   L->c2_idx = take(NS * cap * 4);
   L->c2_score = take(NS * cap * 4);
   // bootstrap scratch (f64 logits) aliases probe_idx + probe_score
   L->scratch = L->probe_idx;
+  L->cstat = take(NI * kChunkLeaves * 4 * 8);
+  L->cidx = take(NI * kCaptureCap * 4);
+  L->cval = take(NI * kCaptureCap * 8);
+  L->ncap = take(NI * 4);
+  L->itemf = take(NI * 4 * 8);
+  L->bound = take(NI * 8);
+  L->fb = take(NI * 4);
+  L->fblist = take(NI * 4);
+  L->nfb = take(64);
+  L->capture_cap = kCaptureCap;
   L->total_bytes = o;
   return LFPS_OK;
 }
@@ -143,6 +156,16 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
   c->c2_idx = reinterpret_cast<int*>(base + L.c2_idx);
   c->c2_score = reinterpret_cast<float*>(base + L.c2_score);
   c->scratch = reinterpret_cast<double*>(base + L.scratch);
+  c->tb.cstat = reinterpret_cast<double*>(base + L.cstat);
+  c->tb.cidx = reinterpret_cast<int*>(base + L.cidx);
+  c->tb.cval = reinterpret_cast<double*>(base + L.cval);
+  c->tb.ncap = reinterpret_cast<int*>(base + L.ncap);
+  c->tb.cap = L.capture_cap;
+  c->tb.itemf = reinterpret_cast<double*>(base + L.itemf);
+  c->tb.bound = reinterpret_cast<double*>(base + L.bound);
+  c->tb.fb = reinterpret_cast<int*>(base + L.fb);
+  c->tb.fblist = reinterpret_cast<int*>(base + L.fblist);
+  c->tb.nfb = reinterpret_cast<int*>(base + L.nfb);
   return LFPS_OK;
 }
 
@@ -224,7 +247,8 @@ int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out) {
   return layout(dims, out);
 }
 
-int lfps_decode_launches(void) { return 10; }
+int lfps_decode_launches(void) { return 13; }  // clear, gate, 4 table kernels, probe,
+                                              // score, topk, attend, update, append, commit
 
 int lfps_profile_enable(int on) {
   std::lock_guard<std::mutex> g(g_prof_mu);
@@ -302,8 +326,8 @@ int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_sta
   const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
   LAUNCH_P("clear_err", sm, lfps::launch_clear_err(c, sm));
   LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
-  LAUNCH_P("scan", sm, lfps::launch_scan(c, m_max, sm));
-  LAUNCH_P("probe", sm, lfps::launch_probe(c, sm));
+  LAUNCH_P("tables", sm, lfps::launch_tables(c, m_max, sm));
+  LAUNCH_P("probe", sm, lfps::launch_probe(c, m_max, sm));
   LAUNCH_P("score", sm, lfps::launch_score(c, qb, m_max, sm));
   LAUNCH_P("topk", sm, lfps::launch_topk(c, -1, sm));
   LAUNCH_P("attend", sm, lfps::launch_attend(c, qb, 0, sm));
