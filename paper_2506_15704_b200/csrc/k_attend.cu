@@ -45,7 +45,7 @@ __device__ __forceinline__ void load_frag(const __nv_bfloat16* row, int hl, floa
 }
 
 template <int PER>
-__global__ void __launch_bounds__(kThreads) attend_kernel(Ctx c, const __nv_bfloat16* q,
+__global__ void __launch_bounds__(kThreads) lfps_attend_kernel(Ctx c, const __nv_bfloat16* q,
                                                           int exact_mode) {
   __shared__ float sink_z[32];
   __shared__ float red_max[kThreads / 32];
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kThreads) attend_kernel(Ctx c, const __nv_bflo
 
 template <int PER>
 cudaError_t launch_attend_d(const Ctx& c, const __nv_bfloat16* q, int exact_mode, cudaStream_t st) {
-  attend_kernel<PER><<<c.NS, kThreads, 0, st>>>(c, q, exact_mode);
+  lfps_attend_kernel<PER><<<c.NS, kThreads, 0, st>>>(c, q, exact_mode);
   return cudaGetLastError();
 }
 

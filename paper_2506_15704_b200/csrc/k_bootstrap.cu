@@ -1,13 +1,13 @@
 // k_bootstrap.cu -- prefill bootstrap on the device (next-row N1).
 //
-// boot_tables_kernel  : Eq. 4 seeding (init_tables, tables.py:247-281); rows
+// lfps_boot_tables_kernel  : Eq. 4 seeding (init_tables, tables.py:247-281); rows
 //                       accumulated oldest first, exactly numpy's axis-0 order,
 //                       so the seeded tables equal the reference's bit for bit.
-// boot_rowsum_kernel  : each prefill weight row sums to 1 within 1e-4
+// lfps_boot_rowsum_kernel  : each prefill weight row sums to 1 within 1e-4
 //                       (prefill_bootstrap, engine.py:84-86).
-// boot_mean_kernel    : K-bar / V-bar over the non-sink rows, rows summed in
+// lfps_boot_mean_kernel    : K-bar / V-bar over the non-sink rows, rows summed in
 //                       order (numpy's keys_ns.mean(axis=0), gate.py:71-72).
-// boot_logit_kernel + boot_sigma_kernel : sigma_hat^2 = var(logits) / |q|^2
+// lfps_boot_logit_kernel + lfps_boot_sigma_kernel : sigma_hat^2 = var(logits) / |q|^2
 //                       with canonical fp64 dots and chunked sums
 //                       (gate.py:61-67, devmath DevArith.head_sigma).
 #include "common.cuh"
@@ -17,7 +17,7 @@ namespace lfps {
 
 namespace {
 
-__global__ void boot_tables_kernel(Ctx c, const float* w, int s_begin, int m0) {
+__global__ void lfps_boot_tables_kernel(Ctx c, const float* w, int s_begin, int m0) {
   const int sl = blockIdx.y;
   const int s = s_begin + sl;
   const int sp = c.s;
@@ -46,7 +46,7 @@ __global__ void boot_tables_kernel(Ctx c, const float* w, int s_begin, int m0) {
   }
 }
 
-__global__ void boot_rowsum_kernel(Ctx c, const float* w, int s_begin, int m0) {
+__global__ void lfps_boot_rowsum_kernel(Ctx c, const float* w, int s_begin, int m0) {
   __shared__ double red[32];
   const int sl = blockIdx.x, r = blockIdx.y;
   const float* row = w + ((size_t)sl * c.s + r) * m0;
@@ -63,7 +63,7 @@ __global__ void boot_rowsum_kernel(Ctx c, const float* w, int s_begin, int m0) {
 }
 
 // one CTA per unit, one thread per (matrix, column): sequential row sums
-__global__ void boot_mean_kernel(Ctx c) {
+__global__ void lfps_boot_mean_kernel(Ctx c) {
   const int u = blockIdx.x;
   const int b = u / c.Hkv, h = u % c.Hkv;
   const int n = c.n_ctx[b];
@@ -91,7 +91,7 @@ __global__ void boot_mean_kernel(Ctx c) {
 }
 
 // logits of every non-sink row for every session of a unit -> scratch
-__global__ void boot_logit_kernel(Ctx c, const __nv_bfloat16* q) {
+__global__ void lfps_boot_logit_kernel(Ctx c, const __nv_bfloat16* q) {
   const int u = blockIdx.y;
   const int b = u / c.Hkv, h = u % c.Hkv;
   const int n = c.n_ctx[b];
@@ -155,7 +155,7 @@ __device__ double block_table_sum(const double* x, int cnt, double mu, double* p
   return tot;
 }
 
-__global__ void boot_sigma_kernel(Ctx c, const __nv_bfloat16* q, int n2) {
+__global__ void lfps_boot_sigma_kernel(Ctx c, const __nv_bfloat16* q, int n2) {
   extern __shared__ double parts[];
   const int s = blockIdx.x;
   const int b = s / c.Hq;
@@ -189,28 +189,28 @@ __global__ void boot_sigma_kernel(Ctx c, const __nv_bfloat16* q, int n2) {
 cudaError_t launch_boot_tables(const Ctx& c, const float* w, int s_begin, int count, int m0,
                                cudaStream_t st) {
   const int blocks = (c.ring_cap + 255) / 256;
-  boot_tables_kernel<<<dim3(blocks < 1024 ? blocks : 1024, count), 256, 0, st>>>(c, w, s_begin, m0);
+  lfps_boot_tables_kernel<<<dim3(blocks < 1024 ? blocks : 1024, count), 256, 0, st>>>(c, w, s_begin, m0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  boot_rowsum_kernel<<<dim3(count, c.s), 256, 0, st>>>(c, w, s_begin, m0);
+  lfps_boot_rowsum_kernel<<<dim3(count, c.s), 256, 0, st>>>(c, w, s_begin, m0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_boot_stats(const Ctx& c, const __nv_bfloat16* q, int m_max, cudaStream_t st) {
   const int units = c.B * c.Hkv;
-  boot_mean_kernel<<<units, 2 * c.d, 0, st>>>(c);
+  lfps_boot_mean_kernel<<<units, 2 * c.d, 0, st>>>(c);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int per_unit = (148 * 8 + units - 1) / units;
   if (per_unit > 256) per_unit = 256;
-  boot_logit_kernel<<<dim3(per_unit, units), 256, 0, st>>>(c, q);
+  lfps_boot_logit_kernel<<<dim3(per_unit, units), 256, 0, st>>>(c, q);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int nch = (m_max + 511) / 512;
   int n2 = 1;
   while (n2 < nch) n2 <<= 1;
   if (n2 < 32) n2 = 32;
-  boot_sigma_kernel<<<c.NS, 256, n2 * sizeof(double), st>>>(c, q, n2);
+  lfps_boot_sigma_kernel<<<c.NS, 256, n2 * sizeof(double), st>>>(c, q, n2);
   return cudaGetLastError();
 }
 

@@ -30,7 +30,7 @@ __device__ __forceinline__ double row_dot(const __nv_bfloat16* row, const double
   return warp_fold(acc);
 }
 
-__global__ void __launch_bounds__(kWarps * 32) gate_kernel(Ctx c, const __nv_bfloat16* q) {
+__global__ void __launch_bounds__(kWarps * 32) lfps_gate_kernel(Ctx c, const __nv_bfloat16* q) {
   const int lane = threadIdx.x & 31;
   const int s = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (s >= c.NS) return;
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kWarps * 32) gate_kernel(Ctx c, const __nv_bfl
 
 cudaError_t launch_gate(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
   const int blocks = (c.NS + kWarps - 1) / kWarps;
-  gate_kernel<<<blocks, kWarps * 32, 0, st>>>(c, q);
+  lfps_gate_kernel<<<blocks, kWarps * 32, 0, st>>>(c, q);
   return cudaGetLastError();
 }
 

@@ -6,7 +6,7 @@ namespace lfps {
 
 namespace {
 
-__global__ void overlap_kernel(const int* sel, const int* sel_cnt, const int* ex,
+__global__ void lfps_overlap_kernel(const int* sel, const int* sel_cnt, const int* ex,
                                const int* ex_cnt, int list_stride, int cnt_stride, double* eta) {
   __shared__ int red[8];
   const int s = blockIdx.x;
@@ -39,7 +39,7 @@ __global__ void overlap_kernel(const int* sel, const int* sel_cnt, const int* ex
 cudaError_t launch_overlap(const Ctx& c, const int* sel, const int* sel_cnt, const int* ex,
                            const int* ex_cnt, int list_stride, int cnt_stride, double* eta,
                            cudaStream_t st) {
-  overlap_kernel<<<c.NS, 256, 0, st>>>(sel, sel_cnt, ex, ex_cnt, list_stride, cnt_stride, eta);
+  lfps_overlap_kernel<<<c.NS, 256, 0, st>>>(sel, sel_cnt, ex, ex_cnt, list_stride, cnt_stride, eta);
   return cudaGetLastError();
 }
 

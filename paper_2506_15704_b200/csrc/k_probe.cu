@@ -38,7 +38,7 @@ __device__ __forceinline__ long long thr_bits(double t) {
   return __double_as_longlong(t);
 }
 
-__global__ void __launch_bounds__(kThreads) probe_kernel(Ctx c) {
+__global__ void __launch_bounds__(kThreads) lfps_probe_kernel(Ctx c) {
   extern __shared__ uint32_t smem[];
   __shared__ int blk[512];
   __shared__ int red[4][kWarps];
@@ -196,10 +196,10 @@ cudaError_t launch_probe(const Ctx& c, int m_max, cudaStream_t st) {
   const size_t smem = 2 * (size_t)((m_max + 31) / 32) * 4;
   static int set = 0;
   if (!set) {
-    cudaFuncSetAttribute(probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(lfps_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     set = 1;
   }
-  probe_kernel<<<c.NS, kThreads, smem, st>>>(c);
+  lfps_probe_kernel<<<c.NS, kThreads, smem, st>>>(c);
   return cudaGetLastError();
 }
 

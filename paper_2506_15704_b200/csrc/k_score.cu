@@ -8,8 +8,8 @@
 // IEEE division.  Restates engine.py:168-170 / numerics.py:33-49 with fp32
 // accumulation (Top-k identical given fp32 scores).
 //
-// score_kernel: gathers the rows of each session's probe list.
-// exact_score_kernel: streams every non-sink row of a (request, KV-head)
+// lfps_score_kernel: gathers the rows of each session's probe list.
+// lfps_exact_score_kernel: streams every non-sink row of a (request, KV-head)
 // once and scores it against all G query heads of the unit (GQA GEMV).
 #include "common.cuh"
 #include "canon.cuh"
@@ -64,7 +64,7 @@ __device__ __forceinline__ float frag_dot(const float* k, const float* q) {
 }
 
 template <int PER>
-__global__ void __launch_bounds__(kThreads) score_kernel(Ctx c, const __nv_bfloat16* q) {
+__global__ void __launch_bounds__(kThreads) lfps_score_kernel(Ctx c, const __nv_bfloat16* q) {
   const int s = blockIdx.y;
   const int p = c.counts[(size_t)s * CNT_N + CNT_PROBE];
   const int half = threadIdx.x >> 4, hl = threadIdx.x & 15;
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kThreads) score_kernel(Ctx c, const __nv_bfloa
 // Exact path: all rows [S, n) of unit u scored for its G sessions.
 // Scores land in probe_score[s][row - S] (implicit index list).
 template <int PER, int G>
-__global__ void __launch_bounds__(kThreads) exact_score_kernel(Ctx c, const __nv_bfloat16* q) {
+__global__ void __launch_bounds__(kThreads) lfps_exact_score_kernel(Ctx c, const __nv_bfloat16* q) {
   const int u = blockIdx.y;
   const int b = u / c.Hkv, h = u % c.Hkv;
   const int n = c.n_ctx[b];
@@ -137,7 +137,7 @@ cudaError_t launch_score_d(const Ctx& c, const __nv_bfloat16* q, int max_list, c
   if (per_session > cap) per_session = cap;
   if (per_session > 64) per_session = 64;
   if (per_session < 2) per_session = 2;
-  score_kernel<PER><<<dim3(per_session, c.NS), kThreads, 0, st>>>(c, q);
+  lfps_score_kernel<PER><<<dim3(per_session, c.NS), kThreads, 0, st>>>(c, q);
   return cudaGetLastError();
 }
 
@@ -151,10 +151,10 @@ cudaError_t launch_exact_d(const Ctx& c, const __nv_bfloat16* q, int m_max, cuda
   if (per_unit < 1) per_unit = 1;
   const dim3 grid(per_unit, units);
   switch (c.G) {
-    case 1: exact_score_kernel<PER, 1><<<grid, kThreads, 0, st>>>(c, q); break;
-    case 2: exact_score_kernel<PER, 2><<<grid, kThreads, 0, st>>>(c, q); break;
-    case 4: exact_score_kernel<PER, 4><<<grid, kThreads, 0, st>>>(c, q); break;
-    case 8: exact_score_kernel<PER, 8><<<grid, kThreads, 0, st>>>(c, q); break;
+    case 1: lfps_exact_score_kernel<PER, 1><<<grid, kThreads, 0, st>>>(c, q); break;
+    case 2: lfps_exact_score_kernel<PER, 2><<<grid, kThreads, 0, st>>>(c, q); break;
+    case 4: lfps_exact_score_kernel<PER, 4><<<grid, kThreads, 0, st>>>(c, q); break;
+    case 8: lfps_exact_score_kernel<PER, 8><<<grid, kThreads, 0, st>>>(c, q); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -3,13 +3,13 @@
 // Restates compute_thresholds (tables.py:295-317) and select_initial
 // (candidates.py:45-58) for every (session, table) item of the batch.
 //
-//   stats_kernel    streams every table once (coalesced 8-byte lane loads,
+//   lfps_stats_kernel    streams every table once (coalesced 8-byte lane loads,
 //                   no inter-CTA synchronisation): per 512-slot chunk the
 //                   mean and centred power sums M2, M3, M4 (canonical
 //                   devmath.chunk_moments), and a capture of every slot whose
 //                   phys value exceeds the item's capture bound L (index and
 //                   value appended to a per-item list).
-//   thresh_kernel   one warp per item: merges the chunk moments (exact
+//   lfps_thresh_kernel   one warp per item: merges the chunk moments (exact
 //                   pairwise updates, canonical tree) into mean, s2, s4 and
 //                   derives tau/scale, mean/scale and the degenerate flag.
 //                   C0 = {slots with phys > tau/scale}; because the capture
@@ -18,7 +18,7 @@
 //                   without a second pass over the table.  If that guarantee
 //                   fails (no bound yet, bound above tau/scale, or the list
 //                   overflowed) the item is queued for the fallback.
-//   fallback_kernel rare: re-reads a queued item and writes its C0 bitmap.
+//   lfps_fallback_kernel rare: re-reads a queued item and writes its C0 bitmap.
 //
 // The capture bound is half of the item's previous-step tau/scale: between
 // steps the lazy scale only shrinks (r < 1), so tau/scale in phys units grows
@@ -132,66 +132,87 @@ __device__ __forceinline__ void chunk_moments(const double* v, int vc, int lane,
 }
 
 // ---------------------------------------------------------------------------
-// stats_kernel: one warp per (item, chunk), grid-stride
+// lfps_stats_kernel: one warp per (item, chunk), grid-stride
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, 3) stats_kernel(Ctx c, int nch_max) {
-  const int lane = threadIdx.x & 31;
-  const long long n_work = (long long)2 * c.NS * nch_max;
-  const long long wstride = (long long)gridDim.x * kWarps;
-  for (long long w = (long long)blockIdx.x * kWarps + (threadIdx.x >> 5); w < n_work; w += wstride) {
-    const int item = (int)(w / nch_max);
-    const int ch = (int)(w % nch_max);
-    const int s = item >> 1;
-    const int m = c.n_ctx[s / c.Hq] - c.S;
-    if (ch * kChunk >= m || c.bypass[s]) continue;
-    const int vc = min(kChunk, m - ch * kChunk);
-    const int base = (item & 1) ? c.sla_base[s] : 0;
-    double v[16];
-    load_chunk(c, item, base, m, ch, lane, v);
-    double mu, m2, m3, m4;
-    chunk_moments(v, vc, lane, mu, m2, m3, m4);
-    double* cs = c.tb.cstat + ((size_t)item * kLeaves + ch) * 4;
-    if (lane == 0) {
-      cs[0] = mu; cs[1] = m2; cs[2] = m3; cs[3] = m4;
+struct ChunkRef {
+  int item, ch, m, vc, base;
+  bool live;
+};
+
+__device__ __forceinline__ ChunkRef chunk_ref(const Ctx& c, long long w, long long n_work,
+                                              int nch_max) {
+  ChunkRef r;
+  r.live = false;
+  r.item = r.ch = r.m = r.vc = r.base = 0;
+  if (w >= n_work) return r;
+  r.item = (int)(w / nch_max);
+  r.ch = (int)(w % nch_max);
+  const int s = r.item >> 1;
+  r.m = c.n_ctx[s / c.Hq] - c.S;
+  r.live = r.ch * kChunk < r.m && !c.bypass[s];
+  r.vc = min(kChunk, r.m - r.ch * kChunk);
+  r.base = (r.item & 1) ? c.sla_base[s] : 0;
+  return r;
+}
+
+__device__ __forceinline__ void chunk_process(const Ctx& c, const ChunkRef& r, const double* v,
+                                              int lane) {
+  double mu, m2, m3, m4;
+  chunk_moments(v, r.vc, lane, mu, m2, m3, m4);
+  double* cs = c.tb.cstat + ((size_t)r.item * kLeaves + r.ch) * 4;
+  if (lane == 0) {
+    cs[0] = mu; cs[1] = m2; cs[2] = m3; cs[3] = m4;
+  }
+  // capture slots above the bound (index + value)
+  const double L = c.tb.bound[r.item];
+  if (L > 0.0) {
+    const long long Lb = __double_as_longlong(L);
+    int nmy = 0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) nmy += (__double_as_longlong(v[e]) > Lb) && (e * 32 + lane < r.vc);
+    int incl = nmy;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(LFPS_FULL, incl, o);
+      if (lane >= o) incl += y;
     }
-    // capture slots above the bound (index + value)
-    const double L = c.tb.bound[item];
-    if (L > 0.0) {
-      const long long Lb = __double_as_longlong(L);
-      int nmy = 0;
+    const int tot = __shfl_sync(LFPS_FULL, incl, 31);
+    if (tot > 0) {
+      int at = 0;
+      if (lane == 31) at = atomicAdd(c.tb.ncap + r.item, tot);
+      at = __shfl_sync(LFPS_FULL, at, 31) + incl - nmy;
+      int* ci = c.tb.cidx + (size_t)r.item * c.tb.cap;
+      double* cv = c.tb.cval + (size_t)r.item * c.tb.cap;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) nmy += (__double_as_longlong(v[e]) > Lb) && (e * 32 + lane < vc);
-      int incl = nmy;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(LFPS_FULL, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int tot = __shfl_sync(LFPS_FULL, incl, 31);
-      if (tot > 0) {
-        int at = 0;
-        if (lane == 31) at = atomicAdd(c.tb.ncap + item, tot);
-        at = __shfl_sync(LFPS_FULL, at, 31) + incl - nmy;
-        int* ci = c.tb.cidx + (size_t)item * c.tb.cap;
-        double* cv = c.tb.cval + (size_t)item * c.tb.cap;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const int i = ch * kChunk + e * 32 + lane;
-          if ((__double_as_longlong(v[e]) > Lb) && (e * 32 + lane < vc)) {
-            if (at < c.tb.cap) {
-              ci[at] = i;
-              cv[at] = v[e];
-            }
-            ++at;
+      for (int e = 0; e < 16; ++e) {
+        const int i = r.ch * kChunk + e * 32 + lane;
+        if ((__double_as_longlong(v[e]) > Lb) && (e * 32 + lane < r.vc)) {
+          if (at < c.tb.cap) {
+            ci[at] = i;
+            cv[at] = v[e];
           }
+          ++at;
         }
       }
     }
   }
 }
 
+__global__ void __launch_bounds__(kThreads, 3) lfps_stats_kernel(Ctx c, int nch_max) {
+  const int lane = threadIdx.x & 31;
+  const long long n_work = (long long)2 * c.NS * nch_max;
+  const long long wstride = (long long)gridDim.x * kWarps;
+  for (long long w = (long long)blockIdx.x * kWarps + (threadIdx.x >> 5); w < n_work; w += wstride) {
+    const ChunkRef r = chunk_ref(c, w, n_work, nch_max);
+    if (!r.live) continue;
+    double v[16];
+    load_chunk(c, r.item, r.base, r.m, r.ch, lane, v);
+    chunk_process(c, r, v, lane);
+  }
+}
+
 // ---------------------------------------------------------------------------
-// thresh_kernel: one warp per item
+// lfps_thresh_kernel: one warp per item
 // ---------------------------------------------------------------------------
 __device__ __noinline__ Mom item_merge(const double* cs, int n_chunks, int m, int lane) {
   Mom stk[4];
@@ -224,7 +245,7 @@ __device__ __noinline__ Mom item_merge(const double* cs, int n_chunks, int m, in
   return acc;
 }
 
-__global__ void __launch_bounds__(kThreads) thresh_kernel(Ctx c) {
+__global__ void __launch_bounds__(kThreads) lfps_thresh_kernel(Ctx c) {
   const int lane = threadIdx.x & 31;
   const int item = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (item >= 2 * c.NS) return;
@@ -271,9 +292,9 @@ __global__ void __launch_bounds__(kThreads) thresh_kernel(Ctx c) {
 }
 
 // ---------------------------------------------------------------------------
-// fallback_kernel: C0 bitmap of queued items (one warp per chunk)
+// lfps_fallback_kernel: C0 bitmap of queued items (one warp per chunk)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) fallback_kernel(Ctx c, int nch_max) {
+__global__ void __launch_bounds__(kThreads) lfps_fallback_kernel(Ctx c, int nch_max) {
   const int lane = threadIdx.x & 31;
   const int nq = *c.tb.nfb;
   const long long n_work = (long long)nq * nch_max;
@@ -299,7 +320,7 @@ __global__ void __launch_bounds__(kThreads) fallback_kernel(Ctx c, int nch_max) 
   }
 }
 
-__global__ void tables_reset_kernel(Ctx c) {
+__global__ void lfps_tables_reset_kernel(Ctx c) {
   const int n = 2 * c.NS;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     c.tb.ncap[i] = 0;
@@ -315,25 +336,25 @@ cudaError_t launch_tables(const Ctx& c, int m_max, cudaStream_t st) {
   if (nch_max > kLeaves) return cudaErrorInvalidValue;
   if (!g_stats_grid) {
     int per_sm = 0, dev = 0, sms = 148;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stats_kernel, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lfps_stats_kernel, kThreads, 0);
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     g_stats_grid = sms * (per_sm > 0 ? per_sm : 1);
   }
-  tables_reset_kernel<<<16, 256, 0, st>>>(c);
+  lfps_tables_reset_kernel<<<16, 256, 0, st>>>(c);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (!c.exhaustive) {
     const long long work = (long long)2 * c.NS * nch_max;
     long long grid = (work + kWarps - 1) / kWarps;
     if (grid > g_stats_grid) grid = g_stats_grid;
-    stats_kernel<<<(int)grid, kThreads, 0, st>>>(c, nch_max);
+    lfps_stats_kernel<<<(int)grid, kThreads, 0, st>>>(c, nch_max);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  thresh_kernel<<<(2 * c.NS + kWarps - 1) / kWarps, kThreads, 0, st>>>(c);
+  lfps_thresh_kernel<<<(2 * c.NS + kWarps - 1) / kWarps, kThreads, 0, st>>>(c);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (!c.exhaustive) {
-    fallback_kernel<<<g_stats_grid, kThreads, 0, st>>>(c, nch_max);
+    lfps_fallback_kernel<<<g_stats_grid, kThreads, 0, st>>>(c, nch_max);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -44,7 +44,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_sums, int* total
   return before;
 }
 
-__global__ void __launch_bounds__(kThreads) topk_kernel(Ctx c, int implicit_base) {
+__global__ void __launch_bounds__(kThreads) lfps_topk_kernel(Ctx c, int implicit_base) {
   __shared__ unsigned hist[256];
   __shared__ int warp_sums[kWarps];
   __shared__ unsigned sel_digit;
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kThreads) topk_kernel(Ctx c, int implicit_base
 }  // namespace
 
 cudaError_t launch_topk(const Ctx& c, int implicit_base, cudaStream_t st) {
-  topk_kernel<<<c.NS, kThreads, 0, st>>>(c, implicit_base);
+  lfps_topk_kernel<<<c.NS, kThreads, 0, st>>>(c, implicit_base);
   return cudaGetLastError();
 }
 

@@ -1,6 +1,6 @@
 // k_update.cu -- tracker update + grow (K6), KV append and commit.
 //
-// update_kernel restates ScoreTablePair.update / grow (tables.py:144-220)
+// lfps_update_kernel restates ScoreTablePair.update / grow (tables.py:144-220)
 // in ring form: u = canonical fp64 softmax of the selected fp32 scores
 // (engine.py:184, devmath.softmax_update); |sum u - 1| <= 1e-6 check;
 // scale *= r with renormalisation below 1e-120 (vertical [0, m) and slash
@@ -21,7 +21,7 @@ namespace {
 
 constexpr int kThreads = 256;
 
-__global__ void __launch_bounds__(kThreads) update_kernel(Ctx c) {
+__global__ void __launch_bounds__(kThreads) lfps_update_kernel(Ctx c) {
   __shared__ double red[9];
   __shared__ int clamp_red[kThreads / 32];
   const int s = blockIdx.x, tid = threadIdx.x;
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads) update_kernel(Ctx c) {
 }
 
 // K/V append of the step's new rows at position n (store.py:64-77).
-__global__ void append_kernel(Ctx c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new) {
+__global__ void lfps_append_kernel(Ctx c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new) {
   if (c.err[0] != 0) return;
   const int u = blockIdx.x;
   const int b = u / c.Hkv, h = u % c.Hkv;
@@ -124,12 +124,12 @@ __global__ void append_kernel(Ctx c, const __nv_bfloat16* k_new, const __nv_bflo
 }
 
 // Publish the new context length after every reader of n is done.
-__global__ void commit_kernel(Ctx c) {
+__global__ void lfps_commit_kernel(Ctx c) {
   if (c.err[0] != 0) return;
   for (int b = threadIdx.x; b < c.B; b += blockDim.x) c.n_ctx[b] += 1;
 }
 
-__global__ void clear_err_kernel(Ctx c) {
+__global__ void lfps_clear_err_kernel(Ctx c) {
   for (int i = threadIdx.x + blockIdx.x * blockDim.x; i <= c.NS; i += blockDim.x * gridDim.x)
     c.err[i] = 0;
 }
@@ -137,23 +137,23 @@ __global__ void clear_err_kernel(Ctx c) {
 }  // namespace
 
 cudaError_t launch_update(const Ctx& c, cudaStream_t st) {
-  update_kernel<<<c.NS, kThreads, 0, st>>>(c);
+  lfps_update_kernel<<<c.NS, kThreads, 0, st>>>(c);
   return cudaGetLastError();
 }
 
 cudaError_t launch_append(const Ctx& c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new,
                           cudaStream_t st) {
-  append_kernel<<<c.B * c.Hkv, 128, 0, st>>>(c, k_new, v_new);
+  lfps_append_kernel<<<c.B * c.Hkv, 128, 0, st>>>(c, k_new, v_new);
   return cudaGetLastError();
 }
 
 cudaError_t launch_commit(const Ctx& c, cudaStream_t st) {
-  commit_kernel<<<1, 256, 0, st>>>(c);
+  lfps_commit_kernel<<<1, 256, 0, st>>>(c);
   return cudaGetLastError();
 }
 
 cudaError_t launch_clear_err(const Ctx& c, cudaStream_t st) {
-  clear_err_kernel<<<(c.NS + 256) / 256, 256, 0, st>>>(c);
+  lfps_clear_err_kernel<<<(c.NS + 256) / 256, 256, 0, st>>>(c);
   return cudaGetLastError();
 }
 
