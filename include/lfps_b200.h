@@ -86,7 +86,12 @@ typedef struct lfps_params {
   int32_t exhaustive;  /* exhaustive_fallback */
   int32_t n_offsets;   /* distinct expansion offsets, <= 16 */
   int32_t offsets[16]; /* each in [-31, 31] */
+  int32_t flags;       /* LFPS_FLAG_* */
 } lfps_params;
+
+/* lfps_params.flags */
+#define LFPS_FLAG_EXPORT_SETS 1  /* write the C0 / C1 bitmaps of every session to
+                                    ws.bits ([NS][2][words]: C0 then C1) */
 
 /* Persistent per-layer state (caller-owned device buffers). */
 typedef struct lfps_state {

@@ -16,6 +16,7 @@ from .errors import DeviceError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "liblfps_b200.so")
 ABI_VERSION = 1
+FLAG_EXPORT_SETS = 1
 
 # per-session device error codes (include/lfps_b200.h)
 ERR_NAMES = {
@@ -43,7 +44,7 @@ class Params(C.Structure):
                 ("k_fraction", C.c_double), ("sqrt_d", C.c_double), ("sqrt_d_f32", C.c_float),
                 ("s", C.c_int32), ("sink_count", C.c_int32), ("local_window", C.c_int32),
                 ("bypass_mode", C.c_int32), ("exhaustive", C.c_int32),
-                ("n_offsets", C.c_int32), ("offsets", C.c_int32 * 16)]
+                ("n_offsets", C.c_int32), ("offsets", C.c_int32 * 16), ("flags", C.c_int32)]
 
 
 class State(C.Structure):

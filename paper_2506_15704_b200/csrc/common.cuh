@@ -34,7 +34,7 @@ struct Ctx {
   // params
   double r, eps, a, frac, sqrt_d;
   float sqrt_d_f32;
-  int s, S, L, bypass_mode, exhaustive, n_off;
+  int s, S, L, bypass_mode, exhaustive, n_off, flags;
   int off[16];
   // state
   const __nv_bfloat16* K;

@@ -116,13 +116,29 @@ __global__ void __launch_bounds__(kThreads) lfps_probe_kernel(Ctx c) {
     if (c.exhaustive) {
       c1 = cand;
     } else {
+      // F at the dilated positions, four positions (eight loads) in flight
       while (cand) {
-        const int bit = __ffs(cand) - 1;
-        cand &= cand - 1;
-        const int i = w * 32 + bit;
-        int p = base + i;
-        if (p >= C) p -= C;
-        if (__ldcg(ver + i) > tfv || __ldcg(ring + p) > tfs) c1 |= 1u << bit;
+        int pos[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          pos[q] = cand ? __ffs(cand) - 1 : -1;
+          cand &= cand - 1;
+        }
+        long long xv[4], xs[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          xv[q] = xs[q] = -1ll;
+          if (pos[q] >= 0) {
+            const int i = w * 32 + pos[q];
+            int p = base + i;
+            if (p >= C) p -= C;
+            xv[q] = __ldcg(ver + i);
+            xs[q] = __ldcg(ring + p);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (pos[q] >= 0 && (xv[q] > tfv || xs[q] > tfs)) c1 |= 1u << pos[q];
       }
     }
     uint32_t tail = 0;
@@ -130,6 +146,10 @@ __global__ void __launch_bounds__(kThreads) lfps_probe_kernel(Ctx c) {
     if (in && j0 + 32 > tail_lo) tail = (LFPS_FULL << max(0, tail_lo - j0)) & valid;
     const uint32_t pr = c1 | tail;
     if (in) pwords[w] = pr;
+    if (in && (c.flags & LFPS_FLAG_EXPORT_SETS)) {
+      c.bits[(size_t)(2 * s) * c.words + w] = cur;      // C0
+      c.bits[(size_t)(2 * s + 1) * c.words + w] = c1;   // C1
+    }
     n0 += __popc(cur);
     n1 += __popc(c1);
     nd += __popc(cur & ~c1);

@@ -132,6 +132,7 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
   c->r = p->r; c->eps = p->epsilon; c->a = p->a; c->frac = p->k_fraction; c->sqrt_d = p->sqrt_d;
   c->sqrt_d_f32 = p->sqrt_d_f32; c->s = p->s; c->S = p->sink_count; c->L = p->local_window;
   c->bypass_mode = p->bypass_mode; c->exhaustive = p->exhaustive; c->n_off = p->n_offsets;
+  c->flags = p->flags;
   for (int i = 0; i < 16; ++i) c->off[i] = i < p->n_offsets ? p->offsets[i] : 0;
   c->K = static_cast<const __nv_bfloat16*>(st->k_cache);
   c->V = static_cast<const __nv_bfloat16*>(st->v_cache);

@@ -21,6 +21,7 @@ import ctypes as C
 import math
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -30,7 +31,7 @@ from .errors import DeviceError, LfpsError
 CNT_C0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP = range(7)
 
 
-def make_params(cfg: LfpsConfig, k_fraction: float) -> _lib.Params:
+def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False) -> _lib.Params:
     err = cfg.device_limits_error()
     if err:
         raise ValueError(err)
@@ -46,6 +47,7 @@ def make_params(cfg: LfpsConfig, k_fraction: float) -> _lib.Params:
     p.n_offsets = len(offs)
     for i, o in enumerate(offs):
         p.offsets[i] = o
+    p.flags = _lib.FLAG_EXPORT_SETS if export_sets else 0
     return p
 
 
@@ -70,7 +72,8 @@ class BatchedSession:
     """Device state of one layer for B requests (see module docstring)."""
 
     def __init__(self, cfg: LfpsConfig, batch: int, kv_heads: int, group: int, n_max: int,
-                 m_cap: int | None = None, device: torch.device | str | None = None):
+                 m_cap: int | None = None, device: torch.device | str | None = None,
+                 export_sets: bool = False):
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
         device = torch.device(device)
@@ -84,6 +87,7 @@ class BatchedSession:
             raise ValueError(err)
         self.lib = _lib.load_library()
         self.cfg = cfg
+        self.export_sets = export_sets
         self.B, self.Hkv, self.G = batch, kv_heads, group
         self.Hq = kv_heads * group
         self.NS = batch * self.Hq
@@ -136,7 +140,7 @@ class BatchedSession:
         self.out = self._region(L.out, torch.float32, (B, Hq, self.d))
         self.thr = self._region(L.thr, torch.float64, (B, Hq, 2, 4))
         self.counts = self._region(L.counts, torch.int32, (B, Hq, 8))
-        self.bits = self._region(L.bits, torch.int32, (NS, 2, 2, L.words))
+        self.bits = self._region(L.bits, torch.int32, (NS, 2, L.words))
         self.probe_idx = self._region(L.probe_idx, torch.int32, (B, Hq, cap))
         self.probe_score = self._region(L.probe_score, torch.float32, (B, Hq, cap))
         self.c2_idx = self._region(L.c2_idx, torch.int32, (B, Hq, cap))
@@ -146,7 +150,7 @@ class BatchedSession:
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
     def _params(self, k_fraction: float = 1.0) -> _lib.Params:
-        return make_params(self.cfg, k_fraction)
+        return make_params(self.cfg, k_fraction, self.export_sets)
 
     # -- bootstrap ----------------------------------------------------------
     def load_prefill(self, b: int, keys: torch.Tensor, values: torch.Tensor):
@@ -295,6 +299,22 @@ class BatchedSession:
     def c2_list(self, b: int, qh: int):
         k = int(self.counts[b, qh, CNT_C2])
         return self.c2_idx[b, qh, :k].cpu().numpy()
+
+    def _bitmap_list(self, b: int, qh: int, which: int):
+        if not self.export_sets:
+            raise LfpsError("C0/C1 sets are exported only with export_sets=True")
+        m = self.n_host[b] - 1 - self.cfg.sink_count     # the step just taken
+        words = self.bits[b * self.Hq + qh, which, : (m + 31) // 32].cpu().numpy()
+        bits = np.unpackbits(words.view(np.uint8), bitorder="little")[:m]
+        return np.nonzero(bits)[0].astype(np.int64) + self.cfg.sink_count
+
+    def c0_list(self, b: int, qh: int):
+        """C0 of the last step (absolute indices), export_sets sessions only."""
+        return self._bitmap_list(b, qh, 0)
+
+    def c1_list(self, b: int, qh: int):
+        """C1 of the last step (absolute indices), export_sets sessions only."""
+        return self._bitmap_list(b, qh, 1)
 
     def probe_list(self, b: int, qh: int):
         p = int(self.counts[b, qh, CNT_PROBE])

@@ -25,7 +25,7 @@ class Pair:
         G = weights.shape[2]
         self.cfg, self.B, self.Hkv, self.G, self.d, self.n0 = cfg, B, Hkv, G, d, n0
         self.sess = BatchedSession(cfg, B, Hkv, G, n_max=n_max or keys.shape[2] + 8,
-                                   m_cap=m_cap, device="cuda")
+                                   m_cap=m_cap, device="cuda", export_sets=True)
         for b in range(B):
             self.sess.load_prefill(b, bf16(keys[b, :, :n0]).cuda(), bf16(values[b, :, :n0]).cuda())
         w = torch.as_tensor(np.ascontiguousarray(weights, dtype=np.float32))
@@ -79,6 +79,8 @@ class Pair:
                     assert c[CNT_C2] == o.c2.size, (tag, "c2")
                     assert c[CNT_CLAMP] == o.clamps, (tag, "clamps")
                     np.testing.assert_array_equal(self.sess.probe_list(b, qh), o.probe, err_msg=tag)
+                    np.testing.assert_array_equal(self.sess.c0_list(b, qh), o.c0, err_msg=tag + " c0")
+                    np.testing.assert_array_equal(self.sess.c1_list(b, qh), o.c1, err_msg=tag + " c1")
                     np.testing.assert_array_equal(self.sess.c2_list(b, qh), o.c2, err_msg=tag)
                 ref = o.output
                 err = np.linalg.norm(out[b, qh] - ref) / max(np.linalg.norm(ref), 1e-12)
