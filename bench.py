@@ -91,24 +91,38 @@ def barrier(world):
         dist.barrier()
 
 
-def allmax(world, x: float) -> float:
+def _reduce(world, x: float, op: str) -> float:
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def allmax(world, x: float) -> float:
+    """Max over ranks (the step time of a multi-GPU run)."""
+    return _reduce(world, x, "max")
 
 
 def allsum(world, x: float) -> float:
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    return _reduce(world, x, "sum")
+
+
+def shard_requests(batch: int, world: int, rank: int) -> tuple[int, int]:
+    """(requests on this rank, first request index): the batch is split into
+    contiguous request ranges; every (request, KV-head) unit is independent,
+    so no collective is needed on the decode path."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank / world size")
+    base, extra = divmod(batch, world)
+    count = base + (1 if rank < extra else 0)
+    first = rank * base + min(rank, extra)
+    if count < 1:
+        raise SystemExit(f"batch {batch} is smaller than the {world} ranks")
+    return count, first
 
 
 # ---------------------------------------------------------------------------
@@ -291,10 +305,7 @@ def run_ours(args, world, rank, local):
     from paper_2506_15704_b200.workload import GqaSpec, populate
 
     batch, ctx, hkv, group, d, frac, desc = CONFIGS[args.config]
-    if batch % world and batch >= world:
-        raise SystemExit(f"batch {batch} does not shard evenly over {world} ranks")
-    b_local = max(1, batch // world)
-    b0 = rank * b_local
+    b_local, b0 = shard_requests(batch, world, rank)
     e2e_steps = 0 if args.profile_only else args.steps
     recall_steps = 0 if args.profile_only else args.recall_steps
     prof_steps = min(args.steps, 8)
