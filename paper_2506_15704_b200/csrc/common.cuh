@@ -88,6 +88,7 @@ cudaError_t launch_score(const Ctx& c, const __nv_bfloat16* q, int max_list, cud
 cudaError_t launch_topk(const Ctx& c, int implicit_base, cudaStream_t st);
 cudaError_t launch_attend(const Ctx& c, const __nv_bfloat16* q, int exact_mode, cudaStream_t st);
 cudaError_t launch_update(const Ctx& c, cudaStream_t st);
+cudaError_t launch_finish(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
 cudaError_t launch_append(const Ctx& c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new,
                           cudaStream_t st);
 cudaError_t launch_commit(const Ctx& c, cudaStream_t st);

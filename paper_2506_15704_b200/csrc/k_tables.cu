@@ -102,13 +102,16 @@ __device__ __forceinline__ void load_chunk(const Ctx& c, int item, int base, int
   }
 }
 
-// chunk moments of 16 lane values (v beyond the valid count vc are 0)
+// chunk moments of 16 lane values (v beyond the valid count vc are 0);
+// FULL: all 512 slots valid (no masking)
+template <bool FULL>
 __device__ __forceinline__ void chunk_moments(const double* v, int vc, int lane, double& mu,
                                               double& m2, double& m3, double& m4) {
   double q[4];
 #pragma unroll
   for (int g = 0; g < 4; ++g) q[g] = cadd(cadd(v[4 * g], v[4 * g + 1]), cadd(v[4 * g + 2], v[4 * g + 3]));
-  mu = cdiv_count(warp_fold(cadd(cadd(q[0], q[1]), cadd(q[2], q[3]))), (double)vc);
+  const double sum = warp_fold(cadd(cadd(q[0], q[1]), cadd(q[2], q[3])));
+  mu = FULL ? cmul(sum, 1.0 / 512.0) : cdiv_count(sum, (double)vc);
   double p2[4], p3[4], p4[4];
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
@@ -116,7 +119,7 @@ __device__ __forceinline__ void chunk_moments(const double* v, int vc, int lane,
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const int e = 4 * g + t;
-      const double d = (e * 32 + lane < vc) ? csub(v[e], mu) : 0.0;
+      const double d = (FULL || e * 32 + lane < vc) ? csub(v[e], mu) : 0.0;
       const double d2 = cmul(d, d);
       t2[t] = d2;
       t3[t] = cmul(d2, d);
@@ -139,26 +142,11 @@ struct ChunkRef {
   bool live;
 };
 
-__device__ __forceinline__ ChunkRef chunk_ref(const Ctx& c, long long w, long long n_work,
-                                              int nch_max) {
-  ChunkRef r;
-  r.live = false;
-  r.item = r.ch = r.m = r.vc = r.base = 0;
-  if (w >= n_work) return r;
-  r.item = (int)(w / nch_max);
-  r.ch = (int)(w % nch_max);
-  const int s = r.item >> 1;
-  r.m = c.n_ctx[s / c.Hq] - c.S;
-  r.live = r.ch * kChunk < r.m && !c.bypass[s];
-  r.vc = min(kChunk, r.m - r.ch * kChunk);
-  r.base = (r.item & 1) ? c.sla_base[s] : 0;
-  return r;
-}
-
 __device__ __forceinline__ void chunk_process(const Ctx& c, const ChunkRef& r, const double* v,
                                               int lane) {
   double mu, m2, m3, m4;
-  chunk_moments(v, r.vc, lane, mu, m2, m3, m4);
+  if (r.vc == kChunk) chunk_moments<true>(v, r.vc, lane, mu, m2, m3, m4);
+  else chunk_moments<false>(v, r.vc, lane, mu, m2, m3, m4);
   double* cs = c.tb.cstat + ((size_t)r.item * kLeaves + r.ch) * 4;
   if (lane == 0) {
     cs[0] = mu; cs[1] = m2; cs[2] = m3; cs[3] = m4;
@@ -167,6 +155,11 @@ __device__ __forceinline__ void chunk_process(const Ctx& c, const ChunkRef& r, c
   const double L = c.tb.bound[r.item];
   if (L > 0.0) {
     const long long Lb = __double_as_longlong(L);
+    // early out: most chunks hold nothing above the bound (invalid slots are 0)
+    long long mx = __double_as_longlong(v[0]);
+#pragma unroll
+    for (int e = 1; e < 16; ++e) mx = max(mx, __double_as_longlong(v[e]));
+    if (!__any_sync(LFPS_FULL, mx > Lb)) return;
     int nmy = 0;
 #pragma unroll
     for (int e = 0; e < 16; ++e) nmy += (__double_as_longlong(v[e]) > Lb) && (e * 32 + lane < r.vc);
@@ -200,11 +193,23 @@ __device__ __forceinline__ void chunk_process(const Ctx& c, const ChunkRef& r, c
 
 __global__ void __launch_bounds__(kThreads, 3) lfps_stats_kernel(Ctx c, int nch_max) {
   const int lane = threadIdx.x & 31;
-  const long long n_work = (long long)2 * c.NS * nch_max;
-  const long long wstride = (long long)gridDim.x * kWarps;
-  for (long long w = (long long)blockIdx.x * kWarps + (threadIdx.x >> 5); w < n_work; w += wstride) {
-    const ChunkRef r = chunk_ref(c, w, n_work, nch_max);
-    if (!r.live) continue;
+  const int n_items = 2 * c.NS;
+  const int stride = gridDim.x * kWarps;
+  const int q = stride / nch_max, rem = stride % nch_max;
+  const int w0 = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  int item = w0 / nch_max, ch = w0 % nch_max;
+  for (; item < n_items; item += q, ch += rem) {
+    if (ch >= nch_max) { ch -= nch_max; ++item; if (item >= n_items) break; }
+    const int s = item >> 1;
+    const int m = c.n_ctx[s / c.Hq] - c.S;
+    if (ch * kChunk >= m || c.bypass[s]) continue;
+    ChunkRef r;
+    r.item = item;
+    r.ch = ch;
+    r.m = m;
+    r.vc = min(kChunk, m - ch * kChunk);
+    r.base = (item & 1) ? c.sla_base[s] : 0;
+    r.live = true;
     double v[16];
     load_chunk(c, r.item, r.base, r.m, r.ch, lane, v);
     chunk_process(c, r, v, lane);

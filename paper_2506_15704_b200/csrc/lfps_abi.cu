@@ -248,8 +248,8 @@ int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out) {
   return layout(dims, out);
 }
 
-int lfps_decode_launches(void) { return 13; }  // clear, gate, 4 table kernels, probe,
-                                              // score, topk, attend, update, append, commit
+int lfps_decode_launches(void) { return 10; }  // clear, gate, 4 table kernels, probe,
+                                              // finish, append, commit
 
 int lfps_profile_enable(int on) {
   std::lock_guard<std::mutex> g(g_prof_mu);
@@ -329,10 +329,7 @@ int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_sta
   LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
   LAUNCH_P("tables", sm, lfps::launch_tables(c, m_max, sm));
   LAUNCH_P("probe", sm, lfps::launch_probe(c, m_max, sm));
-  LAUNCH_P("score", sm, lfps::launch_score(c, qb, m_max, sm));
-  LAUNCH_P("topk", sm, lfps::launch_topk(c, -1, sm));
-  LAUNCH_P("attend", sm, lfps::launch_attend(c, qb, 0, sm));
-  LAUNCH_P("update", sm, lfps::launch_update(c, sm));
+  LAUNCH_P("finish", sm, lfps::launch_finish(c, qb, sm));
   LAUNCH_P("append", sm, lfps::launch_append(c, static_cast<const __nv_bfloat16*>(k_new),
                              static_cast<const __nv_bfloat16*>(v_new), sm));
   LAUNCH_P("commit", sm, lfps::launch_commit(c, sm));
