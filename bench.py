@@ -296,12 +296,60 @@ def run_reference(args, world, rank):
 # our arm
 # ---------------------------------------------------------------------------
 
+def step_bytes(sess, cfg) -> dict:
+    """Algorithmic HBM bytes of the last decode step, per kernel.
+
+    Gathers count DISTINCT rows per (request, KV-head) unit: the G q-heads
+    of a unit read one shared K/V row store.  ``reference`` is SURVEY.md
+    §8(d)'s byte count for the reference algorithm (both fp64 tables read in
+    full every step), for comparison."""
+    import torch
+    from paper_2506_15704_b200.session import CNT_BLOCKS, CNT_C2, CNT_PROBE
+    B, Hkv, G, d, S = sess.B, sess.Hkv, sess.G, sess.d, cfg.sink_count
+    counts = sess.counts.to(torch.int64)
+    probe, c2, blocks = counts[..., CNT_PROBE], counts[..., CNT_C2], counts[..., CNT_BLOCKS]
+    active = (sess.bypass == 0)
+    n_max = max(sess.n_host)
+    row = d * 2
+
+    def distinct(idx, cnt):
+        # rows touched per unit: union over the unit's G sessions, plus sinks
+        U = B * Hkv
+        cap = idx.shape[-1]
+        pos = torch.arange(cap, device=idx.device)
+        li = idx.reshape(U, G, cap).to(torch.int64)
+        ok = pos[None, None, :] < cnt.reshape(U, G)[..., None]
+        mark = torch.zeros(U, n_max + 1, dtype=torch.bool, device=idx.device)
+        uid = torch.arange(U, device=idx.device)[:, None, None].expand_as(li)
+        mark[uid[ok], li[ok]] = True
+        mark[:, :S] = True
+        return mark.sum(1).to(torch.float64)
+
+    k_rows = distinct(sess.probe_idx, probe)
+    v_rows = distinct(sess.c2_idx, c2)
+    nseg = torch.tensor([(n - S) / 512 + 1 for n in sess.n_host], dtype=torch.float64,
+                        device=counts.device).repeat_interleave(Hkv * G).reshape(B, Hkv * G)
+    sel = (blocks.double() * 512 * 8 + 2 * nseg * 40 + probe.double() * (4 + 2 * 8)) * active
+    fin = (k_rows.sum() + v_rows.sum()) * row + sess.NS * (row + d * 4) + (probe.sum() * 8
+                                                                            + c2.sum() * 8)
+    upd = (c2.double() * (2 * 16 + 8)).sum() + sess.NS * 64
+    gate = B * Hkv * (S + cfg.local_window) * row + sess.NS * (row + 8 * d)
+    app = B * Hkv * 2 * row
+    kern = {"select": float(sel.sum()), "finish": float(fin), "update": float(upd),
+            "gate": float(gate), "append": float(app)}
+    m = torch.tensor([n - S for n in sess.n_host], dtype=torch.float64)
+    ref = float((m * 16).sum()) * Hkv * G + float(probe.sum() + c2.sum()) * row
+    return {"kernels": kern, "total": sum(kern.values()), "reference": ref,
+            "blocks_mean": float(blocks.double()[active].mean()),
+            "k_rows_unit": float(k_rows.mean()), "v_rows_unit": float(v_rows.mean())}
+
+
 def run_ours(args, world, rank, local):
     import numpy as np
     import torch
     from paper_2506_15704_b200 import _lib
     from paper_2506_15704_b200.config import LfpsConfig
-    from paper_2506_15704_b200.session import CNT_C2, CNT_PROBE, BatchedSession
+    from paper_2506_15704_b200.session import CNT_BLOCKS, CNT_C2, CNT_PROBE, BatchedSession
     from paper_2506_15704_b200.workload import GqaSpec, populate
 
     batch, ctx, hkv, group, d, frac, desc = CONFIGS[args.config]
@@ -330,26 +378,28 @@ def run_ours(args, world, rank, local):
     n_before = list(sess.n_host)
 
     # ---- timed region: device-resident inputs, no instrumentation ----
+    # every step is bracketed by its own events; L2 is flushed (a 512 MiB
+    # write, 4x the 126 MB L2) before each one, outside the brackets
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
     clocks = ClockSampler(local if world > 1 else 0)
     clocks.start()
     barrier(world)
     torch.cuda.synchronize(dev)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(cuda_stream)
-    for t in range(args.warmup, args.warmup + args.steps):
+    for i, t in enumerate(range(args.warmup, args.warmup + args.steps)):
+        flush.fill_(i & 255)
+        evs[i][0].record(cuda_stream)
         step(t)
-    ev1.record(cuda_stream)
+        evs[i][1].record(cuda_stream)
     torch.cuda.synchronize(dev)
     barrier(world)
     clock_info = clocks.stop()
-    ms_local = ev0.elapsed_time(ev1) / args.steps
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms_local = sum(step_ms) / args.steps
+    del flush
     sess.check_errors("timed steps")
     ms = allmax(world, ms_local)
-    counts = sess.counts.cpu().numpy()
-    bypass = int(sess.bypass.sum())
-    ns_local = sess.NS
-    m_avg = sum(n - cfg.sink_count for n in n_before) / len(n_before) + args.steps / 2
 
     # ---- per-kernel CUDA events on the launch stream (separate pass) ----
     prof_base = args.warmup + args.steps
@@ -361,21 +411,18 @@ def run_ours(args, world, rank, local):
     kt = _lib.profile_collect()
     sess.check_errors("profiled steps")
 
-    # ---- roofline of the dominant kernel (tracker-table scan) ----
+    # ---- algorithmic bytes per kernel (last profiled step) and the roofline ----
     peak, peak_src = measured_peaks()
-    scan_launches, scan_ms = kt.get("tables", (0, 0.0))
-    scan_avg_ms = scan_ms / max(1, scan_launches)
-    active = ns_local - bypass
-    scan_bytes = active * 2 * 8 * m_avg                       # both fp64 tables, read once
-    achieved = scan_bytes / (scan_avg_ms * 1e-3) / 1e9
+    alg = step_bytes(sess, cfg)
     kernel_ms = {k: v[1] / max(1, v[0]) for k, v in kt.items()}
-    step_kernel_ms = sum(kernel_ms.values())
-    # whole-step algorithmic bytes (SURVEY.md §8(d) LFPS formula), last step
+    dominant = max(kernel_ms, key=kernel_ms.get)
+    dom_ms = kernel_ms[dominant]
+    dom_bytes = alg["kernels"].get(dominant, 0)
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    counts = sess.counts.cpu().numpy()
+    bypass = int(sess.bypass.sum())
     probe = counts[..., CNT_PROBE].astype(np.int64)
     c2 = counts[..., CNT_C2].astype(np.int64)
-    rows = 256  # bf16 row of d = 128
-    step_bytes = (scan_bytes + (probe.sum() + c2.sum()) * rows  # gathers (upper bound: per q-head)
-                  + c2.sum() * 32 + sess.B * hkv * 2 * rows + ns_local * (2 * 8 + d * 6))
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
@@ -458,20 +505,26 @@ def run_ours(args, world, rank, local):
         "config": {"workload": desc, "batch": batch, "batch_per_gpu": b_local, "context": ctx,
                    "q_heads": hkv * group, "kv_heads": hkv, "d": d, "topk_fraction": frac,
                    "sharding": "requests across ranks, no collective on the decode path",
-                   "l2": "inputs larger than L2: 4.3 GB of fp64 tables read per step"},
+                   "l2": "flushed before every timed step (512 MiB write); each step timed "
+                         "by its own CUDA events"},
         "gpu_launches": args.steps * _lib.load_library().lfps_decode_launches(),
-        "roofline": {"bound": "hbm", "kernel": "table stage: stats + thresholds (+fallback) kernels",
+        "roofline": {"bound": "hbm", "kernel": dominant,
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None,
-                     "algorithmic_bytes_per_launch": scan_bytes,
-                     "avg_launch_ms": scan_avg_ms, "peak_source": peak_src},
+                     "algorithmic_bytes_per_launch": dom_bytes,
+                     "avg_launch_ms": dom_ms, "peak_source": peak_src},
         "kernel_ms": kernel_ms,
-        "step_algorithmic_bytes": int(step_bytes),
-        "step_achieved_GBps": step_bytes / (ms * 1e-3) / 1e9,
+        "kernel_algorithmic_bytes": alg["kernels"],
+        "step_algorithmic_bytes": int(alg["total"]),
+        "step_achieved_GBps": alg["total"] / (ms * 1e-3) / 1e9,
+        "reference_algorithm_bytes": int(alg["reference"]),
+        "table_blocks_read_mean": alg["blocks_mean"],
         "clocks": clock_info,
         "setup_s": setup_s,
+        "step_ms_min_max": [min(step_ms), max(step_ms)],
         "bypassed_sessions_last_step": bypass,
         "probe_mean": float(probe.mean()), "c2_mean": float(c2.mean()),
+        "k_rows_distinct_per_unit": alg["k_rows_unit"], "v_rows_distinct_per_unit": alg["v_rows_unit"],
     }
     if e2e:
         line["e2e"] = e2e

@@ -45,7 +45,7 @@ extern "C" {
 #define LFPS_API
 #endif
 
-#define LFPS_ABI_VERSION 1
+#define LFPS_ABI_VERSION 2
 
 #define LFPS_OK 0
 #define LFPS_E_INVALID -1   /* bad argument (shape, range, capacity) */
@@ -59,6 +59,7 @@ extern "C" {
 #define LFPS_ERR_WEIGHT_SUM 4         /* tables.py:161-163 */
 #define LFPS_ERR_PREFILL_SUM 5        /* engine.py:84-86 */
 #define LFPS_ERR_ZERO_QUERY 6         /* gate.py:61-63 zero-norm prefill query */
+#define LFPS_ERR_NONFINITE_SCORES 7   /* numerics.py:61-62 via engine.py:177,184 */
 
 /* Problem dimensions of one layer. */
 typedef struct lfps_dims {
@@ -68,7 +69,7 @@ typedef struct lfps_dims {
   int32_t d;         /* head dimension, multiple of 16, <= 256 */
   int32_t n_max;     /* KV rows allocated per (request, KV head) */
   int32_t m_cap;     /* vertical-table slots per session (even); the slash
-                        ring holds m_cap + 2 slots */
+                        table holds lfps_slash_capacity(dims) slots */
 } lfps_dims;
 
 /* LfpsConfig (config.py:11-42) plus the per-call budget. */
@@ -99,9 +100,14 @@ typedef struct lfps_state {
   void* v_cache;          /* bf16 [B, Hkv, n_max, d] */
   int32_t* n_ctx;         /* [B] rows currently in the cache (incl. sinks) */
   double* ver;            /* [NS, m_cap] vertical phys table */
-  double* sla;            /* [NS, m_cap + 2] slash phys ring */
+  double* sla;            /* [NS, slash_cap] slash phys table: logical index i
+                             lives at slot sla_base + i.  The window only grows
+                             (down by one per slash shift, up by one per gated
+                             step), so it never wraps; slash_cap =
+                             lfps_slash_capacity(dims) =
+                             2 * (roundup(m_cap, 512) + 512) */
   double* scale;          /* [NS] lazy decay scale */
-  int32_t* sla_base;      /* [NS] ring slot of logical index 0 */
+  int32_t* sla_base;      /* [NS] slot of slash logical index 0 */
   int64_t* clamp_count;   /* [NS] cumulative clamp counter */
   double* mean_key;       /* [B * Hkv, d] prior K-bar (gate.py:71) */
   double* mean_value;     /* [B * Hkv, d] prior V-bar (gate.py:72) */
@@ -116,23 +122,26 @@ typedef struct lfps_ws_layout {
   size_t err;         /* i32 [1 + NS] err[0] = any, err[1+s] per session */
   size_t out;         /* f32 [NS, d] attention output */
   size_t thr;         /* f64 [NS, 2, 4] tau, mean, degenerate, kappa per table */
-  size_t counts;      /* i32 [NS, 8] |c0| |c1| |probe| c0_dropped k |c2| clamps spare */
+  size_t counts;      /* i32 [NS, 8] |c0| |c1| |probe| c0_dropped k |c2| clamps
+                         table-blocks-read */
   size_t bits;        /* u32 [NS, 2 tables, words] C0 bitmaps of fallback items */
   size_t probe_idx;   /* i32 [NS, list_cap] absolute indices, ascending */
   size_t probe_score; /* f32 [NS, list_cap] */
   size_t c2_idx;      /* i32 [NS, list_cap] */
   size_t c2_score;    /* f32 [NS, list_cap] */
   size_t scratch;     /* f64 [NS, list_cap] bootstrap scratch */
-  size_t cstat;       /* f64 [2 NS, 512, 4] chunk moments */
-  size_t cidx;        /* i32 [2 NS, capture_cap] captured slots */
-  size_t cval;        /* f64 [2 NS, capture_cap] captured phys values */
-  size_t ncap;        /* i32 [2 NS] */
-  size_t itemf;       /* f64 [2 NS, 4] tau/scale, mean/scale, degenerate */
-  size_t bound;       /* f64 [2 NS] capture bound, persists across steps */
-  size_t fb;          /* i32 [2 NS] fallback taken */
-  size_t fblist;      /* i32 [2 NS] */
-  size_t nfb;         /* i32 [1] */
-  int32_t capture_cap;
+  /* Block summaries of the tracker tables.  These PERSIST across steps (a
+     cache of the state, kept in the workspace): item = 2 s + table (0 =
+     vertical, 1 = slash); block b covers table slots [512 b, 512 b + 512)
+     intersected with the item's window.  A zero-filled workspace is valid:
+     valid[s] == 0 makes the next step rebuild every block of session s. */
+  size_t bsum;        /* f64 [2 NS, nblk, 4] segment mean, M2, M3, M4 */
+  size_t bmax;        /* f64 [2 NS, nblk] segment max phys value */
+  size_t dirty;       /* u32 [2 NS, dirty_words] blocks to rebuild */
+  size_t valid;       /* i32 [NS] summaries of session s are current */
+  size_t wstat;       /* f64 [NS, 2] max and normaliser of the update softmax */
+  int32_t nblk;       /* blocks per item (slash_cap / 512) */
+  int32_t dirty_words;
   int32_t words;      /* bitmap words per (session, table, kind) */
   int32_t list_cap;   /* capacity of each per-session list */
 } lfps_ws_layout;
@@ -147,6 +156,9 @@ LFPS_API const char* lfps_last_error(void);
 
 /* Workspace layout for these dimensions. */
 LFPS_API int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out);
+
+/* Slots of one session's slash table (>= 0; negative LFPS_E_* on bad dims). */
+LFPS_API int lfps_slash_capacity(const lfps_dims* dims);
 
 /* Seed the tracker tables of sessions [s_begin, s_begin + count) from their
  * trailing prefill weights (Eq. 4; init_tables, tables.py:247-281).
@@ -166,7 +178,10 @@ LFPS_API int lfps_bootstrap_stats(const lfps_dims* dims, const lfps_params* p,
 /* One LFPS decode step for all B * Hq sessions (decode_step,
  * engine.py:97-201): gate, thresholds, candidates, fp32 probe scoring,
  * Top-k, joint sink+selection attention, table update, then KV append of
- * k_new / v_new and n_ctx += 1.
+ * k_new / v_new and n_ctx += 1.  Table updates, the append and n_ctx are
+ * committed by the last kernels of the step, after every data check of
+ * every session has passed (err[0] == 0), so a failed step changes nothing
+ * but the block-summary cache (which stays consistent with the tables).
  * q: bf16 [B, Hq, d]; k_new, v_new: bf16 [B, Hkv, d]; all device.
  * n_host: the caller's host copy of n_ctx [B] (used for validation and
  * launch sizing; must match the device copy).  Results land in the

@@ -22,12 +22,19 @@ Definitions (DESIGN.md §3 "Canonical arithmetic"):
   over e, the 32 lane sums fold halves (16, 8, 4, 2, 1); chunk partials then
   reduce by a pairwise tree (zero-padded to a power of two).  Used for the
   head-stats variance.
-* ``table_moments`` -- single read of the table: per 512-slot chunk the
-  chunk mean (table_sum order / count) and the chunk's centred power sums
-  M2, M3, M4 (same lane/fold order), then a pairwise tree of exact
-  pairwise-update merges (Chan et al.; Pebay 2008) over the chunks.  Same
-  quantities as the reference's two-pass _phys_moments (tables.py:127-140),
-  different rounding; the golden tests pin identical selections.
+* ``table_moments`` -- per *segment* the segment mean (table_sum order /
+  count) and the segment's centred power sums M2, M3, M4 (same lane/fold
+  order), then a pairwise tree of exact pairwise-update merges (Chan et al.;
+  Pebay 2008) over the segments in logical order.  A segment is a maximal run
+  of logical slots i whose *virtual slot* off + i lies in one 512-aligned
+  block: off = 0 for the vertical table (segments = logical chunks of 512);
+  for the slash table off is the tracker's virtual base (TrackerState.vbase,
+  -m0 at bootstrap, minus one per slash shift), so a slash value keeps its
+  block while its logical index moves.  Block summaries are therefore
+  stable across steps and the device recomputes only the blocks a step
+  touched.  Same quantities as the reference's two-pass _phys_moments
+  (tables.py:127-140), different rounding; the golden tests pin identical
+  selections.
 * ``gdot``        -- fp64 dot: lane l (of 32) accumulates j = l, l+32, ...
   in order, then folds 16..1.  Gate logits, head stats (gate.py:77-98).
 * ``sdot32``      -- fp32 probe score: 16 lanes each own d/16 contiguous
@@ -109,20 +116,38 @@ def _lane_tree(buf: np.ndarray) -> np.ndarray:
     return _fold_halves(buf[:, 0, :])
 
 
-def chunk_moments(x: np.ndarray):
-    """Per-chunk (count, mean, M2, M3, M4) of a table, device order."""
+def segment_bounds(n: int, off: int = 0) -> list[tuple[int, int]]:
+    """(start, length) of the segments of a table of n logical slots whose
+    logical slot 0 sits at virtual slot ``off`` (see table_moments)."""
+    out = []
+    i = 0
+    while i < n:
+        first = TABLE_CHUNK - ((off + i) % TABLE_CHUNK)
+        ln = min(first, n - i)
+        out.append((i, ln))
+        i += ln
+    return out
+
+
+def chunk_moments(x: np.ndarray, off: int = 0):
+    """Per-segment (count, mean, M2, M3, M4) of a table, device order.
+
+    Element j of a segment is held by lane j % 32 at position j // 32."""
     x = np.asarray(x, dtype=np.float64)
-    n = x.shape[0]
-    nch = max(1, -(-n // TABLE_CHUNK))
-    buf = np.zeros(nch * TABLE_CHUNK, dtype=np.float64)
-    buf[:n] = x
-    valid = np.zeros(nch * TABLE_CHUNK, dtype=bool)
-    valid[:n] = True
+    segs = segment_bounds(x.shape[0], off) or [(0, 0)]
+    nch = len(segs)
+    buf = np.zeros((nch, TABLE_CHUNK), dtype=np.float64)
+    valid = np.zeros((nch, TABLE_CHUNK), dtype=bool)
+    cnt = np.zeros(nch, dtype=np.float64)
+    for k, (a, ln) in enumerate(segs):
+        buf[k, :ln] = x[a: a + ln]
+        valid[k, :ln] = True
+        cnt[k] = ln
     shape = (nch, TABLE_CHUNK // TABLE_LANES, TABLE_LANES)
     buf = buf.reshape(shape)
     valid = valid.reshape(shape)
-    cnt = np.minimum(np.maximum(n - np.arange(nch) * TABLE_CHUNK, 0), TABLE_CHUNK).astype(np.float64)
-    mu = _lane_tree(buf) / cnt
+    with np.errstate(invalid="ignore", divide="ignore"):
+        mu = _lane_tree(buf) / cnt
     d = np.where(valid, buf - mu[:, None, None], 0.0)
     d2 = d * d
     d3 = d2 * d
@@ -155,13 +180,13 @@ def merge_moments(a, b):
     return tuple(out)
 
 
-def table_moments(x: np.ndarray) -> tuple[float, float, float]:
-    """(mean_p, sum c^2, sum c^4) of a phys table view in ONE read.
+def table_moments(x: np.ndarray, off: int = 0) -> tuple[float, float, float]:
+    """(mean_p, sum c^2, sum c^4) of a phys table view.
 
-    Restates ScoreTablePair._phys_moments (tables.py:127-140) as chunk
-    moments merged by a pairwise tree over the chunks (zero-count padding to
-    a power of two)."""
-    st = chunk_moments(x)
+    Restates ScoreTablePair._phys_moments (tables.py:127-140) as segment
+    moments merged by a pairwise tree over the segments (zero-count padding
+    to a power of two); ``off`` is the virtual slot of logical slot 0."""
+    st = chunk_moments(x, off)
     nch = st[0].shape[0]
     size = 1
     while size < nch:

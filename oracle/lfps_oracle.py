@@ -52,8 +52,8 @@ class RefArith:
     name = "ref"
 
     @staticmethod
-    def moments(x):
-        # tables.py:135-140 (mean, subtract, square, sum, dot)
+    def moments(x, off=0):
+        # tables.py:135-140 (mean, subtract, square, sum, dot); off unused
         x = np.ascontiguousarray(x, dtype=np.float64)
         mean = float(x.mean())
         c = x - mean
@@ -112,8 +112,8 @@ class DevArith:
     name = "dev"
 
     @staticmethod
-    def moments(x):
-        return dm.table_moments(x)
+    def moments(x, off=0):
+        return dm.table_moments(x, off)
 
     @staticmethod
     def logits64(rows, q, d):
@@ -178,6 +178,7 @@ class TrackerState:
     scale: float = 1.0
     carry: bool = False
     clamp_count: int = 0
+    vbase: int = 0           # virtual slot of slash logical 0 (devmath.table_moments)
 
     def ver_view(self) -> np.ndarray:
         return self.ver[: self.m]
@@ -194,7 +195,7 @@ class TrackerState:
 
     def copy(self) -> "TrackerState":
         return TrackerState(self.ver.copy(), self.ring.copy(), self.base, self.m,
-                            self.scale, self.carry, self.clamp_count)
+                            self.scale, self.carry, self.clamp_count, self.vbase)
 
 
 @dataclass
@@ -281,7 +282,7 @@ def seed_tables(weights: np.ndarray, cfg, mcap: int | None = None,
     ver[:m] = col * coeff
     ring = np.zeros(ring_cap)
     ring[:m] = diag * coeff
-    return TrackerState(ver=ver, ring=ring, base=0, m=m)
+    return TrackerState(ver=ver, ring=ring, base=0, m=m, vbase=-m)
 
 
 def head_priors(keys, values, last_query, cfg, arith) -> HeadPriors:
@@ -340,8 +341,8 @@ def thresholds(tr: TrackerState, cfg, arith):
     if tr.m < 2:
         raise ValueError("thresholds require at least 2 table slots")
     res = []
-    for x in (tr.ver_view(), tr.sla_view()):
-        mean_p, s2_p, s4_p = arith.moments(x)
+    for x, off in ((tr.ver_view(), 0), (tr.sla_view(), tr.vbase)):
+        mean_p, s2_p, s4_p = arith.moments(x, off)
         mean = mean_p * tr.scale
         s2 = s2_p * tr.scale * tr.scale
         if s2 < DEGENERATE_S2:
@@ -421,6 +422,7 @@ def apply_update(tr: TrackerState, c2_log: np.ndarray, u: np.ndarray, r: float,
         tr.ring[slots] *= tr.scale
         tr.scale = 1.0
     tr.base = (tr.base - 1) % C
+    tr.vbase -= 1
     tr.ring[tr.base] = 0.0
     tr.carry = True
     k = c2_log.size

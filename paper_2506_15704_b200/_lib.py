@@ -15,7 +15,7 @@ import threading
 from .errors import DeviceError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "liblfps_b200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 FLAG_EXPORT_SETS = 1
 
 # per-session device error codes (include/lfps_b200.h)
@@ -26,11 +26,12 @@ ERR_NAMES = {
     4: "selection weights must sum to 1",
     5: "each prefill weight vector must sum to 1 over its non-sink range",
     6: "zero-norm prefill query",
+    7: "softmax input contains non-finite scores",
 }
 
 EXPORTS = ("lfps_abi_version", "lfps_last_error", "lfps_workspace_layout",
            "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step",
-           "lfps_exact_topk_step", "lfps_overlap", "lfps_decode_launches",
+           "lfps_exact_topk_step", "lfps_overlap", "lfps_decode_launches", "lfps_slash_capacity",
            "lfps_exact_launches", "lfps_profile_enable", "lfps_profile_collect")
 
 
@@ -60,10 +61,9 @@ class WsLayout(C.Structure):
                 ("err", C.c_size_t), ("out", C.c_size_t), ("thr", C.c_size_t),
                 ("counts", C.c_size_t), ("bits", C.c_size_t), ("probe_idx", C.c_size_t),
                 ("probe_score", C.c_size_t), ("c2_idx", C.c_size_t), ("c2_score", C.c_size_t),
-                ("scratch", C.c_size_t), ("cstat", C.c_size_t), ("cidx", C.c_size_t),
-                ("cval", C.c_size_t), ("ncap", C.c_size_t), ("itemf", C.c_size_t),
-                ("bound", C.c_size_t), ("fb", C.c_size_t), ("fblist", C.c_size_t),
-                ("nfb", C.c_size_t), ("capture_cap", C.c_int32), ("words", C.c_int32),
+                ("scratch", C.c_size_t), ("bsum", C.c_size_t), ("bmax", C.c_size_t),
+                ("dirty", C.c_size_t), ("valid", C.c_size_t), ("wstat", C.c_size_t),
+                ("nblk", C.c_int32), ("dirty_words", C.c_int32), ("words", C.c_int32),
                 ("list_cap", C.c_int32)]
 
 
@@ -84,6 +84,7 @@ def _declare(lib):
     lib.lfps_abi_version.restype = C.c_int
     lib.lfps_last_error.restype = C.c_char_p
     lib.lfps_workspace_layout.argtypes = [P(Dims), P(WsLayout)]
+    lib.lfps_slash_capacity.argtypes = [P(Dims)]
     lib.lfps_bootstrap_tables.argtypes = [P(Dims), P(Params), P(State), P(Workspace), C.c_void_p,
                                           C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
     lib.lfps_bootstrap_stats.argtypes = [P(Dims), P(Params), P(State), P(Workspace), C.c_void_p,
@@ -98,7 +99,7 @@ def _declare(lib):
     lib.lfps_profile_collect.argtypes = [P(KernelTime), C.c_int32, P(C.c_int32)]
     for name in ("lfps_profile_enable", "lfps_profile_collect", "lfps_workspace_layout",
                  "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step", "lfps_exact_topk_step", "lfps_overlap",
-                 "lfps_decode_launches", "lfps_exact_launches"):
+                 "lfps_decode_launches", "lfps_exact_launches", "lfps_slash_capacity"):
         getattr(lib, name).restype = C.c_int
 
 
@@ -126,6 +127,12 @@ def check(rc: int, what: str) -> None:
         if rc == -1:
             raise ValueError(f"{what}: {msg}")
         raise DeviceError(f"{what} failed ({rc}): {msg}")
+
+
+def slash_capacity(dims: Dims) -> int:
+    cap = load_library().lfps_slash_capacity(C.byref(dims))
+    check(min(cap, 0), "slash_capacity")
+    return cap
 
 
 def workspace_layout(dims: Dims) -> WsLayout:

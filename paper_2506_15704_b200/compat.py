@@ -156,11 +156,14 @@ def _regrow(session: HeadSession) -> None:
     new.v_cache[0, 0, :n].copy_(old.v_cache[0, 0, :n])
     m = n - cfg.sink_count
     new.ver[0, : m + 1].copy_(old.ver[0, : m + 1])
-    C = old.m_cap + 2
+    # slash window (logical [0, m] incl. the parked slot) moved by a multiple
+    # of 512 slots so its block alignment -- hence the canonical moment
+    # order -- is unchanged; the fresh workspace rebuilds the block summaries
     base = int(old.sla_base[0])
-    slots = (base + torch.arange(m + 1, device=old.device)) % C
-    new.sla[0, : m + 1].copy_(old.sla[0][slots])
-    new.sla_base.zero_()
+    home = new.sla_cap // 2
+    new_base = home - (m + 1) - ((home - (m + 1) - base) % 512)
+    new.sla[0, new_base: new_base + m + 1].copy_(old.sla[0, base: base + m + 1])
+    new.sla_base.fill_(new_base)
     for name in ("scale", "clamp_count", "mean_key", "mean_value", "sigma_hat_sq", "n_ctx"):
         getattr(new, name).copy_(getattr(old, name))
     new.n_host = list(old.n_host)

@@ -11,24 +11,24 @@
 
 namespace lfps {
 
-// Table-stage scratch (k_tables.cu, k_probe.cu).
-struct TablesWs {
-  double* cstat;   // [2 NS][512][4] chunk moments
-  int* cidx;       // [2 NS][cap] captured slot indices (logical)
-  double* cval;    // [2 NS][cap] captured phys values
-  int* ncap;       // [2 NS] capture counts
-  int cap;
-  double* itemf;   // [2 NS][4] thr0 = tau/scale, thrf = mean/scale, degenerate
-  double* bound;   // [2 NS] capture bound for the next step (persists across steps)
-  int* fb;         // [2 NS] item took the fallback (C0 bitmap in bits)
-  int* fblist;     // [2 NS] queued fallback items
-  int* nfb;        // [1]
+// Persistent block summaries of the tracker tables (k_select.cu, k_update.cu).
+// item = 2 s + table; block b = table slots [512 b, 512 b + 512) within the
+// item's window (vertical [0, m), slash [base, base + m)).
+constexpr int kBlk = 512;
+struct BlockWs {
+  double* bsum;     // [2 NS][nblk][4] segment mean, M2, M3, M4
+  double* bmax;     // [2 NS][nblk] segment max phys value
+  uint32_t* dirty;  // [2 NS][dwords] blocks to rebuild at the next step
+  int* valid;       // [NS] 0: rebuild every block of the session
+  double* wstat;    // [NS][2] update-softmax max and normaliser (finish -> update)
+  int nblk;
+  int dwords;
 };
 
 // Flattened per-launch view of dims + state + workspace (passed by value).
 struct Ctx {
   // dims
-  int B, Hkv, G, Hq, NS, d, n_max, m_cap, ring_cap;
+  int B, Hkv, G, Hq, NS, d, n_max, m_cap, sla_cap, sla_home;
   int words;      // bitmap words per (session, table, kind)
   int list_cap;
   // params
@@ -63,10 +63,11 @@ struct Ctx {
   int* c2_idx;
   float* c2_score;
   double* scratch;
-  TablesWs tb;
+  BlockWs bw;
 };
 
-enum { CNT_C0 = 0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_SPARE, CNT_N };
+// CNT_BLOCKS: table blocks the select kernel read (rebuilt + hot), a diagnostic
+enum { CNT_C0 = 0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_BLOCKS, CNT_N };
 
 __device__ __forceinline__ const __nv_bfloat16* krow(const Ctx& c, int b, int h, int i) {
   return c.K + (((size_t)b * c.Hkv + h) * c.n_max + i) * c.d;
@@ -80,10 +81,12 @@ __device__ __forceinline__ void set_err(const Ctx& c, int s, int code) {
   atomicExch(c.err, 1);
 }
 
+__device__ __forceinline__ double* ver_row(const Ctx& c, int s) { return c.ver + (size_t)s * c.m_cap; }
+__device__ __forceinline__ double* sla_row(const Ctx& c, int s) { return c.sla + (size_t)s * c.sla_cap; }
+
 // ---- host-side launch wrappers (defined in the k_*.cu files) -------------
 cudaError_t launch_gate(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
-cudaError_t launch_tables(const Ctx& c, int m_max, cudaStream_t st);
-cudaError_t launch_probe(const Ctx& c, int m_max, cudaStream_t st);
+cudaError_t launch_select(const Ctx& c, int m_max, cudaStream_t st);
 cudaError_t launch_score(const Ctx& c, const __nv_bfloat16* q, int max_list, cudaStream_t st);
 cudaError_t launch_topk(const Ctx& c, int implicit_base, cudaStream_t st);
 cudaError_t launch_attend(const Ctx& c, const __nv_bfloat16* q, int exact_mode, cudaStream_t st);

@@ -22,10 +22,11 @@ __global__ void lfps_boot_tables_kernel(Ctx c, const float* w, int s_begin, int 
   const int s = s_begin + sl;
   const int sp = c.s;
   const float* ws = w + (size_t)sl * sp * m0;
-  double* ver = c.ver + (size_t)s * c.m_cap;
-  double* sla = c.sla + (size_t)s * c.ring_cap;
+  double* ver = ver_row(c, s);
+  double* sla = sla_row(c, s);
+  const int base0 = c.sla_home - m0;    // the slash window ends at the home slot
   const double coeff = cdiv(1.0, cmul(cmul(2.0, (double)sp), csub(1.0, c.r)));
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c.ring_cap; i += gridDim.x * blockDim.x) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c.sla_cap; i += gridDim.x * blockDim.x) {
     double col = 0.0, diag = 0.0;
     if (i < m0) {
       for (int r = 0; r < sp; ++r) {
@@ -37,12 +38,16 @@ __global__ void lfps_boot_tables_kernel(Ctx c, const float* w, int s_begin, int 
       diag = cmul(diag, coeff);
     }
     if (i < c.m_cap) ver[i] = col;
-    sla[i] = diag;
+    // slot base0 + i holds logical i; zero everywhere else
+    const int li = i - base0;
+    if (li < 0 || li >= m0) sla[i] = 0.0;
+    if (i < m0) sla[base0 + i] = diag;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     c.scale[s] = 1.0;
-    c.sla_base[s] = 0;
+    c.sla_base[s] = base0;
     c.clamp_count[s] = 0;
+    c.bw.valid[s] = 0;                  // the next step rebuilds every block summary
   }
 }
 
@@ -188,7 +193,7 @@ __global__ void lfps_boot_sigma_kernel(Ctx c, const __nv_bfloat16* q, int n2) {
 
 cudaError_t launch_boot_tables(const Ctx& c, const float* w, int s_begin, int count, int m0,
                                cudaStream_t st) {
-  const int blocks = (c.ring_cap + 255) / 256;
+  const int blocks = (c.sla_cap + 255) / 256;
   lfps_boot_tables_kernel<<<dim3(blocks < 1024 ? blocks : 1024, count), 256, 0, st>>>(c, w, s_begin, m0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -1,6 +1,8 @@
 // k_finish.cu -- the per-session back half of a decode step in ONE kernel:
-// candidate scoring (K3), Top-k (K4), sparse attention (K5) and the tracker
-// update + grow (K6).  One 512-thread CTA per (request, q-head) session.
+// candidate scoring (K3), Top-k (K4), sparse attention (K5) and the data
+// checks of the tracker update (K6; the update itself is committed by
+// k_update.cu once every session has passed).  One 512-thread CTA per
+// (request, q-head) session.
 //
 //   scores   z_j = (K[j] . q) / fp32(sqrt d) for every probe row (canonical
 //            fp32 dot, devmath.sdot32; engine.py:168-170), half-warp per
@@ -13,12 +15,10 @@
 //            (engine.py:173-181): every half-warp keeps an online
 //            (max, sum, acc) over its rows, 8 V rows in flight; the 32
 //            partial states are merged at the end (fp32)
-//   update   u = canonical fp64 softmax of the C2 scores, |sum u - 1| check,
-//            decay + renormalisation, slash shift, residual fold, clamp,
-//            grow (tables.py:144-220; same arithmetic as devmath / oracle)
-//
-// The tables are only committed if no session of the batch raised a data
-// error earlier in the step (err[0]).
+//   checks   sinks and C2 scores finite (softmax_weights, numerics.py:61-62,
+//            called at engine.py:177 and :184); u = canonical fp64 softmax
+//            of the C2 scores and |sum u - 1| <= 1e-6 (tables.py:161-163);
+//            the softmax max and normaliser go to wstat for k_update.cu
 #include "common.cuh"
 #include "canon.cuh"
 #include "frag.cuh"
@@ -104,21 +104,10 @@ __global__ void __launch_bounds__(kThreads, 2) lfps_finish_kernel(Ctx c, const _
   const int b = s / c.Hq, h = (s % c.Hq) / c.G;
   const int n = c.n_ctx[b];
   const int S = c.S;
-  const int m = n - S;
-  const int C = c.ring_cap;
-  double* ver = c.ver + (size_t)s * c.m_cap;
-  double* sla = c.sla + (size_t)s * C;
   int* cnt = c.counts + (size_t)s * CNT_N;
-  const bool commit = c.err[0] == 0;
 
   if (c.bypass[s]) {
-    if (tid == 0) {
-      cnt[CNT_K] = 0; cnt[CNT_C2] = 0; cnt[CNT_CLAMP] = 0;
-      if (commit) {                       // grow only (engine.py:133-137)
-        ver[m] = 0.0;
-        sla[(c.sla_base[s] + m) % C] = 0.0;
-      }
-    }
+    if (tid == 0) { cnt[CNT_K] = 0; cnt[CNT_C2] = 0; cnt[CNT_CLAMP] = 0; }
     return;
   }
 
@@ -249,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 2) lfps_finish_kernel(Ctx c, const _
         int row = 0;
         zz[t] = -INFINITY;
         if (j < S) { row = j; zz[t] = sh.sink_z[j]; }
-        else if (j < tot) { row = __ldg(c2i + j - S); zz[t] = __ldg(c2z + j - S); }
+        else if (j < tot) { row = c2i[j - S]; zz[t] = c2z[j - S]; }   // written above
         vr[t] = ld_frag<PER>(vrow(c, b, h, row), hl);
       }
       float bm = mrun;
@@ -291,7 +280,14 @@ __global__ void __launch_bounds__(kThreads, 2) lfps_finish_kernel(Ctx c, const _
     }
   }
 
-  // ---- tracker update + grow (canonical fp64) -------------------------------------------
+  // ---- data checks of the update (committed by k_update.cu) ----------------------------
+  int bad = 0;
+  for (int j = tid; j < k2; j += kThreads) bad |= !isfinite(c2z[j]);
+  if (tid < S) bad |= !isfinite(sh.sink_z[tid]);
+  if (__syncthreads_or(bad)) {
+    if (tid == 0) set_err(c, s, LFPS_ERR_NONFINITE_SCORES);
+    return;
+  }
   double mx = -INFINITY;
   for (int j = tid; j < k2; j += kThreads) mx = fmax(mx, (double)c2z[j]);
   for (int o = 16; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(LFPS_FULL, mx, o));
@@ -308,51 +304,10 @@ __global__ void __launch_bounds__(kThreads, 2) lfps_finish_kernel(Ctx c, const _
   if (tid < kCanon)
     for (int j = tid; j < k2; j += kCanon) acc = cadd(acc, cdiv(cexp(csub((double)c2z[j], mx)), tot));
   const double wsum = canon_sum(acc, sh.red);
-  if (fabs(wsum - 1.0) > 1e-6) {
-    if (tid == 0) set_err(c, s, LFPS_ERR_WEIGHT_SUM);
-    return;
-  }
-  if (!commit) return;
-  int base = c.sla_base[s];
-  double sc = cmul(c.scale[s], c.r);
-  if (sc < 1e-120) {                      // renormalise (tables.py:167-169, 240-244)
-    for (int i = tid; i < m; i += kThreads) ver[i] = cmul(ver[i], sc);
-    for (int i = tid; i <= m; i += kThreads) {
-      const int slot = (base + i) % C;
-      sla[slot] = cmul(sla[slot], sc);
-    }
-    sc = 1.0;
-    __syncthreads();
-  }
-  base = (base - 1 + C) % C;              // slash shift (tables.py:174-177)
-  if (tid == 0) sla[base] = 0.0;
-  __syncthreads();
-  const double inv = cdiv(1.0, cmul(2.0, (double)k2));
-  int clamps = 0;
-  for (int j = tid; j < k2; j += kThreads) {
-    const double u = cdiv(cexp(csub((double)c2z[j], mx)), tot);
-    const double add = cdiv(csub(u, inv), sc);
-    const int li = c2i[j] - S;
-    const int slot = (base + li) % C;
-    const double v0 = ver[li], w0 = sla[slot];
-    double v = cadd(v0, add);
-    if (v < 0.0) { v = 0.0; ++clamps; }
-    double w = cadd(w0, add);
-    if (w < 0.0) { w = 0.0; ++clamps; }
-    ver[li] = v;
-    sla[slot] = w;
-  }
-  for (int o = 16; o >= 1; o >>= 1) clamps += __shfl_xor_sync(LFPS_FULL, clamps, o);
-  if (lane == 0) sh.ired[warp] = clamps;
-  __syncthreads();
   if (tid == 0) {
-    int tc = 0;
-    for (int w = 0; w < kWarps; ++w) tc += sh.ired[w];
-    cnt[CNT_CLAMP] = tc;
-    c.clamp_count[s] += tc;
-    ver[m] = 0.0;                         // grow (tables.py:202-220)
-    c.scale[s] = sc;
-    c.sla_base[s] = base;
+    if (fabs(wsum - 1.0) > 1e-6) set_err(c, s, LFPS_ERR_WEIGHT_SUM);
+    c.bw.wstat[2 * (size_t)s] = mx;
+    c.bw.wstat[2 * (size_t)s + 1] = tot;
   }
 }
 

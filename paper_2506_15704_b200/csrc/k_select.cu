@@ -1,0 +1,493 @@
+// k_select.cu -- thresholds and candidate construction (K1 + K2), one CTA
+// per (request, q-head) session, from PERSISTENT block summaries.
+//
+// Restates compute_thresholds (tables.py:295-317, _phys_moments :127-140),
+// select_initial (candidates.py:45-58), expand (:61-82) and
+// finalize_probe_set (:85-100).
+//
+// Each table is cut into 512-slot blocks of table slots (vertical: slot =
+// logical index; slash: slot = sla_base + logical index, a window that only
+// grows at its ends).  Every block carries a summary of its part of the
+// window: the canonical segment moments (mean, M2, M3, M4) and the maximum
+// phys value.  A decode step changes a table only at its C2 slots and at the
+// one slot it grows by (k_update.cu marks those blocks dirty), and the lazy
+// scale leaves phys values alone, so the summaries of all other blocks stay
+// exact.  Per step this kernel
+//
+//   A  rebuilds the dirty blocks (every block when the session's summaries
+//      are not valid: first step, after a renormalisation);
+//   B  merges the window's segment moments in the canonical pairwise tree
+//      (devmath.table_moments) -> tau, mean, degenerate, kappa; exactly the
+//      same arithmetic as rebuilding every block;
+//   C  C0 = {slots with phys > tau / scale}: only "hot" blocks (max above
+//      the threshold) can hold members, and only those are read;
+//   D  C1 = F & dilate(C0, offsets), F read at dilated slots only;
+//      probe = C1 | local tail, compacted into a sorted absolute index list.
+//
+// All comparisons are exact fp64 (on bit patterns: phys values are +0 or
+// positive).  Table bytes read per step: dirty + hot blocks, not 2 m.
+#include "common.cuh"
+#include "canon.cuh"
+
+namespace lfps {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kLeaves = 512;                  // segments per window: m <= 511 * 512
+constexpr int kLeavesPerLane = kLeaves / 32;
+constexpr int kMaxTasks = 2 * kLeaves;
+
+struct Mom {
+  double n, mu, m2, m3, m4;
+};
+
+// exact pairwise update (devmath.merge_moments), fixed op order
+__device__ __forceinline__ Mom merge(const Mom& a, const Mom& b) {
+  if (b.n == 0.0) return a;
+  if (a.n == 0.0) return b;
+  Mom r;
+  r.n = cadd(a.n, b.n);
+  const double delta = csub(b.mu, a.mu);
+  const double dn = cdiv_count(delta, r.n);
+  const double dn2 = cmul(dn, dn);
+  const double t = cmul(cmul(cmul(delta, dn), a.n), b.n);
+  r.mu = cadd(a.mu, cmul(b.n, dn));
+  r.m2 = cadd(cadd(a.m2, b.m2), t);
+  r.m3 = cadd(cadd(cadd(a.m3, b.m3), cmul(cmul(t, dn), csub(a.n, b.n))),
+              cmul(cmul(3.0, dn), csub(cmul(a.n, b.m2), cmul(b.n, a.m2))));
+  const double nn = cadd(csub(cmul(a.n, a.n), cmul(a.n, b.n)), cmul(b.n, b.n));
+  r.m4 = cadd(cadd(cadd(cadd(a.m4, b.m4), cmul(cmul(t, dn2), nn)),
+                   cmul(cmul(6.0, dn2), cadd(cmul(cmul(a.n, a.n), b.m2), cmul(cmul(b.n, b.n), a.m2)))),
+              cmul(cmul(4.0, dn), csub(cmul(a.n, b.m3), cmul(b.n, a.m3))));
+  return r;
+}
+
+__device__ __forceinline__ Mom shfl_mom(const Mom& a, int mask) {
+  Mom r;
+  r.n = __shfl_xor_sync(LFPS_FULL, a.n, mask);
+  r.mu = __shfl_xor_sync(LFPS_FULL, a.mu, mask);
+  r.m2 = __shfl_xor_sync(LFPS_FULL, a.m2, mask);
+  r.m3 = __shfl_xor_sync(LFPS_FULL, a.m3, mask);
+  r.m4 = __shfl_xor_sync(LFPS_FULL, a.m4, mask);
+  return r;
+}
+
+// an item's window [lo, lo + m) of table slots and its blocks
+struct Window {
+  int lo, m, first, nseg;
+};
+
+__device__ __forceinline__ Window make_window(int lo, int m) {
+  Window w;
+  w.lo = lo;
+  w.m = m;
+  w.first = lo / kBlk;
+  w.nseg = (lo + m - 1) / kBlk - w.first + 1;
+  return w;
+}
+
+// segment of block blk: slots [a, a + vc)
+__device__ __forceinline__ void segment(const Window& w, int blk, int& a, int& vc) {
+  a = max(blk * kBlk, w.lo);
+  vc = min(blk * kBlk + kBlk, w.lo + w.m) - a;
+}
+
+// element j of the segment -> lane j % 32, position j / 32 (0 beyond vc)
+__device__ __forceinline__ void load_seg(const double* row, int a, int vc, int lane, double* v) {
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int j = e * 32 + lane;
+    v[e] = j < vc ? __ldcg(row + a + j) : 0.0;
+  }
+}
+
+// segment mean and centred power sums (devmath.chunk_moments)
+template <bool FULL>
+__device__ __forceinline__ void seg_moments(const double* v, int vc, int lane, double& mu,
+                                            double& m2, double& m3, double& m4) {
+  double q[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) q[g] = cadd(cadd(v[4 * g], v[4 * g + 1]), cadd(v[4 * g + 2], v[4 * g + 3]));
+  const double sum = warp_fold(cadd(cadd(q[0], q[1]), cadd(q[2], q[3])));
+  mu = FULL ? cmul(sum, 1.0 / 512.0) : cdiv_count(sum, (double)vc);
+  double p2[4], p3[4], p4[4];
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    double t2[4], t3[4], t4[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int e = 4 * g + t;
+      const double d = (FULL || e * 32 + lane < vc) ? csub(v[e], mu) : 0.0;
+      const double d2 = cmul(d, d);
+      t2[t] = d2;
+      t3[t] = cmul(d2, d);
+      t4[t] = cmul(d2, d2);
+    }
+    p2[g] = cadd(cadd(t2[0], t2[1]), cadd(t2[2], t2[3]));
+    p3[g] = cadd(cadd(t3[0], t3[1]), cadd(t3[2], t3[3]));
+    p4[g] = cadd(cadd(t4[0], t4[1]), cadd(t4[2], t4[3]));
+  }
+  m2 = warp_fold(cadd(cadd(p2[0], p2[1]), cadd(p2[2], p2[3])));
+  m3 = warp_fold(cadd(cadd(p3[0], p3[1]), cadd(p3[2], p3[3])));
+  m4 = warp_fold(cadd(cadd(p4[0], p4[1]), cadd(p4[2], p4[3])));
+}
+
+// canonical merge of the window's segments (pairwise tree over 512 leaves,
+// leaf i = segment i; lane l owns leaves [16 l, 16 l + 16))
+__device__ __noinline__ Mom item_merge(const double* bs, Window w, int lane) {
+  Mom stk[4];
+  Mom cur;
+#pragma unroll
+  for (int k = 0; k < kLeavesPerLane; ++k) {
+    const int i = lane * kLeavesPerLane + k;
+    cur = {0.0, 0.0, 0.0, 0.0, 0.0};
+    if (i < w.nseg) {
+      int a, vc;
+      segment(w, w.first + i, a, vc);
+      cur.n = (double)vc;
+      const double2* p = reinterpret_cast<const double2*>(bs + 4 * (size_t)(w.first + i));
+      const double2 x = __ldcg(p), y = __ldcg(p + 1);
+      cur.mu = x.x; cur.m2 = x.y; cur.m3 = y.x; cur.m4 = y.y;
+    }
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+      if ((k >> l) & 1) {
+        cur = merge(stk[l], cur);
+      } else {
+        stk[l] = cur;
+        break;
+      }
+    }
+  }
+  Mom acc = cur;
+#pragma unroll
+  for (int h = 1; h <= 16; h <<= 1) {
+    const Mom o = shfl_mom(acc, h);
+    acc = (lane & h) ? merge(o, acc) : merge(acc, o);
+  }
+  return acc;
+}
+
+// bits of C0 at positions j - delta for j in word w (|delta| <= 31)
+__device__ __forceinline__ uint32_t shifted(uint32_t prev, uint32_t cur, uint32_t next, int delta) {
+  if (delta == 0) return cur;
+  if (delta > 0) return (cur << delta) | (prev >> (32 - delta));
+  const int k = -delta;
+  return (cur >> k) | (next << (32 - k));
+}
+
+__device__ __forceinline__ long long thr_bits(double t) {
+  // values compared are +0 or positive: NaN never passes, -inf always passes
+  if (isnan(t)) return 0x7fffffffffffffffll;
+  if (t < 0.0) return -1ll;
+  return __double_as_longlong(t);
+}
+
+__device__ __forceinline__ long long warp_max64(long long x) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) x = max(x, (long long)__shfl_xor_sync(LFPS_FULL, x, o));
+  return x;
+}
+
+struct SelectShared {
+  int ntask, nhot;
+  int task[kMaxTasks];
+  double thr0[2], thrf[2];
+  int deg[2];
+  int blk[512];
+  int red[4][kWarps];
+};
+
+__global__ void __launch_bounds__(kThreads) lfps_select_kernel(Ctx c) {
+  extern __shared__ uint32_t smem[];
+  __shared__ SelectShared sh;
+  const int s = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* cnt = c.counts + (size_t)s * CNT_N;
+  if (c.bypass[s]) {
+    if (tid < CNT_N) cnt[tid] = 0;
+    return;
+  }
+  const int b = s / c.Hq;
+  const int n = c.n_ctx[b];
+  const int S = c.S;
+  const int m = n - S;
+  const int W = (m + 31) / 32;
+  const int nblk = (W + 31) / 32;
+  uint32_t* c0w = smem;            // [W] C0 bitmap (logical index)
+  uint32_t* pwords = smem + W;     // [W] probe bitmap
+  const double* ver = ver_row(c, s);
+  const int base = c.sla_base[s];
+  const double* sla = sla_row(c, s) + base;   // logical view
+  const Window wv = make_window(0, m);
+  const Window wsl = make_window(base, m);
+  const int nb = c.bw.nblk;
+
+  // ---- A: rebuild dirty blocks --------------------------------------------------
+  if (tid == 0) sh.ntask = 0;
+  __syncthreads();
+  if (!c.exhaustive) {
+    const bool valid = c.bw.valid[s] != 0;
+    if (tid < 64) {
+      const int t = tid >> 5, wd = tid & 31;
+      const Window& w = t ? wsl : wv;
+      if (wd < c.bw.dwords) {
+        uint32_t* dp = c.bw.dirty + (size_t)(2 * s + t) * c.bw.dwords + wd;
+        uint32_t bits = valid ? *dp : LFPS_FULL;
+        if (valid && bits) *dp = 0u;
+        const int lo = w.first - wd * 32, hi = w.first + w.nseg - wd * 32;   // window blocks
+        const uint32_t in_lo = lo <= 0 ? LFPS_FULL : (lo >= 32 ? 0u : (LFPS_FULL << lo));
+        const uint32_t in_hi = hi >= 32 ? LFPS_FULL : (hi <= 0 ? 0u : (LFPS_FULL >> (32 - hi)));
+        bits &= in_lo & in_hi;
+        if (bits) {
+          int pos = atomicAdd(&sh.ntask, __popc(bits));
+          while (bits) {
+            const int k = __ffs(bits) - 1;
+            bits &= bits - 1;
+            sh.task[pos++] = (t << 16) | (wd * 32 + k);
+          }
+        }
+      }
+    }
+    if (!valid && tid < 2 * c.bw.dwords) {   // clear stale marks of a rebuilt session
+      c.bw.dirty[(size_t)(2 * s + (tid / c.bw.dwords)) * c.bw.dwords + tid % c.bw.dwords] = 0u;
+    }
+    __syncthreads();
+    for (int k = warp; k < sh.ntask; k += kWarps) {
+      const int task = sh.task[k];
+      const int t = task >> 16, blk = task & 0xffff;
+      const Window& w = t ? wsl : wv;
+      int a, vc;
+      segment(w, blk, a, vc);
+      const double* row = t ? sla_row(c, s) : ver;
+      double v[16];
+      load_seg(row, a, vc, lane, v);
+      double mu, m2, m3, m4;
+      if (vc == kBlk) seg_moments<true>(v, vc, lane, mu, m2, m3, m4);
+      else seg_moments<false>(v, vc, lane, mu, m2, m3, m4);
+      long long mx = 0;
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if (e * 32 + lane < vc) mx = max(mx, __double_as_longlong(v[e]));
+      mx = warp_max64(mx);
+      if (lane == 0) {
+        const size_t it = (size_t)(2 * s + t) * nb + blk;
+        double2* p = reinterpret_cast<double2*>(c.bw.bsum + 4 * it);
+        p[0] = make_double2(mu, m2);
+        p[1] = make_double2(m3, m4);
+        c.bw.bmax[it] = __longlong_as_double(mx);
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- B: thresholds (compute_thresholds) -------------------------------------------
+  if (warp < 2) {
+    const int t = warp;
+    double* thr = c.thr + (size_t)(2 * s + t) * 4;
+    if (c.exhaustive) {
+      if (lane == 0) {
+        sh.thr0[t] = -INFINITY; sh.thrf[t] = -INFINITY; sh.deg[t] = 0;
+        thr[0] = -INFINITY; thr[1] = -INFINITY; thr[2] = 0.0; thr[3] = NAN;
+      }
+    } else {
+      const Mom tot = item_merge(c.bw.bsum + (size_t)(2 * s + t) * nb * 4, t ? wsl : wv, lane);
+      if (lane == 0) {
+        const double sc = c.scale[s];
+        const double mean = cmul(tot.mu, sc);
+        const bool deg = cmul(cmul(tot.m2, sc), sc) < 1e-12;
+        double tau = NAN, kappa = NAN, thr0 = NAN;
+        if (!deg) {
+          kappa = cdiv(tot.m4, cmul(tot.m2, tot.m2));
+          if (kappa == 0.0) set_err(c, s, LFPS_ERR_KAPPA_ZERO);
+          tau = cdiv(cmul(c.a, mean), kappa);
+          thr0 = cdiv(tau, sc);
+        }
+        sh.thr0[t] = thr0;
+        sh.thrf[t] = cdiv(mean, sc);
+        sh.deg[t] = deg ? 1 : 0;
+        thr[0] = tau; thr[1] = mean; thr[2] = deg ? 1.0 : 0.0; thr[3] = kappa;
+      }
+    }
+  }
+  if (tid == 0) {
+    sh.nhot = 0;
+    if (!c.exhaustive) c.bw.valid[s] = 1;
+  }
+  for (int w = tid; w < W; w += kThreads)
+    c0w[w] = !c.exhaustive ? 0u : ((w == W - 1 && (m & 31)) ? ((1u << (m & 31)) - 1u) : LFPS_FULL);
+  __syncthreads();
+
+  // ---- C: C0 from the hot blocks (select_initial) ----------------------------------
+  if (!c.exhaustive) {
+    for (int t = 0; t < 2; ++t) {
+      if (sh.deg[t]) continue;                       // a degenerate table contributes nothing
+      const long long tb = thr_bits(sh.thr0[t]);
+      const Window& w = t ? wsl : wv;
+      const double* bm = c.bw.bmax + (size_t)(2 * s + t) * nb;
+      for (int i = tid; i < w.nseg; i += kThreads) {
+        if (__double_as_longlong(__ldcg(bm + w.first + i)) > tb) {
+          const int pos = atomicAdd(&sh.nhot, 1);
+          sh.task[pos] = (t << 16) | (w.first + i);
+        }
+      }
+    }
+    __syncthreads();
+    for (int k = warp; k < sh.nhot; k += kWarps) {
+      const int task = sh.task[k];
+      const int t = task >> 16, blk = task & 0xffff;
+      const Window& w = t ? wsl : wv;
+      int a, vc;
+      segment(w, blk, a, vc);
+      double v[16];
+      load_seg(t ? sla_row(c, s) : ver, a, vc, lane, v);
+      const long long tb = thr_bits(sh.thr0[t]);
+      const int L0 = a - w.lo;                         // logical index of element 0
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const uint32_t wd = __ballot_sync(LFPS_FULL, e * 32 + lane < vc &&
+                                                         __double_as_longlong(v[e]) > tb);
+        if (lane == 0 && wd) {
+          const int L = L0 + e * 32;
+          const int sft = L & 31, wi = L >> 5;
+          atomicOr(&c0w[wi], wd << sft);
+          if (sft && (wd >> (32 - sft))) atomicOr(&c0w[wi + 1], wd >> (32 - sft));
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- D: C1 = F & dilate(C0); probe = C1 | tail -----------------------------------
+  const long long tfv = thr_bits(sh.thrf[0]);
+  const long long tfs = thr_bits(sh.thrf[1]);
+  const long long* verb = reinterpret_cast<const long long*>(ver);
+  const long long* slab = reinterpret_cast<const long long*>(sla);
+  const int tail_lo = max(0, m - c.L);
+  const uint32_t last_valid = (m & 31) ? ((1u << (m & 31)) - 1u) : LFPS_FULL;
+  int n0 = 0, n1 = 0, nd = 0;
+  for (int bk = warp; bk < nblk; bk += kWarps) {
+    const int w = bk * 32 + lane;
+    const bool in = w < W;
+    const uint32_t cur = in ? c0w[w] : 0u;
+    const uint32_t prev = (in && w > 0) ? c0w[w - 1] : 0u;
+    const uint32_t next = (in && w + 1 < W) ? c0w[w + 1] : 0u;
+    uint32_t dil = 0;
+    for (int k = 0; k < c.n_off; ++k) dil |= shifted(prev, cur, next, c.off[k]);
+    const uint32_t valid = !in ? 0u : (w == W - 1 ? last_valid : LFPS_FULL);
+    uint32_t cand = dil & valid;
+    uint32_t c1 = 0;
+    if (c.exhaustive) {
+      c1 = cand;
+    } else {
+      // F at the dilated positions, four positions (eight loads) in flight
+      while (cand) {
+        int pos[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          pos[q] = cand ? __ffs(cand) - 1 : -1;
+          cand &= cand - 1;
+        }
+        long long xv[4], xs[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          xv[q] = xs[q] = -1ll;
+          if (pos[q] >= 0) {
+            const int i = w * 32 + pos[q];
+            xv[q] = __ldcg(verb + i);
+            xs[q] = __ldcg(slab + i);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (pos[q] >= 0 && (xv[q] > tfv || xs[q] > tfs)) c1 |= 1u << pos[q];
+      }
+    }
+    uint32_t tail = 0;
+    const int j0 = w * 32;
+    if (in && j0 + 32 > tail_lo) tail = (LFPS_FULL << max(0, tail_lo - j0)) & valid;
+    const uint32_t pr = c1 | tail;
+    if (in) pwords[w] = pr;
+    if (in && (c.flags & LFPS_FLAG_EXPORT_SETS)) {
+      c.bits[(size_t)(2 * s) * c.words + w] = cur;      // C0
+      c.bits[(size_t)(2 * s + 1) * c.words + w] = c1;   // C1
+    }
+    n0 += __popc(cur);
+    n1 += __popc(c1);
+    nd += __popc(cur & ~c1);
+    int bc = __popc(pr);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) bc += __shfl_xor_sync(LFPS_FULL, bc, o);
+    if (lane == 0) sh.blk[bk] = bc;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    n0 += __shfl_xor_sync(LFPS_FULL, n0, o);
+    n1 += __shfl_xor_sync(LFPS_FULL, n1, o);
+    nd += __shfl_xor_sync(LFPS_FULL, nd, o);
+  }
+  if (lane == 0) { sh.red[0][warp] = n0; sh.red[1][warp] = n1; sh.red[2][warp] = nd; }
+  __syncthreads();
+  if (warp == 0) {
+    int carry = 0;
+    for (int base2 = 0; base2 < nblk; base2 += 32) {
+      const int i = base2 + lane;
+      const int v = i < nblk ? sh.blk[i] : 0;
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(LFPS_FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      if (i < nblk) sh.blk[i] = carry + x - v;
+      carry += __shfl_sync(LFPS_FULL, x, 31);
+    }
+    if (lane == 0) {
+      int t0 = 0, t1 = 0, t3 = 0;
+      for (int k = 0; k < kWarps; ++k) { t0 += sh.red[0][k]; t1 += sh.red[1][k]; t3 += sh.red[2][k]; }
+      cnt[CNT_C0] = t0;
+      cnt[CNT_C1] = t1;
+      cnt[CNT_PROBE] = carry;
+      cnt[CNT_DROP] = t3;
+      cnt[CNT_BLOCKS] = sh.ntask + sh.nhot;
+    }
+  }
+  __syncthreads();
+  int* out = c.probe_idx + (size_t)s * c.list_cap;
+  for (int bk = warp; bk < nblk; bk += kWarps) {
+    const int w = bk * 32 + lane;
+    uint32_t pr = w < W ? pwords[w] : 0u;
+    const int pc = __popc(pr);
+    int x = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(LFPS_FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    int pos = sh.blk[bk] + x - pc;
+    while (pr) {
+      const int bit = __ffs(pr) - 1;
+      out[pos++] = S + w * 32 + bit;
+      pr &= pr - 1;
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_select(const Ctx& c, int m_max, cudaStream_t st) {
+  const size_t smem = 2 * (size_t)((m_max + 31) / 32) * 4;
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(lfps_select_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  lfps_select_kernel<<<c.NS, kThreads, smem, st>>>(c);
+  return cudaGetLastError();
+}
+
+}  // namespace lfps

@@ -1,14 +1,18 @@
-// k_update.cu -- tracker update + grow (K6), KV append and commit.
+// k_update.cu -- commit of a decode step: tracker update + grow (K6), KV
+// append and the context count.
 //
 // lfps_update_kernel restates ScoreTablePair.update / grow (tables.py:144-220)
-// in ring form: u = canonical fp64 softmax of the selected fp32 scores
-// (engine.py:184, devmath.softmax_update); |sum u - 1| <= 1e-6 check;
-// scale *= r with renormalisation below 1e-120 (vertical [0, m) and slash
-// logical [0, m] multiplied by the new scale); slash shift = ring base - 1
+// on the linear slash window: u = canonical fp64 softmax of the selected
+// fp32 scores (engine.py:184, devmath.softmax_update; its max and
+// normaliser come from the finish kernel, which also ran the |sum u - 1|
+// check); scale *= r with renormalisation below 1e-120 (vertical [0, m) and
+// slash logical [0, m] multiplied by the new scale); slash shift = base - 1
 // with the new logical slot 0 zeroed and the old top parked at logical m;
 // add = (u - 1/(2k)) / scale folded into both tables at C2; negative
 // entries clamped to 0 and counted; grow: vertical slot m = 0, slash slot m
-// keeps the parked value (zero on bypassed steps, which only grow).
+// keeps the parked value (a gated step only grows, with a zero slash slot).
+// Every block whose slots changed is marked dirty for k_select.cu; a
+// renormalisation invalidates all of the session's block summaries.
 //
 // Nothing is committed if any session of the batch raised a data error
 // (err[0] != 0): the whole step is atomic (engine.py:8-9).
@@ -20,63 +24,49 @@ namespace lfps {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kMaxDirtyWords = 32;
 
 __global__ void __launch_bounds__(kThreads) lfps_update_kernel(Ctx c) {
-  __shared__ double red[9];
+  __shared__ uint32_t dmark[2][kMaxDirtyWords];
   __shared__ int clamp_red[kThreads / 32];
   const int s = blockIdx.x, tid = threadIdx.x;
   if (c.err[0] != 0) return;
   const int b = s / c.Hq;
   const int n = c.n_ctx[b];
   const int m = n - c.S;
-  const int C = c.ring_cap;
-  double* ver = c.ver + (size_t)s * c.m_cap;
-  double* sla = c.sla + (size_t)s * C;
+  double* ver = ver_row(c, s);
+  double* sla = sla_row(c, s);
   int base = c.sla_base[s];
+  const int dw = c.bw.dwords;
+  uint32_t* dirty = c.bw.dirty + (size_t)(2 * s) * dw;
   if (c.bypass[s]) {
-    if (tid == 0) {
+    if (tid == 0) {                     // grow only (engine.py:133-137)
       ver[m] = 0.0;
-      sla[(base + m) % C] = 0.0;       // no parked carry on a gated step
+      sla[base + m] = 0.0;              // no parked carry on a gated step
+      const int bv = m / kBlk, bs = (base + m) / kBlk;
+      dirty[bv >> 5] |= 1u << (bv & 31);
+      dirty[dw + (bs >> 5)] |= 1u << (bs & 31);
     }
     return;
   }
+  for (int i = tid; i < 2 * kMaxDirtyWords; i += kThreads) (&dmark[0][0])[i] = 0u;
   const int k2 = c.counts[(size_t)s * CNT_N + CNT_C2];
   const int* idx = c.c2_idx + (size_t)s * c.list_cap;
   const float* z = c.c2_score + (size_t)s * c.list_cap;
-  // max (exact in any order)
-  double mx = -INFINITY;
-  for (int j = tid; j < k2; j += kThreads) mx = fmax(mx, (double)z[j]);
-  for (int o = 16; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(LFPS_FULL, mx, o));
-  if ((tid & 31) == 0) red[tid >> 5] = mx;
-  __syncthreads();
-  mx = red[0];
-  for (int w = 1; w < kThreads / 32; ++w) mx = fmax(mx, red[w]);
-  __syncthreads();
-  // canonical sum of exponentials: thread t owns j = t, t + 256, ...
-  double acc = 0.0;
-  for (int j = tid; j < k2; j += kThreads) acc = cadd(acc, cexp(csub((double)z[j], mx)));
-  const double tot = block_fold256(acc, red);
-  // sum of the normalised weights (tables.py:161-163)
-  acc = 0.0;
-  for (int j = tid; j < k2; j += kThreads) acc = cadd(acc, cdiv(cexp(csub((double)z[j], mx)), tot));
-  const double wsum = block_fold256(acc, red);
-  if (fabs(wsum - 1.0) > 1e-6) {
-    if (tid == 0) set_err(c, s, LFPS_ERR_WEIGHT_SUM);
-    return;
-  }
+  const double mx = c.bw.wstat[2 * (size_t)s];
+  const double tot = c.bw.wstat[2 * (size_t)s + 1];
   // decay with renormalisation (tables.py:167-169, 240-244)
   double sc = cmul(c.scale[s], c.r);
+  bool renorm = false;
   if (sc < 1e-120) {
     for (int i = tid; i < m; i += kThreads) ver[i] = cmul(ver[i], sc);
-    for (int i = tid; i <= m; i += kThreads) {
-      const int slot = (base + i) % C;
-      sla[slot] = cmul(sla[slot], sc);
-    }
+    for (int i = tid; i <= m; i += kThreads) sla[base + i] = cmul(sla[base + i], sc);
     sc = 1.0;
-    __syncthreads();
+    renorm = true;
   }
   // slash shift (tables.py:174-177)
-  base = (base - 1 + C) % C;
+  base -= 1;
+  __syncthreads();
   if (tid == 0) sla[base] = 0.0;
   __syncthreads();
   // residual fold and clamp (tables.py:179-199)
@@ -89,23 +79,37 @@ __global__ void __launch_bounds__(kThreads) lfps_update_kernel(Ctx c) {
     double v = cadd(ver[li], add);
     if (v < 0.0) { v = 0.0; ++clamps; }
     ver[li] = v;
-    const int slot = (base + li) % C;
+    const int slot = base + li;
     double w = cadd(sla[slot], add);
     if (w < 0.0) { w = 0.0; ++clamps; }
     sla[slot] = w;
+    const int bv = li / kBlk, bs = slot / kBlk;
+    atomicOr(&dmark[0][bv >> 5], 1u << (bv & 31));
+    atomicOr(&dmark[1][bs >> 5], 1u << (bs & 31));
   }
   for (int o = 16; o >= 1; o >>= 1) clamps += __shfl_xor_sync(LFPS_FULL, clamps, o);
   if ((tid & 31) == 0) clamp_red[tid >> 5] = clamps;
+  if (tid == 0) {
+    // grow (tables.py:202-220): vertical slot m, slash slot base (new logical 0)
+    const int bv = m / kBlk, bs = base / kBlk;
+    atomicOr(&dmark[0][bv >> 5], 1u << (bv & 31));
+    atomicOr(&dmark[1][bs >> 5], 1u << (bs & 31));
+  }
   __syncthreads();
+  if (tid < 2 * dw) {
+    const int t = tid / dw, w = tid % dw;
+    const uint32_t mk = dmark[t][w];
+    if (mk) dirty[t * dw + w] |= mk;
+  }
   if (tid == 0) {
     int tc = 0;
     for (int w = 0; w < kThreads / 32; ++w) tc += clamp_red[w];
     c.counts[(size_t)s * CNT_N + CNT_CLAMP] = tc;
     c.clamp_count[s] += tc;
-    // grow (tables.py:202-220): the parked slash value at logical m stays
-    ver[m] = 0.0;
+    ver[m] = 0.0;                       // the parked slash value at logical m stays
     c.scale[s] = sc;
     c.sla_base[s] = base;
+    if (renorm) c.bw.valid[s] = 0;
   }
 }
 

@@ -30,7 +30,8 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(LFPS_E_CUDA, "%s: %s", where, cudaGetErrorString(e));
 }
 
-constexpr int kMaxM = 262144;           // k_tables.cu: <= 512 chunks of 512 slots
+constexpr int kMaxMcap = 510 * 512;     // slash table <= 1022 blocks (32 dirty words)
+constexpr int kMaxM = kMaxMcap - 2;     // k_select.cu: a window spans <= 512 blocks
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -42,6 +43,8 @@ int check_dims(const lfps_dims* d) {
   if (!(d->d == 32 || d->d == 64 || d->d == 128 || d->d == 256))
     return fail(LFPS_E_UNSUPPORTED, "head dimension must be 32, 64, 128 or 256, got %d", d->d);
   if (d->m_cap < 2 || (d->m_cap & 1)) return fail(LFPS_E_INVALID, "m_cap must be even and >= 2");
+  if (d->m_cap > kMaxMcap)
+    return fail(LFPS_E_UNSUPPORTED, "m_cap must be <= %d", kMaxMcap);
   if (d->n_max < 2) return fail(LFPS_E_INVALID, "n_max must be >= 2");
   if ((long long)d->batch * d->kv_heads * d->group * 2 > 65535)
     return fail(LFPS_E_UNSUPPORTED, "too many sessions for one launch (B*Hq <= 32767)");
@@ -75,8 +78,11 @@ int check_params(const lfps_params* p, const lfps_dims* d) {
   return LFPS_OK;
 }
 
-constexpr int kCaptureCap = 8192;       // captured slots per (session, table) per step
-constexpr int kChunkLeaves = 512;       // k_tables.cu kLeaves
+// slash table: 2 * roundup(m_cap, 512) + 1024 slots; the window starts out
+// ending at the home slot roundup(m_cap, 512) + 512 and can grow m_cap slots
+// down (slash shifts) and m_cap slots up (gated steps) without wrapping
+int slash_home(int m_cap) { return (m_cap + lfps::kBlk - 1) / lfps::kBlk * lfps::kBlk + lfps::kBlk; }
+int slash_cap(int m_cap) { return 2 * slash_home(m_cap); }
 
 int layout(const lfps_dims* d, lfps_ws_layout* L) {
   const size_t NS = (size_t)d->batch * d->kv_heads * d->group;
@@ -85,6 +91,8 @@ int layout(const lfps_dims* d, lfps_ws_layout* L) {
   memset(L, 0, sizeof(*L));
   L->list_cap = d->m_cap;
   L->words = (int)((cap + 511) / 512 * 16);   // whole 512-slot chunks
+  L->nblk = slash_cap(d->m_cap) / lfps::kBlk;
+  L->dirty_words = (L->nblk + 31) / 32;
   size_t o = 0;
   auto take = [&](size_t bytes) { const size_t at = o; o = align_up(o + bytes, 256); return at; };
   L->rho = take(NS * 8);
@@ -100,16 +108,11 @@ int layout(const lfps_dims* d, lfps_ws_layout* L) {
   L->c2_score = take(NS * cap * 4);
   // bootstrap scratch (f64 logits) aliases probe_idx + probe_score
   L->scratch = L->probe_idx;
-  L->cstat = take(NI * kChunkLeaves * 4 * 8);
-  L->cidx = take(NI * kCaptureCap * 4);
-  L->cval = take(NI * kCaptureCap * 8);
-  L->ncap = take(NI * 4);
-  L->itemf = take(NI * 4 * 8);
-  L->bound = take(NI * 8);
-  L->fb = take(NI * 4);
-  L->fblist = take(NI * 4);
-  L->nfb = take(64);
-  L->capture_cap = kCaptureCap;
+  L->bsum = take(NI * (size_t)L->nblk * 4 * 8);
+  L->bmax = take(NI * (size_t)L->nblk * 8);
+  L->dirty = take(NI * (size_t)L->dirty_words * 4);
+  L->valid = take(NS * 4);
+  L->wstat = take(NS * 2 * 8);
   L->total_bytes = o;
   return LFPS_OK;
 }
@@ -128,7 +131,8 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
   memset(c, 0, sizeof(*c));
   c->B = d->batch; c->Hkv = d->kv_heads; c->G = d->group; c->Hq = d->kv_heads * d->group;
   c->NS = c->B * c->Hq; c->d = d->d; c->n_max = d->n_max; c->m_cap = d->m_cap;
-  c->ring_cap = d->m_cap + 2; c->words = L.words; c->list_cap = L.list_cap;
+  c->sla_cap = slash_cap(d->m_cap); c->sla_home = slash_home(d->m_cap);
+  c->words = L.words; c->list_cap = L.list_cap;
   c->r = p->r; c->eps = p->epsilon; c->a = p->a; c->frac = p->k_fraction; c->sqrt_d = p->sqrt_d;
   c->sqrt_d_f32 = p->sqrt_d_f32; c->s = p->s; c->S = p->sink_count; c->L = p->local_window;
   c->bypass_mode = p->bypass_mode; c->exhaustive = p->exhaustive; c->n_off = p->n_offsets;
@@ -157,16 +161,13 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
   c->c2_idx = reinterpret_cast<int*>(base + L.c2_idx);
   c->c2_score = reinterpret_cast<float*>(base + L.c2_score);
   c->scratch = reinterpret_cast<double*>(base + L.scratch);
-  c->tb.cstat = reinterpret_cast<double*>(base + L.cstat);
-  c->tb.cidx = reinterpret_cast<int*>(base + L.cidx);
-  c->tb.cval = reinterpret_cast<double*>(base + L.cval);
-  c->tb.ncap = reinterpret_cast<int*>(base + L.ncap);
-  c->tb.cap = L.capture_cap;
-  c->tb.itemf = reinterpret_cast<double*>(base + L.itemf);
-  c->tb.bound = reinterpret_cast<double*>(base + L.bound);
-  c->tb.fb = reinterpret_cast<int*>(base + L.fb);
-  c->tb.fblist = reinterpret_cast<int*>(base + L.fblist);
-  c->tb.nfb = reinterpret_cast<int*>(base + L.nfb);
+  c->bw.bsum = reinterpret_cast<double*>(base + L.bsum);
+  c->bw.bmax = reinterpret_cast<double*>(base + L.bmax);
+  c->bw.dirty = reinterpret_cast<uint32_t*>(base + L.dirty);
+  c->bw.valid = reinterpret_cast<int*>(base + L.valid);
+  c->bw.wstat = reinterpret_cast<double*>(base + L.wstat);
+  c->bw.nblk = L.nblk;
+  c->bw.dwords = L.dirty_words;
   return LFPS_OK;
 }
 
@@ -248,8 +249,14 @@ int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out) {
   return layout(dims, out);
 }
 
-int lfps_decode_launches(void) { return 10; }  // clear, gate, 4 table kernels, probe,
-                                              // finish, append, commit
+int lfps_decode_launches(void) { return 7; }  // clear, gate, select, finish, update,
+                                             // append, commit
+
+int lfps_slash_capacity(const lfps_dims* dims) {
+  int rc = check_dims(dims);
+  if (rc) return rc;
+  return slash_cap(dims->m_cap);
+}
 
 int lfps_profile_enable(int on) {
   std::lock_guard<std::mutex> g(g_prof_mu);
@@ -327,9 +334,9 @@ int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_sta
   const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
   LAUNCH_P("clear_err", sm, lfps::launch_clear_err(c, sm));
   LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
-  LAUNCH_P("tables", sm, lfps::launch_tables(c, m_max, sm));
-  LAUNCH_P("probe", sm, lfps::launch_probe(c, m_max, sm));
+  LAUNCH_P("select", sm, lfps::launch_select(c, m_max, sm));
   LAUNCH_P("finish", sm, lfps::launch_finish(c, qb, sm));
+  LAUNCH_P("update", sm, lfps::launch_update(c, sm));
   LAUNCH_P("append", sm, lfps::launch_append(c, static_cast<const __nv_bfloat16*>(k_new),
                              static_cast<const __nv_bfloat16*>(v_new), sm));
   LAUNCH_P("commit", sm, lfps::launch_commit(c, sm));

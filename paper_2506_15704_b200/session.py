@@ -28,7 +28,7 @@ from . import _lib
 from .config import LfpsConfig
 from .errors import DeviceError, LfpsError
 
-CNT_C0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP = range(7)
+CNT_C0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_BLOCKS = range(8)
 
 
 def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False) -> _lib.Params:
@@ -62,7 +62,7 @@ class BatchedStepResult:
     output: torch.Tensor       # f32 [B, Hq, d]
     rho: torch.Tensor          # f64 [B, Hq]
     bypassed: torch.Tensor     # i32 [B, Hq]
-    counts: torch.Tensor       # i32 [B, Hq, 8]: c0 c1 probe c0_dropped k c2 clamps -
+    counts: torch.Tensor       # i32 [B, Hq, 8]: c0 c1 probe c0_dropped k c2 clamps blocks
     c2_idx: torch.Tensor       # i32 [B, Hq, list_cap] (first counts[..., 5] valid)
     c2_score: torch.Tensor     # f32 [B, Hq, list_cap]
     err: torch.Tensor          # i32 [1 + B*Hq]
@@ -98,6 +98,7 @@ class BatchedSession:
         self.m_cap = m_cap
         self.dims = _lib.Dims(batch, kv_heads, group, cfg.d, self.n_max, m_cap)
         self.layout = _lib.workspace_layout(self.dims)
+        self.sla_cap = _lib.slash_capacity(self.dims)
         dev = self.device
         f64, i32 = torch.float64, torch.int32
         self.k_cache = torch.zeros(batch, kv_heads, self.n_max, cfg.d, dtype=torch.bfloat16,
@@ -106,7 +107,7 @@ class BatchedSession:
         self.n_ctx = torch.zeros(batch, dtype=i32, device=dev)
         self.n_host = [0] * batch
         self.ver = torch.zeros(self.NS, m_cap, dtype=f64, device=dev)
-        self.sla = torch.zeros(self.NS, m_cap + 2, dtype=f64, device=dev)
+        self.sla = torch.zeros(self.NS, self.sla_cap, dtype=f64, device=dev)
         self.scale = torch.ones(self.NS, dtype=f64, device=dev)
         self.sla_base = torch.zeros(self.NS, dtype=i32, device=dev)
         self.clamp_count = torch.zeros(self.NS, dtype=torch.int64, device=dev)
@@ -291,9 +292,7 @@ class BatchedSession:
         b = s // self.Hq
         m = self.n_host[b] - self.cfg.sink_count
         base = int(self.sla_base[s])
-        C_ = self.m_cap + 2
-        slots = (base + torch.arange(m, device=self.device)) % C_
-        return (self.ver[s, :m].cpu().numpy(), self.sla[s][slots].cpu().numpy(),
+        return (self.ver[s, :m].cpu().numpy(), self.sla[s, base: base + m].cpu().numpy(),
                 float(self.scale[s]))
 
     def c2_list(self, b: int, qh: int):

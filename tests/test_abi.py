@@ -24,7 +24,8 @@ def test_header_declares_the_boundary():
     for want in ("lfps_abi_version", "lfps_last_error", "lfps_workspace_layout",
                  "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step",
                  "lfps_exact_topk_step", "lfps_overlap", "lfps_profile_enable",
-                 "lfps_profile_collect", "lfps_decode_launches", "lfps_exact_launches"):
+                 "lfps_profile_collect", "lfps_decode_launches", "lfps_exact_launches",
+                 "lfps_slash_capacity"):
         assert want in names
 
 
@@ -59,16 +60,20 @@ def test_workspace_layout_regions_are_disjoint_and_aligned():
     dims = _lib.Dims(4, 8, 4, 128, 33000, 33000)
     lay = _lib.workspace_layout(dims)
     offs = sorted((getattr(lay, f), f) for f, _ in _lib.WsLayout._fields_
-                  if f not in ("total_bytes", "words", "list_cap", "capture_cap", "scratch"))
+                  if f not in ("total_bytes", "words", "list_cap", "nblk", "dirty_words",
+                               "scratch"))
     for (a, _), (b, _) in zip(offs, offs[1:]):
         assert b > a
     assert all(o % 256 == 0 for o, _ in offs)
     assert lay.total_bytes > offs[-1][0]
-    assert lay.list_cap == 33000 and lay.words * 32 >= 33000 and lay.capture_cap > 0
+    assert lay.list_cap == 33000 and lay.words * 32 >= 33000
+    assert lay.nblk * 512 == _lib.slash_capacity(dims) >= 2 * 33000
+    assert lay.dirty_words * 32 >= lay.nblk and lay.dirty_words <= 32
 
 
 @pytest.mark.parametrize("bad", [
     dict(batch=0), dict(group=3), dict(d=100), dict(m_cap=33001), dict(n_max=1),
+    dict(m_cap=510 * 512 + 2),
 ])
 def test_invalid_dims_rejected_on_host(bad):
     kw = dict(batch=1, kv_heads=1, group=4, d=128, n_max=4096, m_cap=4096)
