@@ -129,6 +129,7 @@ typedef struct lfps_ws_layout {
   size_t probe_score; /* f32 [NS, list_cap] */
   size_t c2_idx;      /* i32 [NS, list_cap] */
   size_t c2_score;    /* f32 [NS, list_cap] */
+  size_t uw;          /* f64 [NS, list_cap] update weights u of C2 */
   size_t scratch;     /* f64 [NS, list_cap] bootstrap scratch */
   /* Block summaries of the tracker tables.  These PERSIST across steps (a
      cache of the state, kept in the workspace): item = 2 s + table (0 =

@@ -60,7 +60,7 @@ class WsLayout(C.Structure):
     _fields_ = [("total_bytes", C.c_size_t), ("rho", C.c_size_t), ("bypass", C.c_size_t),
                 ("err", C.c_size_t), ("out", C.c_size_t), ("thr", C.c_size_t),
                 ("counts", C.c_size_t), ("bits", C.c_size_t), ("probe_idx", C.c_size_t),
-                ("probe_score", C.c_size_t), ("c2_idx", C.c_size_t), ("c2_score", C.c_size_t),
+                ("probe_score", C.c_size_t), ("c2_idx", C.c_size_t), ("c2_score", C.c_size_t), ("uw", C.c_size_t),
                 ("scratch", C.c_size_t), ("bsum", C.c_size_t), ("bmax", C.c_size_t),
                 ("dirty", C.c_size_t), ("valid", C.c_size_t), ("wstat", C.c_size_t),
                 ("nblk", C.c_int32), ("dirty_words", C.c_int32), ("words", C.c_int32),

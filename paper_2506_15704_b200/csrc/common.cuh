@@ -62,6 +62,7 @@ struct Ctx {
   float* probe_score;
   int* c2_idx;
   float* c2_score;
+  double* uw;       // [NS, list_cap] update weights u of C2 (finish -> update)
   double* scratch;
   BlockWs bw;
 };

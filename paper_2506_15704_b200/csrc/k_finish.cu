@@ -1,54 +1,124 @@
 // k_finish.cu -- the per-session back half of a decode step in ONE kernel:
 // candidate scoring (K3), Top-k (K4), sparse attention (K5) and the data
-// checks of the tracker update (K6; the update itself is committed by
-// k_update.cu once every session has passed).  One 512-thread CTA per
-// (request, q-head) session.
+// checks + update weights of the tracker update (K6; the update itself is
+// committed by k_update.cu once every session has passed).  One 256-thread
+// CTA per (request, q-head) session.
 //
-//   scores   z_j = (K[j] . q) / fp32(sqrt d) for every probe row (canonical
-//            fp32 dot, devmath.sdot32; engine.py:168-170), half-warp per
-//            row, 8 rows in flight per half-warp
+//   rows     K / V rows stream through shared memory in tiles of 32 rows,
+//            4 stages deep, gathered with cp.async (16 B per thread, L2
+//            only): no registers hold in-flight data.  (Per-row TMA bulk
+//            copies were measured 2x slower: one 256-B request per row
+//            saturates the SM's TMA unit.)
+//   scores   z_j = (K[j] . q) / fp32(sqrt d) in the canonical order of
+//            devmath.sdot32 (engine.py:168-170): 8 lanes per row, lane l
+//            owns partials l and l + 8 (d/16 contiguous elements each, two
+//            sequential chains in one packed FFMA2), fold 8 (in-lane), 4, 2,
+//            1 (shuffles), IEEE division
 //   top-k    k = max(1, round_half_even(frac * n)) (engine.py:167); if
-//            k >= |probe| C2 = probe, else an MSB-first 4 x 8-bit radix select
-//            of the k-th largest key with lowest-index ties
-//            (topk_from_scores, attention.py:34-47)
+//            k >= |probe| C2 = probe and scores + attention are ONE pass
+//            over the rows; else all scores first, an MSB-first 4 x 8-bit
+//            radix select of the k-th largest key with lowest-index ties
+//            (topk_from_scores, attention.py:34-47), then the attention pass
 //   attend   joint softmax over [sink logits, C2 logits] and sum w V
-//            (engine.py:173-181): every half-warp keeps an online
-//            (max, sum, acc) over its rows, 8 V rows in flight; the 32
-//            partial states are merged at the end (fp32)
+//            (engine.py:173-181): every 8-lane group keeps an online
+//            (max, sum, acc) over its rows (packed fp32x2 FMAs), the 32
+//            group states are merged at the end (fp32)
 //   checks   sinks and C2 scores finite (softmax_weights, numerics.py:61-62,
 //            called at engine.py:177 and :184); u = canonical fp64 softmax
-//            of the C2 scores and |sum u - 1| <= 1e-6 (tables.py:161-163);
-//            the softmax max and normaliser go to wstat for k_update.cu
+//            of the C2 scores (devmath.softmax_update) written to uw for the
+//            update, and |sum u - 1| <= 1e-6 (tables.py:161-163)
 #include "common.cuh"
 #include "canon.cuh"
-#include "frag.cuh"
+#include "ptx.cuh"
 
 namespace lfps {
 
 namespace {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kHalves = kThreads / 16;
-// rows in flight per half-warp (register budget: 64 per thread at 2 CTAs/SM)
-template <int PER>
-constexpr int rows_in_flight() { return PER >= 16 ? 3 : (PER == 8 ? 6 : 8); }
-constexpr int kCanon = 256;            // canonical block-sum width (devmath.BLOCK_THREADS)
+constexpr int kGroups8 = kThreads / 8;   // 8-lane row groups
+constexpr int kTile = 32;                // rows per stage (one per row group)
+constexpr int kStages = 4;
+constexpr int kCanon = 256;              // canonical block-sum width (devmath.BLOCK_THREADS)
+constexpr int kMaxE = 8;                 // exponentials cached per thread (|C2| <= 2048)
+
+enum Mode { kFused = 0, kScore = 1, kAttend = 2 };
+
+// ---- packed fp32x2 arithmetic (FFMA2 / FMUL2: each half rounds like FFMA / FMUL) ----
+__device__ __forceinline__ unsigned long long pk2(float2 v) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+__device__ __forceinline__ float2 up2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
+  return up2(r);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+  return up2(r);
+}
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
+// PQ = d / 16 elements per canonical partial; a lane holds partials a = l8
+// and b = l8 + 8 of a row, PQ / 2 packed bf16 words each
+template <int PQ>
+struct Part {
+  uint32_t a[PQ / 2], b[PQ / 2];
+};
+
+template <int PQ>
+__device__ __forceinline__ Part<PQ> ld_part(const __nv_bfloat16* row, int l8) {
+  Part<PQ> r;
+  const uint32_t* p = reinterpret_cast<const uint32_t*>(row);
+#pragma unroll
+  for (int t = 0; t < PQ / 2; ++t) {
+    r.a[t] = p[l8 * (PQ / 2) + t];
+    r.b[t] = p[(l8 + 8) * (PQ / 2) + t];
+  }
+  return r;
+}
+
+// canonical fp32 dot of one row with q (devmath.sdot32) -> z, all 8 lanes
+template <int PQ>
+__device__ __forceinline__ float row_score(const Part<PQ>& k, const float2* q2, float sqrt_d) {
+  float2 p = make_float2(0.0f, 0.0f);
+#pragma unroll
+  for (int t = 0; t < PQ / 2; ++t) {
+    p = ffma2(make_float2(bf_lo(k.a[t]), bf_lo(k.b[t])), q2[2 * t], p);
+    p = ffma2(make_float2(bf_hi(k.a[t]), bf_hi(k.b[t])), q2[2 * t + 1], p);
+  }
+  float v = __fadd_rn(p.x, p.y);                        // fold 8 (in-lane)
+  // only this 8-lane group takes part: groups of a warp may hold no row
+  const unsigned gm = 0xffu << (threadIdx.x & 24);
+#pragma unroll
+  for (int h = 4; h >= 1; h >>= 1) v = __fadd_rn(v, __shfl_xor_sync(gm, v, h));
+  return __fdiv_rn(v, sqrt_d);
+}
 
 struct FinishShared {
   float sink_z[32];
-  float part_m[kHalves];
-  float part_s[kHalves];
+  float part_m[kGroups8];
+  float part_s[kGroups8];
+  float gmax[kWarps];
   double red[16];
-  int ired[kWarps];
+  int warp_sums[kWarps];
   unsigned hist[256];
   unsigned sel_digit;
   int sel_want;
-  int warp_sums[kWarps];
 };
 
-// exclusive block scan over the 512 threads
-__device__ __forceinline__ int scan512(int v, int* warp_sums, int* total) {
+// exclusive block scan over the 256 threads
+__device__ __forceinline__ int scan256(int v, int* warp_sums, int* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int x = v;
 #pragma unroll
@@ -58,28 +128,23 @@ __device__ __forceinline__ int scan512(int v, int* warp_sums, int* total) {
   }
   if (lane == 31) warp_sums[warp] = x;
   __syncthreads();
-  if (warp == 0) {
-    int w = lane < kWarps ? warp_sums[lane] : 0;
+  int before = 0, all = 0;
 #pragma unroll
-    for (int o = 1; o < kWarps; o <<= 1) {
-      const int y = __shfl_up_sync(LFPS_FULL, w, o);
-      if (lane >= o) w += y;
-    }
-    if (lane < kWarps) warp_sums[lane] = w;
+  for (int k = 0; k < kWarps; ++k) {
+    const int w = warp_sums[k];
+    before += k < warp ? w : 0;
+    all += w;
   }
   __syncthreads();
-  const int before = (warp > 0 ? warp_sums[warp - 1] : 0) + x - v;
-  *total = warp_sums[kWarps - 1];
-  __syncthreads();
-  return before;
+  *total = all;
+  return before + x - v;
 }
 
-// canonical 256-wide block sum (devmath.block_sum) of per-thread partials of
-// threads 0..255; threads >= 256 pass 0 and are ignored; all threads get it
+// canonical 256-wide block sum (devmath.block_sum); all threads get it
 __device__ __forceinline__ double canon_sum(double acc, double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   acc = warp_fold(acc);
-  if (lane == 0 && warp < 8) red[warp] = acc;
+  if (lane == 0) red[warp] = acc;
   __syncthreads();
   if (warp == 0) {
     double v = lane < 8 ? red[lane] : 0.0;
@@ -93,14 +158,101 @@ __device__ __forceinline__ double canon_sum(double acc, double* red) {
   return out;
 }
 
-template <int PER>
-__global__ void __launch_bounds__(kThreads, 2) lfps_finish_kernel(Ctx c, const __nv_bfloat16* q) {
-  constexpr int kNR = rows_in_flight<PER>();
-  extern __shared__ float part_acc[];              // [kHalves][PER * 16]
+// Online-softmax state of one 8-lane row group (all 8 lanes hold m, s).
+template <int PQ>
+struct Attn {
+  float m, s;
+  float2 acc[PQ];     // dims (a * PQ + e, b * PQ + e)
+  __device__ __forceinline__ void init() {
+    m = -INFINITY;
+    s = 0.0f;
+#pragma unroll
+    for (int e = 0; e < PQ; ++e) acc[e] = make_float2(0.0f, 0.0f);
+  }
+  __device__ __forceinline__ void absorb(float z, const Part<PQ>& v) {
+    if (z > m) {
+      const float r = __expf(m - z);
+      s *= r;
+#pragma unroll
+      for (int e = 0; e < PQ; ++e) acc[e] = fmul2(acc[e], make_float2(r, r));
+      m = z;
+    }
+    const float w = __expf(z - m);
+    s += w;
+    const float2 w2 = make_float2(w, w);
+#pragma unroll
+    for (int t = 0; t < PQ / 2; ++t) {
+      acc[2 * t] = ffma2(make_float2(bf_lo(v.a[t]), bf_lo(v.b[t])), w2, acc[2 * t]);
+      acc[2 * t + 1] = ffma2(make_float2(bf_hi(v.a[t]), bf_hi(v.b[t])), w2, acc[2 * t + 1]);
+    }
+  }
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Stream rows [0, nrows) through shared memory, kStages tiles of kTile rows
+// deep: every thread copies 16-byte chunks of one row (cp.async, L2 only),
+// 8 threads per row; row_of(rid) gives the cache row of list entry rid, and
+// visit(rid, k_row, v_row) consumes a staged row (8-lane group `grp` owns
+// tile row `grp`).  Each thread fetches its row index one tile before it
+// issues the copies, so the index load is off the critical path.
+template <int MODE, int PQ, typename RowOf, typename Visit>
+__device__ __forceinline__ void stream_rows(const Ctx& c, uint8_t* stages,
+                                            const __nv_bfloat16* kb, const __nv_bfloat16* vb,
+                                            int nrows, RowOf row_of, Visit visit) {
+  constexpr bool kK = MODE != kAttend, kV = MODE != kScore;
+  constexpr int D = PQ * 16;
+  constexpr int kRowB = D * 2;                        // bytes per row
+  constexpr int kChunks = kRowB / 16;                 // 16-byte chunks per row
+  constexpr int kStageB = kTile * kRowB * 2;          // K block then V block
+  const int grp = threadIdx.x >> 3, l8 = threadIdx.x & 7;
+  const int ntiles = (nrows + kTile - 1) / kTile;
+  auto fetch = [&](int tile) {
+    const int rid = tile * kTile + grp;
+    return (tile < ntiles && rid < nrows) ? row_of(rid) : -1;
+  };
+  auto issue = [&](int tile, int row) {
+    if (tile < ntiles && row >= 0) {
+      uint8_t* st = stages + (size_t)(tile % kStages) * kStageB + grp * kRowB;
+#pragma unroll
+      for (int ch = l8; ch < kChunks; ch += 8) {
+        if (kK) cp_async16(st + ch * 16, reinterpret_cast<const uint8_t*>(kb + (size_t)row * D) + ch * 16);
+        if (kV) cp_async16(st + kTile * kRowB + ch * 16,
+                           reinterpret_cast<const uint8_t*>(vb + (size_t)row * D) + ch * 16);
+      }
+    }
+    cp_async_commit();                                // one group per tile, even if empty
+  };
+#pragma unroll 1
+  for (int t = 0; t < kStages - 1; ++t) issue(t, fetch(t));
+  int ahead = fetch(kStages - 1);
+#pragma unroll 1
+  for (int tile = 0; tile < ntiles; ++tile) {
+    cp_async_wait<kStages - 2>();                     // this thread's copies of `tile` landed
+    __syncthreads();                                  // everyone's; stage (tile - 1) is free
+    issue(tile + kStages - 1, ahead);
+    ahead = fetch(tile + kStages);
+    const uint8_t* st = stages + (size_t)(tile % kStages) * kStageB;
+    const int rid = tile * kTile + grp;
+    if (rid < nrows)
+      visit(rid, reinterpret_cast<const __nv_bfloat16*>(st + grp * kRowB),
+            reinterpret_cast<const __nv_bfloat16*>(st + (kTile + grp) * kRowB));
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
+template <int PQ>
+__global__ void __launch_bounds__(kThreads, 3) lfps_finish_kernel(Ctx c, const __nv_bfloat16* q) {
+  extern __shared__ __align__(128) uint8_t stages[];      // kStages x [K tile | V tile]
   __shared__ FinishShared sh;
   const int s = blockIdx.x, tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int hw = tid >> 4, hl = tid & 15;
+  const int lane = tid & 31, warp = tid >> 5, l8 = tid & 7, grp = tid >> 3;
   const int b = s / c.Hq, h = (s % c.Hq) / c.G;
   const int n = c.n_ctx[b];
   const int S = c.S;
@@ -110,57 +262,67 @@ __global__ void __launch_bounds__(kThreads, 2) lfps_finish_kernel(Ctx c, const _
     if (tid == 0) { cnt[CNT_K] = 0; cnt[CNT_C2] = 0; cnt[CNT_CLAMP] = 0; }
     return;
   }
-
-  // ---- scores of the probe rows and the sinks ----------------------------------
   const int p = cnt[CNT_PROBE];
   const int* pidx = c.probe_idx + (size_t)s * c.list_cap;
   float* pz = c.probe_score + (size_t)s * c.list_cap;
-  const __nv_bfloat16* kbase = krow(c, b, h, 0);
-  float qf[PER];
+  const __nv_bfloat16* kb = krow(c, b, h, 0);
+  const __nv_bfloat16* vb = vrow(c, b, h, 0);
+  // q as (partial a, partial b) element pairs
+  float2 q2[PQ];
   {
-    const RawFrag<PER> qr = ld_frag<PER>(q + (size_t)s * c.d, hl);
-    unpack<PER>(qr, qf);
-  }
-  // warp-uniform trip count: half_fold shuffles over the full warp
-  for (int jw = warp * 2 * kNR; jw < p; jw += kHalves * kNR) {
-    const int j0 = jw + (hw & 1) * kNR;
-    RawFrag<PER> kr[kNR];
+    const Part<PQ> qp = ld_part<PQ>(q + (size_t)s * c.d, l8);
 #pragma unroll
-    for (int t = 0; t < kNR; ++t) {
-      const int j = j0 + t;
-      const int row = j < p ? __ldg(pidx + j) : 0;
-      kr[t] = ld_frag<PER>(kbase + (size_t)row * c.d, hl);
-    }
-#pragma unroll
-    for (int t = 0; t < kNR; ++t) {
-      const float z = half_fold(frag_dot<PER>(kr[t], qf));
-      if (hl == 0 && j0 + t < p) pz[j0 + t] = __fdiv_rn(z, c.sqrt_d_f32);
+    for (int t = 0; t < PQ / 2; ++t) {
+      q2[2 * t] = make_float2(bf_lo(qp.a[t]), bf_lo(qp.b[t]));
+      q2[2 * t + 1] = make_float2(bf_hi(qp.a[t]), bf_hi(qp.b[t]));
     }
   }
-  if (2 * warp < S) {                      // whole warps (S may be odd)
-    const RawFrag<PER> kr = ld_frag<PER>(kbase + (size_t)(hw < S ? hw : 0) * c.d, hl);
-    const float z = half_fold(frag_dot<PER>(kr, qf));
-    if (hl == 0 && hw < S) sh.sink_z[hw] = __fdiv_rn(z, c.sqrt_d_f32);
-  }
-  __syncthreads();
-
-  // ---- Top-k ---------------------------------------------------------------------
   int k = (int)rint(c.frac * (double)n);
   if (k < 1) k = 1;
   int* c2i = c.c2_idx + (size_t)s * c.list_cap;
   float* c2z = c.c2_score + (size_t)s * c.list_cap;
-  int k2;
+  const int k2 = k >= p ? p : k;
+  if (tid == 0) { cnt[CNT_K] = k; cnt[CNT_C2] = k2; }
+
+  Attn<PQ> at;
+  at.init();
+  int bad = 0;
+  float mxc = -INFINITY;                                // max C2 score of this group
+
   if (k >= p) {
-    for (int j = tid; j < p; j += kThreads) {
-      c2i[j] = pidx[j];
-      c2z[j] = pz[j];
-    }
-    k2 = p;
+    // ---- C2 = probe (the common case): score and attend in ONE pass ---------------------
+    for (int j = tid; j < p; j += kThreads) c2i[j] = pidx[j];
+    stream_rows<kFused, PQ>(
+        c, stages, kb, vb, S + p,
+        [&](int rid) { return rid < S ? rid : __ldg(pidx + rid - S); },
+        [&](int rid, const __nv_bfloat16* kr, const __nv_bfloat16* vr) {
+          const float z = row_score<PQ>(ld_part<PQ>(kr, l8), q2, c.sqrt_d_f32);
+          bad |= !isfinite(z);
+          if (rid >= S) {
+            mxc = fmaxf(mxc, z);
+            if (l8 == 0) c2z[rid - S] = z;
+          } else if (l8 == 0) {
+            sh.sink_z[rid] = z;
+          }
+          at.absorb(z, ld_part<PQ>(vr, l8));
+        });
   } else {
+    // ---- scores of the sinks and the probe rows -------------------------------------------
+    stream_rows<kScore, PQ>(
+        c, stages, kb, vb, S + p,
+        [&](int rid) { return rid < S ? rid : __ldg(pidx + rid - S); },
+        [&](int rid, const __nv_bfloat16* kr, const __nv_bfloat16*) {
+          const float z = row_score<PQ>(ld_part<PQ>(kr, l8), q2, c.sqrt_d_f32);
+          if (l8 == 0) {
+            if (rid < S) sh.sink_z[rid] = z;
+            else pz[rid - S] = z;
+          }
+        });
+    // ---- Top-k: MSB-first radix select of the k-th largest key ---------------------------
     uint32_t prefix = 0, mask = 0;
     int want = k;
     for (int shift = 24; shift >= 0; shift -= 8) {
-      if (tid < 256) sh.hist[tid] = 0;
+      sh.hist[tid] = 0;
       __syncthreads();
       for (int j = tid; j < p; j += kThreads) {
         const uint32_t key = score_key(pz[j]);
@@ -207,9 +369,9 @@ __global__ void __launch_bounds__(kThreads, 2) lfps_finish_kernel(Ctx c, const _
       const int gt = (j < p) && key > kth;
       const int eq = (j < p) && key == kth;
       int eq_tot, take_tot;
-      const int eq_before = scan512(eq, sh.warp_sums, &eq_tot);
+      const int eq_before = scan256(eq, sh.warp_sums, &eq_tot);
       const int take = gt || (eq && eq_seen + eq_before < need_eq);
-      const int pos = scan512(take, sh.warp_sums, &take_tot);
+      const int pos = scan256(take, sh.warp_sums, &take_tot);
       if (take) {
         c2i[out_n + pos] = pidx[j];
         c2z[out_n + pos] = pz[j];
@@ -217,92 +379,98 @@ __global__ void __launch_bounds__(kThreads, 2) lfps_finish_kernel(Ctx c, const _
       out_n += take_tot;
       eq_seen += eq_tot;
     }
-    k2 = out_n;
+    __syncthreads();
+    // ---- attention over sinks u C2 ------------------------------------------------------
+    stream_rows<kAttend, PQ>(
+        c, stages, kb, vb, S + k2,
+        [&](int rid) { return rid < S ? rid : c2i[rid - S]; },
+        [&](int rid, const __nv_bfloat16*, const __nv_bfloat16* vr) {
+          const float z = rid < S ? sh.sink_z[rid] : c2z[rid - S];
+          bad |= !isfinite(z);
+          if (rid >= S) mxc = fmaxf(mxc, z);
+          at.absorb(z, ld_part<PQ>(vr, l8));
+        });
   }
-  if (tid == 0) { cnt[CNT_K] = k; cnt[CNT_C2] = k2; }
-  __syncthreads();
 
-  // ---- attention over sinks u C2: per-half online softmax ----------------------------
+  // ---- merge the 32 group states into the output (stages reused as scratch) ----------
   {
-    float mrun = -INFINITY, srun = 0.0f;
-    float acc[PER];
+    constexpr int D = PQ * 16;
+    constexpr int kG = kThreads / D;                    // threads per output element
+    constexpr int kPer = kGroups8 / kG;                 // groups each of them merges
+    float* part = reinterpret_cast<float*>(stages);     // [kGroups8][D]
 #pragma unroll
-    for (int e = 0; e < PER; ++e) acc[e] = 0.0f;
-    const int tot = S + k2;
-    for (int j0 = hw * kNR; j0 < tot; j0 += kHalves * kNR) {
-      RawFrag<PER> vr[kNR];
-      float zz[kNR];
-#pragma unroll
-      for (int t = 0; t < kNR; ++t) {
-        const int j = j0 + t;
-        int row = 0;
-        zz[t] = -INFINITY;
-        if (j < S) { row = j; zz[t] = sh.sink_z[j]; }
-        else if (j < tot) { row = c2i[j - S]; zz[t] = c2z[j - S]; }   // written above
-        vr[t] = ld_frag<PER>(vrow(c, b, h, row), hl);
-      }
-      float bm = mrun;
-#pragma unroll
-      for (int t = 0; t < kNR; ++t) bm = fmaxf(bm, zz[t]);
-      const float rescale = mrun == -INFINITY ? 0.0f : expf(mrun - bm);
-      srun *= rescale;
-#pragma unroll
-      for (int e = 0; e < PER; ++e) acc[e] *= rescale;
-#pragma unroll
-      for (int t = 0; t < kNR; ++t) {
-        if (zz[t] == -INFINITY) continue;
-        const float w = expf(zz[t] - bm);
-        srun += w;
-        float vf[PER];
-        unpack<PER>(vr[t], vf);
-#pragma unroll
-        for (int e = 0; e < PER; ++e) acc[e] = fmaf(w, vf[e], acc[e]);
-      }
-      mrun = bm;
+    for (int e = 0; e < PQ; ++e) {
+      part[grp * D + l8 * PQ + e] = at.acc[e].x;
+      part[grp * D + (l8 + 8) * PQ + e] = at.acc[e].y;
     }
-#pragma unroll
-    for (int e = 0; e < PER; ++e) part_acc[hw * (PER * 16) + hl * PER + e] = acc[e];
-    if (hl == 0) { sh.part_m[hw] = mrun; sh.part_s[hw] = srun; }
+    if (l8 == 0) { sh.part_m[grp] = at.m; sh.part_s[grp] = at.s; }
     __syncthreads();
     float M = -INFINITY;
-#pragma unroll 4
-    for (int x = 0; x < kHalves; ++x) M = fmaxf(M, sh.part_m[x]);
-    float* out = c.out + (size_t)s * c.d;
-    for (int t = tid; t < c.d; t += kThreads) {
-      float num = 0.0f, den = 0.0f;
-      for (int x = 0; x < kHalves; ++x) {
-        if (sh.part_m[x] == -INFINITY) continue;
-        const float f = expf(sh.part_m[x] - M);
-        num = fmaf(f, part_acc[x * (PER * 16) + t], num);
-        den = fmaf(f, sh.part_s[x], den);
+#pragma unroll 8
+    for (int x = 0; x < kGroups8; ++x) M = fmaxf(M, sh.part_m[x]);
+    const int t = tid % D, g = tid / D;
+    float num = 0.0f, den = 0.0f;
+#pragma unroll
+    for (int xi = 0; xi < kPer; ++xi) {
+      const int x = g * kPer + xi;
+      if (sh.part_m[x] == -INFINITY) continue;
+      const float f = __expf(sh.part_m[x] - M);
+      num = fmaf(f, part[x * D + t], num);
+      den = fmaf(f, sh.part_s[x], den);
+    }
+    __syncthreads();                                     // part is reused below
+    part[g * D + t] = num;
+    part[kG * D + g * D + t] = den;
+    __syncthreads();
+    if (tid < D) {
+      float nsum = 0.0f, dsum = 0.0f;
+#pragma unroll
+      for (int x = 0; x < kG; ++x) {
+        nsum += part[x * D + tid];
+        dsum += part[kG * D + x * D + tid];
       }
-      out[t] = num / den;
+      c.out[(size_t)s * c.d + tid] = nsum / dsum;
     }
   }
 
-  // ---- data checks of the update (committed by k_update.cu) ----------------------------
-  int bad = 0;
-  for (int j = tid; j < k2; j += kThreads) bad |= !isfinite(c2z[j]);
-  if (tid < S) bad |= !isfinite(sh.sink_z[tid]);
+  // ---- data checks and the update weights u (committed by k_update.cu) ----------------
   if (__syncthreads_or(bad)) {
     if (tid == 0) set_err(c, s, LFPS_ERR_NONFINITE_SCORES);
     return;
   }
-  double mx = -INFINITY;
-  for (int j = tid; j < k2; j += kThreads) mx = fmax(mx, (double)c2z[j]);
-  for (int o = 16; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(LFPS_FULL, mx, o));
-  if (lane == 0) sh.red[warp] = mx;
+  for (int o = 16; o >= 1; o >>= 1) mxc = fmaxf(mxc, __shfl_xor_sync(LFPS_FULL, mxc, o));
+  if (lane == 0) sh.gmax[warp] = mxc;
   __syncthreads();
-  mx = sh.red[0];
-  for (int w = 1; w < kWarps; ++w) mx = fmax(mx, sh.red[w]);
-  __syncthreads();
+  float mf = sh.gmax[0];
+#pragma unroll
+  for (int w = 1; w < kWarps; ++w) mf = fmaxf(mf, sh.gmax[w]);
+  const double mx = (double)mf;
+  double e[kMaxE];
   double acc = 0.0;
-  if (tid < kCanon)
-    for (int j = tid; j < k2; j += kCanon) acc = cadd(acc, cexp(csub((double)c2z[j], mx)));
+#pragma unroll
+  for (int i = 0; i < kMaxE; ++i) {
+    const int j = tid + i * kCanon;
+    e[i] = j < k2 ? cexp(csub((double)c2z[j], mx)) : 0.0;
+    if (j < k2) acc = cadd(acc, e[i]);
+  }
+  for (int j = tid + kMaxE * kCanon; j < k2; j += kCanon) acc = cadd(acc, cexp(csub((double)c2z[j], mx)));
   const double tot = canon_sum(acc, sh.red);
+  double* uw = c.uw + (size_t)s * c.list_cap;
   acc = 0.0;
-  if (tid < kCanon)
-    for (int j = tid; j < k2; j += kCanon) acc = cadd(acc, cdiv(cexp(csub((double)c2z[j], mx)), tot));
+#pragma unroll
+  for (int i = 0; i < kMaxE; ++i) {
+    const int j = tid + i * kCanon;
+    if (j < k2) {
+      const double u = cdiv(e[i], tot);
+      uw[j] = u;
+      acc = cadd(acc, u);
+    }
+  }
+  for (int j = tid + kMaxE * kCanon; j < k2; j += kCanon) {
+    const double u = cdiv(cexp(csub((double)c2z[j], mx)), tot);
+    uw[j] = u;
+    acc = cadd(acc, u);
+  }
   const double wsum = canon_sum(acc, sh.red);
   if (tid == 0) {
     if (fabs(wsum - 1.0) > 1e-6) set_err(c, s, LFPS_ERR_WEIGHT_SUM);
@@ -311,10 +479,17 @@ __global__ void __launch_bounds__(kThreads, 2) lfps_finish_kernel(Ctx c, const _
   }
 }
 
-template <int PER>
+template <int PQ>
 cudaError_t launch_finish_d(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
-  const size_t smem = (size_t)kHalves * PER * 16 * sizeof(float);
-  lfps_finish_kernel<PER><<<c.NS, kThreads, smem, st>>>(c, q);
+  const size_t smem = (size_t)kStages * kTile * (c.d * 2) * 2;
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(lfps_finish_kernel<PQ>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  lfps_finish_kernel<PQ><<<c.NS, kThreads, smem, st>>>(c, q);
   return cudaGetLastError();
 }
 

@@ -134,40 +134,60 @@ __device__ __forceinline__ void seg_moments(const double* v, int vc, int lane, d
   m4 = warp_fold(cadd(cadd(p4[0], p4[1]), cadd(p4[2], p4[3])));
 }
 
-// canonical merge of the window's segments (pairwise tree over 512 leaves,
-// leaf i = segment i; lane l owns leaves [16 l, 16 l + 16))
-__device__ __noinline__ Mom item_merge(const double* bs, Window w, int lane) {
-  Mom stk[4];
-  Mom cur;
-#pragma unroll
-  for (int k = 0; k < kLeavesPerLane; ++k) {
-    const int i = lane * kLeavesPerLane + k;
-    cur = {0.0, 0.0, 0.0, 0.0, 0.0};
-    if (i < w.nseg) {
-      int a, vc;
-      segment(w, w.first + i, a, vc);
-      cur.n = (double)vc;
-      const double2* p = reinterpret_cast<const double2*>(bs + 4 * (size_t)(w.first + i));
-      const double2 x = __ldcg(p), y = __ldcg(p + 1);
-      cur.mu = x.x; cur.m2 = x.y; cur.m3 = y.x; cur.m4 = y.y;
-    }
-#pragma unroll
-    for (int l = 0; l < 4; ++l) {
-      if ((k >> l) & 1) {
-        cur = merge(stk[l], cur);
-      } else {
-        stk[l] = cur;
-        break;
-      }
-    }
+// canonical merge of one quarter of the window's segments: the pairwise tree
+// over 512 leaves (leaf i = segment i) is four 128-leaf subtrees merged
+// ((q0, q1), (q2, q3)); warp quarter qd owns leaves [128 qd, 128 qd + 128),
+// lane l the four leaves [128 qd + 4 l, + 4)
+__device__ __forceinline__ Mom leaf(const double* bs, const Window& w, int i) {
+  Mom r = {0.0, 0.0, 0.0, 0.0, 0.0};
+  if (i < w.nseg) {
+    int a, vc;
+    segment(w, w.first + i, a, vc);
+    r.n = (double)vc;
+    const double2* p = reinterpret_cast<const double2*>(bs + 4 * (size_t)(w.first + i));
+    const double2 x = __ldcg(p), y = __ldcg(p + 1);
+    r.mu = x.x; r.m2 = x.y; r.m3 = y.x; r.m4 = y.y;
   }
-  Mom acc = cur;
+  return r;
+}
+
+__device__ __noinline__ Mom quarter_merge(const double* bs, Window w, int qd, int lane) {
+  const int i0 = qd * 128 + lane * 4;
+  Mom acc = {0.0, 0.0, 0.0, 0.0, 0.0};
+  if (i0 < w.nseg) {
+    const Mom a = merge(leaf(bs, w, i0), leaf(bs, w, i0 + 1));
+    const Mom b = merge(leaf(bs, w, i0 + 2), leaf(bs, w, i0 + 3));
+    acc = merge(a, b);
+  }
 #pragma unroll
   for (int h = 1; h <= 16; h <<= 1) {
     const Mom o = shfl_mom(acc, h);
     acc = (lane & h) ? merge(o, acc) : merge(acc, o);
   }
   return acc;
+}
+
+// exclusive scan over the 256 threads of the block; total in *total
+__device__ __forceinline__ int block_scan(int v, int* warp_sums, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(LFPS_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  int before = 0, all = 0;
+#pragma unroll
+  for (int k = 0; k < kWarps; ++k) {
+    const int ws = warp_sums[k];
+    before += k < warp ? ws : 0;
+    all += ws;
+  }
+  __syncthreads();
+  *total = all;
+  return before + x - v;
 }
 
 // bits of C0 at positions j - delta for j in word w (|delta| <= 31)
@@ -194,13 +214,14 @@ __device__ __forceinline__ long long warp_max64(long long x) {
 struct SelectShared {
   int ntask, nhot;
   int task[kMaxTasks];
+  Mom part[2][4];
   double thr0[2], thrf[2];
   int deg[2];
-  int blk[512];
-  int red[4][kWarps];
+  int wsum[kWarps];
+  int red[3][kWarps];
 };
 
-__global__ void __launch_bounds__(kThreads) lfps_select_kernel(Ctx c) {
+__global__ void __launch_bounds__(kThreads, 3) lfps_select_kernel(Ctx c) {
   extern __shared__ uint32_t smem[];
   __shared__ SelectShared sh;
   const int s = blockIdx.x;
@@ -215,9 +236,10 @@ __global__ void __launch_bounds__(kThreads) lfps_select_kernel(Ctx c) {
   const int S = c.S;
   const int m = n - S;
   const int W = (m + 31) / 32;
-  const int nblk = (W + 31) / 32;
-  uint32_t* c0w = smem;            // [W] C0 bitmap (logical index)
-  uint32_t* pwords = smem + W;     // [W] probe bitmap
+  uint32_t* c0w = smem;                      // [W] C0 bitmap (logical index)
+  int* alist = reinterpret_cast<int*>(smem + W);  // [W] active word list
+  uint32_t* act = smem + 2 * W;              // [AW] active words (C0 word +- 1, tail)
+  const int AW = (W + 31) / 32;
   const double* ver = ver_row(c, s);
   const int base = c.sla_base[s];
   const double* sla = sla_row(c, s) + base;   // logical view
@@ -283,41 +305,48 @@ __global__ void __launch_bounds__(kThreads) lfps_select_kernel(Ctx c) {
     __syncthreads();
   }
 
-  // ---- B: thresholds (compute_thresholds) -------------------------------------------
-  if (warp < 2) {
-    const int t = warp;
-    double* thr = c.thr + (size_t)(2 * s + t) * 4;
-    if (c.exhaustive) {
-      if (lane == 0) {
-        sh.thr0[t] = -INFINITY; sh.thrf[t] = -INFINITY; sh.deg[t] = 0;
-        thr[0] = -INFINITY; thr[1] = -INFINITY; thr[2] = 0.0; thr[3] = NAN;
-      }
-    } else {
-      const Mom tot = item_merge(c.bw.bsum + (size_t)(2 * s + t) * nb * 4, t ? wsl : wv, lane);
-      if (lane == 0) {
-        const double sc = c.scale[s];
-        const double mean = cmul(tot.mu, sc);
-        const bool deg = cmul(cmul(tot.m2, sc), sc) < 1e-12;
-        double tau = NAN, kappa = NAN, thr0 = NAN;
-        if (!deg) {
-          kappa = cdiv(tot.m4, cmul(tot.m2, tot.m2));
-          if (kappa == 0.0) set_err(c, s, LFPS_ERR_KAPPA_ZERO);
-          tau = cdiv(cmul(c.a, mean), kappa);
-          thr0 = cdiv(tau, sc);
-        }
-        sh.thr0[t] = thr0;
-        sh.thrf[t] = cdiv(mean, sc);
-        sh.deg[t] = deg ? 1 : 0;
-        thr[0] = tau; thr[1] = mean; thr[2] = deg ? 1.0 : 0.0; thr[3] = kappa;
-      }
-    }
+  // ---- B: thresholds (compute_thresholds), 4 warps per table --------------------------
+  const int tB = warp >> 2, qd = warp & 3;
+  if (!c.exhaustive) {
+    const Mom q = quarter_merge(c.bw.bsum + (size_t)(2 * s + tB) * nb * 4, tB ? wsl : wv, qd, lane);
+    if (lane == 0) sh.part[tB][qd] = q;
   }
+  for (int w = tid; w < W; w += kThreads)
+    c0w[w] = !c.exhaustive ? 0u : ((w == W - 1 && (m & 31)) ? ((1u << (m & 31)) - 1u) : LFPS_FULL);
+  for (int w = tid; w < AW; w += kThreads)
+    act[w] = !c.exhaustive ? 0u : ((w == AW - 1 && (W & 31)) ? ((1u << (W & 31)) - 1u) : LFPS_FULL);
   if (tid == 0) {
     sh.nhot = 0;
     if (!c.exhaustive) c.bw.valid[s] = 1;
   }
-  for (int w = tid; w < W; w += kThreads)
-    c0w[w] = !c.exhaustive ? 0u : ((w == W - 1 && (m & 31)) ? ((1u << (m & 31)) - 1u) : LFPS_FULL);
+  __syncthreads();
+  if (tid == 0 && !c.exhaustive) {       // tail words are always active
+    for (int w = max(0, m - c.L) >> 5; w < W; ++w) act[w >> 5] |= 1u << (w & 31);
+  }
+  if (lane == 0 && qd == 0) {
+    const int t = tB;
+    double* thr = c.thr + (size_t)(2 * s + t) * 4;
+    if (c.exhaustive) {
+      sh.thr0[t] = -INFINITY; sh.thrf[t] = -INFINITY; sh.deg[t] = 0;
+      thr[0] = -INFINITY; thr[1] = -INFINITY; thr[2] = 0.0; thr[3] = NAN;
+    } else {
+      const Mom tot = merge(merge(sh.part[t][0], sh.part[t][1]), merge(sh.part[t][2], sh.part[t][3]));
+      const double sc = c.scale[s];
+      const double mean = cmul(tot.mu, sc);
+      const bool deg = cmul(cmul(tot.m2, sc), sc) < 1e-12;
+      double tau = NAN, kappa = NAN, thr0 = NAN;
+      if (!deg) {
+        kappa = cdiv(tot.m4, cmul(tot.m2, tot.m2));
+        if (kappa == 0.0) set_err(c, s, LFPS_ERR_KAPPA_ZERO);
+        tau = cdiv(cmul(c.a, mean), kappa);
+        thr0 = cdiv(tau, sc);
+      }
+      sh.thr0[t] = thr0;
+      sh.thrf[t] = cdiv(mean, sc);
+      sh.deg[t] = deg ? 1 : 0;
+      thr[0] = tau; thr[1] = mean; thr[2] = deg ? 1.0 : 0.0; thr[3] = kappa;
+    }
+  }
   __syncthreads();
 
   // ---- C: C0 from the hot blocks (select_initial) ----------------------------------
@@ -353,124 +382,107 @@ __global__ void __launch_bounds__(kThreads) lfps_select_kernel(Ctx c) {
           const int L = L0 + e * 32;
           const int sft = L & 31, wi = L >> 5;
           atomicOr(&c0w[wi], wd << sft);
-          if (sft && (wd >> (32 - sft))) atomicOr(&c0w[wi + 1], wd >> (32 - sft));
+          const bool hi = sft && (wd >> (32 - sft));
+          if (hi) atomicOr(&c0w[wi + 1], wd >> (32 - sft));
+          // the words whose dilation can see these bits become active
+          for (int x = max(0, wi - 1); x <= min(W - 1, wi + (hi ? 2 : 1)); ++x)
+            atomicOr(&act[x >> 5], 1u << (x & 31));
         }
       }
     }
     __syncthreads();
   }
 
-  // ---- D: C1 = F & dilate(C0); probe = C1 | tail -----------------------------------
-  const long long tfv = thr_bits(sh.thrf[0]);
-  const long long tfs = thr_bits(sh.thrf[1]);
-  const long long* verb = reinterpret_cast<const long long*>(ver);
-  const long long* slab = reinterpret_cast<const long long*>(sla);
-  const int tail_lo = max(0, m - c.L);
-  const uint32_t last_valid = (m & 31) ? ((1u << (m & 31)) - 1u) : LFPS_FULL;
-  int n0 = 0, n1 = 0, nd = 0;
-  for (int bk = warp; bk < nblk; bk += kWarps) {
-    const int w = bk * 32 + lane;
-    const bool in = w < W;
-    const uint32_t cur = in ? c0w[w] : 0u;
-    const uint32_t prev = (in && w > 0) ? c0w[w - 1] : 0u;
-    const uint32_t next = (in && w + 1 < W) ? c0w[w + 1] : 0u;
-    uint32_t dil = 0;
-    for (int k = 0; k < c.n_off; ++k) dil |= shifted(prev, cur, next, c.off[k]);
-    const uint32_t valid = !in ? 0u : (w == W - 1 ? last_valid : LFPS_FULL);
-    uint32_t cand = dil & valid;
-    uint32_t c1 = 0;
-    if (c.exhaustive) {
-      c1 = cand;
-    } else {
-      // F at the dilated positions, four positions (eight loads) in flight
-      while (cand) {
-        int pos[4];
+  // ---- D: C1 = F & dilate(C0); probe = C1 | tail, over the active words only ----
+  {
+    int na;
+    const uint32_t aw = tid < AW ? act[tid] : 0u;      // AW <= 256
+    int pos = block_scan(__popc(aw), sh.wsum, &na);
+    for (uint32_t x = aw; x; x &= x - 1) alist[pos++] = tid * 32 + __ffs(x) - 1;
+    if (c.flags & LFPS_FLAG_EXPORT_SETS) {
+      for (int w = tid; w < W; w += kThreads) {
+        c.bits[(size_t)(2 * s) * c.words + w] = c0w[w];   // C0
+        c.bits[(size_t)(2 * s + 1) * c.words + w] = 0u;   // C1 (active words below)
+      }
+    }
+    __syncthreads();
+    const long long tfv = thr_bits(sh.thrf[0]);
+    const long long tfs = thr_bits(sh.thrf[1]);
+    const long long* verb = reinterpret_cast<const long long*>(ver);
+    const long long* slab = reinterpret_cast<const long long*>(sla);
+    const int tail_lo = max(0, m - c.L);
+    const uint32_t last_valid = (m & 31) ? ((1u << (m & 31)) - 1u) : LFPS_FULL;
+    int* out = c.probe_idx + (size_t)s * c.list_cap;
+    int n0 = 0, n1 = 0, nd = 0, written = 0;
+    for (int r = 0; r < na; r += kThreads) {
+      const int j = r + tid;
+      const int w = j < na ? alist[j] : -1;
+      uint32_t pr = 0u;
+      if (w >= 0) {
+        const uint32_t cur = c0w[w];
+        const uint32_t prev = w > 0 ? c0w[w - 1] : 0u;
+        const uint32_t next = w + 1 < W ? c0w[w + 1] : 0u;
+        uint32_t dil = 0;
+        for (int k = 0; k < c.n_off; ++k) dil |= shifted(prev, cur, next, c.off[k]);
+        const uint32_t valid = w == W - 1 ? last_valid : LFPS_FULL;
+        uint32_t cand = dil & valid;
+        uint32_t c1 = 0;
+        if (c.exhaustive) {
+          c1 = cand;
+        } else {
+          // F at the dilated positions, four positions (eight loads) in flight
+          while (cand) {
+            int ps[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          pos[q] = cand ? __ffs(cand) - 1 : -1;
-          cand &= cand - 1;
-        }
-        long long xv[4], xs[4];
+            for (int q = 0; q < 4; ++q) {
+              ps[q] = cand ? __ffs(cand) - 1 : -1;
+              cand &= cand - 1;
+            }
+            long long xv[4], xs[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          xv[q] = xs[q] = -1ll;
-          if (pos[q] >= 0) {
-            const int i = w * 32 + pos[q];
-            xv[q] = __ldcg(verb + i);
-            xs[q] = __ldcg(slab + i);
+            for (int q = 0; q < 4; ++q) {
+              xv[q] = xs[q] = -1ll;
+              if (ps[q] >= 0) {
+                const int i = w * 32 + ps[q];
+                xv[q] = __ldcg(verb + i);
+                xs[q] = __ldcg(slab + i);
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (ps[q] >= 0 && (xv[q] > tfv || xs[q] > tfs)) c1 |= 1u << ps[q];
           }
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (pos[q] >= 0 && (xv[q] > tfv || xs[q] > tfs)) c1 |= 1u << pos[q];
+        uint32_t tail = 0;
+        const int j0 = w * 32;
+        if (j0 + 32 > tail_lo) tail = (LFPS_FULL << max(0, tail_lo - j0)) & valid;
+        pr = c1 | tail;
+        if (c.flags & LFPS_FLAG_EXPORT_SETS) c.bits[(size_t)(2 * s + 1) * c.words + w] = c1;
+        n0 += __popc(cur);
+        n1 += __popc(c1);
+        nd += __popc(cur & ~c1);
       }
+      int tot;
+      int at = written + block_scan(__popc(pr), sh.wsum, &tot);
+      for (; pr; pr &= pr - 1) out[at++] = S + w * 32 + __ffs(pr) - 1;
+      written += tot;
     }
-    uint32_t tail = 0;
-    const int j0 = w * 32;
-    if (in && j0 + 32 > tail_lo) tail = (LFPS_FULL << max(0, tail_lo - j0)) & valid;
-    const uint32_t pr = c1 | tail;
-    if (in) pwords[w] = pr;
-    if (in && (c.flags & LFPS_FLAG_EXPORT_SETS)) {
-      c.bits[(size_t)(2 * s) * c.words + w] = cur;      // C0
-      c.bits[(size_t)(2 * s + 1) * c.words + w] = c1;   // C1
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      n0 += __shfl_xor_sync(LFPS_FULL, n0, o);
+      n1 += __shfl_xor_sync(LFPS_FULL, n1, o);
+      nd += __shfl_xor_sync(LFPS_FULL, nd, o);
     }
-    n0 += __popc(cur);
-    n1 += __popc(c1);
-    nd += __popc(cur & ~c1);
-    int bc = __popc(pr);
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) bc += __shfl_xor_sync(LFPS_FULL, bc, o);
-    if (lane == 0) sh.blk[bk] = bc;
-  }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) {
-    n0 += __shfl_xor_sync(LFPS_FULL, n0, o);
-    n1 += __shfl_xor_sync(LFPS_FULL, n1, o);
-    nd += __shfl_xor_sync(LFPS_FULL, nd, o);
-  }
-  if (lane == 0) { sh.red[0][warp] = n0; sh.red[1][warp] = n1; sh.red[2][warp] = nd; }
-  __syncthreads();
-  if (warp == 0) {
-    int carry = 0;
-    for (int base2 = 0; base2 < nblk; base2 += 32) {
-      const int i = base2 + lane;
-      const int v = i < nblk ? sh.blk[i] : 0;
-      int x = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(LFPS_FULL, x, o);
-        if (lane >= o) x += y;
-      }
-      if (i < nblk) sh.blk[i] = carry + x - v;
-      carry += __shfl_sync(LFPS_FULL, x, 31);
-    }
-    if (lane == 0) {
+    if (lane == 0) { sh.red[0][warp] = n0; sh.red[1][warp] = n1; sh.red[2][warp] = nd; }
+    __syncthreads();
+    if (tid == 0) {
       int t0 = 0, t1 = 0, t3 = 0;
       for (int k = 0; k < kWarps; ++k) { t0 += sh.red[0][k]; t1 += sh.red[1][k]; t3 += sh.red[2][k]; }
       cnt[CNT_C0] = t0;
       cnt[CNT_C1] = t1;
-      cnt[CNT_PROBE] = carry;
+      cnt[CNT_PROBE] = written;
       cnt[CNT_DROP] = t3;
       cnt[CNT_BLOCKS] = sh.ntask + sh.nhot;
-    }
-  }
-  __syncthreads();
-  int* out = c.probe_idx + (size_t)s * c.list_cap;
-  for (int bk = warp; bk < nblk; bk += kWarps) {
-    const int w = bk * 32 + lane;
-    uint32_t pr = w < W ? pwords[w] : 0u;
-    const int pc = __popc(pr);
-    int x = pc;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(LFPS_FULL, x, o);
-      if (lane >= o) x += y;
-    }
-    int pos = sh.blk[bk] + x - pc;
-    while (pr) {
-      const int bit = __ffs(pr) - 1;
-      out[pos++] = S + w * 32 + bit;
-      pr &= pr - 1;
     }
   }
 }
@@ -478,7 +490,8 @@ __global__ void __launch_bounds__(kThreads) lfps_select_kernel(Ctx c) {
 }  // namespace
 
 cudaError_t launch_select(const Ctx& c, int m_max, cudaStream_t st) {
-  const size_t smem = 2 * (size_t)((m_max + 31) / 32) * 4;
+  const int W = (m_max + 31) / 32;
+  const size_t smem = (2 * (size_t)W + (W + 31) / 32) * 4;
   static bool set = false;
   if (!set) {
     cudaError_t e = cudaFuncSetAttribute(lfps_select_kernel,

@@ -3,9 +3,8 @@
 //
 // lfps_update_kernel restates ScoreTablePair.update / grow (tables.py:144-220)
 // on the linear slash window: u = canonical fp64 softmax of the selected
-// fp32 scores (engine.py:184, devmath.softmax_update; its max and
-// normaliser come from the finish kernel, which also ran the |sum u - 1|
-// check); scale *= r with renormalisation below 1e-120 (vertical [0, m) and
+// fp32 scores (engine.py:184, devmath.softmax_update), computed and checked
+// (|sum u - 1| <= 1e-6) by the finish kernel, read from uw; scale *= r with renormalisation below 1e-120 (vertical [0, m) and
 // slash logical [0, m] multiplied by the new scale); slash shift = base - 1
 // with the new logical slot 0 zeroed and the old top parked at logical m;
 // add = (u - 1/(2k)) / scale folded into both tables at C2; negative
@@ -52,9 +51,7 @@ __global__ void __launch_bounds__(kThreads) lfps_update_kernel(Ctx c) {
   for (int i = tid; i < 2 * kMaxDirtyWords; i += kThreads) (&dmark[0][0])[i] = 0u;
   const int k2 = c.counts[(size_t)s * CNT_N + CNT_C2];
   const int* idx = c.c2_idx + (size_t)s * c.list_cap;
-  const float* z = c.c2_score + (size_t)s * c.list_cap;
-  const double mx = c.bw.wstat[2 * (size_t)s];
-  const double tot = c.bw.wstat[2 * (size_t)s + 1];
+  const double* uw = c.uw + (size_t)s * c.list_cap;
   // decay with renormalisation (tables.py:167-169, 240-244)
   double sc = cmul(c.scale[s], c.r);
   bool renorm = false;
@@ -73,8 +70,7 @@ __global__ void __launch_bounds__(kThreads) lfps_update_kernel(Ctx c) {
   const double inv = cdiv(1.0, cmul(2.0, (double)k2));
   int clamps = 0;
   for (int j = tid; j < k2; j += kThreads) {
-    const double u = cdiv(cexp(csub((double)z[j], mx)), tot);
-    const double add = cdiv(csub(u, inv), sc);
+    const double add = cdiv(csub(uw[j], inv), sc);
     const int li = idx[j] - c.S;
     double v = cadd(ver[li], add);
     if (v < 0.0) { v = 0.0; ++clamps; }

@@ -106,6 +106,7 @@ int layout(const lfps_dims* d, lfps_ws_layout* L) {
   L->probe_score = take(NS * cap * 4);
   L->c2_idx = take(NS * cap * 4);
   L->c2_score = take(NS * cap * 4);
+  L->uw = take(NS * cap * 8);
   // bootstrap scratch (f64 logits) aliases probe_idx + probe_score
   L->scratch = L->probe_idx;
   L->bsum = take(NI * (size_t)L->nblk * 4 * 8);
@@ -160,6 +161,7 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
   c->probe_score = reinterpret_cast<float*>(base + L.probe_score);
   c->c2_idx = reinterpret_cast<int*>(base + L.c2_idx);
   c->c2_score = reinterpret_cast<float*>(base + L.c2_score);
+  c->uw = reinterpret_cast<double*>(base + L.uw);
   c->scratch = reinterpret_cast<double*>(base + L.scratch);
   c->bw.bsum = reinterpret_cast<double*>(base + L.bsum);
   c->bw.bmax = reinterpret_cast<double*>(base + L.bmax);
