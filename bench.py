@@ -344,6 +344,33 @@ def step_bytes(sess, cfg) -> dict:
             "k_rows_unit": float(k_rows.mean()), "v_rows_unit": float(v_rows.mean())}
 
 
+def phase_trace(sess, step, t, dev) -> dict:
+    """One extra (untimed) step with LFPS_FLAG_TRACE: mean per-CTA phase
+    durations of the select and finish kernels (clock64, us at the max SM
+    clock) and each kernel's span over all CTAs (globaltimer)."""
+    import torch
+    sess.trace = True
+    sess.trace_buf.zero_()
+    step(t)
+    torch.cuda.synchronize(dev)
+    sess.trace = False
+    tr = sess.trace_buf.cpu().double()[sess.bypass.flatten().cpu() == 0]
+    ghz = 1.965
+
+    def us(col):
+        return float(col.mean()) / ghz / 1e3
+
+    return {
+        "select": {"A_rebuild": us(tr[:, 1]), "B_merge": us(tr[:, 2] - tr[:, 1]),
+                   "C_hot": us(tr[:, 3] - tr[:, 2]), "D_probe": us(tr[:, 4] - tr[:, 3]),
+                   "cta_total": us(tr[:, 4]), "span": float(tr[:, 12].max() - tr[:, 15].min()) / 1e3},
+        "finish": {"rows": us(tr[:, 8]), "merge": us(tr[:, 9] - tr[:, 8]),
+                   "checks": us(tr[:, 10] - tr[:, 9]), "cta_total": us(tr[:, 10]),
+                   "span": float(tr[:, 14].max() - tr[:, 13].min()) / 1e3},
+        "note": "mean per-CTA phase time (clock64 at 1.965 GHz) and kernel span (globaltimer) "
+                "of one extra untimed step"}
+
+
 def run_ours(args, world, rank, local):
     import numpy as np
     import torch
@@ -410,6 +437,7 @@ def run_ours(args, world, rank, local):
     _lib.profile_enable(False)
     kt = _lib.profile_collect()
     sess.check_errors("profiled steps")
+    phases = phase_trace(sess, step, prof_base + prof_steps - 1, dev)
 
     # ---- algorithmic bytes per kernel (last profiled step) and the roofline ----
     peak, peak_src = measured_peaks()
@@ -514,6 +542,7 @@ def run_ours(args, world, rank, local):
                      "algorithmic_bytes_per_launch": dom_bytes,
                      "avg_launch_ms": dom_ms, "peak_source": peak_src},
         "kernel_ms": kernel_ms,
+        "phase_us": phases,
         "kernel_algorithmic_bytes": alg["kernels"],
         "step_algorithmic_bytes": int(alg["total"]),
         "step_achieved_GBps": alg["total"] / (ms * 1e-3) / 1e9,

@@ -91,6 +91,9 @@ typedef struct lfps_params {
 } lfps_params;
 
 /* lfps_params.flags */
+#define LFPS_FLAG_TRACE 2        /* per-session phase timestamps (clock64 deltas and
+                                    globaltimer) of the select and finish kernels
+                                    to ws.trace ([NS][16] int64) */
 #define LFPS_FLAG_EXPORT_SETS 1  /* write the C0 / C1 bitmaps of every session to
                                     ws.bits ([NS][2][words]: C0 then C1) */
 
@@ -141,6 +144,7 @@ typedef struct lfps_ws_layout {
   size_t dirty;       /* u32 [2 NS, dirty_words] blocks to rebuild */
   size_t valid;       /* i32 [NS] summaries of session s are current */
   size_t wstat;       /* f64 [NS, 2] max and normaliser of the update softmax */
+  size_t trace;       /* i64 [NS, 16] phase timestamps (LFPS_FLAG_TRACE) */
   int32_t nblk;       /* blocks per item (slash_cap / 512) */
   int32_t dirty_words;
   int32_t words;      /* bitmap words per (session, table, kind) */

@@ -17,6 +17,7 @@ from .errors import DeviceError
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "liblfps_b200.so")
 ABI_VERSION = 2
 FLAG_EXPORT_SETS = 1
+FLAG_TRACE = 2
 
 # per-session device error codes (include/lfps_b200.h)
 ERR_NAMES = {
@@ -62,7 +63,7 @@ class WsLayout(C.Structure):
                 ("counts", C.c_size_t), ("bits", C.c_size_t), ("probe_idx", C.c_size_t),
                 ("probe_score", C.c_size_t), ("c2_idx", C.c_size_t), ("c2_score", C.c_size_t), ("uw", C.c_size_t),
                 ("scratch", C.c_size_t), ("bsum", C.c_size_t), ("bmax", C.c_size_t),
-                ("dirty", C.c_size_t), ("valid", C.c_size_t), ("wstat", C.c_size_t),
+                ("dirty", C.c_size_t), ("valid", C.c_size_t), ("wstat", C.c_size_t), ("trace", C.c_size_t),
                 ("nblk", C.c_int32), ("dirty_words", C.c_int32), ("words", C.c_int32),
                 ("list_cap", C.c_int32)]
 

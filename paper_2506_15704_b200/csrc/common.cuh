@@ -35,6 +35,7 @@ struct Ctx {
   double r, eps, a, frac, sqrt_d;
   float sqrt_d_f32;
   int s, S, L, bypass_mode, exhaustive, n_off, flags;
+  int s_off, s_cnt;   // session range [s_off, s_off + s_cnt) of a per-session launch
   int off[16];
   // state
   const __nv_bfloat16* K;
@@ -63,6 +64,7 @@ struct Ctx {
   int* c2_idx;
   float* c2_score;
   double* uw;       // [NS, list_cap] update weights u of C2 (finish -> update)
+  long long* trace; // [NS, 16] phase timestamps (LFPS_FLAG_TRACE)
   double* scratch;
   BlockWs bw;
 };
@@ -80,6 +82,18 @@ __device__ __forceinline__ const __nv_bfloat16* vrow(const Ctx& c, int b, int h,
 __device__ __forceinline__ void set_err(const Ctx& c, int s, int code) {
   c.err[1 + s] = code;
   atomicExch(c.err, 1);
+}
+
+// phase timestamps (LFPS_FLAG_TRACE): slot k of session s = clock64() - t0;
+// slot 15 / 14 hold the globaltimer at select entry / finish exit
+__device__ __forceinline__ long long now_clk() { return clock64(); }
+__device__ __forceinline__ long long now_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_at(const Ctx& c, int s, int slot, long long t0) {
+  if ((c.flags & LFPS_FLAG_TRACE) && threadIdx.x == 0) c.trace[(size_t)s * 16 + slot] = now_clk() - t0;
 }
 
 __device__ __forceinline__ double* ver_row(const Ctx& c, int s) { return c.ver + (size_t)s * c.m_cap; }

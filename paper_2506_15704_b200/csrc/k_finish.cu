@@ -80,10 +80,20 @@ template <int PQ>
 __device__ __forceinline__ Part<PQ> ld_part(const __nv_bfloat16* row, int l8) {
   Part<PQ> r;
   const uint32_t* p = reinterpret_cast<const uint32_t*>(row);
+  if constexpr (PQ % 8 == 0) {            // 16-byte vector loads
 #pragma unroll
-  for (int t = 0; t < PQ / 2; ++t) {
-    r.a[t] = p[l8 * (PQ / 2) + t];
-    r.b[t] = p[(l8 + 8) * (PQ / 2) + t];
+    for (int t = 0; t < PQ / 2; t += 4) {
+      const uint4 x = *reinterpret_cast<const uint4*>(p + l8 * (PQ / 2) + t);
+      const uint4 y = *reinterpret_cast<const uint4*>(p + (l8 + 8) * (PQ / 2) + t);
+      r.a[t] = x.x; r.a[t + 1] = x.y; r.a[t + 2] = x.z; r.a[t + 3] = x.w;
+      r.b[t] = y.x; r.b[t + 1] = y.y; r.b[t + 2] = y.z; r.b[t + 3] = y.w;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < PQ / 2; ++t) {
+      r.a[t] = p[l8 * (PQ / 2) + t];
+      r.b[t] = p[(l8 + 8) * (PQ / 2) + t];
+    }
   }
   return r;
 }
@@ -251,7 +261,7 @@ template <int PQ>
 __global__ void __launch_bounds__(kThreads, 3) lfps_finish_kernel(Ctx c, const __nv_bfloat16* q) {
   extern __shared__ __align__(128) uint8_t stages[];      // kStages x [K tile | V tile]
   __shared__ FinishShared sh;
-  const int s = blockIdx.x, tid = threadIdx.x;
+  const int s = c.s_off + blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5, l8 = tid & 7, grp = tid >> 3;
   const int b = s / c.Hq, h = (s % c.Hq) / c.G;
   const int n = c.n_ctx[b];
@@ -263,6 +273,8 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_finish_kernel(Ctx c, const _
     return;
   }
   const int p = cnt[CNT_PROBE];
+  const long long t0 = now_clk();
+  if ((c.flags & LFPS_FLAG_TRACE) && tid == 0) c.trace[(size_t)s * 16 + 13] = now_ns();
   const int* pidx = c.probe_idx + (size_t)s * c.list_cap;
   float* pz = c.probe_score + (size_t)s * c.list_cap;
   const __nv_bfloat16* kb = krow(c, b, h, 0);
@@ -291,7 +303,6 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_finish_kernel(Ctx c, const _
 
   if (k >= p) {
     // ---- C2 = probe (the common case): score and attend in ONE pass ---------------------
-    for (int j = tid; j < p; j += kThreads) c2i[j] = pidx[j];
     stream_rows<kFused, PQ>(
         c, stages, kb, vb, S + p,
         [&](int rid) { return rid < S ? rid : __ldg(pidx + rid - S); },
@@ -306,6 +317,7 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_finish_kernel(Ctx c, const _
           }
           at.absorb(z, ld_part<PQ>(vr, l8));
         });
+    for (int j = tid; j < p; j += kThreads) c2i[j] = __ldg(pidx + j);
   } else {
     // ---- scores of the sinks and the probe rows -------------------------------------------
     stream_rows<kScore, PQ>(
@@ -392,6 +404,7 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_finish_kernel(Ctx c, const _
         });
   }
 
+  trace_at(c, s, 8, t0);
   // ---- merge the 32 group states into the output (stages reused as scratch) ----------
   {
     constexpr int D = PQ * 16;
@@ -433,6 +446,7 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_finish_kernel(Ctx c, const _
     }
   }
 
+  trace_at(c, s, 9, t0);
   // ---- data checks and the update weights u (committed by k_update.cu) ----------------
   if (__syncthreads_or(bad)) {
     if (tid == 0) set_err(c, s, LFPS_ERR_NONFINITE_SCORES);
@@ -476,6 +490,10 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_finish_kernel(Ctx c, const _
     if (fabs(wsum - 1.0) > 1e-6) set_err(c, s, LFPS_ERR_WEIGHT_SUM);
     c.bw.wstat[2 * (size_t)s] = mx;
     c.bw.wstat[2 * (size_t)s + 1] = tot;
+    if (c.flags & LFPS_FLAG_TRACE) {
+      c.trace[(size_t)s * 16 + 10] = now_clk() - t0;
+      c.trace[(size_t)s * 16 + 14] = now_ns();
+    }
   }
 }
 
@@ -489,7 +507,7 @@ cudaError_t launch_finish_d(const Ctx& c, const __nv_bfloat16* q, cudaStream_t s
     if (e != cudaSuccess) return e;
     set = true;
   }
-  lfps_finish_kernel<PQ><<<c.NS, kThreads, smem, st>>>(c, q);
+  lfps_finish_kernel<PQ><<<c.s_cnt, kThreads, smem, st>>>(c, q);
   return cudaGetLastError();
 }
 

@@ -32,7 +32,9 @@ __device__ __forceinline__ double row_dot(const __nv_bfloat16* row, const double
 
 __global__ void __launch_bounds__(kWarps * 32) lfps_gate_kernel(Ctx c, const __nv_bfloat16* q) {
   const int lane = threadIdx.x & 31;
-  const int s = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int sidx = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (sidx >= c.s_cnt) return;
+  const int s = c.s_off + sidx;
   if (s >= c.NS) return;
   const int b = s / c.Hq, qh = s % c.Hq, h = qh / c.G;
   const int n = c.n_ctx[b];
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kWarps * 32) lfps_gate_kernel(Ctx c, const __n
 }  // namespace
 
 cudaError_t launch_gate(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
-  const int blocks = (c.NS + kWarps - 1) / kWarps;
+  const int blocks = (c.s_cnt + kWarps - 1) / kWarps;
   lfps_gate_kernel<<<blocks, kWarps * 32, 0, st>>>(c, q);
   return cudaGetLastError();
 }

@@ -99,7 +99,7 @@ __device__ __forceinline__ void load_seg(const double* row, int a, int vc, int l
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     const int j = e * 32 + lane;
-    v[e] = j < vc ? __ldcg(row + a + j) : 0.0;
+    v[e] = j < vc ? __ldg(row + a + j) : 0.0;   // tables are read-only here: L1 path
   }
 }
 
@@ -221,10 +221,10 @@ struct SelectShared {
   int red[3][kWarps];
 };
 
-__global__ void __launch_bounds__(kThreads, 3) lfps_select_kernel(Ctx c) {
+__global__ void __launch_bounds__(kThreads, 4) lfps_select_kernel(Ctx c) {
   extern __shared__ uint32_t smem[];
   __shared__ SelectShared sh;
-  const int s = blockIdx.x;
+  const int s = c.s_off + blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int* cnt = c.counts + (size_t)s * CNT_N;
   if (c.bypass[s]) {
@@ -237,8 +237,8 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_select_kernel(Ctx c) {
   const int m = n - S;
   const int W = (m + 31) / 32;
   uint32_t* c0w = smem;                      // [W] C0 bitmap (logical index)
-  int* alist = reinterpret_cast<int*>(smem + W);  // [W] active word list
-  uint32_t* act = smem + 2 * W;              // [AW] active words (C0 word +- 1, tail)
+  uint16_t* alist = reinterpret_cast<uint16_t*>(smem + W);   // [W] active word list
+  uint32_t* act = smem + W + (W + 1) / 2;    // [AW] active words (C0 word +- 1, tail)
   const int AW = (W + 31) / 32;
   const double* ver = ver_row(c, s);
   const int base = c.sla_base[s];
@@ -246,6 +246,8 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_select_kernel(Ctx c) {
   const Window wv = make_window(0, m);
   const Window wsl = make_window(base, m);
   const int nb = c.bw.nblk;
+  const long long tclk0 = now_clk();
+  if ((c.flags & LFPS_FLAG_TRACE) && tid == 0) c.trace[(size_t)s * 16 + 15] = now_ns();
 
   // ---- A: rebuild dirty blocks --------------------------------------------------
   if (tid == 0) sh.ntask = 0;
@@ -305,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_select_kernel(Ctx c) {
     __syncthreads();
   }
 
+  trace_at(c, s, 1, tclk0);
   // ---- B: thresholds (compute_thresholds), 4 warps per table --------------------------
   const int tB = warp >> 2, qd = warp & 3;
   if (!c.exhaustive) {
@@ -349,6 +352,7 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_select_kernel(Ctx c) {
   }
   __syncthreads();
 
+  trace_at(c, s, 2, tclk0);
   // ---- C: C0 from the hot blocks (select_initial) ----------------------------------
   if (!c.exhaustive) {
     for (int t = 0; t < 2; ++t) {
@@ -393,12 +397,13 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_select_kernel(Ctx c) {
     __syncthreads();
   }
 
+  trace_at(c, s, 3, tclk0);
   // ---- D: C1 = F & dilate(C0); probe = C1 | tail, over the active words only ----
   {
     int na;
     const uint32_t aw = tid < AW ? act[tid] : 0u;      // AW <= 256
     int pos = block_scan(__popc(aw), sh.wsum, &na);
-    for (uint32_t x = aw; x; x &= x - 1) alist[pos++] = tid * 32 + __ffs(x) - 1;
+    for (uint32_t x = aw; x; x &= x - 1) alist[pos++] = (uint16_t)(tid * 32 + __ffs(x) - 1);
     if (c.flags & LFPS_FLAG_EXPORT_SETS) {
       for (int w = tid; w < W; w += kThreads) {
         c.bits[(size_t)(2 * s) * c.words + w] = c0w[w];   // C0
@@ -444,8 +449,8 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_select_kernel(Ctx c) {
               xv[q] = xs[q] = -1ll;
               if (ps[q] >= 0) {
                 const int i = w * 32 + ps[q];
-                xv[q] = __ldcg(verb + i);
-                xs[q] = __ldcg(slab + i);
+                xv[q] = __ldg(verb + i);
+                xs[q] = __ldg(slab + i);
               }
             }
 #pragma unroll
@@ -483,6 +488,10 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_select_kernel(Ctx c) {
       cnt[CNT_PROBE] = written;
       cnt[CNT_DROP] = t3;
       cnt[CNT_BLOCKS] = sh.ntask + sh.nhot;
+      if (c.flags & LFPS_FLAG_TRACE) {
+        c.trace[(size_t)s * 16 + 4] = now_clk() - tclk0;
+        c.trace[(size_t)s * 16 + 12] = now_ns();
+      }
     }
   }
 }
@@ -491,15 +500,18 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_select_kernel(Ctx c) {
 
 cudaError_t launch_select(const Ctx& c, int m_max, cudaStream_t st) {
   const int W = (m_max + 31) / 32;
-  const size_t smem = (2 * (size_t)W + (W + 31) / 32) * 4;
+  const size_t smem = ((size_t)W + (W + 1) / 2 + (W + 31) / 32) * 4;
   static bool set = false;
   if (!set) {
     cudaError_t e = cudaFuncSetAttribute(lfps_select_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(lfps_select_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
     set = true;
   }
-  lfps_select_kernel<<<c.NS, kThreads, smem, st>>>(c);
+  lfps_select_kernel<<<c.s_cnt, kThreads, smem, st>>>(c);
   return cudaGetLastError();
 }
 

@@ -114,6 +114,7 @@ int layout(const lfps_dims* d, lfps_ws_layout* L) {
   L->dirty = take(NI * (size_t)L->dirty_words * 4);
   L->valid = take(NS * 4);
   L->wstat = take(NS * 2 * 8);
+  L->trace = take(NS * 16 * 8);
   L->total_bytes = o;
   return LFPS_OK;
 }
@@ -131,7 +132,7 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
     return fail(LFPS_E_INVALID, "workspace too small: %zu < %zu bytes", ws->bytes, L.total_bytes);
   memset(c, 0, sizeof(*c));
   c->B = d->batch; c->Hkv = d->kv_heads; c->G = d->group; c->Hq = d->kv_heads * d->group;
-  c->NS = c->B * c->Hq; c->d = d->d; c->n_max = d->n_max; c->m_cap = d->m_cap;
+  c->NS = c->B * c->Hq; c->s_off = 0; c->s_cnt = c->NS; c->d = d->d; c->n_max = d->n_max; c->m_cap = d->m_cap;
   c->sla_cap = slash_cap(d->m_cap); c->sla_home = slash_home(d->m_cap);
   c->words = L.words; c->list_cap = L.list_cap;
   c->r = p->r; c->eps = p->epsilon; c->a = p->a; c->frac = p->k_fraction; c->sqrt_d = p->sqrt_d;
@@ -168,6 +169,7 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
   c->bw.dirty = reinterpret_cast<uint32_t*>(base + L.dirty);
   c->bw.valid = reinterpret_cast<int*>(base + L.valid);
   c->bw.wstat = reinterpret_cast<double*>(base + L.wstat);
+  c->trace = reinterpret_cast<long long*>(base + L.trace);
   c->bw.nblk = L.nblk;
   c->bw.dwords = L.dirty_words;
   return LFPS_OK;

@@ -31,7 +31,8 @@ from .errors import DeviceError, LfpsError
 CNT_C0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_BLOCKS = range(8)
 
 
-def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False) -> _lib.Params:
+def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False,
+                trace: bool = False) -> _lib.Params:
     err = cfg.device_limits_error()
     if err:
         raise ValueError(err)
@@ -47,7 +48,7 @@ def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False) -
     p.n_offsets = len(offs)
     for i, o in enumerate(offs):
         p.offsets[i] = o
-    p.flags = _lib.FLAG_EXPORT_SETS if export_sets else 0
+    p.flags = (_lib.FLAG_EXPORT_SETS if export_sets else 0) | (_lib.FLAG_TRACE if trace else 0)
     return p
 
 
@@ -88,6 +89,7 @@ class BatchedSession:
         self.lib = _lib.load_library()
         self.cfg = cfg
         self.export_sets = export_sets
+        self.trace = False          # LFPS_FLAG_TRACE: per-session phase timestamps
         self.B, self.Hkv, self.G = batch, kv_heads, group
         self.Hq = kv_heads * group
         self.NS = batch * self.Hq
@@ -146,12 +148,13 @@ class BatchedSession:
         self.probe_score = self._region(L.probe_score, torch.float32, (B, Hq, cap))
         self.c2_idx = self._region(L.c2_idx, torch.int32, (B, Hq, cap))
         self.c2_score = self._region(L.c2_score, torch.float32, (B, Hq, cap))
+        self.trace_buf = self._region(L.trace, torch.int64, (NS, 16))
 
     def _stream(self):
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
     def _params(self, k_fraction: float = 1.0) -> _lib.Params:
-        return make_params(self.cfg, k_fraction, self.export_sets)
+        return make_params(self.cfg, k_fraction, self.export_sets, self.trace)
 
     # -- bootstrap ----------------------------------------------------------
     def load_prefill(self, b: int, keys: torch.Tensor, values: torch.Tensor):
