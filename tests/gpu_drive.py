@@ -24,6 +24,7 @@ class Pair:
         B, Hkv, _, d = keys.shape
         G = weights.shape[2]
         self.cfg, self.B, self.Hkv, self.G, self.d, self.n0 = cfg, B, Hkv, G, d, n0
+        self.weights, self.finals = weights, finals
         self.sess = BatchedSession(cfg, B, Hkv, G, n_max=n_max or keys.shape[2] + 8,
                                    m_cap=m_cap, device="cuda", export_sets=True)
         for b in range(B):

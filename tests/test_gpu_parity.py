@@ -130,3 +130,41 @@ def test_exact_path_matches_oracle_and_overlap():
             want = lo.overlap_ratio(o.c2, exact_idx[0, qh, :int(exact_cnt[0, qh, 5])].cpu().numpy(),
                                     int(exact_cnt[0, qh, 5]))
             assert eta[0, qh] == pytest.approx(want, abs=0)
+
+
+@pytest.mark.parametrize("frac,dup", [(0.05, 0), (0.05, 700), (0.3, 0), (1.0, 0)])
+def test_exact_topk_ties_and_budgets(frac, dup):
+    """Exact path against topk_oracle (full stable sort, attention.py:100-113)
+    with planted exact ties: `dup` rows get the same key, so the k-th score
+    is shared by many rows and the lower-index rule decides (attention.py:
+    34-47); frac 1.0 selects every non-sink row."""
+    from oracle import lfps_oracle as lo
+    import gpu_drive
+    pair, K, V, Q = _gqa_pair(batch=1, kv_heads=2, n0=6000, steps=1, seed=9)
+    if dup:
+        rng = np.random.default_rng(5)
+        rows = rng.choice(np.arange(4, 6000), size=dup, replace=False)
+        for h in range(pair.Hkv):
+            K[0, h, rows] = K[0, h, rows[0]]
+        pair = _rebuild(pair, K, V)
+    sess = pair.sess
+    q = Q[:, :, :, 0]
+    qd = gpu_drive.bf16(q.reshape(1, -1, pair.d)).cuda()
+    res = sess.exact_topk_step(qd, frac)
+    torch.cuda.synchronize()
+    for h in range(pair.Hkv):
+        kv, trs, prs = pair.units[h]
+        for g in range(pair.G):
+            qh = h * pair.G + g
+            k = max(1, round(frac * kv.n))
+            want = lo.topk_oracle(kv, q[0, h, g], k, 4, "fp32")
+            np.testing.assert_array_equal(sess.c2_list(0, qh), want)
+            _, out = lo.exact_topk_step(kv, q[0, h, g], k, pair.cfg, score="fp32")
+            got = res.output[0, qh].cpu().numpy()
+            assert np.linalg.norm(got - out) / np.linalg.norm(out) <= 1e-5
+
+
+def _rebuild(pair, K, V):
+    """A fresh Pair over modified keys/values (same weights and finals)."""
+    from gpu_drive import Pair
+    return Pair(pair.cfg, K, V, pair.weights, pair.finals, pair.n0)
