@@ -151,7 +151,7 @@ __device__ __forceinline__ Mom leaf(const double* bs, const Window& w, int i) {
   return r;
 }
 
-__device__ __noinline__ Mom quarter_merge(const double* bs, Window w, int qd, int lane) {
+__device__ __forceinline__ Mom quarter_merge(const double* bs, Window w, int qd, int lane) {
   const int i0 = qd * 128 + lane * 4;
   Mom acc = {0.0, 0.0, 0.0, 0.0, 0.0};
   if (i0 < w.nseg) {
@@ -221,7 +221,7 @@ struct SelectShared {
   int red[3][kWarps];
 };
 
-__global__ void __launch_bounds__(kThreads, 4) lfps_select_kernel(Ctx c) {
+__global__ void __launch_bounds__(kThreads, 3) lfps_select_kernel(Ctx c) {
   extern __shared__ uint32_t smem[];
   __shared__ SelectShared sh;
   const int s = c.s_off + blockIdx.x;
@@ -378,20 +378,22 @@ __global__ void __launch_bounds__(kThreads, 4) lfps_select_kernel(Ctx c) {
       load_seg(t ? sla_row(c, s) : ver, a, vc, lane, v);
       const long long tb = thr_bits(sh.thr0[t]);
       const int L0 = a - w.lo;                         // logical index of element 0
+      uint32_t mine = 0;                               // lane e keeps ballot word e
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
         const uint32_t wd = __ballot_sync(LFPS_FULL, e * 32 + lane < vc &&
                                                          __double_as_longlong(v[e]) > tb);
-        if (lane == 0 && wd) {
-          const int L = L0 + e * 32;
-          const int sft = L & 31, wi = L >> 5;
-          atomicOr(&c0w[wi], wd << sft);
-          const bool hi = sft && (wd >> (32 - sft));
-          if (hi) atomicOr(&c0w[wi + 1], wd >> (32 - sft));
-          // the words whose dilation can see these bits become active
-          for (int x = max(0, wi - 1); x <= min(W - 1, wi + (hi ? 2 : 1)); ++x)
-            atomicOr(&act[x >> 5], 1u << (x & 31));
-        }
+        if (lane == e) mine = wd;
+      }
+      if (lane < 16 && mine) {                         // 16 lanes publish in parallel
+        const int L = L0 + lane * 32;
+        const int sft = L & 31, wi = L >> 5;
+        atomicOr(&c0w[wi], mine << sft);
+        const bool hi = sft && (mine >> (32 - sft));
+        if (hi) atomicOr(&c0w[wi + 1], mine >> (32 - sft));
+        // the words whose dilation can see these bits become active
+        for (int x = max(0, wi - 1); x <= min(W - 1, wi + (hi ? 2 : 1)); ++x)
+          atomicOr(&act[x >> 5], 1u << (x & 31));
       }
     }
     __syncthreads();
