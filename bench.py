@@ -488,6 +488,8 @@ def run_ours(args, world, rank, local):
     if recall_steps:
         etas, precs, ex_ms = [], [], []
         exact_kernel_ms = {}
+        sess.exact_topk_step(stream.q[0], frac)        # warm-up (module load); read-only
+        torch.cuda.synchronize(dev)
         base = args.warmup + args.steps + prof_steps + e2e_steps
         for t in range(base, base + recall_steps):
             torch.cuda.synchronize(dev)

@@ -145,6 +145,7 @@ typedef struct lfps_ws_layout {
   size_t valid;       /* i32 [NS] summaries of session s are current */
   size_t wstat;       /* f64 [NS, 2] max and normaliser of the update softmax */
   size_t trace;       /* i64 [NS, 16] phase timestamps (LFPS_FLAG_TRACE) */
+  size_t done;        /* u32 commit-kernel completion counter (kept at 0) */
   int32_t nblk;       /* blocks per item (slash_cap / 512) */
   int32_t dirty_words;
   int32_t words;      /* bitmap words per (session, table, kind) */

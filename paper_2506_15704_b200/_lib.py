@@ -64,6 +64,7 @@ class WsLayout(C.Structure):
                 ("probe_score", C.c_size_t), ("c2_idx", C.c_size_t), ("c2_score", C.c_size_t), ("uw", C.c_size_t),
                 ("scratch", C.c_size_t), ("bsum", C.c_size_t), ("bmax", C.c_size_t),
                 ("dirty", C.c_size_t), ("valid", C.c_size_t), ("wstat", C.c_size_t), ("trace", C.c_size_t),
+                ("done", C.c_size_t),
                 ("nblk", C.c_int32), ("dirty_words", C.c_int32), ("words", C.c_int32),
                 ("list_cap", C.c_int32)]
 

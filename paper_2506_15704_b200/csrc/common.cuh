@@ -65,6 +65,7 @@ struct Ctx {
   float* c2_score;
   double* uw;       // [NS, list_cap] update weights u of C2 (finish -> update)
   long long* trace; // [NS, 16] phase timestamps (LFPS_FLAG_TRACE)
+  unsigned* done;   // [1] CTAs finished in the commit kernel (last one bumps n_ctx)
   double* scratch;
   BlockWs bw;
 };
@@ -104,11 +105,9 @@ cudaError_t launch_gate(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
 cudaError_t launch_select(const Ctx& c, int m_max, cudaStream_t st);
 cudaError_t launch_topk(const Ctx& c, int implicit_base, cudaStream_t st);
 cudaError_t launch_attend(const Ctx& c, const __nv_bfloat16* q, int exact_mode, cudaStream_t st);
-cudaError_t launch_update(const Ctx& c, cudaStream_t st);
-cudaError_t launch_finish(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
-cudaError_t launch_append(const Ctx& c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new,
+cudaError_t launch_update(const Ctx& c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new,
                           cudaStream_t st);
-cudaError_t launch_commit(const Ctx& c, cudaStream_t st);
+cudaError_t launch_finish(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
 cudaError_t launch_boot_tables(const Ctx& c, const float* w, int s_begin, int count, int m0,
                                cudaStream_t st);
 cudaError_t launch_boot_stats(const Ctx& c, const __nv_bfloat16* q, int m_max, cudaStream_t st);

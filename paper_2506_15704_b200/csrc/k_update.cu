@@ -1,5 +1,5 @@
-// k_update.cu -- commit of a decode step: tracker update + grow (K6), KV
-// append and the context count.
+// k_update.cu -- commit of a decode step in ONE kernel: tracker update +
+// grow (K6), KV append and the context count.
 //
 // lfps_update_kernel restates ScoreTablePair.update / grow (tables.py:144-220)
 // on the linear slash window: u = canonical fp64 softmax of the selected
@@ -24,13 +24,22 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxDirtyWords = 32;
+constexpr int kUnroll = 4;               // C2 entries per thread in flight
 
-__global__ void __launch_bounds__(kThreads) lfps_update_kernel(Ctx c) {
+__device__ __forceinline__ void mark(uint32_t (*dmark)[kMaxDirtyWords], int t, int blk) {
+  atomicOr(&dmark[t][blk >> 5], 1u << (blk & 31));
+}
+
+// One CTA per session: the session's table update, the unit's KV append (by
+// the unit's first q-head), and -- in the last CTA to finish -- the context
+// count of every request (store.py:64-77 append, then engine.py:188-191).
+__global__ void __launch_bounds__(kThreads) lfps_update_kernel(Ctx c, const __nv_bfloat16* k_new,
+                                                               const __nv_bfloat16* v_new) {
   __shared__ uint32_t dmark[2][kMaxDirtyWords];
   __shared__ int clamp_red[kThreads / 32];
   const int s = blockIdx.x, tid = threadIdx.x;
-  if (c.err[0] != 0) return;
-  const int b = s / c.Hq;
+  if (c.err[0] != 0) return;                  // a failed step commits nothing
+  const int b = s / c.Hq, qh = s % c.Hq;
   const int n = c.n_ctx[b];
   const int m = n - c.S;
   double* ver = ver_row(c, s);
@@ -38,6 +47,16 @@ __global__ void __launch_bounds__(kThreads) lfps_update_kernel(Ctx c) {
   int base = c.sla_base[s];
   const int dw = c.bw.dwords;
   uint32_t* dirty = c.bw.dirty + (size_t)(2 * s) * dw;
+  // KV append of the unit's new row at position n (one session per unit)
+  if (qh % c.G == 0) {
+    const int u = b * c.Hkv + qh / c.G;
+    __nv_bfloat16* kd = c.Kw + ((size_t)u * c.n_max + n) * c.d;
+    __nv_bfloat16* vd = c.Vw + ((size_t)u * c.n_max + n) * c.d;
+    for (int t = tid; t < c.d; t += kThreads) {
+      kd[t] = k_new[(size_t)u * c.d + t];
+      vd[t] = v_new[(size_t)u * c.d + t];
+    }
+  }
   if (c.bypass[s]) {
     if (tid == 0) {                     // grow only (engine.py:133-137)
       ver[m] = 0.0;
@@ -46,87 +65,92 @@ __global__ void __launch_bounds__(kThreads) lfps_update_kernel(Ctx c) {
       dirty[bv >> 5] |= 1u << (bv & 31);
       dirty[dw + (bs >> 5)] |= 1u << (bs & 31);
     }
-    return;
+  } else {
+    for (int i = tid; i < 2 * kMaxDirtyWords; i += kThreads) (&dmark[0][0])[i] = 0u;
+    const int k2 = c.counts[(size_t)s * CNT_N + CNT_C2];
+    const int* idx = c.c2_idx + (size_t)s * c.list_cap;
+    const double* uw = c.uw + (size_t)s * c.list_cap;
+    // decay with renormalisation (tables.py:167-169, 240-244)
+    double sc = cmul(c.scale[s], c.r);
+    bool renorm = false;
+    if (sc < 1e-120) {
+      for (int i = tid; i < m; i += kThreads) ver[i] = cmul(ver[i], sc);
+      for (int i = tid; i <= m; i += kThreads) sla[base + i] = cmul(sla[base + i], sc);
+      sc = 1.0;
+      renorm = true;
+    }
+    // slash shift (tables.py:174-177)
+    base -= 1;
+    __syncthreads();
+    if (tid == 0) sla[base] = 0.0;
+    __syncthreads();
+    // residual fold and clamp (tables.py:179-199), kUnroll entries in flight
+    const double inv = cdiv(1.0, cmul(2.0, (double)k2));
+    int clamps = 0;
+    for (int j0 = tid; j0 < k2; j0 += kThreads * kUnroll) {
+      int li[kUnroll];
+      double u[kUnroll], v0[kUnroll], w0[kUnroll];
+#pragma unroll
+      for (int r = 0; r < kUnroll; ++r) {
+        const int j = j0 + r * kThreads;
+        li[r] = j < k2 ? idx[j] - c.S : -1;
+        u[r] = j < k2 ? uw[j] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < kUnroll; ++r) {
+        v0[r] = li[r] >= 0 ? ver[li[r]] : 0.0;
+        w0[r] = li[r] >= 0 ? sla[base + li[r]] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < kUnroll; ++r) {
+        if (li[r] < 0) continue;
+        const double add = cdiv(csub(u[r], inv), sc);
+        double v = cadd(v0[r], add);
+        if (v < 0.0) { v = 0.0; ++clamps; }
+        ver[li[r]] = v;
+        const int slot = base + li[r];
+        double w = cadd(w0[r], add);
+        if (w < 0.0) { w = 0.0; ++clamps; }
+        sla[slot] = w;
+        mark(dmark, 0, li[r] / kBlk);
+        mark(dmark, 1, slot / kBlk);
+      }
+    }
+    for (int o = 16; o >= 1; o >>= 1) clamps += __shfl_xor_sync(LFPS_FULL, clamps, o);
+    if ((tid & 31) == 0) clamp_red[tid >> 5] = clamps;
+    if (tid == 0) {
+      // grow (tables.py:202-220): vertical slot m, slash slot base (new logical 0)
+      mark(dmark, 0, m / kBlk);
+      mark(dmark, 1, base / kBlk);
+    }
+    __syncthreads();
+    if (tid < 2 * dw) {
+      const int t = tid / dw, w = tid % dw;
+      const uint32_t mk = dmark[t][w];
+      if (mk) dirty[t * dw + w] |= mk;
+    }
+    if (tid == 0) {
+      int tc = 0;
+      for (int w = 0; w < kThreads / 32; ++w) tc += clamp_red[w];
+      c.counts[(size_t)s * CNT_N + CNT_CLAMP] = tc;
+      c.clamp_count[s] += tc;
+      ver[m] = 0.0;                       // the parked slash value at logical m stays
+      c.scale[s] = sc;
+      c.sla_base[s] = base;
+      if (renorm) c.bw.valid[s] = 0;
+    }
   }
-  for (int i = tid; i < 2 * kMaxDirtyWords; i += kThreads) (&dmark[0][0])[i] = 0u;
-  const int k2 = c.counts[(size_t)s * CNT_N + CNT_C2];
-  const int* idx = c.c2_idx + (size_t)s * c.list_cap;
-  const double* uw = c.uw + (size_t)s * c.list_cap;
-  // decay with renormalisation (tables.py:167-169, 240-244)
-  double sc = cmul(c.scale[s], c.r);
-  bool renorm = false;
-  if (sc < 1e-120) {
-    for (int i = tid; i < m; i += kThreads) ver[i] = cmul(ver[i], sc);
-    for (int i = tid; i <= m; i += kThreads) sla[base + i] = cmul(sla[base + i], sc);
-    sc = 1.0;
-    renorm = true;
-  }
-  // slash shift (tables.py:174-177)
-  base -= 1;
+  // the last CTA publishes the new context lengths (every n_ctx reader is done)
   __syncthreads();
-  if (tid == 0) sla[base] = 0.0;
-  __syncthreads();
-  // residual fold and clamp (tables.py:179-199)
-  const double inv = cdiv(1.0, cmul(2.0, (double)k2));
-  int clamps = 0;
-  for (int j = tid; j < k2; j += kThreads) {
-    const double add = cdiv(csub(uw[j], inv), sc);
-    const int li = idx[j] - c.S;
-    double v = cadd(ver[li], add);
-    if (v < 0.0) { v = 0.0; ++clamps; }
-    ver[li] = v;
-    const int slot = base + li;
-    double w = cadd(sla[slot], add);
-    if (w < 0.0) { w = 0.0; ++clamps; }
-    sla[slot] = w;
-    const int bv = li / kBlk, bs = slot / kBlk;
-    atomicOr(&dmark[0][bv >> 5], 1u << (bv & 31));
-    atomicOr(&dmark[1][bs >> 5], 1u << (bs & 31));
-  }
-  for (int o = 16; o >= 1; o >>= 1) clamps += __shfl_xor_sync(LFPS_FULL, clamps, o);
-  if ((tid & 31) == 0) clamp_red[tid >> 5] = clamps;
   if (tid == 0) {
-    // grow (tables.py:202-220): vertical slot m, slash slot base (new logical 0)
-    const int bv = m / kBlk, bs = base / kBlk;
-    atomicOr(&dmark[0][bv >> 5], 1u << (bv & 31));
-    atomicOr(&dmark[1][bs >> 5], 1u << (bs & 31));
+    __threadfence();
+    const unsigned prev = atomicAdd(c.done, 1u);
+    if (prev == gridDim.x - 1) {
+      __threadfence();
+      for (int r = 0; r < c.B; ++r) c.n_ctx[r] += 1;
+      *c.done = 0u;
+    }
   }
-  __syncthreads();
-  if (tid < 2 * dw) {
-    const int t = tid / dw, w = tid % dw;
-    const uint32_t mk = dmark[t][w];
-    if (mk) dirty[t * dw + w] |= mk;
-  }
-  if (tid == 0) {
-    int tc = 0;
-    for (int w = 0; w < kThreads / 32; ++w) tc += clamp_red[w];
-    c.counts[(size_t)s * CNT_N + CNT_CLAMP] = tc;
-    c.clamp_count[s] += tc;
-    ver[m] = 0.0;                       // the parked slash value at logical m stays
-    c.scale[s] = sc;
-    c.sla_base[s] = base;
-    if (renorm) c.bw.valid[s] = 0;
-  }
-}
-
-// K/V append of the step's new rows at position n (store.py:64-77).
-__global__ void lfps_append_kernel(Ctx c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new) {
-  if (c.err[0] != 0) return;
-  const int u = blockIdx.x;
-  const int b = u / c.Hkv, h = u % c.Hkv;
-  const int n = c.n_ctx[b];
-  __nv_bfloat16* kd = c.Kw + (((size_t)b * c.Hkv + h) * c.n_max + n) * c.d;
-  __nv_bfloat16* vd = c.Vw + (((size_t)b * c.Hkv + h) * c.n_max + n) * c.d;
-  for (int t = threadIdx.x; t < c.d; t += blockDim.x) {
-    kd[t] = k_new[(size_t)u * c.d + t];
-    vd[t] = v_new[(size_t)u * c.d + t];
-  }
-}
-
-// Publish the new context length after every reader of n is done.
-__global__ void lfps_commit_kernel(Ctx c) {
-  if (c.err[0] != 0) return;
-  for (int b = threadIdx.x; b < c.B; b += blockDim.x) c.n_ctx[b] += 1;
 }
 
 __global__ void lfps_clear_err_kernel(Ctx c) {
@@ -136,19 +160,9 @@ __global__ void lfps_clear_err_kernel(Ctx c) {
 
 }  // namespace
 
-cudaError_t launch_update(const Ctx& c, cudaStream_t st) {
-  lfps_update_kernel<<<c.NS, kThreads, 0, st>>>(c);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_append(const Ctx& c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new,
+cudaError_t launch_update(const Ctx& c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new,
                           cudaStream_t st) {
-  lfps_append_kernel<<<c.B * c.Hkv, 128, 0, st>>>(c, k_new, v_new);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_commit(const Ctx& c, cudaStream_t st) {
-  lfps_commit_kernel<<<1, 256, 0, st>>>(c);
+  lfps_update_kernel<<<c.NS, kThreads, 0, st>>>(c, k_new, v_new);
   return cudaGetLastError();
 }
 

@@ -115,6 +115,7 @@ int layout(const lfps_dims* d, lfps_ws_layout* L) {
   L->valid = take(NS * 4);
   L->wstat = take(NS * 2 * 8);
   L->trace = take(NS * 16 * 8);
+  L->done = take(64);
   L->total_bytes = o;
   return LFPS_OK;
 }
@@ -170,6 +171,7 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
   c->bw.valid = reinterpret_cast<int*>(base + L.valid);
   c->bw.wstat = reinterpret_cast<double*>(base + L.wstat);
   c->trace = reinterpret_cast<long long*>(base + L.trace);
+  c->done = reinterpret_cast<unsigned*>(base + L.done);
   c->bw.nblk = L.nblk;
   c->bw.dwords = L.dirty_words;
   return LFPS_OK;
@@ -253,8 +255,8 @@ int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out) {
   return layout(dims, out);
 }
 
-int lfps_decode_launches(void) { return 7; }  // clear, gate, select, finish, update,
-                                             // append, commit
+int lfps_decode_launches(void) { return 5; }  // clear, gate, select, finish,
+                                             // update (with append and commit)
 
 int lfps_slash_capacity(const lfps_dims* dims) {
   int rc = check_dims(dims);
@@ -340,10 +342,8 @@ int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_sta
   LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
   LAUNCH_P("select", sm, lfps::launch_select(c, m_max, sm));
   LAUNCH_P("finish", sm, lfps::launch_finish(c, qb, sm));
-  LAUNCH_P("update", sm, lfps::launch_update(c, sm));
-  LAUNCH_P("append", sm, lfps::launch_append(c, static_cast<const __nv_bfloat16*>(k_new),
-                             static_cast<const __nv_bfloat16*>(v_new), sm));
-  LAUNCH_P("commit", sm, lfps::launch_commit(c, sm));
+  LAUNCH_P("update", sm, lfps::launch_update(c, static_cast<const __nv_bfloat16*>(k_new),
+                                              static_cast<const __nv_bfloat16*>(v_new), sm));
   return LFPS_OK;
 }
 
