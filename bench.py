@@ -51,7 +51,7 @@ UNIT = "us/step"
 def parse():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=tuple(CONFIGS), default="c4")
@@ -143,15 +143,20 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+            return
+        t0 = time.time()                   # the timed region starts once sampling runs
+        while time.time() - t0 < 5.0:
+            if os.path.exists(self.path) and os.path.getsize(self.path) > 0:
+                break
+            time.sleep(0.02)
 
     def stop(self) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
         self.proc.terminate()
         self.proc.wait()
         sm, smax, reasons = [], [], set()
@@ -384,9 +389,10 @@ def run_ours(args, world, rank, local):
     e2e_steps = 0 if args.profile_only else args.steps
     recall_steps = 0 if args.profile_only else args.recall_steps
     prof_steps = min(args.steps, 8)
-    T = args.warmup + args.steps + prof_steps + e2e_steps + recall_steps
+    T = args.warmup + args.steps + prof_steps + 1 + e2e_steps + recall_steps
+    T_in = min(T, 64)          # distinct synthetic step inputs, cycled
     cfg = LfpsConfig(d=d)
-    spec = GqaSpec(batch=b_local, kv_heads=hkv, group=group, d=d, n_prefill=ctx, steps=T,
+    spec = GqaSpec(batch=b_local, kv_heads=hkv, group=group, d=d, n_prefill=ctx, steps=T_in,
                    seed=42 + 7919 * b0)
     dev = torch.device("cuda", torch.cuda.current_device())
     t_setup = time.time()
@@ -396,6 +402,7 @@ def run_ours(args, world, rank, local):
     cuda_stream = torch.cuda.current_stream(dev)
 
     def step(t):
+        t %= T_in
         sess.decode_step(stream.q[t], stream.k_new[t], stream.v_new[t], frac)
 
     for t in range(args.warmup):
@@ -469,9 +476,9 @@ def run_ours(args, world, rank, local):
         base = args.warmup + args.steps + prof_steps
         e0.record(cuda_stream)
         for t in range(base, base + e2e_steps):
-            qd.copy_(qh[t], non_blocking=True)
-            kd.copy_(kh[t], non_blocking=True)
-            vd.copy_(vh[t], non_blocking=True)
+            qd.copy_(qh[t % T_in], non_blocking=True)
+            kd.copy_(kh[t % T_in], non_blocking=True)
+            vd.copy_(vh[t % T_in], non_blocking=True)
             sess.decode_step(qd, kd, vd, frac)
             out_h.copy_(sess.out, non_blocking=True)
         e1.record(cuda_stream)
@@ -499,7 +506,7 @@ def run_ours(args, world, rank, local):
             prof = t == base + recall_steps - 1
             if prof:
                 _lib.profile_enable(True)
-            sess.exact_topk_step(stream.q[t], frac)
+            sess.exact_topk_step(stream.q[t % T_in], frac)
             b.record(cuda_stream)
             if prof:
                 torch.cuda.synchronize(dev)
