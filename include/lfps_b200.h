@@ -91,6 +91,9 @@ typedef struct lfps_params {
 } lfps_params;
 
 /* lfps_params.flags */
+#define LFPS_FLAG_UNIT_FINISH 4  /* finish GQA units (G <= 4, d 128/256) over the
+                                    union of their probe rows with tensor-core
+                                    softmax.V (k_finish_unit.cu); opt-in */
 #define LFPS_FLAG_TRACE 2        /* per-session phase timestamps (clock64 deltas and
                                     globaltimer) of the select and finish kernels
                                     to ws.trace ([NS][16] int64) */

@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libl
 ABI_VERSION = 2
 FLAG_EXPORT_SETS = 1
 FLAG_TRACE = 2
+FLAG_UNIT_FINISH = 4
 
 # per-session device error codes (include/lfps_b200.h)
 ERR_NAMES = {

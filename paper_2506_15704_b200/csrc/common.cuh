@@ -108,6 +108,7 @@ cudaError_t launch_attend(const Ctx& c, const __nv_bfloat16* q, int exact_mode, 
 cudaError_t launch_update(const Ctx& c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new,
                           cudaStream_t st);
 cudaError_t launch_finish(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
+cudaError_t launch_finish_unit(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
 cudaError_t launch_boot_tables(const Ctx& c, const float* w, int s_begin, int count, int m0,
                                cudaStream_t st);
 cudaError_t launch_boot_stats(const Ctx& c, const __nv_bfloat16* q, int m_max, cudaStream_t st);

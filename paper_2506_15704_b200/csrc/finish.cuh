@@ -1,0 +1,266 @@
+// finish.cuh -- the per-session back half of a decode step (see k_finish.cu),
+// as a device function shared by the per-session and per-unit kernels.
+#pragma once
+
+#include "rows.cuh"
+
+namespace lfps {
+namespace fin {
+
+using namespace rows;
+
+struct FinishShared {
+  float sink_z[32];
+  float part_m[kGroups8];
+  float part_s[kGroups8];
+  float gmax[kWarps];
+  double red[16];
+  int warp_sums[kWarps];
+  unsigned hist[256];
+  unsigned sel_digit;
+  int sel_want;
+};
+
+// The whole back half of one session's step, run by a 256-thread CTA.
+// `stages` is kStages x [K tile | V tile] of dynamic shared memory.
+template <int PQ>
+__device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16* q, int s,
+                                               uint8_t* stages, FinishShared& sh) {
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, l8 = tid & 7, grp = tid >> 3;
+  const int b = s / c.Hq, h = (s % c.Hq) / c.G;
+  const int n = c.n_ctx[b];
+  const int S = c.S;
+  int* cnt = c.counts + (size_t)s * CNT_N;
+
+  if (c.bypass[s]) {
+    if (tid == 0) { cnt[CNT_K] = 0; cnt[CNT_C2] = 0; cnt[CNT_CLAMP] = 0; }
+    return;
+  }
+  const int p = cnt[CNT_PROBE];
+  const long long t0 = now_clk();
+  if ((c.flags & LFPS_FLAG_TRACE) && tid == 0) c.trace[(size_t)s * 16 + 13] = now_ns();
+  const int* pidx = c.probe_idx + (size_t)s * c.list_cap;
+  float* pz = c.probe_score + (size_t)s * c.list_cap;
+  const __nv_bfloat16* kb = krow(c, b, h, 0);
+  const __nv_bfloat16* vb = vrow(c, b, h, 0);
+  // q as (partial a, partial b) element pairs
+  float2 q2[PQ];
+  {
+    const Part<PQ> qp = ld_part<PQ>(q + (size_t)s * c.d, l8);
+#pragma unroll
+    for (int t = 0; t < PQ / 2; ++t) {
+      q2[2 * t] = make_float2(bf_lo(qp.a[t]), bf_lo(qp.b[t]));
+      q2[2 * t + 1] = make_float2(bf_hi(qp.a[t]), bf_hi(qp.b[t]));
+    }
+  }
+  int k = (int)rint(c.frac * (double)n);
+  if (k < 1) k = 1;
+  int* c2i = c.c2_idx + (size_t)s * c.list_cap;
+  float* c2z = c.c2_score + (size_t)s * c.list_cap;
+  const int k2 = k >= p ? p : k;
+  if (tid == 0) { cnt[CNT_K] = k; cnt[CNT_C2] = k2; }
+
+  Attn<PQ> at;
+  at.init();
+  int bad = 0;
+  float mxc = -INFINITY;                                // max C2 score of this group
+
+  if (k >= p) {
+    // ---- C2 = probe (the common case): score and attend in ONE pass ---------------------
+    stream_rows<kFused, PQ>(
+        c, stages, kb, vb, S + p,
+        [&](int rid) { return rid < S ? rid : __ldg(pidx + rid - S); },
+        [&](int rid, const __nv_bfloat16* kr, const __nv_bfloat16* vr) {
+          const float z = row_score<PQ>(ld_part<PQ>(kr, l8), q2, c.sqrt_d_f32);
+          bad |= !isfinite(z);
+          if (rid >= S) {
+            mxc = fmaxf(mxc, z);
+            if (l8 == 0) c2z[rid - S] = z;
+          } else if (l8 == 0) {
+            sh.sink_z[rid] = z;
+          }
+          at.absorb(z, ld_part<PQ>(vr, l8));
+        });
+    for (int j = tid; j < p; j += kThreads) c2i[j] = __ldg(pidx + j);
+  } else {
+    // ---- scores of the sinks and the probe rows -------------------------------------------
+    stream_rows<kScore, PQ>(
+        c, stages, kb, vb, S + p,
+        [&](int rid) { return rid < S ? rid : __ldg(pidx + rid - S); },
+        [&](int rid, const __nv_bfloat16* kr, const __nv_bfloat16*) {
+          const float z = row_score<PQ>(ld_part<PQ>(kr, l8), q2, c.sqrt_d_f32);
+          if (l8 == 0) {
+            if (rid < S) sh.sink_z[rid] = z;
+            else pz[rid - S] = z;
+          }
+        });
+    // ---- Top-k: MSB-first radix select of the k-th largest key ---------------------------
+    uint32_t prefix = 0, mask = 0;
+    int want = k;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      sh.hist[tid] = 0;
+      __syncthreads();
+      for (int j = tid; j < p; j += kThreads) {
+        const uint32_t key = score_key(pz[j]);
+        if ((key & mask) == prefix) atomicAdd(&sh.hist[(key >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (tid < 32) {
+        unsigned loc = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) loc += sh.hist[255 - 8 * tid - t];
+        unsigned incl = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(LFPS_FULL, incl, o);
+          if (tid >= o) incl += y;
+        }
+        const unsigned excl = incl - loc;
+        if (excl < (unsigned)want && incl >= (unsigned)want) {
+          unsigned cum = excl;
+          for (int t = 0; t < 8; ++t) {
+            const unsigned dgt = 255 - 8 * tid - t;
+            const unsigned hc = sh.hist[dgt];
+            if (cum + hc >= (unsigned)want) {
+              sh.sel_digit = dgt;
+              sh.sel_want = want - (int)cum;
+              break;
+            }
+            cum += hc;
+          }
+        }
+      }
+      __syncthreads();
+      prefix |= sh.sel_digit << shift;
+      mask |= 255u << shift;
+      want = sh.sel_want;
+      __syncthreads();
+    }
+    const uint32_t kth = prefix;
+    const int need_eq = want;
+    int out_n = 0, eq_seen = 0;
+    for (int t0 = 0; t0 < p; t0 += kThreads) {
+      const int j = t0 + tid;
+      const uint32_t key = j < p ? score_key(pz[j]) : 0u;
+      const int gt = (j < p) && key > kth;
+      const int eq = (j < p) && key == kth;
+      int eq_tot, take_tot;
+      const int eq_before = scan256(eq, sh.warp_sums, &eq_tot);
+      const int take = gt || (eq && eq_seen + eq_before < need_eq);
+      const int pos = scan256(take, sh.warp_sums, &take_tot);
+      if (take) {
+        c2i[out_n + pos] = pidx[j];
+        c2z[out_n + pos] = pz[j];
+      }
+      out_n += take_tot;
+      eq_seen += eq_tot;
+    }
+    __syncthreads();
+    // ---- attention over sinks u C2 ------------------------------------------------------
+    stream_rows<kAttend, PQ>(
+        c, stages, kb, vb, S + k2,
+        [&](int rid) { return rid < S ? rid : c2i[rid - S]; },
+        [&](int rid, const __nv_bfloat16*, const __nv_bfloat16* vr) {
+          const float z = rid < S ? sh.sink_z[rid] : c2z[rid - S];
+          bad |= !isfinite(z);
+          if (rid >= S) mxc = fmaxf(mxc, z);
+          at.absorb(z, ld_part<PQ>(vr, l8));
+        });
+  }
+
+  trace_at(c, s, 8, t0);
+  // ---- merge the 32 group states into the output (stages reused as scratch) ----------
+  {
+    constexpr int D = PQ * 16;
+    constexpr int kG = kThreads / D;                    // threads per output element
+    constexpr int kPer = kGroups8 / kG;                 // groups each of them merges
+    float* part = reinterpret_cast<float*>(stages);     // [kGroups8][D]
+#pragma unroll
+    for (int e = 0; e < PQ; ++e) {
+      part[grp * D + l8 * PQ + e] = at.acc[e].x;
+      part[grp * D + (l8 + 8) * PQ + e] = at.acc[e].y;
+    }
+    if (l8 == 0) { sh.part_m[grp] = at.m; sh.part_s[grp] = at.s; }
+    __syncthreads();
+    float M = -INFINITY;
+#pragma unroll 8
+    for (int x = 0; x < kGroups8; ++x) M = fmaxf(M, sh.part_m[x]);
+    const int t = tid % D, g = tid / D;
+    float num = 0.0f, den = 0.0f;
+#pragma unroll
+    for (int xi = 0; xi < kPer; ++xi) {
+      const int x = g * kPer + xi;
+      if (sh.part_m[x] == -INFINITY) continue;
+      const float f = __expf(sh.part_m[x] - M);
+      num = fmaf(f, part[x * D + t], num);
+      den = fmaf(f, sh.part_s[x], den);
+    }
+    __syncthreads();                                     // part is reused below
+    part[g * D + t] = num;
+    part[kG * D + g * D + t] = den;
+    __syncthreads();
+    if (tid < D) {
+      float nsum = 0.0f, dsum = 0.0f;
+#pragma unroll
+      for (int x = 0; x < kG; ++x) {
+        nsum += part[x * D + tid];
+        dsum += part[kG * D + x * D + tid];
+      }
+      c.out[(size_t)s * c.d + tid] = nsum / dsum;
+    }
+  }
+
+  trace_at(c, s, 9, t0);
+  // ---- data checks and the update weights u (committed by k_update.cu) ----------------
+  if (__syncthreads_or(bad)) {
+    if (tid == 0) set_err(c, s, LFPS_ERR_NONFINITE_SCORES);
+    return;
+  }
+  for (int o = 16; o >= 1; o >>= 1) mxc = fmaxf(mxc, __shfl_xor_sync(LFPS_FULL, mxc, o));
+  if (lane == 0) sh.gmax[warp] = mxc;
+  __syncthreads();
+  float mf = sh.gmax[0];
+#pragma unroll
+  for (int w = 1; w < kWarps; ++w) mf = fmaxf(mf, sh.gmax[w]);
+  const double mx = (double)mf;
+  double e[kMaxE];
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < kMaxE; ++i) {
+    const int j = tid + i * kCanon;
+    e[i] = j < k2 ? cexp(csub((double)c2z[j], mx)) : 0.0;
+    if (j < k2) acc = cadd(acc, e[i]);
+  }
+  for (int j = tid + kMaxE * kCanon; j < k2; j += kCanon) acc = cadd(acc, cexp(csub((double)c2z[j], mx)));
+  const double tot = canon_sum(acc, sh.red);
+  double* uw = c.uw + (size_t)s * c.list_cap;
+  acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < kMaxE; ++i) {
+    const int j = tid + i * kCanon;
+    if (j < k2) {
+      const double u = cdiv(e[i], tot);
+      uw[j] = u;
+      acc = cadd(acc, u);
+    }
+  }
+  for (int j = tid + kMaxE * kCanon; j < k2; j += kCanon) {
+    const double u = cdiv(cexp(csub((double)c2z[j], mx)), tot);
+    uw[j] = u;
+    acc = cadd(acc, u);
+  }
+  const double wsum = canon_sum(acc, sh.red);
+  if (tid == 0) {
+    if (fabs(wsum - 1.0) > 1e-6) set_err(c, s, LFPS_ERR_WEIGHT_SUM);
+    c.bw.wstat[2 * (size_t)s] = mx;
+    c.bw.wstat[2 * (size_t)s + 1] = tot;
+    if (c.flags & LFPS_FLAG_TRACE) {
+      c.trace[(size_t)s * 16 + 10] = now_clk() - t0;
+      c.trace[(size_t)s * 16 + 14] = now_ns();
+    }
+  }
+}
+
+}  // namespace fin
+}  // namespace lfps

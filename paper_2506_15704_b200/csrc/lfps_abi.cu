@@ -6,6 +6,7 @@
 // Algorithm 1 (engine.py:97-201).
 #include <cstdio>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <cmath>
 #include <mutex>
@@ -341,7 +342,14 @@ int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_sta
   LAUNCH_P("clear_err", sm, lfps::launch_clear_err(c, sm));
   LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
   LAUNCH_P("select", sm, lfps::launch_select(c, m_max, sm));
-  LAUNCH_P("finish", sm, lfps::launch_finish(c, qb, sm));
+  // LFPS_FLAG_UNIT_FINISH: GQA units of <= 4 q-heads (d 128 / 256) finish per
+  // unit over the union of their probe rows (tensor-core softmax.V); measured
+  // slower than the per-session kernel at C4 (2 CTAs/SM), so
+  // it is opt-in
+  const bool per_unit = (c.flags & LFPS_FLAG_UNIT_FINISH) && (c.G <= 4) &&
+                        (c.d == 128 || c.d == 256);
+  if (per_unit) LAUNCH_P("finish", sm, lfps::launch_finish_unit(c, qb, sm));
+  else LAUNCH_P("finish", sm, lfps::launch_finish(c, qb, sm));
   LAUNCH_P("update", sm, lfps::launch_update(c, static_cast<const __nv_bfloat16*>(k_new),
                                               static_cast<const __nv_bfloat16*>(v_new), sm));
   return LFPS_OK;

@@ -32,7 +32,7 @@ CNT_C0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_BLOCKS = rang
 
 
 def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False,
-                trace: bool = False) -> _lib.Params:
+                trace: bool = False, unit_finish: bool = False) -> _lib.Params:
     err = cfg.device_limits_error()
     if err:
         raise ValueError(err)
@@ -48,7 +48,8 @@ def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False,
     p.n_offsets = len(offs)
     for i, o in enumerate(offs):
         p.offsets[i] = o
-    p.flags = (_lib.FLAG_EXPORT_SETS if export_sets else 0) | (_lib.FLAG_TRACE if trace else 0)
+    p.flags = ((_lib.FLAG_EXPORT_SETS if export_sets else 0) | (_lib.FLAG_TRACE if trace else 0)
+               | (_lib.FLAG_UNIT_FINISH if unit_finish else 0))
     return p
 
 
@@ -90,6 +91,7 @@ class BatchedSession:
         self.cfg = cfg
         self.export_sets = export_sets
         self.trace = False          # LFPS_FLAG_TRACE: per-session phase timestamps
+        self.unit_finish = False    # LFPS_FLAG_UNIT_FINISH: per-unit finish kernel
         self.B, self.Hkv, self.G = batch, kv_heads, group
         self.Hq = kv_heads * group
         self.NS = batch * self.Hq
@@ -154,7 +156,7 @@ class BatchedSession:
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
     def _params(self, k_fraction: float = 1.0) -> _lib.Params:
-        return make_params(self.cfg, k_fraction, self.export_sets, self.trace)
+        return make_params(self.cfg, k_fraction, self.export_sets, self.trace, self.unit_finish)
 
     # -- bootstrap ----------------------------------------------------------
     def load_prefill(self, b: int, keys: torch.Tensor, values: torch.Tensor):

@@ -168,3 +168,19 @@ def _rebuild(pair, K, V):
     """A fresh Pair over modified keys/values (same weights and finals)."""
     from gpu_drive import Pair
     return Pair(pair.cfg, K, V, pair.weights, pair.finals, pair.n0)
+
+
+@pytest.mark.parametrize("unit", [True, False])
+@pytest.mark.parametrize("group,d", [(4, 128), (2, 128), (1, 256)])
+def test_unit_finish_shapes_bit_exact(group, d, unit):
+    """The per-unit finish (union of a unit's probe rows, tensor-core softmax.V)
+    against the oracle for the G and d it serves, over several steps with
+    mixed bypassed and Top-k sessions: 1% makes |probe| > k for some sessions
+    (per-session path inside the unit CTA), 5% keeps C2 = probe (union path)."""
+    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, group=group, d=d, n0=2500, steps=6, seed=21)
+    pair.sess.unit_finish = unit
+    n0 = pair.n0
+    for t in range(6):
+        frac = 0.05 if t % 3 else 0.01
+        res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], frac)
+        pair.compare_step(res, outs)
