@@ -56,11 +56,12 @@ def test_golden_trajectory_bit_exact(name):
                 np.testing.assert_array_equal(pair.sess.probe_list(0, gi), ref_probe[rec])
 
 
-def _gqa_pair(batch=2, kv_heads=2, group=4, n0=3000, steps=8, d=128, seed=3, **cfg_kw):
+def _gqa_pair(batch=2, kv_heads=2, group=4, n0=3000, steps=8, d=128, seed=3, spec_kw=None,
+              **cfg_kw):
     from paper_2506_15704_b200.config import LfpsConfig
     from paper_2506_15704_b200.workload import GqaSpec, gen_unit
     spec = GqaSpec(batch=batch, kv_heads=kv_heads, group=group, d=d, n_prefill=n0, steps=steps,
-                   seed=seed, slash_offsets=(64, 65), band_width=6)
+                   seed=seed, slash_offsets=(64, 65), band_width=6, **(spec_kw or {}))
     cfg = LfpsConfig(d=d, **cfg_kw)
     K, V, W, F, Q = [], [], [], [], []
     for b in range(batch):
@@ -184,3 +185,16 @@ def test_unit_finish_shapes_bit_exact(group, d, unit):
         frac = 0.05 if t % 3 else 0.01
         res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], frac)
         pair.compare_step(res, outs)
+
+
+def test_long_trajectory_crosses_slash_blocks():
+    """1100 steps: the slash window start crosses two 512-slot block
+    boundaries and the vertical window grows into new blocks, so the
+    persistent block summaries are rebuilt, re-merged and re-segmented many
+    times (k_select.cu).  Sets and outputs are compared every step against
+    the oracle, the tables every tenth step."""
+    pair, K, V, Q = _gqa_pair(batch=1, kv_heads=1, group=2, d=32, n0=700, steps=1100, seed=33)
+    n0 = pair.n0
+    for t in range(1100):
+        res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], 0.05)
+        pair.compare_step(res, outs, tables=(t % 10 == 0))
