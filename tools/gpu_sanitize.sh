@@ -1,0 +1,7 @@
+set -x
+mkdir -p gpurun_out
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 20 python tools/sanitize_run.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo $tool rc $?
+  tail -4 gpurun_out/sanitize_$tool.log
+done

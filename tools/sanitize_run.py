@@ -1,0 +1,34 @@
+"""Small end-to-end run for compute-sanitizer (memcheck / racecheck / synccheck):
+decode steps through the per-session and the per-unit finish, a Top-k (1%)
+step, and the exact path, on a B=1, 2 KV-head, G=4, n=2048 batch."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+from gpu_drive import Pair  # noqa: E402
+from paper_2506_15704_b200.config import LfpsConfig  # noqa: E402
+from paper_2506_15704_b200.workload import GqaSpec, gen_unit  # noqa: E402
+
+spec = GqaSpec(batch=1, kv_heads=2, group=4, d=128, n_prefill=2048, steps=6, seed=1,
+               slash_offsets=(64, 65), band_width=6)
+units = [gen_unit(spec, 0, h) for h in range(2)]
+K = np.stack([u.keys.float().numpy() for u in units])[None]
+V = np.stack([u.values.float().numpy() for u in units])[None]
+W = np.stack([u.weights.numpy() for u in units])[None]
+F = np.stack([u.final_query.float().numpy() for u in units])[None]
+Q = np.stack([u.queries.float().numpy() for u in units])[None]
+pair = Pair(LfpsConfig(d=128), K, V, W, F, 2048)
+for t in range(6):
+    pair.sess.unit_finish = t % 2 == 1
+    frac = 0.01 if t == 4 else 0.05
+    res, outs = pair.step(Q[:, :, :, t], K[:, :, 2048 + t], V[:, :, 2048 + t], frac)
+    pair.compare_step(res, outs)
+import gpu_drive  # noqa: E402
+qd = gpu_drive.bf16(Q[:, :, :, 0].reshape(1, -1, 128)).cuda()
+pair.sess.exact_topk_step(qd, 0.05)
+torch.cuda.synchronize()
+print("sanitize run ok")
