@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=6, help="steps per CPU worker sample")
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = all host cores")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-split", action="store_true",
+                    help="disable LFPS_FLAG_SPLIT (two session halves on two streams)")
+    ap.add_argument("--unit-finish", action="store_true", help="LFPS_FLAG_UNIT_FINISH")
     ap.add_argument("--profile-only", action="store_true",
                     help="short run for ncu: no e2e, recall or cpu legs")
     return ap.parse_args()
@@ -398,6 +401,8 @@ def run_ours(args, world, rank, local):
     t_setup = time.time()
     sess = BatchedSession(cfg, b_local, hkv, group, n_max=ctx + T + 8, device=dev)
     stream = populate(sess, spec)
+    sess.split = not args.no_split
+    sess.unit_finish = args.unit_finish
     setup_s = time.time() - t_setup
     cuda_stream = torch.cuda.current_stream(dev)
 

@@ -19,6 +19,7 @@ ABI_VERSION = 2
 FLAG_EXPORT_SETS = 1
 FLAG_TRACE = 2
 FLAG_UNIT_FINISH = 4
+FLAG_SPLIT = 8
 
 # per-session device error codes (include/lfps_b200.h)
 ERR_NAMES = {

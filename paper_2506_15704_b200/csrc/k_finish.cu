@@ -49,6 +49,9 @@ cudaError_t launch_finish_d(const Ctx& c, const __nv_bfloat16* q, cudaStream_t s
   if (!set) {
     cudaError_t e = cudaFuncSetAttribute(lfps_finish_kernel<PQ>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(lfps_finish_kernel<PQ>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
     if (e != cudaSuccess) return e;
     set = true;
   }

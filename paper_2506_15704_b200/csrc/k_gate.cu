@@ -30,7 +30,7 @@ __device__ __forceinline__ double row_dot(const __nv_bfloat16* row, const double
   return warp_fold(acc);
 }
 
-__global__ void __launch_bounds__(kWarps * 32) lfps_gate_kernel(Ctx c, const __nv_bfloat16* q) {
+__global__ void __launch_bounds__(kWarps * 32, 6) lfps_gate_kernel(Ctx c, const __nv_bfloat16* q) {
   const int lane = threadIdx.x & 31;
   const int sidx = blockIdx.x * kWarps + (threadIdx.x >> 5);
   if (sidx >= c.s_cnt) return;

@@ -24,7 +24,7 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxDirtyWords = 32;
-constexpr int kUnroll = 4;               // C2 entries per thread in flight
+constexpr int kUnroll = 2;               // C2 entries per thread in flight
 
 __device__ __forceinline__ void mark(uint32_t (*dmark)[kMaxDirtyWords], int t, int blk) {
   atomicOr(&dmark[t][blk >> 5], 1u << (blk & 31));
@@ -33,7 +33,7 @@ __device__ __forceinline__ void mark(uint32_t (*dmark)[kMaxDirtyWords], int t, i
 // One CTA per session: the session's table update, the unit's KV append (by
 // the unit's first q-head), and -- in the last CTA to finish -- the context
 // count of every request (store.py:64-77 append, then engine.py:188-191).
-__global__ void __launch_bounds__(kThreads) lfps_update_kernel(Ctx c, const __nv_bfloat16* k_new,
+__global__ void __launch_bounds__(kThreads, 6) lfps_update_kernel(Ctx c, const __nv_bfloat16* k_new,
                                                                const __nv_bfloat16* v_new) {
   __shared__ uint32_t dmark[2][kMaxDirtyWords];
   __shared__ int clamp_red[kThreads / 32];

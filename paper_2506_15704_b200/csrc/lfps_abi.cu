@@ -241,6 +241,34 @@ cudaEvent_t prof_event() {
     }                                                              \
   } while (0)
 
+// ---- internal streams for session-group concurrency (LFPS_FLAG_SPLIT) -------
+struct Pipe {
+  int dev = -1;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+};
+std::mutex g_pipe_mu;
+Pipe g_pipe[16];
+
+cudaError_t get_pipe(Pipe** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
+  std::lock_guard<std::mutex> g(g_pipe_mu);
+  Pipe& p = g_pipe[dev];
+  if (p.dev < 0) {
+    for (int i = 0; i < 2; ++i) {
+      if ((e = cudaStreamCreateWithFlags(&p.st[i], cudaStreamNonBlocking)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&p.join[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+    }
+    if ((e = cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+    p.dev = dev;
+  }
+  *out = &p;
+  return cudaSuccess;
+}
+
 }  // namespace
 
 extern "C" {
@@ -340,6 +368,28 @@ int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_sta
   cudaStream_t sm = static_cast<cudaStream_t>(stream);
   const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
   LAUNCH_P("clear_err", sm, lfps::launch_clear_err(c, sm));
+  if ((c.flags & LFPS_FLAG_SPLIT) && !g_prof_on && c.NS >= 256) {
+    // two session halves, each gate -> select -> finish on its own stream
+    Pipe* pp = nullptr;
+    LAUNCH(get_pipe(&pp));
+    LAUNCH(cudaEventRecord(pp->fork, sm));
+    const int half = (c.NS / 2 + 31) / 32 * 32;
+    for (int g = 0; g < 2; ++g) {
+      lfps::Ctx cg = c;
+      cg.s_off = g ? half : 0;
+      cg.s_cnt = g ? c.NS - half : half;
+      cudaStream_t gs = pp->st[g];
+      LAUNCH(cudaStreamWaitEvent(gs, pp->fork, 0));
+      LAUNCH(lfps::launch_gate(cg, qb, gs));
+      LAUNCH(lfps::launch_select(cg, m_max, gs));
+      LAUNCH(lfps::launch_finish(cg, qb, gs));
+      LAUNCH(cudaEventRecord(pp->join[g], gs));
+      LAUNCH(cudaStreamWaitEvent(sm, pp->join[g], 0));
+    }
+    LAUNCH_P("update", sm, lfps::launch_update(c, static_cast<const __nv_bfloat16*>(k_new),
+                                                static_cast<const __nv_bfloat16*>(v_new), sm));
+    return LFPS_OK;
+  }
   LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
   LAUNCH_P("select", sm, lfps::launch_select(c, m_max, sm));
   // LFPS_FLAG_UNIT_FINISH: GQA units of <= 4 q-heads (d 128 / 256) finish per

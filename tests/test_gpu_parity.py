@@ -198,3 +198,15 @@ def test_long_trajectory_crosses_slash_blocks():
     for t in range(1100):
         res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], 0.05)
         pair.compare_step(res, outs, tables=(t % 10 == 0))
+
+
+@pytest.mark.parametrize("split", [True, False])
+def test_split_streams_bit_exact(split):
+    """256 sessions (8 requests x 8 KV heads x 4): LFPS_FLAG_SPLIT runs the two
+    session halves on two internal streams; results are identical."""
+    pair, K, V, Q = _gqa_pair(batch=8, kv_heads=8, group=4, d=64, n0=700, steps=2, seed=41)
+    pair.sess.split = split
+    n0 = pair.n0
+    for t in range(2):
+        res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], 0.05)
+        pair.compare_step(res, outs, tables=(t == 1))
