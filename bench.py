@@ -498,7 +498,7 @@ def run_ours(args, world, rank, local):
     # ---- recall vs the exact full-scan path, and its device time ----
     recall = None
     if recall_steps:
-        etas, precs, ex_ms = [], [], []
+        etas, precs, ex_ms, errs_l, errs_x = [], [], [], [], []
         exact_kernel_ms = {}
         sess.exact_topk_step(stream.q[0], frac)        # warm-up (module load); read-only
         torch.cuda.synchronize(dev)
@@ -507,6 +507,7 @@ def run_ours(args, world, rank, local):
             torch.cuda.synchronize(dev)
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
+            full = sess.full_attention(stream.q[t % T_in])       # N4: full attention
             a.record(cuda_stream)
             prof = t == base + recall_steps - 1
             if prof:
@@ -519,11 +520,15 @@ def run_ours(args, world, rank, local):
                 exact_kernel_ms = {k: v[1] / max(1, v[0]) for k, v in _lib.profile_collect().items()}
             ex_idx = sess.c2_idx.clone()
             ex_cnt = sess.counts.clone()
+            ex_out = sess.out.clone()
             torch.cuda.synchronize(dev)
             ex_ms.append(a.elapsed_time(b))
             step(t)
             eta = sess.overlap(sess.c2_idx, sess.counts, ex_idx, ex_cnt)
             keep = sess.bypass == 0
+            fn = full.double().norm(dim=-1).clamp_min(1e-12)
+            errs_l.append(((sess.out.double() - full.double()).norm(dim=-1) / fn).flatten().cpu())
+            errs_x.append(((ex_out.double() - full.double()).norm(dim=-1) / fn).flatten().cpu())
             etas.append(eta[keep].cpu().numpy())
             # precision: share of the LFPS selection inside the exact Top-k
             c2n = sess.counts[..., CNT_C2].double()
@@ -538,7 +543,13 @@ def run_ours(args, world, rank, local):
                   "note": "eta = |C2 & I_exact| / k (attention.py:116-124); at 5% budget "
                           "|C2| = |probe| < k, so eta <= |probe| / k",
                   "exact_us_per_step": allmax(world, statistics.median(ex_ms[:-1] or ex_ms)) * 1e3,
-                  "exact_kernel_ms": exact_kernel_ms}
+                  "exact_kernel_ms": exact_kernel_ms,
+                  "output_error_vs_full": {
+                      "lfps_mean": float(torch.cat(errs_l).mean()),
+                      "exact_topk_mean": float(torch.cat(errs_x).mean()),
+                      "note": "relative L2 vs full softmax attention over every row "
+                              "(full_attention_oracle / output_error, attention.py:88-134), "
+                              "computed on the device"}}
 
     if rank != 0:
         return

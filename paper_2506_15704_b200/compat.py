@@ -242,6 +242,17 @@ def exact_topk_step(session: HeadSession, q, k_fraction: float):
     return sess.c2_list(0, 0).astype(np.int64), res.output[0, 0].double().cpu().numpy()
 
 
+def full_attention_oracle(q, session: HeadSession) -> AttentionOutput:
+    """Exact softmax attention over every stored position (attention.py:88-97),
+    on the device; q is a d-vector, the session supplies the rows."""
+    sess = session.device_session
+    d = session.config.d
+    out = sess.full_attention(_bf16(q, (d,), "q").reshape(1, 1, d).to(sess.device))
+    torch.cuda.synchronize(sess.device)
+    n = sess.n_host[0]
+    return AttentionOutput(out[0, 0].double().cpu().numpy(), np.arange(n, dtype=np.int64), None)
+
+
 def overlap_ratio(c, i_exact, k: int) -> float:
     """eta = |C2 cap I| / k (attention.py:116-124); a host metric."""
     if k < 1:

@@ -129,6 +129,7 @@ class BatchedSession:
         self.ws = _lib.Workspace(_ptr(self.ws_buf), self.layout.total_bytes)
         self._views()
         self.step_count = 0
+        self.tables_stale = False
 
     # -- workspace views ----------------------------------------------------
     def _region(self, off: int, dtype, shape):
@@ -236,6 +237,8 @@ class BatchedSession:
         raises it."""
         if not 0.0 < k_fraction <= 1.0:
             raise ValueError(f"k_fraction must be in (0, 1], got {k_fraction}")
+        if self.tables_stale:
+            raise ValueError("tables out of sync with the KV store (append_rows was used)")
         for name, t, shape in (("q", q, (self.B, self.Hq, self.d)),
                                ("new_key", k_new, (self.B, self.Hkv, self.d)),
                                ("new_value", v_new, (self.B, self.Hkv, self.d))):
@@ -254,6 +257,24 @@ class BatchedSession:
         self.n_host = [n + 1 for n in self.n_host]
         self.step_count += 1
         return self.result()
+
+    def append_rows(self, k_new: torch.Tensor, v_new: torch.Tensor):
+        """Append one K/V row per unit WITHOUT an LFPS step (store.append,
+        store.py:64-77): the replay of the exact and full-attention reference
+        modes (replay.run_trace).  The tracker tables no longer match the
+        context afterwards, so further LFPS steps on this session raise."""
+        for name, t in (("new_key", k_new), ("new_value", v_new)):
+            if tuple(t.shape) != (self.B, self.Hkv, self.d) or t.dtype != torch.bfloat16:
+                raise ValueError(f"{name} must be bf16 [{self.B}, {self.Hkv}, {self.d}]")
+        for b in range(self.B):
+            n = self.n_host[b]
+            if n >= self.n_max:
+                raise ValueError(f"request {b}: KV cache full")
+            self.k_cache[b, :, n].copy_(k_new[b])
+            self.v_cache[b, :, n].copy_(v_new[b])
+        self.n_ctx += 1
+        self.n_host = [n + 1 for n in self.n_host]
+        self.tables_stale = True
 
     def rollback_host_count(self):
         """Undo the host mirror advance after a step that committed nothing."""
@@ -278,6 +299,14 @@ class BatchedSession:
             C.byref(self.ws), C.c_void_p(q.contiguous().data_ptr()), n_host, self._stream()),
             "exact_topk_step")
         return self.result()
+
+    def full_attention(self, q: torch.Tensor) -> torch.Tensor:
+        """Exact softmax attention over every cached row of every session
+        (full_attention_oracle, attention.py:88-97) on the device: the exact
+        path with k_fraction = 1 selects all non-sink rows and attends them
+        jointly with the sinks.  Returns a copy of the f32 [B, Hq, d] output;
+        the workspace lists and counts are overwritten (like exact_topk_step)."""
+        return self.exact_topk_step(q, 1.0).output.clone()
 
     def overlap(self, sel_idx: torch.Tensor, sel_counts: torch.Tensor,
                 exact_idx: torch.Tensor, exact_counts: torch.Tensor) -> torch.Tensor:

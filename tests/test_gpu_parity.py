@@ -210,3 +210,23 @@ def test_split_streams_bit_exact(split):
     for t in range(2):
         res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], 0.05)
         pair.compare_step(res, outs, tables=(t == 1))
+
+
+def test_full_attention_matches_oracle():
+    """N4: full softmax attention over every row on the device against the
+    reference's full_attention_oracle arithmetic (fp64, attention.py:88-97)."""
+    import math
+    import gpu_drive
+    pair, K, V, Q = _gqa_pair(batch=1, kv_heads=2, n0=3000, steps=1, seed=13)
+    q = Q[:, :, :, 0]
+    out = pair.sess.full_attention(gpu_drive.bf16(q.reshape(1, -1, pair.d)).cuda()).cpu().numpy()
+    for h in range(pair.Hkv):
+        kv = pair.units[h][0]
+        keys, values = kv.keys[:kv.n], kv.values[:kv.n]
+        for g in range(pair.G):
+            z = keys @ q[0, h, g] / math.sqrt(pair.d)
+            w = np.exp(z - z.max())
+            w /= w.sum()
+            ref = w @ values
+            got = out[0, h * pair.G + g]
+            assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-5
