@@ -18,14 +18,21 @@ from .errors import (BadMagicError, ChecksumError, DeviceError, LayoutError, Lfp
 __version__ = "0.1.0"
 
 
-_LAZY = {"BatchedSession": "session", "BatchedStepResult": "session"}
+_LAZY = {"BatchedSession": "session", "BatchedStepResult": "session",
+         # trace container (N2), reports (N3), GPU replay
+         "TraceFile": "tracefile", "HeadTrace": "tracefile", "read_trace": "tracefile",
+         "write_trace": "tracefile", "load_trace": "tracefile", "save_trace": "tracefile",
+         "RunReport": "report", "StepRecord": "report", "emit_json": "report",
+         "emit_csv": "report", "compute_aggregates": "report",
+         "run_trace": "replay", "config_for_trace": "replay"}
 
 
 def __getattr__(name):
     # device-backed names load lazily so that importing the package (configs,
     # errors, the C-ABI loader) works on machines without a GPU
     import importlib
-    if name.startswith("__") or name in ("session", "compat", "workload", "_lib"):
+    if name.startswith("__") or name in ("session", "compat", "workload", "_lib", "tracefile",
+                                         "report", "replay"):
         raise AttributeError(name)
     mod = importlib.import_module(__name__ + "." + _LAZY.get(name, "compat"))
     if hasattr(mod, name):
