@@ -7,16 +7,21 @@
 // {z > kth} plus the lowest-index entries with z == kth, emitted in index
 // order.  Keys are order-preserving uint32 maps of the fp32 scores with -0.0
 // canonicalised to +0.0 (canon.cuh score_key).  One 512-thread CTA per
-// session, three streaming passes over its m scores:
+// session; the m scores (512 KiB at 128k) are streamed twice:
 //
-//   1  2048-bin histogram of the top 11 key bits (shared-memory atomics)
-//      -> the bin holding the k-th largest key, and how many keys lie above;
-//   2  that bin's (key, index) pairs are collected (shared memory, or the
-//      session's uw scratch when they do not fit), and every warp counts the
-//      keys of its index chunk that lie in higher bins;
-//   3  an MSB-first 3 x 7-bit radix select over the candidates gives the
-//      exact k-th key; each warp then re-walks its chunk and writes its
-//      selections at ballot/popc offsets, so the output is sorted.
+//   0  a strided sample of 4096 keys is sorted in shared memory; the sample
+//      ranks around k m / 4096 (+- 4 sqrt(rank) + 16) bound a key window
+//      [lo, hi] that holds the k-th largest key with overwhelming probability;
+//   1  one pass counts the keys above hi per warp chunk and collects the
+//      window's (key, index) pairs in shared memory;
+//   2  if the window provably holds the k-th key (keys above hi < k <=
+//      keys above hi + window size, and the window fit), an MSB-first radix
+//      select over the window finds it exactly; otherwise the kernel falls
+//      back to a 2048-bin histogram pass over all keys plus the same select
+//      on the k-th bin;
+//   3  every warp re-walks its index chunk and writes its selections at
+//      warp-scan offsets, so the output is sorted.
+// Loads are float4 (4 keys per lane) with two in flight.
 #include "common.cuh"
 #include "canon.cuh"
 
@@ -26,20 +31,74 @@ namespace {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kBins = 2048;                 // top 11 key bits
+constexpr int kSample = 4096;
+constexpr int kBins = 2048;                 // fallback: top 11 key bits
 constexpr int kShift = 21;
-constexpr int kSmemCand = 6144;             // candidates kept in shared memory
+constexpr int kCand = 6144;                 // window candidates kept in shared memory
 
 struct TopkShared {
-  unsigned hist[kBins];
-  uint2 cand[kSmemCand];                    // (key, index)
+  unsigned samp[kSample];                   // sample keys, sorted descending (also histogram)
+  uint2 cand[kCand];                        // (key, index)
   int wsum[kWarps];
-  int above[kWarps];                        // keys in higher bins, per warp chunk
-  int gtc[kWarps], eqc[kWarps];             // candidates > kth / == kth, per warp chunk
-  int ncand;
-  int sel_bin, sel_want;
+  int above[kWarps];                        // keys above the window, per warp chunk
+  int gtc[kWarps], eqc[kWarps];             // window keys > kth / == kth, per warp chunk
+  int ncand, over;
+  unsigned hist[256];
   unsigned sel_digit;
+  int sel_want;
 };
+
+__device__ __forceinline__ uint32_t key_at(const float* z, int j) { return score_key(z[j]); }
+
+// MSB-first radix select over keys[0, nk) restricted to (key & mask) ==
+// prefix: the key value whose descending rank contains `want` (1-based),
+// i.e. the want-th largest; returns it and sets *need_eq to how many keys
+// equal to it are still to be taken.
+__device__ uint32_t radix_select(TopkShared& sh, const uint2* keys, int nk, uint32_t prefix,
+                                 uint32_t mask, int first_shift, int want, int* need_eq) {
+  const int tid = threadIdx.x;
+  for (int shift = first_shift; shift >= 0; shift -= 8) {
+    if (tid < 256) sh.hist[tid] = 0;
+    __syncthreads();
+    for (int i = tid; i < nk; i += kThreads) {
+      const uint32_t key = keys[i].x;
+      if ((key & mask) == prefix) atomicAdd(&sh.hist[(key >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      unsigned loc = 0;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) loc += sh.hist[255 - 8 * tid - t];
+      unsigned incl = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(LFPS_FULL, incl, o);
+        if (tid >= o) incl += y;
+      }
+      const unsigned excl = incl - loc;
+      if (excl < (unsigned)want && incl >= (unsigned)want) {
+        unsigned cum = excl;
+        for (int t = 0; t < 8; ++t) {
+          const unsigned dgt = 255 - 8 * tid - t;
+          const unsigned hc = sh.hist[dgt];
+          if (cum + hc >= (unsigned)want) {
+            sh.sel_digit = dgt;
+            sh.sel_want = want - (int)cum;
+            break;
+          }
+          cum += hc;
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= sh.sel_digit << shift;
+    mask |= 255u << shift;
+    want = sh.sel_want;
+    __syncthreads();
+  }
+  *need_eq = want;
+  return prefix;
+}
 
 __global__ void __launch_bounds__(kThreads) lfps_exact_topk_kernel(Ctx c) {
   extern __shared__ uint8_t dyn[];
@@ -65,17 +124,104 @@ __global__ void __launch_bounds__(kThreads) lfps_exact_topk_kernel(Ctx c) {
     if (tid == 0) cnt[CNT_C2] = p;
     return;
   }
-  // ---- pass 1: histogram of the top key bits -------------------------------------
-  for (int i = tid; i < kBins; i += kThreads) sh.hist[i] = 0;
-  if (tid == 0) sh.ncand = 0;
+  // warp chunks: multiples of 128 keys (float4 per lane), the last one short
+  const int chunk = ((p + kWarps - 1) / kWarps + 127) / 128 * 128;
+  const int j0 = min(p, warp * chunk), j1 = min(p, j0 + chunk);
+  const bool vec_ok = (reinterpret_cast<uintptr_t>(z) & 15) == 0;
+
+  // ---- 0: sorted sample -> key window [lo, hi] -----------------------------------
+  uint32_t lo = 0, hi = 0xffffffffu;
+  bool use_window = p > 4 * kSample;
+  if (use_window) {
+    for (int i = tid; i < kSample; i += kThreads)
+      sh.samp[i] = key_at(z, (int)(((long long)i * p) / kSample));
+    __syncthreads();
+    // bitonic sort, descending
+    for (int size = 2; size <= kSample; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = tid; i < kSample / 2; i += kThreads) {
+          const int a = 2 * i - (i & (stride - 1));
+          const int bb = a + stride;
+          const bool desc = ((a & size) == 0);
+          const unsigned x = sh.samp[a], y = sh.samp[bb];
+          if ((x < y) == desc) { sh.samp[a] = y; sh.samp[bb] = x; }
+        }
+        __syncthreads();
+      }
+    }
+    const int r = (int)(((long long)k * kSample) / p);
+    const int delta = 4 * (int)sqrtf((float)r + 1.0f) + 16;
+    const int rh = r - delta, rl = r + delta;
+    hi = rh <= 0 ? 0xffffffffu : sh.samp[rh];
+    lo = rl >= kSample ? 0u : sh.samp[rl];
+    if (tid == 0) { sh.ncand = 0; sh.over = 0; }
+    __syncthreads();
+  }
+
+  // ---- 1: keys above the window per chunk; window candidates ------------------------
+  int above = 0;
+  if (use_window) {
+    auto visit = [&](uint32_t key, int j) {
+      if (key > hi) {
+        ++above;
+      } else if (key >= lo) {
+        const int at = atomicAdd(&sh.ncand, 1);
+        if (at < kCand) sh.cand[at] = make_uint2(key, (uint32_t)j);
+      }
+    };
+    if (vec_ok) {
+      // four float4 loads (16 keys) in flight per lane
+      for (int base0 = j0 + 4 * lane; base0 < j1; base0 += 512) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int base = base0 + 128 * u;
+          v[u] = base + 3 < j1 ? __ldg(reinterpret_cast<const float4*>(z + base))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int base = base0 + 128 * u;
+          if (base + 3 < j1) {
+            visit(score_key(v[u].x), base); visit(score_key(v[u].y), base + 1);
+            visit(score_key(v[u].z), base + 2); visit(score_key(v[u].w), base + 3);
+          } else {
+            for (int j = base; j < j1; ++j) visit(key_at(z, j), j);
+          }
+        }
+      }
+    } else {
+      for (int j = j0 + lane; j < j1; j += 32) visit(key_at(z, j), j);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) above += __shfl_xor_sync(LFPS_FULL, above, o);
+  if (lane == 0) { sh.above[warp] = above; sh.gtc[warp] = 0; sh.eqc[warp] = 0; }
   __syncthreads();
-  for (int j = tid; j < p; j += kThreads) atomicAdd(&sh.hist[score_key(z[j]) >> kShift], 1u);
-  __syncthreads();
-  {
-    // thread t owns bins [kBins - 4 t - 4, kBins - 4 t) (descending order)
+  int tot_above = 0;
+  for (int w = 0; w < kWarps; ++w) tot_above += sh.above[w];
+  const int nc = use_window ? sh.ncand : 0;
+  // the window provably holds the k-th key?
+  use_window = use_window && nc <= kCand && tot_above < k && tot_above + nc >= k;
+
+  uint32_t kth;
+  int need_eq;
+  const uint2* cand = sh.cand;
+  int ncand = nc;
+  if (use_window) {
+    kth = radix_select(sh, cand, ncand, 0u, 0u, 24, k - tot_above, &need_eq);
+  } else {
+    // ---- fallback: 2048-bin histogram over all keys, then the k-th bin ----------------
+    unsigned* hist = sh.samp;                      // 2048 bins
+    for (int i = tid; i < kBins; i += kThreads) hist[i] = 0;
+    if (tid == 0) sh.ncand = 0;
+    __syncthreads();
+    for (int j = tid; j < p; j += kThreads) atomicAdd(&hist[key_at(z, j) >> kShift], 1u);
+    __syncthreads();
+    // thread t owns bins [kBins - 4 t - 4, kBins - 4 t) (descending)
     unsigned loc = 0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) loc += sh.hist[kBins - 1 - 4 * tid - i];
+    for (int i = 0; i < 4; ++i) loc += hist[kBins - 1 - 4 * tid - i];
     unsigned x = loc;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -91,9 +237,9 @@ __global__ void __launch_bounds__(kThreads) lfps_exact_topk_kernel(Ctx c) {
       unsigned cum = excl;
       for (int i = 0; i < 4; ++i) {
         const int bin = kBins - 1 - 4 * tid - i;
-        const unsigned hc = sh.hist[bin];
+        const unsigned hc = hist[bin];
         if (cum + hc >= (unsigned)k) {
-          sh.sel_bin = bin;
+          sh.sel_digit = (unsigned)bin;
           sh.sel_want = k - (int)cum;
           break;
         }
@@ -101,104 +247,100 @@ __global__ void __launch_bounds__(kThreads) lfps_exact_topk_kernel(Ctx c) {
       }
     }
     __syncthreads();
-  }
-  const unsigned bstar = (unsigned)sh.sel_bin;
-  const int nc = (int)sh.hist[bstar];
-  uint2* cand = nc <= kSmemCand ? sh.cand : reinterpret_cast<uint2*>(c.uw + (size_t)s * c.list_cap);
-  // ---- pass 2: candidates of the k-th bin; keys above it per warp chunk ----------------
-  const int chunk = (p + kWarps - 1) / kWarps;
-  const int j0 = warp * chunk, j1 = min(p, j0 + chunk);
-  int above = 0;
-  for (int j = j0 + lane; j < j1; j += 32) {
-    const uint32_t key = score_key(z[j]);
-    const uint32_t bin = key >> kShift;
-    above += bin > bstar;
-    if (bin == bstar) {
-      const int at = atomicAdd(&sh.ncand, 1);
-      cand[at] = make_uint2(key, (uint32_t)j);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) above += __shfl_xor_sync(LFPS_FULL, above, o);
-  if (lane == 0) { sh.above[warp] = above; sh.gtc[warp] = 0; sh.eqc[warp] = 0; }
-  __syncthreads();
-  // ---- pass 3: radix select within the bin (3 x 7 bits) -----------------------------
-  uint32_t prefix = bstar << kShift, mask = ~0u << kShift;
-  int want = sh.sel_want;
-  for (int shift = 14; shift >= 0; shift -= 7) {
-    if (tid < 128) sh.hist[tid] = 0;
+    const unsigned bstar = sh.sel_digit;
+    const int want = sh.sel_want;
+    ncand = (int)hist[bstar];
+    uint2* store = ncand <= kCand ? sh.cand : reinterpret_cast<uint2*>(c.uw + (size_t)s * c.list_cap);
     __syncthreads();
-    for (int i = tid; i < nc; i += kThreads) {
-      const uint32_t key = cand[i].x;
-      if ((key & mask) == prefix) atomicAdd(&sh.hist[(key >> shift) & 127u], 1u);
-    }
-    __syncthreads();
-    if (tid < 32) {
-      // lane l owns digits [127 - 4 l - 3, 127 - 4 l]; suffix counts from the top
-      unsigned loc = 0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) loc += sh.hist[127 - 4 * tid - t];
-      unsigned incl = loc;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(LFPS_FULL, incl, o);
-        if (tid >= o) incl += y;
-      }
-      const unsigned excl = incl - loc;
-      if (excl < (unsigned)want && incl >= (unsigned)want) {
-        unsigned cum = excl;
-        for (int t = 0; t < 4; ++t) {
-          const unsigned dgt = 127 - 4 * tid - t;
-          const unsigned hc = sh.hist[dgt];
-          if (cum + hc >= (unsigned)want) {
-            sh.sel_digit = dgt;
-            sh.sel_want = want - (int)cum;
-            break;
-          }
-          cum += hc;
-        }
+    int ab = 0;
+    for (int j = j0 + lane; j < j1; j += 32) {
+      const uint32_t key = key_at(z, j);
+      const uint32_t bin = key >> kShift;
+      ab += bin > bstar;
+      if (bin == bstar) {
+        const int at = atomicAdd(&sh.ncand, 1);
+        store[at] = make_uint2(key, (uint32_t)j);
       }
     }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) ab += __shfl_xor_sync(LFPS_FULL, ab, o);
+    if (lane == 0) sh.above[warp] = ab;
     __syncthreads();
-    prefix |= sh.sel_digit << shift;
-    mask |= 127u << shift;
-    want = sh.sel_want;
-    __syncthreads();
+    cand = store;
+    kth = radix_select(sh, cand, ncand, bstar << kShift, ~0u << kShift, 16, want, &need_eq);
+    // radix_select's top pass (bits 16..23) covers the remaining 21 bits in 3
+    // passes of 8 (bits above 21 already fixed by the prefix)
   }
-  const uint32_t kth = prefix;
-  const int need_eq = want;                        // equal keys to take, lowest index first
-  // per-warp-chunk counts of candidates above / equal to kth
-  for (int i = tid; i < nc; i += kThreads) {
+
+  // per-warp-chunk counts of window / bin keys above and equal to kth
+  for (int i = tid; i < ncand; i += kThreads) {
     const uint2 e = cand[i];
     const int w = (int)e.y / chunk;
     if (e.x > kth) atomicAdd(&sh.gtc[w], 1);
     else if (e.x == kth) atomicAdd(&sh.eqc[w], 1);
   }
   __syncthreads();
-  // ---- ordered emission: warp w walks its chunk in index order --------------------------
+  // ---- 3: ordered emission: warp w walks its chunk in index order ---------------------
   int out_at = 0, eq_at = 0;
   for (int w = 0; w < warp; ++w) {
     const int eq = sh.eqc[w];
-    const int eq_take = max(0, min(eq, need_eq - eq_at));
-    out_at += sh.above[w] + sh.gtc[w] + eq_take;
+    out_at += sh.above[w] + sh.gtc[w] + max(0, min(eq, need_eq - eq_at));
     eq_at += eq;
   }
-  for (int base = j0; base < j1; base += 32) {
-    const int j = base + lane;
-    const uint32_t key = j < j1 ? score_key(z[j]) : 0u;
-    const bool gt = j < j1 && key > kth;
-    const bool eq = j < j1 && key == kth;
-    const uint32_t eqm = __ballot_sync(LFPS_FULL, eq);
-    const int my_eq = eq_at + __popc(eqm & ((1u << lane) - 1u));
-    const bool take = gt || (eq && my_eq < need_eq);
-    const uint32_t tm = __ballot_sync(LFPS_FULL, take);
-    if (take) {
-      const int pos = out_at + __popc(tm & ((1u << lane) - 1u));
-      out_i[pos] = S + j;
-      out_z[pos] = z[j];
+  for (int base = j0; base < j1; base += 128) {
+    // lane owns 4 consecutive keys: j = base + 4 lane + e
+    uint32_t keys[4];
+    int ntake = 0, neq = 0;
+    if (vec_ok && base + 4 * lane + 3 < j1) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(z + base + 4 * lane));
+      keys[0] = score_key(v.x); keys[1] = score_key(v.y);
+      keys[2] = score_key(v.z); keys[3] = score_key(v.w);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = base + 4 * lane + e;
+        keys[e] = j < j1 ? key_at(z, j) : 0u;
+      }
     }
-    out_at += __popc(tm);
-    eq_at += __popc(eqm);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) neq += base + 4 * lane + e < j1 && keys[e] == kth;
+    // exclusive warp scans of equal-key counts (index order = lane-major)
+    int eqx = neq;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(LFPS_FULL, eqx, o);
+      if (lane >= o) eqx += y;
+    }
+    const int eq_total = __shfl_sync(LFPS_FULL, eqx, 31);
+    int my_eq = eq_at + eqx - neq;
+    bool take[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = base + 4 * lane + e;
+      const bool eq = j < j1 && keys[e] == kth;
+      take[e] = j < j1 && (keys[e] > kth || (eq && my_eq < need_eq));
+      my_eq += eq;
+      ntake += take[e];
+    }
+    int tx = ntake;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(LFPS_FULL, tx, o);
+      if (lane >= o) tx += y;
+    }
+    const int take_total = __shfl_sync(LFPS_FULL, tx, 31);
+    int pos = out_at + tx - ntake;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (take[e]) {
+        const int j = base + 4 * lane + e;
+        out_i[pos] = S + j;
+        out_z[pos] = z[j];
+        ++pos;
+      }
+    }
+    out_at += take_total;
+    eq_at += eq_total;
   }
   if (warp == kWarps - 1 && lane == 0) cnt[CNT_C2] = out_at;
 }

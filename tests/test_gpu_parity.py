@@ -133,18 +133,21 @@ def test_exact_path_matches_oracle_and_overlap():
             assert eta[0, qh] == pytest.approx(want, abs=0)
 
 
-@pytest.mark.parametrize("frac,dup", [(0.05, 0), (0.05, 700), (0.3, 0), (1.0, 0)])
-def test_exact_topk_ties_and_budgets(frac, dup):
+@pytest.mark.parametrize("n0,frac,dup", [(6000, 0.05, 0), (6000, 0.05, 700), (6000, 0.3, 0),
+                                         (6000, 1.0, 0), (20000, 0.05, 0), (20000, 0.05, 1500),
+                                         (20000, 0.01, 0)])
+def test_exact_topk_ties_and_budgets(n0, frac, dup):
     """Exact path against topk_oracle (full stable sort, attention.py:100-113)
     with planted exact ties: `dup` rows get the same key, so the k-th score
     is shared by many rows and the lower-index rule decides (attention.py:
-    34-47); frac 1.0 selects every non-sink row."""
+    34-47); frac 1.0 selects every non-sink row.  n0 = 20000 takes the
+    sampled-window selection (k_topk.cu), 6000 the histogram path."""
     from oracle import lfps_oracle as lo
     import gpu_drive
-    pair, K, V, Q = _gqa_pair(batch=1, kv_heads=2, n0=6000, steps=1, seed=9)
+    pair, K, V, Q = _gqa_pair(batch=1, kv_heads=2, n0=n0, steps=1, seed=9)
     if dup:
         rng = np.random.default_rng(5)
-        rows = rng.choice(np.arange(4, 6000), size=dup, replace=False)
+        rows = rng.choice(np.arange(4, n0), size=dup, replace=False)
         for h in range(pair.Hkv):
             K[0, h, rows] = K[0, h, rows[0]]
         pair = _rebuild(pair, K, V)
