@@ -10,7 +10,6 @@ namespace fin {
 using namespace rows;
 
 struct FinishShared {
-  RowPipe pipe;
   float sink_z[32];
   float part_m[kGroups8];
   float part_s[kGroups8];
@@ -62,8 +61,6 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
   const int k2 = k >= p ? p : k;
   if (tid == 0) { cnt[CNT_K] = k; cnt[CNT_C2] = k2; }
 
-  pipe_init(sh.pipe);
-  int seq = 0;
   Attn<PQ> at;
   at.init();
   int bad = 0;
@@ -72,7 +69,7 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
   if (k >= p) {
     // ---- C2 = probe (the common case): score and attend in ONE pass ---------------------
     stream_rows<kFused, PQ>(
-        c, stages, sh.pipe, seq, kb, vb, S + p,
+        c, stages, kb, vb, S + p,
         [&](int rid) { return rid < S ? rid : __ldg(pidx + rid - S); },
         [&](int rid, const __nv_bfloat16* kr, const __nv_bfloat16* vr) {
           const float z = row_score<PQ>(ld_part<PQ>(kr, l8), q2, c.sqrt_d_f32);
@@ -89,7 +86,7 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
   } else {
     // ---- scores of the sinks and the probe rows -------------------------------------------
     stream_rows<kScore, PQ>(
-        c, stages, sh.pipe, seq, kb, vb, S + p,
+        c, stages, kb, vb, S + p,
         [&](int rid) { return rid < S ? rid : __ldg(pidx + rid - S); },
         [&](int rid, const __nv_bfloat16* kr, const __nv_bfloat16*) {
           const float z = row_score<PQ>(ld_part<PQ>(kr, l8), q2, c.sqrt_d_f32);
@@ -162,7 +159,7 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
     __syncthreads();
     // ---- attention over sinks u C2 ------------------------------------------------------
     stream_rows<kAttend, PQ>(
-        c, stages, sh.pipe, seq, kb, vb, S + k2,
+        c, stages, kb, vb, S + k2,
         [&](int rid) { return rid < S ? rid : c2i[rid - S]; },
         [&](int rid, const __nv_bfloat16*, const __nv_bfloat16* vr) {
           const float z = rid < S ? sh.sink_z[rid] : c2z[rid - S];

@@ -17,7 +17,6 @@ namespace {
 using namespace rows;
 
 struct AttendShared {
-  RowPipe pipe;
   float sink_z[32];
   float part_m[kGroups8];
   float part_s[kGroups8];
@@ -45,10 +44,8 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_exact_attend_kernel(Ctx c, c
       q2[2 * t + 1] = make_float2(bf_hi(qp.a[t]), bf_hi(qp.b[t]));
     }
   }
-  pipe_init(sh.pipe);
-  int seq = 0;
   stream_rows<kScore, PQ>(
-      c, stages, sh.pipe, seq, kb, vb, S, [&](int rid) { return rid; },
+      c, stages, kb, vb, S, [&](int rid) { return rid; },
       [&](int rid, const __nv_bfloat16* kr, const __nv_bfloat16*) {
         const float z = row_score<PQ>(ld_part<PQ>(kr, l8), q2, c.sqrt_d_f32);
         if (l8 == 0) sh.sink_z[rid] = z;
@@ -56,7 +53,7 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_exact_attend_kernel(Ctx c, c
   Attn<PQ> at;
   at.init();
   stream_rows<kAttend, PQ>(
-      c, stages, sh.pipe, seq, kb, vb, S + k2, [&](int rid) { return rid < S ? rid : __ldg(c2i + rid - S); },
+      c, stages, kb, vb, S + k2, [&](int rid) { return rid < S ? rid : __ldg(c2i + rid - S); },
       [&](int rid, const __nv_bfloat16*, const __nv_bfloat16* vr) {
         const float z = rid < S ? sh.sink_z[rid] : __ldg(c2z + rid - S);
         at.absorb(z, ld_part<PQ>(vr, l8));

@@ -170,41 +170,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Per-stage mbarriers of the row pipeline (shared memory): full[s] completes
-// when every thread's cp.async copies for the stage's current tile have
-// landed (cp.async.mbarrier.arrive.noinc, kThreads arrivals); empty[s] when
-// all kWarps warps have consumed it.  `seq` counts tiles across calls so the
-// phase parities stay consistent when a kernel streams more than once.
-struct RowPipe {
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
-};
-
-__device__ __forceinline__ void pipe_init(RowPipe& pp) {
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; ++i) {
-      mbar_init(&pp.full[i], kThreads);
-      mbar_init(&pp.empty[i], kWarps);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
 // Stream rows [0, nrows) through shared memory, kStages tiles of kTile rows
 // deep: every thread copies 16-byte chunks of one row (cp.async, L2 only),
 // 8 threads per row; row_of(rid) gives the cache row of list entry rid, and
 // visit(rid, k_row, v_row) consumes a staged row (8-lane group `grp` owns
-// tile row `grp`).  There is no CTA-wide barrier per tile: a warp waits only
-// for its tile's data (full) and, before refilling a stage, for every warp
-// to have left it (empty), so warps drift up to kStages - 2 tiles apart.
-// Each thread fetches its row index one tile before it issues the copies.
+// tile row `grp`).  Each thread fetches its row index one tile before it
+// issues the copies, so the index load is off the critical path.
 template <int MODE, int PQ, typename RowOf, typename Visit>
-__device__ __forceinline__ void stream_rows(const Ctx& c, uint8_t* stages, RowPipe& pp, int& seq,
+__device__ __forceinline__ void stream_rows(const Ctx& c, uint8_t* stages,
                                             const __nv_bfloat16* kb, const __nv_bfloat16* vb,
                                             int nrows, RowOf row_of, Visit visit) {
   constexpr bool kK = MODE != kAttend, kV = MODE != kScore;
@@ -212,19 +185,15 @@ __device__ __forceinline__ void stream_rows(const Ctx& c, uint8_t* stages, RowPi
   constexpr int kRowB = D * 2;                        // bytes per row
   constexpr int kChunks = kRowB / 16;                 // 16-byte chunks per row
   constexpr int kStageB = kTile * kRowB * 2;          // K block then V block
-  const int grp = threadIdx.x >> 3, l8 = threadIdx.x & 7, lane = threadIdx.x & 31;
+  const int grp = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int ntiles = (nrows + kTile - 1) / kTile;
-  const int base = seq;
   auto fetch = [&](int tile) {
     const int rid = tile * kTile + grp;
     return (tile < ntiles && rid < nrows) ? row_of(rid) : -1;
   };
   auto issue = [&](int tile, int row) {
-    if (tile >= ntiles) return;
-    const int sq = base + tile, st_i = sq % kStages;
-    if (sq >= kStages) mbar_wait(&pp.empty[st_i], (uint32_t)((sq / kStages - 1) & 1));
-    if (row >= 0) {
-      uint8_t* st = stages + (size_t)st_i * kStageB + grp * kRowB;
+    if (tile < ntiles && row >= 0) {
+      uint8_t* st = stages + (size_t)(tile % kStages) * kStageB + grp * kRowB;
 #pragma unroll
       for (int ch = l8; ch < kChunks; ch += 8) {
         if (kK) cp_async16(st + ch * 16, reinterpret_cast<const uint8_t*>(kb + (size_t)row * D) + ch * 16);
@@ -232,27 +201,25 @@ __device__ __forceinline__ void stream_rows(const Ctx& c, uint8_t* stages, RowPi
                            reinterpret_cast<const uint8_t*>(vb + (size_t)row * D) + ch * 16);
       }
     }
-    cp_async_arrive(&pp.full[st_i]);                  // every thread, even without copies
+    cp_async_commit();                                // one group per tile, even if empty
   };
 #pragma unroll 1
   for (int t = 0; t < kStages - 1; ++t) issue(t, fetch(t));
   int ahead = fetch(kStages - 1);
 #pragma unroll 1
   for (int tile = 0; tile < ntiles; ++tile) {
-    const int sq = base + tile, st_i = sq % kStages;
-    mbar_wait(&pp.full[st_i], (uint32_t)((sq / kStages) & 1));
-    const uint8_t* st = stages + (size_t)st_i * kStageB;
+    cp_async_wait<kStages - 2>();                     // this thread's copies of `tile` landed
+    __syncthreads();                                  // everyone's; stage (tile - 1) is free
+    issue(tile + kStages - 1, ahead);
+    ahead = fetch(tile + kStages);
+    const uint8_t* st = stages + (size_t)(tile % kStages) * kStageB;
     const int rid = tile * kTile + grp;
     if (rid < nrows)
       visit(rid, reinterpret_cast<const __nv_bfloat16*>(st + grp * kRowB),
             reinterpret_cast<const __nv_bfloat16*>(st + (kTile + grp) * kRowB));
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&pp.empty[st_i]);
-    issue(tile + kStages - 1, ahead);                 // refills the stage of tile - 1
-    ahead = fetch(tile + kStages);
   }
-  seq = base + ntiles;
-  __syncthreads();                                    // stages may be reused by the caller
+  cp_async_wait<0>();
+  __syncthreads();
 }
 
 }  // namespace rows
