@@ -36,7 +36,7 @@ namespace {
 using namespace fin;
 
 template <int PQ>
-__global__ void __launch_bounds__(kThreads, 3) lfps_finish_kernel(Ctx c, const __nv_bfloat16* q) {
+__global__ void __launch_bounds__(kThreads, 4) lfps_finish_kernel(Ctx c, const __nv_bfloat16* q) {
   extern __shared__ __align__(128) uint8_t stages[];      // kStages x [K tile | V tile]
   __shared__ FinishShared sh;
   finish_session<PQ>(c, q, c.s_off + blockIdx.x, stages, sh);

@@ -15,7 +15,7 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kGroups8 = kThreads / 8;   // 8-lane row groups
 constexpr int kTile = 32;                // rows per stage (one per row group)
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 constexpr int kCanon = 256;              // canonical block-sum width (devmath.BLOCK_THREADS)
 constexpr int kMaxE = 8;                 // exponentials cached per thread (|C2| <= 2048)
 
