@@ -221,7 +221,7 @@ struct SelectShared {
   int red[3][kWarps];
 };
 
-__global__ void __launch_bounds__(kThreads, 3) lfps_select_kernel(Ctx c) {
+__global__ void __launch_bounds__(kThreads, 4) lfps_select_kernel(Ctx c) {
   extern __shared__ uint32_t smem[];
   __shared__ SelectShared sh;
   const int s = c.s_off + blockIdx.x;
