@@ -459,6 +459,12 @@ def run_ours(args, world, rank, local):
     dom_ms = kernel_ms[dominant]
     dom_bytes = alg["kernels"].get(dominant, 0)
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    if os.path.exists(tpath) and args.config == "c4":
+        with open(tpath) as f:
+            tk = json.load(f)["kernels"].get(dominant)
+        traffic = tk["traffic_bytes"] if tk else None
     counts = sess.counts.cpu().numpy()
     bypass = int(sess.bypass.sum())
     probe = counts[..., CNT_PROBE].astype(np.int64)
@@ -572,7 +578,9 @@ def run_ours(args, world, rank, local):
         "gpu_launches": args.steps * _lib.load_library().lfps_decode_launches(),
         "roofline": {"bound": "hbm", "kernel": dominant,
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full, dram read+write "
+                                       "per launch of this kernel at C4)" if traffic else None,
                      "algorithmic_bytes_per_launch": dom_bytes,
                      "avg_launch_ms": dom_ms, "peak_source": peak_src},
         "kernel_ms": kernel_ms,
