@@ -380,6 +380,7 @@ def phase_trace(sess, step, t, dev) -> dict:
 
 
 def run_ours(args, world, rank, local):
+    import ctypes as C
     import numpy as np
     import torch
     from paper_2506_15704_b200 import _lib
@@ -575,7 +576,8 @@ def run_ours(args, world, rank, local):
                    "sharding": "requests across ranks, no collective on the decode path",
                    "l2": "flushed before every timed step (512 MiB write); each step timed "
                          "by its own CUDA events"},
-        "gpu_launches": args.steps * _lib.load_library().lfps_decode_launches(),
+        "gpu_launches": args.steps * _lib.load_library().lfps_decode_launches(
+            C.byref(sess.dims), sess._params(frac).flags),
         "roofline": {"bound": "hbm", "kernel": dominant,
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,

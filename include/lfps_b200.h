@@ -230,8 +230,9 @@ typedef struct lfps_kernel_time {
 LFPS_API int lfps_profile_enable(int on);
 LFPS_API int lfps_profile_collect(lfps_kernel_time* out, int32_t cap, int32_t* n_out);
 
-/* Number of kernels lfps_decode_step / lfps_exact_topk_step launch. */
-LFPS_API int lfps_decode_launches(void);
+/* Number of kernels lfps_decode_step launches for these dims and params
+ * flags (dims may be NULL: the serial sequence), and lfps_exact_topk_step. */
+LFPS_API int lfps_decode_launches(const lfps_dims* dims, int32_t flags);
 LFPS_API int lfps_exact_launches(void);
 
 #ifdef __cplusplus

@@ -100,6 +100,7 @@ def _declare(lib):
     lib.lfps_overlap.argtypes = [P(Dims), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
     lib.lfps_profile_enable.argtypes = [C.c_int]
+    lib.lfps_decode_launches.argtypes = [C.c_void_p, C.c_int32]
     lib.lfps_profile_collect.argtypes = [P(KernelTime), C.c_int32, P(C.c_int32)]
     for name in ("lfps_profile_enable", "lfps_profile_collect", "lfps_workspace_layout",
                  "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step", "lfps_exact_topk_step", "lfps_overlap",

@@ -284,8 +284,14 @@ int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out) {
   return layout(dims, out);
 }
 
-int lfps_decode_launches(void) { return 5; }  // clear, gate, select, finish,
-                                             // update (with append and commit)
+// clear, gate, select, finish, update (with append and commit); with
+// LFPS_FLAG_SPLIT (and >= 256 sessions) gate/select/finish run per half
+int lfps_decode_launches(const lfps_dims* dims, int32_t flags) {
+  if (dims && (flags & LFPS_FLAG_SPLIT) &&
+      (long long)dims->batch * dims->kv_heads * dims->group >= 256)
+    return 8;
+  return 5;
+}
 
 int lfps_slash_capacity(const lfps_dims* dims) {
   int rc = check_dims(dims);
