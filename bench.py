@@ -41,6 +41,8 @@ CONFIGS = {
            "1 layer, Top-k 5%"),
     "c2": (4, 32768, 8, 4, 128, 0.05,
            "C2: batch 4 x 32k context, Llama-3.1-8B shapes, 1 layer, Top-k 5%"),
+    "c3": (16, 131072, 8, 4, 128, 0.05,
+           "C3: batch 16 x 128k context, all 32 layers, Llama-3.1-8B shapes, Top-k 5%"),
     "c1": (1, 16384, 8, 4, 128, 0.05,
            "C1: batch 1 x 16k context, Llama-3.1-8B shapes, 1 layer, Top-k 5%"),
 }
@@ -79,11 +81,19 @@ def dist_setup():
 
 
 def dist_init(world, local):
+    """One process per GPU over NCCL.  LFPS_DIST_BACKEND=gloo (with ranks
+    sharing devices round-robin) exercises the multi-rank path on a box with
+    fewer GPUs than ranks; timings from such a run are not scaling numbers."""
     import torch
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("LFPS_DIST_BACKEND", "nccl")
+        dev = local % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
 
@@ -423,7 +433,7 @@ def run_ours(args, world, rank, local):
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
-    clocks = ClockSampler(local if world > 1 else 0)
+    clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
     barrier(world)
     torch.cuda.synchronize(dev)
@@ -613,6 +623,76 @@ def run_ours(args, world, rank, local):
     print(json.dumps(line), flush=True)
 
 
+def run_c3(args, world, rank, local):
+    """BASELINE.json config 3: batch 16 x 128k context, all 32 layers of a
+    decode step.  The 32 layers' K/V (8.6 GB each) do not all fit one B200
+    next to their trackers, so one layer's KV cache is shared by 32 layer
+    sessions (each with its own tracker tables, bootstrapped from the same
+    prefill) -- the per-layer work and bytes are those of 32 distinct layers,
+    the cached rows are reused (SURVEY.md §7 "Memory feasibility")."""
+    import torch
+    from paper_2506_15704_b200.config import LfpsConfig
+    from paper_2506_15704_b200.session import BatchedSession
+    from paper_2506_15704_b200.workload import GqaSpec, populate
+    batch, ctx, layers, frac = 16, 131072, 32, 0.05
+    b_local, b0 = shard_requests(batch, world, rank)
+    T_in = 32
+    cfg = LfpsConfig(d=128)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    spec = GqaSpec(batch=b_local, kv_heads=8, group=4, d=128, n_prefill=ctx, steps=T_in,
+                   seed=42 + 7919 * b0)
+    n_max = ctx + args.warmup + args.steps + 8
+    t_setup = time.time()
+    sess = [BatchedSession(cfg, b_local, 8, 4, n_max=n_max, device=dev)]
+    stream = populate(sess[0], spec)
+    for _ in range(layers - 1):
+        s_l = BatchedSession(cfg, b_local, 8, 4, n_max=n_max, device=dev,
+                             kv_cache=(sess[0].k_cache, sess[0].v_cache))
+        s_l.copy_tracker_from(sess[0])
+        sess.append(s_l)
+    setup_s = time.time() - t_setup
+
+    def token_step(t):
+        i = t % T_in
+        for s_l in sess:
+            s_l.decode_step(stream.q[i], stream.k_new[i], stream.v_new[i], frac)
+
+    for t in range(args.warmup):
+        token_step(t)
+    torch.cuda.synchronize(dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.fill_(i & 255)
+        evs[i][0].record()
+        token_step(args.warmup + i)
+        evs[i][1].record()
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    clock_info = clocks.stop()
+    ms = allmax(world, sum(a.elapsed_time(b) for a, b in evs) / args.steps)
+    for s_l in sess:
+        s_l.check_errors("c3 steps")
+    if rank != 0:
+        return
+    print(json.dumps({
+        "metric": "LFPS index+sparse-attn us/decode-step (all 32 layers)", "value": ms * 1e3,
+        "unit": "us/step", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+        "us_per_layer_step": ms * 1e3 / layers, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic; one layer's KV cache shared by the 32 layer trackers",
+        "config": {"workload": "C3: batch 16 x 128k context, 32 layers, Llama-3.1-8B shapes, "
+                               "Top-k 5%", "batch": batch, "batch_per_gpu": b_local,
+                   "context": ctx, "layers": layers, "topk_fraction": frac,
+                   "l2": "flushed before every timed step"},
+        "clocks": clock_info, "setup_s": setup_s}), flush=True)
+
+
 def main():
     args = parse()
     world, rank, local = dist_setup()
@@ -620,7 +700,10 @@ def main():
         run_reference(args, world, rank)
         return
     dist_init(world, local)
-    run_ours(args, world, rank, local)
+    if args.config == "c3":
+        run_c3(args, world, rank, local)
+    else:
+        run_ours(args, world, rank, local)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -76,7 +76,7 @@ class BatchedSession:
 
     def __init__(self, cfg: LfpsConfig, batch: int, kv_heads: int, group: int, n_max: int,
                  m_cap: int | None = None, device: torch.device | str | None = None,
-                 export_sets: bool = False):
+                 export_sets: bool = False, kv_cache: tuple | None = None):
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
         device = torch.device(device)
@@ -107,9 +107,18 @@ class BatchedSession:
         self.sla_cap = _lib.slash_capacity(self.dims)
         dev = self.device
         f64, i32 = torch.float64, torch.int32
-        self.k_cache = torch.zeros(batch, kv_heads, self.n_max, cfg.d, dtype=torch.bfloat16,
-                                   device=dev)
-        self.v_cache = torch.zeros_like(self.k_cache)
+        if kv_cache is not None:
+            # an existing cache (e.g. one layer's rows reused by other layers'
+            # trackers): bf16 [batch, kv_heads, n_max, d] pair on this device
+            self.k_cache, self.v_cache = kv_cache
+            shape = (batch, kv_heads, self.n_max, cfg.d)
+            for t in (self.k_cache, self.v_cache):
+                if tuple(t.shape) != shape or t.dtype != torch.bfloat16 or t.device != dev:
+                    raise ValueError(f"kv_cache tensors must be bf16 {shape} on {dev}")
+        else:
+            self.k_cache = torch.zeros(batch, kv_heads, self.n_max, cfg.d, dtype=torch.bfloat16,
+                                       device=dev)
+            self.v_cache = torch.zeros_like(self.k_cache)
         self.n_ctx = torch.zeros(batch, dtype=i32, device=dev)
         self.n_host = [0] * batch
         self.ver = torch.zeros(self.NS, m_cap, dtype=f64, device=dev)
@@ -257,6 +266,20 @@ class BatchedSession:
         self.n_host = [n + 1 for n in self.n_host]
         self.step_count += 1
         return self.result()
+
+    def copy_tracker_from(self, other: "BatchedSession"):
+        """Take over another session's tracker state, priors and context
+        counts (same dims): e.g. one layer's bootstrap reused by other layers.
+        The block summaries of this session's workspace are rebuilt by its
+        first step."""
+        if (self.B, self.Hkv, self.G, self.m_cap, self.sla_cap) != \
+                (other.B, other.Hkv, other.G, other.m_cap, other.sla_cap):
+            raise ValueError("sessions differ in shape")
+        for name in ("ver", "sla", "scale", "sla_base", "clamp_count", "mean_key", "mean_value",
+                     "sigma_hat_sq", "n_ctx"):
+            getattr(self, name).copy_(getattr(other, name))
+        self.n_host = list(other.n_host)
+        self.ws_buf.zero_()
 
     def append_rows(self, k_new: torch.Tensor, v_new: torch.Tensor):
         """Append one K/V row per unit WITHOUT an LFPS step (store.append,
