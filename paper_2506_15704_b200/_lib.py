@@ -14,7 +14,10 @@ import threading
 
 from .errors import DeviceError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "liblfps_b200.so")
+# LFPS_LIB selects another in-tree build of the same sources (tools/build_variant.sh
+# experiments); the default is the library __graft_entry__.build() makes
+LIB_PATH = os.environ.get("LFPS_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "lib", "liblfps_b200.so")
 ABI_VERSION = 2
 FLAG_EXPORT_SETS = 1
 FLAG_TRACE = 2

@@ -44,16 +44,7 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
   float* pz = c.probe_score + (size_t)s * c.list_cap;
   const __nv_bfloat16* kb = krow(c, b, h, 0);
   const __nv_bfloat16* vb = vrow(c, b, h, 0);
-  // q as (partial a, partial b) element pairs
-  float2 q2[PQ];
-  {
-    const Part<PQ> qp = ld_part<PQ>(q + (size_t)s * c.d, l8);
-#pragma unroll
-    for (int t = 0; t < PQ / 2; ++t) {
-      q2[2 * t] = make_float2(bf_lo(qp.a[t]), bf_lo(qp.b[t]));
-      q2[2 * t + 1] = make_float2(bf_hi(qp.a[t]), bf_hi(qp.b[t]));
-    }
-  }
+  const Part<PQ> qp = ld_part<PQ>(q + (size_t)s * c.d, l8);   // packed bf16 partials of q
   int k = (int)rint(c.frac * (double)n);
   if (k < 1) k = 1;
   int* c2i = c.c2_idx + (size_t)s * c.list_cap;
@@ -63,36 +54,51 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
 
   Attn<PQ> at;
   at.init();
-  int bad = 0;
+  float chk = 0.0f;                                     // NaN once any score is not finite
   float mxc = -INFINITY;                                // max C2 score of this group
+  float* c2zS = c2z - S;                                // indexed by list entry rid >= S
+  float* pzS = pz - S;
+  const int* pidxS = pidx - S;
 
   if (k >= p) {
     // ---- C2 = probe (the common case): score and attend in ONE pass ---------------------
+    auto keep = [&](int rid, float z) {                 // a C2 / sink score of this group
+      chk = __fmaf_rn(z, 0.0f, chk);
+      if (rid >= S) {
+        mxc = fmaxf(mxc, z);
+        if (l8 == 0) c2zS[rid] = z;
+      } else if (l8 == 0) {
+        sh.sink_z[rid] = z;
+      }
+    };
     stream_rows<kFused, PQ>(
-        c, stages, kb, vb, S + p,
-        [&](int rid) { return rid < S ? rid : __ldg(pidx + rid - S); },
-        [&](int rid, const __nv_bfloat16* kr, const __nv_bfloat16* vr) {
-          const float z = row_score<PQ>(ld_part<PQ>(kr, l8), q2, c.sqrt_d_f32);
-          bad |= !isfinite(z);
-          if (rid >= S) {
-            mxc = fmaxf(mxc, z);
-            if (l8 == 0) c2z[rid - S] = z;
-          } else if (l8 == 0) {
-            sh.sink_z[rid] = z;
+        stages, kb, vb, S + p, [&](int rid) { return rid < S ? rid : __ldg(pidxS + rid); },
+        [&](const Rows2& r) {
+          const float2 z = score_rows<PQ>(r, qp, c.sqrt_d_f32);
+          if (r.ok[1]) {
+            keep(r.rid[0], z.x);
+            keep(r.rid[1], z.y);
+            at.absorb2(z.x * kLog2e, ld_part_s<PQ>(r.v[0], l8), z.y * kLog2e, ld_part_s<PQ>(r.v[1], l8));
+          } else if (r.ok[0]) {
+            keep(r.rid[0], z.x);
+            at.absorb(z.x * kLog2e, ld_part_s<PQ>(r.v[0], l8));
           }
-          at.absorb(z, ld_part<PQ>(vr, l8));
         });
     for (int j = tid; j < p; j += kThreads) c2i[j] = __ldg(pidx + j);
   } else {
     // ---- scores of the sinks and the probe rows -------------------------------------------
     stream_rows<kScore, PQ>(
-        c, stages, kb, vb, S + p,
-        [&](int rid) { return rid < S ? rid : __ldg(pidx + rid - S); },
-        [&](int rid, const __nv_bfloat16* kr, const __nv_bfloat16*) {
-          const float z = row_score<PQ>(ld_part<PQ>(kr, l8), q2, c.sqrt_d_f32);
+        stages, kb, vb, S + p, [&](int rid) { return rid < S ? rid : __ldg(pidxS + rid); },
+        [&](const Rows2& r) {
+          const float2 z = score_rows<PQ>(r, qp, c.sqrt_d_f32);
           if (l8 == 0) {
-            if (rid < S) sh.sink_z[rid] = z;
-            else pz[rid - S] = z;
+#pragma unroll
+            for (int i = 0; i < kR; ++i) {
+              if (!r.ok[i]) continue;
+              const float zi = i ? z.y : z.x;
+              if (r.rid[i] < S) sh.sink_z[r.rid[i]] = zi;
+              else pzS[r.rid[i]] = zi;
+            }
           }
         });
     // ---- Top-k: MSB-first radix select of the k-th largest key ---------------------------
@@ -158,14 +164,21 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
     }
     __syncthreads();
     // ---- attention over sinks u C2 ------------------------------------------------------
+    auto zof = [&](int rid) {
+      const float z = rid < S ? sh.sink_z[rid] : c2zS[rid];
+      chk = __fmaf_rn(z, 0.0f, chk);
+      if (rid >= S) mxc = fmaxf(mxc, z);
+      return z * kLog2e;
+    };
     stream_rows<kAttend, PQ>(
-        c, stages, kb, vb, S + k2,
-        [&](int rid) { return rid < S ? rid : c2i[rid - S]; },
-        [&](int rid, const __nv_bfloat16*, const __nv_bfloat16* vr) {
-          const float z = rid < S ? sh.sink_z[rid] : c2z[rid - S];
-          bad |= !isfinite(z);
-          if (rid >= S) mxc = fmaxf(mxc, z);
-          at.absorb(z, ld_part<PQ>(vr, l8));
+        stages, kb, vb, S + k2, [&](int rid) { return rid < S ? rid : c2i[rid - S]; },
+        [&](const Rows2& r) {
+          if (r.ok[1]) {
+            const float za = zof(r.rid[0]), zb = zof(r.rid[1]);
+            at.absorb2(za, ld_part_s<PQ>(r.v[0], l8), zb, ld_part_s<PQ>(r.v[1], l8));
+          } else if (r.ok[0]) {
+            at.absorb(zof(r.rid[0]), ld_part_s<PQ>(r.v[0], l8));
+          }
         });
   }
 
@@ -192,7 +205,7 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
     for (int xi = 0; xi < kPer; ++xi) {
       const int x = g * kPer + xi;
       if (sh.part_m[x] == -INFINITY) continue;
-      const float f = __expf(sh.part_m[x] - M);
+      const float f = ex2(sh.part_m[x] - M);
       num = fmaf(f, part[x * D + t], num);
       den = fmaf(f, sh.part_s[x], den);
     }
@@ -213,7 +226,7 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
 
   trace_at(c, s, 9, t0);
   // ---- data checks and the update weights u (committed by k_update.cu) ----------------
-  if (__syncthreads_or(bad)) {
+  if (__syncthreads_or(!(chk == 0.0f))) {
     if (tid == 0) set_err(c, s, LFPS_ERR_NONFINITE_SCORES);
     return;
   }

@@ -23,7 +23,7 @@ struct AttendShared {
 };
 
 template <int PQ>
-__global__ void __launch_bounds__(kThreads, 3) lfps_exact_attend_kernel(Ctx c, const __nv_bfloat16* q) {
+__global__ void __launch_bounds__(kThreads, kRowCtas) lfps_exact_attend_kernel(Ctx c, const __nv_bfloat16* q) {
   extern __shared__ __align__(128) uint8_t stages[];
   __shared__ AttendShared sh;
   const int s = blockIdx.x, tid = threadIdx.x;
@@ -35,28 +35,25 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_exact_attend_kernel(Ctx c, c
   const float* c2z = c.c2_score + (size_t)s * c.list_cap;
   const __nv_bfloat16* kb = krow(c, b, h, 0);
   const __nv_bfloat16* vb = vrow(c, b, h, 0);
-  float2 q2[PQ];
-  {
-    const Part<PQ> qp = ld_part<PQ>(q + (size_t)s * c.d, l8);
-#pragma unroll
-    for (int t = 0; t < PQ / 2; ++t) {
-      q2[2 * t] = make_float2(bf_lo(qp.a[t]), bf_lo(qp.b[t]));
-      q2[2 * t + 1] = make_float2(bf_hi(qp.a[t]), bf_hi(qp.b[t]));
-    }
-  }
+  const Part<PQ> qp = ld_part<PQ>(q + (size_t)s * c.d, l8);
   stream_rows<kScore, PQ>(
-      c, stages, kb, vb, S, [&](int rid) { return rid; },
-      [&](int rid, const __nv_bfloat16* kr, const __nv_bfloat16*) {
-        const float z = row_score<PQ>(ld_part<PQ>(kr, l8), q2, c.sqrt_d_f32);
-        if (l8 == 0) sh.sink_z[rid] = z;
+      stages, kb, vb, S, [&](int rid) { return rid; },
+      [&](const Rows2& r) {
+        const float2 z = score_rows<PQ>(r, qp, c.sqrt_d_f32);
+        if (l8 == 0 && r.ok[0]) sh.sink_z[r.rid[0]] = z.x;
+        if (l8 == 0 && r.ok[1]) sh.sink_z[r.rid[1]] = z.y;
       });
   Attn<PQ> at;
   at.init();
+  auto zof = [&](int rid) { return (rid < S ? sh.sink_z[rid] : __ldg(c2z + rid - S)) * kLog2e; };
   stream_rows<kAttend, PQ>(
-      c, stages, kb, vb, S + k2, [&](int rid) { return rid < S ? rid : __ldg(c2i + rid - S); },
-      [&](int rid, const __nv_bfloat16*, const __nv_bfloat16* vr) {
-        const float z = rid < S ? sh.sink_z[rid] : __ldg(c2z + rid - S);
-        at.absorb(z, ld_part<PQ>(vr, l8));
+      stages, kb, vb, S + k2, [&](int rid) { return rid < S ? rid : __ldg(c2i + rid - S); },
+      [&](const Rows2& r) {
+        if (r.ok[1]) {
+          at.absorb2(zof(r.rid[0]), ld_part_s<PQ>(r.v[0], l8), zof(r.rid[1]), ld_part_s<PQ>(r.v[1], l8));
+        } else if (r.ok[0]) {
+          at.absorb(zof(r.rid[0]), ld_part_s<PQ>(r.v[0], l8));
+        }
       });
   // merge the 32 group states (stages reused as scratch)
   constexpr int D = PQ * 16;
@@ -79,7 +76,7 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_exact_attend_kernel(Ctx c, c
   for (int xi = 0; xi < kPer; ++xi) {
     const int x = g * kPer + xi;
     if (sh.part_m[x] == -INFINITY) continue;
-    const float f = __expf(sh.part_m[x] - M);
+    const float f = ex2(sh.part_m[x] - M);
     num = fmaf(f, part[x * D + t], num);
     den = fmaf(f, sh.part_s[x], den);
   }
@@ -100,7 +97,7 @@ __global__ void __launch_bounds__(kThreads, 3) lfps_exact_attend_kernel(Ctx c, c
 
 template <int PQ>
 cudaError_t launch_attend_d(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
-  const size_t smem = (size_t)kStages * kTile * (c.d * 2) * 2;
+  const size_t smem = rows_smem(c.d);
   static bool set = false;
   if (!set) {
     cudaError_t e = cudaFuncSetAttribute(lfps_exact_attend_kernel<PQ>,

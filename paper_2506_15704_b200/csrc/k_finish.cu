@@ -4,16 +4,18 @@
 // committed by k_update.cu once every session has passed).  One 256-thread
 // CTA per (request, q-head) session.
 //
-//   rows     K / V rows stream through shared memory in tiles of 32 rows,
-//            4 stages deep, gathered with cp.async (16 B per thread, L2
-//            only): no registers hold in-flight data.  (Per-row TMA bulk
-//            copies were measured 2x slower: one 256-B request per row
-//            saturates the SM's TMA unit.)
+//   rows     K / V rows stream through shared memory in tiles of 64 rows
+//            (two per 8-lane group), 2 stages deep, gathered with cp.async
+//            (16 B per thread, L2 only): no registers hold in-flight data;
+//            64 KB per CTA -> 3 CTAs / SM.  (Per-row TMA bulk copies were
+//            measured 2x slower: one 256-B request per row saturates the SM's
+//            TMA unit; 3 stages at 2 CTAs / SM measured slower than 2 at 3.)
 //   scores   z_j = (K[j] . q) / fp32(sqrt d) in the canonical order of
 //            devmath.sdot32 (engine.py:168-170): 8 lanes per row, lane l
 //            owns partials l and l + 8 (d/16 contiguous elements each, two
-//            sequential chains in one packed FFMA2), fold 8 (in-lane), 4, 2,
-//            1 (shuffles), IEEE division
+//            chains of fma.rn.f32.bf16 -- no bf16 widening), fold 8
+//            (in-lane), 4, 2, 1 (shuffles; the group's two rows share them
+//            in a reduce-scatter), IEEE division
 //   top-k    k = max(1, round_half_even(frac * n)) (engine.py:167); if
 //            k >= |probe| C2 = probe and scores + attention are ONE pass
 //            over the rows; else all scores first, an MSB-first 4 x 8-bit
@@ -21,8 +23,9 @@
 //            (topk_from_scores, attention.py:34-47), then the attention pass
 //   attend   joint softmax over [sink logits, C2 logits] and sum w V
 //            (engine.py:173-181): every 8-lane group keeps an online
-//            (max, sum, acc) over its rows (packed fp32x2 FMAs), the 32
-//            group states are merged at the end (fp32)
+//            (max, sum, acc) over its rows in the base-2 domain (MUFU.EX2,
+//            packed fp32x2 FMAs), the 32 group states are merged at the end
+//            (fp32)
 //   checks   sinks and C2 scores finite (softmax_weights, numerics.py:61-62,
 //            called at engine.py:177 and :184); u = canonical fp64 softmax
 //            of the C2 scores (devmath.softmax_update) written to uw for the
@@ -36,7 +39,7 @@ namespace {
 using namespace fin;
 
 template <int PQ>
-__global__ void __launch_bounds__(kThreads, 4) lfps_finish_kernel(Ctx c, const __nv_bfloat16* q) {
+__global__ void __launch_bounds__(kThreads, kRowCtas) lfps_finish_kernel(Ctx c, const __nv_bfloat16* q) {
   extern __shared__ __align__(128) uint8_t stages[];      // kStages x [K tile | V tile]
   __shared__ FinishShared sh;
   finish_session<PQ>(c, q, c.s_off + blockIdx.x, stages, sh);
@@ -44,7 +47,7 @@ __global__ void __launch_bounds__(kThreads, 4) lfps_finish_kernel(Ctx c, const _
 
 template <int PQ>
 cudaError_t launch_finish_d(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
-  const size_t smem = (size_t)kStages * kTile * (c.d * 2) * 2;
+  const size_t smem = rows_smem(c.d);
   static bool set = false;
   if (!set) {
     cudaError_t e = cudaFuncSetAttribute(lfps_finish_kernel<PQ>,

@@ -137,6 +137,13 @@ __device__ __forceinline__ double group_canon_sum(const double* acc, int g, int 
   return a[0];
 }
 
+// bytes of the stage region: the unit pipeline's stages (padded V rows), or
+// the per-session fallback's stream_rows stages if larger
+__host__ __device__ constexpr size_t unit_stage_bytes(int d) {
+  return (size_t)kStages * kTile * (d * 2 + d * 2 + 16) > rows_smem(d)
+             ? (size_t)kStages * kTile * (d * 2 + d * 2 + 16) : rows_smem(d);
+}
+
 template <int PQ, int G>
 __global__ void __launch_bounds__(kThreads, 2) lfps_finish_unit_kernel(Ctx c, const __nv_bfloat16* q) {
   extern __shared__ __align__(128) uint8_t dyn[];
@@ -144,10 +151,11 @@ __global__ void __launch_bounds__(kThreads, 2) lfps_finish_unit_kernel(Ctx c, co
   constexpr int kRowB = D * 2;
   constexpr int kVStride = kRowB + 16;                   // padded V rows (ldmatrix.trans)
   constexpr int kStageB = kTile * (kRowB + kVStride);
-  uint8_t* stages = dyn;                                 // kStages x [K tile | V tile]
-  __nv_bfloat16* atile = reinterpret_cast<__nv_bfloat16*>(dyn + kStages * kStageB);
-  UnitShared& sh = *reinterpret_cast<UnitShared*>(dyn + kStages * kStageB +
-                                                  kMaxG * kARows * kAStride * 2);
+  // kStages x [K tile | V tile]; also the per-session fallback's stream_rows stages
+  constexpr size_t kStageTot = unit_stage_bytes(D);
+  uint8_t* stages = dyn;
+  __nv_bfloat16* atile = reinterpret_cast<__nv_bfloat16*>(dyn + kStageTot);
+  UnitShared& sh = *reinterpret_cast<UnitShared*>(dyn + kStageTot + kMaxG * kARows * kAStride * 2);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, l8 = tid & 7, grp = tid >> 3;
   const int u = blockIdx.x;
   const int b = u / c.Hkv, h = u % c.Hkv;
@@ -582,8 +590,7 @@ __global__ void __launch_bounds__(kThreads, 2) lfps_finish_unit_kernel(Ctx c, co
 cudaError_t launch_finish_unit(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
   auto go = [&](auto kern, int pq) -> cudaError_t {
     const int d = pq * 16;
-    const size_t smem = (size_t)kStages * kTile * (d * 2 + d * 2 + 16) +
-                        (size_t)kMaxG * kARows * kAStride * 2 + sizeof(UnitShared);
+    const size_t smem = unit_stage_bytes(d) + (size_t)kMaxG * kARows * kAStride * 2 + sizeof(UnitShared);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<c.B * c.Hkv, kThreads, smem, st>>>(c, q);

@@ -1,7 +1,7 @@
 // rows.cuh -- shared machinery of the row-gather kernels (k_finish.cu,
-// k_attend.cu, k_score.cu): canonical fp32 row scores in 8-lane groups with
-// packed FFMA2, the online-softmax attention state, and the cp.async-staged
-// row pipeline.  256-thread CTAs.
+// k_attend.cu, k_score.cu): canonical fp32 row scores in 8-lane groups, the
+// online-softmax attention state, and the cp.async-staged row pipeline.
+// 256-thread CTAs.
 #pragma once
 
 #include "common.cuh"
@@ -14,8 +14,21 @@ namespace rows {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kGroups8 = kThreads / 8;   // 8-lane row groups
-constexpr int kTile = 32;                // rows per stage (one per row group)
-constexpr int kStages = 3;
+constexpr int kTile = 32;                // k_finish_unit.cu: rows per stage (one per row group)
+constexpr int kStages = 3;               // k_finish_unit.cu: stages
+constexpr int kR = 2;                    // stream_rows: max rows per 8-lane group per tile
+// rows per group per tile for d = 16 PQ: two (one tile = 64 rows), one for
+// d = 256 so that a stage stays at 32 KB
+__host__ __device__ constexpr int rows_per_group(int pq) { return pq >= 16 ? 1 : 2; }
+#ifndef LFPS_ROW_STAGES
+#define LFPS_ROW_STAGES 2
+#endif
+constexpr int kStagesR = LFPS_ROW_STAGES;   // stream_rows: stages
+constexpr int kRowCtas = kStagesR == 2 ? 3 : 2;   // resident stream_rows CTAs per SM (smem)
+// dynamic shared memory of a stream_rows kernel (K block + V block per stage)
+__host__ __device__ constexpr size_t rows_smem(int d) {
+  return (size_t)kStagesR * kGroups8 * rows_per_group(d / 16) * d * 2 * 2;
+}
 constexpr int kCanon = 256;              // canonical block-sum width (devmath.BLOCK_THREADS)
 constexpr int kMaxE = 8;                 // exponentials cached per thread (|C2| <= 2048)
 
@@ -74,23 +87,105 @@ __device__ __forceinline__ Part<PQ> ld_part(const __nv_bfloat16* row, int l8) {
   return r;
 }
 
-// canonical fp32 dot of one row with q (devmath.sdot32) -> z, all 8 lanes
+// fma.rn.f32.bf16 (FHFMA.BF16): the exact bf16 x bf16 product added to an
+// fp32 accumulator with ONE rounding -- the same IEEE operation as FFMA of the
+// widened operands, without the widening (bit identity over 2^30 patterns
+// incl. subnormals, and full FFMA issue rate: profiles/r01_arith_probe.txt).
+// lo / hi select the bf16 halves of packed words.
+__device__ __forceinline__ float fma_lo(uint32_t a, uint32_t b, float c) {
+  float d;
+  asm("{\n\t.reg .b16 al, ah, bl, bh;\n\t"
+      "mov.b32 {al, ah}, %1;\n\tmov.b32 {bl, bh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, al, bl, %3;\n\t}"
+      : "=f"(d) : "r"(a), "r"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float fma_hi(uint32_t a, uint32_t b, float c) {
+  float d;
+  asm("{\n\t.reg .b16 al, ah, bl, bh;\n\t"
+      "mov.b32 {al, ah}, %1;\n\tmov.b32 {bl, bh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, ah, bh, %3;\n\t}"
+      : "=f"(d) : "r"(a), "r"(b), "f"(c));
+  return d;
+}
+
+// canonical partials of one row (devmath.sdot32): lane l8 accumulates partial
+// l8 (pa) and partial l8 + 8 (pb), d/16 contiguous elements each in order from
+// +0, then folds 8 in-lane; k and q are packed bf16
 template <int PQ>
-__device__ __forceinline__ float row_score(const Part<PQ>& k, const float2* q2, float sqrt_d) {
-  float2 p = make_float2(0.0f, 0.0f);
+__device__ __forceinline__ float row_dot(const Part<PQ>& k, const Part<PQ>& q) {
+  float pa = 0.0f, pb = 0.0f;
 #pragma unroll
   for (int t = 0; t < PQ / 2; ++t) {
-    p = ffma2(make_float2(bf_lo(k.a[t]), bf_lo(k.b[t])), q2[2 * t], p);
-    p = ffma2(make_float2(bf_hi(k.a[t]), bf_hi(k.b[t])), q2[2 * t + 1], p);
+    pa = fma_lo(k.a[t], q.a[t], pa);
+    pb = fma_lo(k.b[t], q.b[t], pb);
+    pa = fma_hi(k.a[t], q.a[t], pa);
+    pb = fma_hi(k.b[t], q.b[t], pb);
   }
-  float v = __fadd_rn(p.x, p.y);                        // fold 8 (in-lane)
-  // only this 8-lane group takes part: groups of a warp may hold no row
-  const unsigned gm = 0xffu << (threadIdx.x & 24);
+  return __fadd_rn(pa, pb);
+}
+
+// canonical fp32 score of one row per 8-lane group -> z in all 8 lanes: fold
+// 4, 2, 1 across the group, IEEE division.  Every lane of the warp must call
+// it (full-warp shuffles): groups without a row pass any finite data.
+template <int PQ>
+__device__ __forceinline__ float row_score(const Part<PQ>& k, const Part<PQ>& q, float sqrt_d) {
+  float v = row_dot<PQ>(k, q);
 #pragma unroll
-  for (int h = 4; h >= 1; h >>= 1) v = __fadd_rn(v, __shfl_xor_sync(gm, v, h));
+  for (int h = 4; h >= 1; h >>= 1) v = __fadd_rn(v, __shfl_xor_sync(LFPS_FULL, v, h));
   return __fdiv_rn(v, sqrt_d);
 }
 
+// ld_part from a 32-bit shared-window address (row start)
+template <int PQ>
+__device__ __forceinline__ Part<PQ> ld_part_s(uint32_t row, int l8) {
+  Part<PQ> r;
+  if constexpr (PQ % 8 == 0) {
+#pragma unroll
+    for (int t = 0; t < PQ / 2; t += 4) {
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(r.a[t]), "=r"(r.a[t + 1]), "=r"(r.a[t + 2]), "=r"(r.a[t + 3])
+                   : "r"(row + (l8 * (PQ / 2) + t) * 4));
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(r.b[t]), "=r"(r.b[t + 1]), "=r"(r.b[t + 2]), "=r"(r.b[t + 3])
+                   : "r"(row + ((l8 + 8) * (PQ / 2) + t) * 4));
+    }
+  } else if constexpr (PQ == 4) {
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(r.a[0]), "=r"(r.a[1]) : "r"(row + l8 * 8));
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(r.b[0]), "=r"(r.b[1]) : "r"(row + (l8 + 8) * 8));
+  } else {
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(r.a[0]) : "r"(row + l8 * 4));
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(r.b[0]) : "r"(row + (l8 + 8) * 4));
+  }
+  return r;
+}
+
+// canonical scores of TWO rows per 8-lane group (a, b) -> (z_a, z_b) in all 8
+// lanes.  Reduce-scatter: lanes 0-3 fold row a, lanes 4-7 row b, so one
+// shuffle serves both rows at fold 4 and each lane divides once.  Every add
+// is x_l + x_(l^h) of the same canonical tree as row_score (IEEE addition
+// commutes), so the scores are bit-identical to devmath.sdot32.
+template <int PQ>
+__device__ __forceinline__ float2 row_score2(const Part<PQ>& ka, const Part<PQ>& kb,
+                                             const Part<PQ>& q, float sqrt_d) {
+  const float va = row_dot<PQ>(ka, q), vb = row_dot<PQ>(kb, q);
+  const bool hi = (threadIdx.x & 4) != 0;
+  float v = __fadd_rn(hi ? vb : va, __shfl_xor_sync(LFPS_FULL, hi ? va : vb, 4));
+  v = __fadd_rn(v, __shfl_xor_sync(LFPS_FULL, v, 2));
+  v = __fadd_rn(v, __shfl_xor_sync(LFPS_FULL, v, 1));
+  const float z = __fdiv_rn(v, sqrt_d);
+  const float zo = __shfl_xor_sync(LFPS_FULL, z, 4);
+  return hi ? make_float2(zo, z) : make_float2(z, zo);
+}
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+// 2^x (MUFU.EX2, flush-to-zero): softmax weights in the base-2 domain
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // exclusive block scan over the 256 threads
 __device__ __forceinline__ int scan256(int v, int* warp_sums, int* total) {
@@ -133,7 +228,9 @@ __device__ __forceinline__ double canon_sum(double acc, double* red) {
   return out;
 }
 
-// Online-softmax state of one 8-lane row group (all 8 lanes hold m, s).
+// Online-softmax state of one 8-lane row group (all 8 lanes hold m, s), in
+// the base-2 domain: absorb() takes zl = z * log2(e), weights are
+// 2^(zl - m).  fp32, checked against the fp64 oracle to a tolerance.
 template <int PQ>
 struct Attn {
   float m, s;
@@ -144,15 +241,15 @@ struct Attn {
 #pragma unroll
     for (int e = 0; e < PQ; ++e) acc[e] = make_float2(0.0f, 0.0f);
   }
-  __device__ __forceinline__ void absorb(float z, const Part<PQ>& v) {
-    if (z > m) {
-      const float r = __expf(m - z);
+  __device__ __forceinline__ void absorb(float zl, const Part<PQ>& v) {
+    if (zl > m) {
+      const float r = ex2(m - zl);
       s *= r;
 #pragma unroll
       for (int e = 0; e < PQ; ++e) acc[e] = fmul2(acc[e], make_float2(r, r));
-      m = z;
+      m = zl;
     }
-    const float w = __expf(z - m);
+    const float w = ex2(zl - m);
     s += w;
     const float2 w2 = make_float2(w, w);
 #pragma unroll
@@ -161,62 +258,142 @@ struct Attn {
       acc[2 * t + 1] = ffma2(make_float2(bf_hi(v.a[t]), bf_hi(v.b[t])), w2, acc[2 * t + 1]);
     }
   }
+  // two rows at once (one max test / rescale)
+  __device__ __forceinline__ void absorb2(float za, const Part<PQ>& va, float zb, const Part<PQ>& vb) {
+    const float zm = fmaxf(za, zb);
+    if (zm > m) {
+      const float r = ex2(m - zm);
+      s *= r;
+#pragma unroll
+      for (int e = 0; e < PQ; ++e) acc[e] = fmul2(acc[e], make_float2(r, r));
+      m = zm;
+    }
+    const float wa = ex2(za - m), wb = ex2(zb - m);
+    s += wa + wb;
+    const float2 a2 = make_float2(wa, wa), b2 = make_float2(wb, wb);
+#pragma unroll
+    for (int t = 0; t < PQ / 2; ++t) {
+      acc[2 * t] = ffma2(make_float2(bf_lo(va.a[t]), bf_lo(va.b[t])), a2, acc[2 * t]);
+      acc[2 * t + 1] = ffma2(make_float2(bf_hi(va.a[t]), bf_hi(va.b[t])), a2, acc[2 * t + 1]);
+    }
+#pragma unroll
+    for (int t = 0; t < PQ / 2; ++t) {
+      acc[2 * t] = ffma2(make_float2(bf_lo(vb.a[t]), bf_lo(vb.b[t])), b2, acc[2 * t]);
+      acc[2 * t + 1] = ffma2(make_float2(bf_hi(vb.a[t]), bf_hi(vb.b[t])), b2, acc[2 * t + 1]);
+    }
+  }
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// Stream rows [0, nrows) through shared memory, kStages tiles of kTile rows
-// deep: every thread copies 16-byte chunks of one row (cp.async, L2 only),
-// 8 threads per row; row_of(rid) gives the cache row of list entry rid, and
-// visit(rid, k_row, v_row) consumes a staged row (8-lane group `grp` owns
-// tile row `grp`).  Each thread fetches its row index one tile before it
-// issues the copies, so the index load is off the critical path.
+// The rows of one tile an 8-lane group owns: tile rows grp and grp + 32
+// (row 1 only when rows_per_group = 2; otherwise ok[1] = false).  rid = list
+// entry, ok = rid < nrows (ok[1] implies ok[0]), k / v = 32-bit shared
+// addresses of the staged K and V rows.
+struct Rows2 {
+  int rid[kR];
+  bool ok[kR];
+  uint32_t k[kR], v[kR];
+};
+
+// scores of a group's staged rows (k[0], k[1] when present) -> (z0, z1)
+template <int PQ, typename RowsT>
+__device__ __forceinline__ float2 score_rows(const RowsT& r, const Part<PQ>& q, float sqrt_d) {
+  const int l8 = threadIdx.x & 7;
+  if constexpr (rows_per_group(PQ) == 2) {
+    return row_score2<PQ>(ld_part_s<PQ>(r.k[0], l8), ld_part_s<PQ>(r.k[1], l8), q, sqrt_d);
+  } else {
+    const float z = row_score<PQ>(ld_part_s<PQ>(r.k[0], l8), q, sqrt_d);
+    return make_float2(z, z);
+  }
+}
+
+// Stream rows [0, nrows) through shared memory, kStagesR tiles of
+// 32 x rows_per_group rows deep: every thread copies 16-byte chunks of its group's rows
+// (cp.async, L2 only), 8 threads per row; row_of(rid) gives the cache row of
+// list entry rid.  visit(const Rows2&) is called by EVERY thread for every
+// tile, so visits may use full-warp shuffles; a row with ok = false has a
+// stale stage slot (any bits) that the visit must not commit.  Each thread
+// fetches its row indices one tile before it issues the copies, so the index
+// loads are off the critical path.
 template <int MODE, int PQ, typename RowOf, typename Visit>
-__device__ __forceinline__ void stream_rows(const Ctx& c, uint8_t* stages,
-                                            const __nv_bfloat16* kb, const __nv_bfloat16* vb,
-                                            int nrows, RowOf row_of, Visit visit) {
+__device__ __forceinline__ void stream_rows(uint8_t* stages, const __nv_bfloat16* kb,
+                                            const __nv_bfloat16* vb, int nrows, RowOf row_of,
+                                            Visit visit) {
   constexpr bool kK = MODE != kAttend, kV = MODE != kScore;
   constexpr int D = PQ * 16;
   constexpr int kRowB = D * 2;                        // bytes per row
   constexpr int kChunks = kRowB / 16;                 // 16-byte chunks per row
-  constexpr int kStageB = kTile * kRowB * 2;          // K block then V block
+  constexpr int R = rows_per_group(PQ);
+  constexpr int kTileR = kGroups8 * R;                // rows per tile
+  constexpr int kBlkB = kTileR * kRowB;               // K block (then V block) of a stage
+  constexpr int kStageB = 2 * kBlkB;
+  constexpr int kRowStep = kGroups8 * kRowB;          // group row 0 -> group row 1
   const int grp = threadIdx.x >> 3, l8 = threadIdx.x & 7;
-  const int ntiles = (nrows + kTile - 1) / kTile;
-  auto fetch = [&](int tile) {
-    const int rid = tile * kTile + grp;
-    return (tile < ntiles && rid < nrows) ? row_of(rid) : -1;
-  };
-  auto issue = [&](int tile, int row) {
-    if (tile < ntiles && row >= 0) {
-      uint8_t* st = stages + (size_t)(tile % kStages) * kStageB + grp * kRowB;
+  const int ntiles = (nrows + kTileR - 1) / kTileR;
+  const uint32_t sb = smem_u32(stages) + grp * kRowB;
+  const uint32_t my_cp = sb + l8 * 16;                // this thread's first chunk, stage 0
+  const uint8_t* kb8 = reinterpret_cast<const uint8_t*>(kb) + l8 * 16;
+  const uint8_t* vb8 = reinterpret_cast<const uint8_t*>(vb) + l8 * 16;
+  auto fetch = [&](int tile, int* row) {
 #pragma unroll
-      for (int ch = l8; ch < kChunks; ch += 8) {
-        if (kK) cp_async16(st + ch * 16, reinterpret_cast<const uint8_t*>(kb + (size_t)row * D) + ch * 16);
-        if (kV) cp_async16(st + kTile * kRowB + ch * 16,
-                           reinterpret_cast<const uint8_t*>(vb + (size_t)row * D) + ch * 16);
+    for (int r = 0; r < R; ++r) {
+      const int rid = tile * kTileR + r * kGroups8 + grp;
+      row[r] = rid < nrows ? row_of(rid) : -1;        // rid >= nrows also past the last tile
+    }
+  };
+  auto issue = [&](int stage, const int* row) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (row[r] >= 0) {
+        const uint32_t st = my_cp + stage * kStageB + r * kRowStep;
+        const size_t off = (size_t)row[r] * kRowB;
+#pragma unroll
+        for (int ch = 0; ch < kChunks; ch += 8) {
+          if (kChunks % 8 != 0 && ch + l8 >= kChunks) continue;   // d = 32: 4 chunks per row
+          if (kK) cp_async16_s(st + ch * 16, kb8 + off + ch * 16);
+          if (kV) cp_async16_s(st + kBlkB + ch * 16, vb8 + off + ch * 16);
+        }
       }
     }
     cp_async_commit();                                // one group per tile, even if empty
   };
+  int ahead[kR];
 #pragma unroll 1
-  for (int t = 0; t < kStages - 1; ++t) issue(t, fetch(t));
-  int ahead = fetch(kStages - 1);
+  for (int t = 0; t < kStagesR - 1; ++t) {
+    fetch(t, ahead);
+    issue(t, ahead);
+  }
+  fetch(kStagesR - 1, ahead);
+  int rs = 0, ws = kStagesR - 1;                      // read / write stages
 #pragma unroll 1
   for (int tile = 0; tile < ntiles; ++tile) {
-    cp_async_wait<kStages - 2>();                     // this thread's copies of `tile` landed
+    cp_async_wait<kStagesR - 2>();                    // this thread's copies of `tile` landed
     __syncthreads();                                  // everyone's; stage (tile - 1) is free
-    issue(tile + kStages - 1, ahead);
-    ahead = fetch(tile + kStages);
-    const uint8_t* st = stages + (size_t)(tile % kStages) * kStageB;
-    const int rid = tile * kTile + grp;
-    if (rid < nrows)
-      visit(rid, reinterpret_cast<const __nv_bfloat16*>(st + grp * kRowB),
-            reinterpret_cast<const __nv_bfloat16*>(st + (kTile + grp) * kRowB));
+    issue(ws, ahead);
+    fetch(tile + kStagesR, ahead);
+    ws = ws + 1 == kStagesR ? 0 : ws + 1;
+    Rows2 rw;
+    rw.ok[kR - 1] = false;
+    rw.rid[kR - 1] = 0;
+    rw.k[kR - 1] = rw.v[kR - 1] = 0u;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      rw.rid[r] = tile * kTileR + r * kGroups8 + grp;
+      rw.ok[r] = rw.rid[r] < nrows;
+      rw.k[r] = sb + rs * kStageB + r * kRowStep;
+      rw.v[r] = rw.k[r] + kBlkB;
+    }
+    rs = rs + 1 == kStagesR ? 0 : rs + 1;
+    visit(rw);
   }
   cp_async_wait<0>();
   __syncthreads();
