@@ -102,6 +102,7 @@ __device__ __forceinline__ double* sla_row(const Ctx& c, int s) { return c.sla +
 
 // ---- host-side launch wrappers (defined in the k_*.cu files) -------------
 cudaError_t launch_gate(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
+cudaError_t launch_stats(const Ctx& c, cudaStream_t st);
 cudaError_t launch_select(const Ctx& c, int m_max, cudaStream_t st);
 cudaError_t launch_topk(const Ctx& c, int implicit_base, cudaStream_t st);
 cudaError_t launch_attend(const Ctx& c, const __nv_bfloat16* q, int exact_mode, cudaStream_t st);

@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6) lfps_gate_kernel(Ctx c, const 
   const int n = c.n_ctx[b];
   const int S = c.S, L = c.L, d = c.d;
   const int m = n - S;
+  if (lane == 0) c.counts[(size_t)s * CNT_N + CNT_BLOCKS] = 0;   // summed by k_select.cu
 
   double qv[kMaxPerLane];
   const uint16_t* qs = reinterpret_cast<const uint16_t*>(q + (size_t)s * d);

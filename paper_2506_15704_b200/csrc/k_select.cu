@@ -1,5 +1,8 @@
-// k_select.cu -- thresholds and candidate construction (K1 + K2), one CTA
-// per (request, q-head) session, from PERSISTENT block summaries.
+// k_select.cu -- thresholds and candidate construction (K1 + K2) from
+// PERSISTENT block summaries, as two kernels:
+//
+//   lfps_stats_kernel   one 128-thread CTA per (session, table): A + B
+//   lfps_select_kernel  one 256-thread CTA per session: C + D
 //
 // Restates compute_thresholds (tables.py:295-317, _phys_moments :127-140),
 // select_initial (candidates.py:45-58), expand (:61-82) and
@@ -12,17 +15,21 @@
 // phys value.  A decode step changes a table only at its C2 slots and at the
 // one slot it grows by (k_update.cu marks those blocks dirty), and the lazy
 // scale leaves phys values alone, so the summaries of all other blocks stay
-// exact.  Per step this kernel
+// exact.  Per step
 //
 //   A  rebuilds the dirty blocks (every block when the session's summaries
 //      are not valid: first step, after a renormalisation);
 //   B  merges the window's segment moments in the canonical pairwise tree
-//      (devmath.table_moments) -> tau, mean, degenerate, kappa; exactly the
-//      same arithmetic as rebuilding every block;
+//      (devmath.table_moments) -> tau, mean, degenerate, kappa in thr[];
+//      exactly the same arithmetic as rebuilding every block;
 //   C  C0 = {slots with phys > tau / scale}: only "hot" blocks (max above
 //      the threshold) can hold members, and only those are read;
 //   D  C1 = F & dilate(C0, offsets), F read at dilated slots only;
 //      probe = C1 | local tail, compacted into a sorted absolute index list.
+//
+// A + B are fp64 latency chains per table: running them per (session, table)
+// in 128-thread CTAs (8 per SM) doubles the sessions in flight over one
+// 256-thread CTA per session doing both tables.
 //
 // All comparisons are exact fp64 (on bit patterns: phys values are +0 or
 // positive).  Table bytes read per step: dirty + hot blocks, not 2 m.
@@ -36,7 +43,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kLeaves = 512;                  // segments per window: m <= 511 * 512
-constexpr int kLeavesPerLane = kLeaves / 32;
 constexpr int kMaxTasks = 2 * kLeaves;
 
 struct Mom {
@@ -211,28 +217,146 @@ __device__ __forceinline__ long long warp_max64(long long x) {
   return x;
 }
 
+struct StatsShared {
+  int ntask;
+  int task[kLeaves];
+  Mom part[4];
+};
+
+#ifndef LFPS_STATS_CTAS
+#define LFPS_STATS_CTAS 8
+#endif
+#ifndef LFPS_SELECT_CTAS
+#define LFPS_SELECT_CTAS 4
+#endif
+constexpr int kStatsThreads = 128;
+constexpr int kStatsWarps = kStatsThreads / 32;
+
+// A + B of one (session, table): rebuild the dirty blocks, merge the
+// window's segment moments, write thr[(2 s + t) * 4 + {tau, mean, deg, kappa}].
+__global__ void __launch_bounds__(kStatsThreads, LFPS_STATS_CTAS) lfps_stats_kernel(Ctx c) {
+  __shared__ StatsShared sh;
+  const int s = c.s_off + (blockIdx.x >> 1), t = blockIdx.x & 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (c.exhaustive) return;
+  const int b = s / c.Hq;
+  const int dw = c.bw.dwords;
+  // independent prologue loads, issued together (one round trip, not four)
+  const int byp = c.bypass[s];
+  const int n = c.n_ctx[b];
+  const int base = t ? c.sla_base[s] : 0;
+  const bool valid = c.bw.valid[s] != 0;
+  uint32_t* dp = c.bw.dirty + (size_t)(2 * s + t) * dw + tid;
+  const uint32_t dbits = tid < dw ? *dp : 0u;
+  if (byp) return;
+  const int m = n - c.S;
+  const Window w = make_window(base, m);
+  const int nb = c.bw.nblk;
+  const double* row = t ? sla_row(c, s) : ver_row(c, s);
+  const long long tclk0 = now_clk();
+  if ((c.flags & LFPS_FLAG_TRACE) && tid == 0 && t == 0) c.trace[(size_t)s * 16 + 15] = now_ns();
+
+  // ---- A: rebuild dirty blocks ------------------------------------------------------
+  if (tid == 0) sh.ntask = 0;
+  __syncthreads();
+  if (tid < dw) {
+    uint32_t bits = valid ? dbits : LFPS_FULL;
+    if (bits) *dp = 0u;                             // also clears stale marks of a rebuild
+    const int lo = w.first - tid * 32, hi = w.first + w.nseg - tid * 32;   // window blocks
+    const uint32_t in_lo = lo <= 0 ? LFPS_FULL : (lo >= 32 ? 0u : (LFPS_FULL << lo));
+    const uint32_t in_hi = hi >= 32 ? LFPS_FULL : (hi <= 0 ? 0u : (LFPS_FULL >> (32 - hi)));
+    bits &= in_lo & in_hi;
+    if (bits) {
+      int pos = atomicAdd(&sh.ntask, __popc(bits));
+      while (bits) {
+        const int k = __ffs(bits) - 1;
+        bits &= bits - 1;
+        sh.task[pos++] = tid * 32 + k;
+      }
+    }
+  }
+  __syncthreads();
+  for (int k = warp; k < sh.ntask; k += kStatsWarps) {
+    const int blk = sh.task[k];
+    int a, vc;
+    segment(w, blk, a, vc);
+    double v[16];
+    load_seg(row, a, vc, lane, v);
+    double mu, m2, m3, m4;
+    if (vc == kBlk) seg_moments<true>(v, vc, lane, mu, m2, m3, m4);
+    else seg_moments<false>(v, vc, lane, mu, m2, m3, m4);
+    long long mx = 0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      if (e * 32 + lane < vc) mx = max(mx, __double_as_longlong(v[e]));
+    mx = warp_max64(mx);
+    if (lane == 0) {
+      const size_t it = (size_t)(2 * s + t) * nb + blk;
+      double2* p = reinterpret_cast<double2*>(c.bw.bsum + 4 * it);
+      p[0] = make_double2(mu, m2);
+      p[1] = make_double2(m3, m4);
+      c.bw.bmax[it] = __longlong_as_double(mx);
+    }
+  }
+  __syncthreads();
+  if (t == 0) trace_at(c, s, 1, tclk0);
+
+  // ---- B: thresholds (compute_thresholds), one quarter of the tree per warp ----------
+  const Mom q = quarter_merge(c.bw.bsum + (size_t)(2 * s + t) * nb * 4, w, warp, lane);
+  if (lane == 0) sh.part[warp] = q;
+  __syncthreads();
+  if (tid == 0) {
+    const Mom tot = merge(merge(sh.part[0], sh.part[1]), merge(sh.part[2], sh.part[3]));
+    const double sc = c.scale[s];
+    const double mean = cmul(tot.mu, sc);
+    const bool deg = cmul(cmul(tot.m2, sc), sc) < 1e-12;
+    double tau = NAN, kappa = NAN;
+    if (!deg) {
+      kappa = cdiv(tot.m4, cmul(tot.m2, tot.m2));
+      if (kappa == 0.0) set_err(c, s, LFPS_ERR_KAPPA_ZERO);
+      tau = cdiv(cmul(c.a, mean), kappa);
+    }
+    double* thr = c.thr + (size_t)(2 * s + t) * 4;
+    thr[0] = tau; thr[1] = mean; thr[2] = deg ? 1.0 : 0.0; thr[3] = kappa;
+    atomicAdd(c.counts + (size_t)s * CNT_N + CNT_BLOCKS, sh.ntask);
+    if (t == 0 && (c.flags & LFPS_FLAG_TRACE)) c.trace[(size_t)s * 16 + 2] = now_clk() - tclk0;
+  }
+}
+
 struct SelectShared {
-  int ntask, nhot;
+  int nhot;
   int task[kMaxTasks];
-  Mom part[2][4];
+  uint16_t fbuf[kWarps][1024];   // a warp's candidate positions: lane << 5 | bit
+  int fword[kWarps][32];         // C0 word of each lane
+  uint32_t fc1[kWarps][32];      // C1 bits of each lane's word
   double thr0[2], thrf[2];
   int deg[2];
   int wsum[kWarps];
   int red[3][kWarps];
 };
 
-__global__ void __launch_bounds__(kThreads, 4) lfps_select_kernel(Ctx c) {
+// C + D of one session from the thresholds of lfps_stats_kernel.
+__global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel(Ctx c) {
   extern __shared__ uint32_t smem[];
   __shared__ SelectShared sh;
   const int s = c.s_off + blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int* cnt = c.counts + (size_t)s * CNT_N;
-  if (c.bypass[s]) {
+  const int b = s / c.Hq;
+  // independent prologue loads, issued together (one round trip, not four)
+  const int byp = c.bypass[s];
+  const int n = c.n_ctx[b];
+  const int base = c.sla_base[s];
+  double tau = 0.0, mean = 0.0, degv = 0.0, sc = 1.0;
+  if (tid < 2 && !c.exhaustive) {
+    const double* thr = c.thr + (size_t)(2 * s + tid) * 4;
+    tau = thr[0]; mean = thr[1]; degv = thr[2];
+    sc = c.scale[s];
+  }
+  if (byp) {
     if (tid < CNT_N) cnt[tid] = 0;
     return;
   }
-  const int b = s / c.Hq;
-  const int n = c.n_ctx[b];
   const int S = c.S;
   const int m = n - S;
   const int W = (m + 31) / 32;
@@ -241,118 +365,34 @@ __global__ void __launch_bounds__(kThreads, 4) lfps_select_kernel(Ctx c) {
   uint32_t* act = smem + W + (W + 1) / 2;    // [AW] active words (C0 word +- 1, tail)
   const int AW = (W + 31) / 32;
   const double* ver = ver_row(c, s);
-  const int base = c.sla_base[s];
   const double* sla = sla_row(c, s) + base;   // logical view
   const Window wv = make_window(0, m);
   const Window wsl = make_window(base, m);
   const int nb = c.bw.nblk;
   const long long tclk0 = now_clk();
-  if ((c.flags & LFPS_FLAG_TRACE) && tid == 0) c.trace[(size_t)s * 16 + 15] = now_ns();
 
-  // ---- A: rebuild dirty blocks --------------------------------------------------
-  if (tid == 0) sh.ntask = 0;
-  __syncthreads();
-  if (!c.exhaustive) {
-    const bool valid = c.bw.valid[s] != 0;
-    if (tid < 64) {
-      const int t = tid >> 5, wd = tid & 31;
-      const Window& w = t ? wsl : wv;
-      if (wd < c.bw.dwords) {
-        uint32_t* dp = c.bw.dirty + (size_t)(2 * s + t) * c.bw.dwords + wd;
-        uint32_t bits = valid ? *dp : LFPS_FULL;
-        if (valid && bits) *dp = 0u;
-        const int lo = w.first - wd * 32, hi = w.first + w.nseg - wd * 32;   // window blocks
-        const uint32_t in_lo = lo <= 0 ? LFPS_FULL : (lo >= 32 ? 0u : (LFPS_FULL << lo));
-        const uint32_t in_hi = hi >= 32 ? LFPS_FULL : (hi <= 0 ? 0u : (LFPS_FULL >> (32 - hi)));
-        bits &= in_lo & in_hi;
-        if (bits) {
-          int pos = atomicAdd(&sh.ntask, __popc(bits));
-          while (bits) {
-            const int k = __ffs(bits) - 1;
-            bits &= bits - 1;
-            sh.task[pos++] = (t << 16) | (wd * 32 + k);
-          }
-        }
-      }
-    }
-    if (!valid && tid < 2 * c.bw.dwords) {   // clear stale marks of a rebuilt session
-      c.bw.dirty[(size_t)(2 * s + (tid / c.bw.dwords)) * c.bw.dwords + tid % c.bw.dwords] = 0u;
-    }
-    __syncthreads();
-    for (int k = warp; k < sh.ntask; k += kWarps) {
-      const int task = sh.task[k];
-      const int t = task >> 16, blk = task & 0xffff;
-      const Window& w = t ? wsl : wv;
-      int a, vc;
-      segment(w, blk, a, vc);
-      const double* row = t ? sla_row(c, s) : ver;
-      double v[16];
-      load_seg(row, a, vc, lane, v);
-      double mu, m2, m3, m4;
-      if (vc == kBlk) seg_moments<true>(v, vc, lane, mu, m2, m3, m4);
-      else seg_moments<false>(v, vc, lane, mu, m2, m3, m4);
-      long long mx = 0;
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-        if (e * 32 + lane < vc) mx = max(mx, __double_as_longlong(v[e]));
-      mx = warp_max64(mx);
-      if (lane == 0) {
-        const size_t it = (size_t)(2 * s + t) * nb + blk;
-        double2* p = reinterpret_cast<double2*>(c.bw.bsum + 4 * it);
-        p[0] = make_double2(mu, m2);
-        p[1] = make_double2(m3, m4);
-        c.bw.bmax[it] = __longlong_as_double(mx);
-      }
-    }
-    __syncthreads();
-  }
-
-  trace_at(c, s, 1, tclk0);
-  // ---- B: thresholds (compute_thresholds), 4 warps per table --------------------------
-  const int tB = warp >> 2, qd = warp & 3;
-  if (!c.exhaustive) {
-    const Mom q = quarter_merge(c.bw.bsum + (size_t)(2 * s + tB) * nb * 4, tB ? wsl : wv, qd, lane);
-    if (lane == 0) sh.part[tB][qd] = q;
-  }
   for (int w = tid; w < W; w += kThreads)
     c0w[w] = !c.exhaustive ? 0u : ((w == W - 1 && (m & 31)) ? ((1u << (m & 31)) - 1u) : LFPS_FULL);
   for (int w = tid; w < AW; w += kThreads)
     act[w] = !c.exhaustive ? 0u : ((w == AW - 1 && (W & 31)) ? ((1u << (W & 31)) - 1u) : LFPS_FULL);
-  if (tid == 0) {
-    sh.nhot = 0;
-    if (!c.exhaustive) c.bw.valid[s] = 1;
-  }
-  __syncthreads();
-  if (tid == 0 && !c.exhaustive) {       // tail words are always active
-    for (int w = max(0, m - c.L) >> 5; w < W; ++w) act[w >> 5] |= 1u << (w & 31);
-  }
-  if (lane == 0 && qd == 0) {
-    const int t = tB;
+  if (tid == 0) sh.nhot = 0;
+  if (tid < 2) {
+    const int t = tid;
     double* thr = c.thr + (size_t)(2 * s + t) * 4;
     if (c.exhaustive) {
       sh.thr0[t] = -INFINITY; sh.thrf[t] = -INFINITY; sh.deg[t] = 0;
       thr[0] = -INFINITY; thr[1] = -INFINITY; thr[2] = 0.0; thr[3] = NAN;
     } else {
-      const Mom tot = merge(merge(sh.part[t][0], sh.part[t][1]), merge(sh.part[t][2], sh.part[t][3]));
-      const double sc = c.scale[s];
-      const double mean = cmul(tot.mu, sc);
-      const bool deg = cmul(cmul(tot.m2, sc), sc) < 1e-12;
-      double tau = NAN, kappa = NAN, thr0 = NAN;
-      if (!deg) {
-        kappa = cdiv(tot.m4, cmul(tot.m2, tot.m2));
-        if (kappa == 0.0) set_err(c, s, LFPS_ERR_KAPPA_ZERO);
-        tau = cdiv(cmul(c.a, mean), kappa);
-        thr0 = cdiv(tau, sc);
-      }
-      sh.thr0[t] = thr0;
+      sh.deg[t] = degv != 0.0;
+      sh.thr0[t] = sh.deg[t] ? NAN : cdiv(tau, sc);
       sh.thrf[t] = cdiv(mean, sc);
-      sh.deg[t] = deg ? 1 : 0;
-      thr[0] = tau; thr[1] = mean; thr[2] = deg ? 1.0 : 0.0; thr[3] = kappa;
     }
   }
   __syncthreads();
-
-  trace_at(c, s, 2, tclk0);
+  if (tid == 0 && !c.exhaustive) {       // tail words are always active
+    for (int w = max(0, m - c.L) >> 5; w < W; ++w) act[w >> 5] |= 1u << (w & 31);
+    c.bw.valid[s] = 1;                   // both tables' summaries are current
+  }
   // ---- C: C0 from the hot blocks (select_initial) ----------------------------------
   if (!c.exhaustive) {
     for (int t = 0; t < 2; ++t) {
@@ -424,42 +464,59 @@ __global__ void __launch_bounds__(kThreads, 4) lfps_select_kernel(Ctx c) {
     for (int r = 0; r < na; r += kThreads) {
       const int j = r + tid;
       const int w = j < na ? alist[j] : -1;
-      uint32_t pr = 0u;
+      uint32_t cur = 0u, cand = 0u, valid = LFPS_FULL;
       if (w >= 0) {
-        const uint32_t cur = c0w[w];
+        cur = c0w[w];
         const uint32_t prev = w > 0 ? c0w[w - 1] : 0u;
         const uint32_t next = w + 1 < W ? c0w[w + 1] : 0u;
         uint32_t dil = 0;
         for (int k = 0; k < c.n_off; ++k) dil |= shifted(prev, cur, next, c.off[k]);
-        const uint32_t valid = w == W - 1 ? last_valid : LFPS_FULL;
-        uint32_t cand = dil & valid;
-        uint32_t c1 = 0;
-        if (c.exhaustive) {
-          c1 = cand;
-        } else {
-          // F at the dilated positions, four positions (eight loads) in flight
-          while (cand) {
-            int ps[4];
+        valid = w == W - 1 ? last_valid : LFPS_FULL;
+        cand = dil & valid;
+      }
+      uint32_t c1 = cand;
+      if (!c.exhaustive) {
+        // F at the dilated positions.  The warp's candidates are flattened
+        // into one list and read 32 lanes x 4 deep, so a dense word (a band:
+        // 32 candidates) costs the warp no more round trips than a sparse one.
+        const int k = __popc(cand);
+        int off = k;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              ps[q] = cand ? __ffs(cand) - 1 : -1;
-              cand &= cand - 1;
-            }
-            long long xv[4], xs[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              xv[q] = xs[q] = -1ll;
-              if (ps[q] >= 0) {
-                const int i = w * 32 + ps[q];
-                xv[q] = __ldg(verb + i);
-                xs[q] = __ldg(slab + i);
-              }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (ps[q] >= 0 && (xv[q] > tfv || xs[q] > tfs)) c1 |= 1u << ps[q];
-          }
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(LFPS_FULL, off, o);
+          if (lane >= o) off += y;
         }
+        const int K = __shfl_sync(LFPS_FULL, off, 31);
+        off -= k;
+        uint16_t* buf = sh.fbuf[warp];
+        for (uint32_t x = cand; x; x &= x - 1) buf[off++] = (uint16_t)((lane << 5) | (__ffs(x) - 1));
+        sh.fword[warp][lane] = w;
+        sh.fc1[warp][lane] = 0u;
+        __syncwarp();
+        for (int g0 = lane; g0 < K; g0 += 128) {
+          int e[4];
+          long long xv[4], xs[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) e[q] = g0 + 32 * q < K ? buf[g0 + 32 * q] : -1;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            xv[q] = xs[q] = -1ll;
+            if (e[q] >= 0) {
+              const int i = sh.fword[warp][e[q] >> 5] * 32 + (e[q] & 31);
+              xv[q] = __ldg(verb + i);
+              xs[q] = __ldg(slab + i);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (e[q] >= 0 && (xv[q] > tfv || xs[q] > tfs))
+              atomicOr(&sh.fc1[warp][e[q] >> 5], 1u << (e[q] & 31));
+        }
+        __syncwarp();
+        c1 = sh.fc1[warp][lane];
+      }
+      uint32_t pr = 0u;
+      if (w >= 0) {
         uint32_t tail = 0;
         const int j0 = w * 32;
         if (j0 + 32 > tail_lo) tail = (LFPS_FULL << max(0, tail_lo - j0)) & valid;
@@ -489,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, 4) lfps_select_kernel(Ctx c) {
       cnt[CNT_C1] = t1;
       cnt[CNT_PROBE] = written;
       cnt[CNT_DROP] = t3;
-      cnt[CNT_BLOCKS] = sh.ntask + sh.nhot;
+      cnt[CNT_BLOCKS] += sh.nhot;          // + the rebuilt blocks of lfps_stats_kernel
       if (c.flags & LFPS_FLAG_TRACE) {
         c.trace[(size_t)s * 16 + 4] = now_clk() - tclk0;
         c.trace[(size_t)s * 16 + 12] = now_ns();
@@ -499,6 +556,11 @@ __global__ void __launch_bounds__(kThreads, 4) lfps_select_kernel(Ctx c) {
 }
 
 }  // namespace
+
+cudaError_t launch_stats(const Ctx& c, cudaStream_t st) {
+  lfps_stats_kernel<<<2 * c.s_cnt, kStatsThreads, 0, st>>>(c);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_select(const Ctx& c, int m_max, cudaStream_t st) {
   const int W = (m_max + 31) / 32;

@@ -242,10 +242,14 @@ cudaEvent_t prof_event() {
   } while (0)
 
 // ---- internal streams for session-group concurrency (LFPS_FLAG_SPLIT) -------
+#ifndef LFPS_SPLIT_GROUPS
+#define LFPS_SPLIT_GROUPS 2
+#endif
+constexpr int kSplitGroups = LFPS_SPLIT_GROUPS;   // session groups of LFPS_FLAG_SPLIT
 struct Pipe {
   int dev = -1;
-  cudaStream_t st[2] = {nullptr, nullptr};
-  cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+  cudaStream_t st[kSplitGroups] = {};
+  cudaEvent_t fork = nullptr, join[kSplitGroups] = {};
 };
 std::mutex g_pipe_mu;
 Pipe g_pipe[16];
@@ -258,7 +262,7 @@ cudaError_t get_pipe(Pipe** out) {
   std::lock_guard<std::mutex> g(g_pipe_mu);
   Pipe& p = g_pipe[dev];
   if (p.dev < 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kSplitGroups; ++i) {
       if ((e = cudaStreamCreateWithFlags(&p.st[i], cudaStreamNonBlocking)) != cudaSuccess) return e;
       if ((e = cudaEventCreateWithFlags(&p.join[i], cudaEventDisableTiming)) != cudaSuccess) return e;
     }
@@ -289,8 +293,8 @@ int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out) {
 int lfps_decode_launches(const lfps_dims* dims, int32_t flags) {
   if (dims && (flags & LFPS_FLAG_SPLIT) &&
       (long long)dims->batch * dims->kv_heads * dims->group >= 256)
-    return 8;
-  return 5;
+    return 2 + 4 * kSplitGroups;
+  return 6;
 }
 
 int lfps_slash_capacity(const lfps_dims* dims) {
@@ -375,18 +379,19 @@ int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_sta
   const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
   LAUNCH_P("clear_err", sm, lfps::launch_clear_err(c, sm));
   if ((c.flags & LFPS_FLAG_SPLIT) && !g_prof_on && c.NS >= 256) {
-    // two session halves, each gate -> select -> finish on its own stream
+    // two session halves, each gate -> stats -> select -> finish on its own stream
     Pipe* pp = nullptr;
     LAUNCH(get_pipe(&pp));
     LAUNCH(cudaEventRecord(pp->fork, sm));
-    const int half = (c.NS / 2 + 31) / 32 * 32;
-    for (int g = 0; g < 2; ++g) {
+    const int per = (c.NS / kSplitGroups + 31) / 32 * 32;
+    for (int g = 0; g < kSplitGroups; ++g) {
       lfps::Ctx cg = c;
-      cg.s_off = g ? half : 0;
-      cg.s_cnt = g ? c.NS - half : half;
+      cg.s_off = g * per;
+      cg.s_cnt = g == kSplitGroups - 1 ? c.NS - g * per : per;
       cudaStream_t gs = pp->st[g];
       LAUNCH(cudaStreamWaitEvent(gs, pp->fork, 0));
       LAUNCH(lfps::launch_gate(cg, qb, gs));
+      LAUNCH(lfps::launch_stats(cg, gs));
       LAUNCH(lfps::launch_select(cg, m_max, gs));
       LAUNCH(lfps::launch_finish(cg, qb, gs));
       LAUNCH(cudaEventRecord(pp->join[g], gs));
@@ -397,6 +402,7 @@ int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_sta
     return LFPS_OK;
   }
   LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
+  LAUNCH_P("stats", sm, lfps::launch_stats(c, sm));
   LAUNCH_P("select", sm, lfps::launch_select(c, m_max, sm));
   // LFPS_FLAG_UNIT_FINISH: GQA units of <= 4 q-heads (d 128 / 256) finish per
   // unit over the union of their probe rows (tensor-core softmax.V); measured
