@@ -2,7 +2,7 @@
 //
 // Restates gate_logits + sparsity_from_logits + bypass_output
 // (pkg/src/lfps/gate.py:77-147) and the gate part of decode_step
-// (engine.py:127-146) for every session of the batch: one warp per session,
+// (engine.py:127-146) for every session of the batch: one CTA per session,
 // fp64 throughout, canonical dot/exp/sum order (canon.cuh).  Sink rows,
 // the trailing local rows and the priors are read straight from the bf16 KV
 // cache and the fp64 prior buffers.
@@ -13,7 +13,6 @@ namespace lfps {
 
 namespace {
 
-constexpr int kWarps = 8;
 constexpr int kMaxPerLane = 8;  // d <= 256
 
 // Canonical fp64 dot of a bf16 row with the lane-resident query (gdot):
@@ -30,17 +29,26 @@ __device__ __forceinline__ double row_dot(const __nv_bfloat16* row, const double
   return warp_fold(acc);
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 6) lfps_gate_kernel(Ctx c, const __nv_bfloat16* q) {
-  const int lane = threadIdx.x & 31;
-  const int sidx = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  if (sidx >= c.s_cnt) return;
-  const int s = c.s_off + sidx;
+// One 128-thread CTA per session: the S + L logit rows are spread over the 4
+// warps (each a canonical warp gdot), then warp 0 finishes the gate.  (One
+// warp per session walked the rows serially: 2048 warps could not fill the
+// GPU and each was a ~70-deep chain of warp folds.)
+constexpr int kGateWarps = 4;
+constexpr int kMaxRows = 96;     // S <= 31, L <= 64
+
+__global__ void __launch_bounds__(kGateWarps * 32) lfps_gate_kernel(Ctx c, const __nv_bfloat16* q) {
+  __shared__ double lg[kMaxRows];   // logits: sinks [0, S), local rows [S, S + L)
+  __shared__ double ev[kMaxRows];
+  __shared__ double gsh;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int s = c.s_off + blockIdx.x;
   if (s >= c.NS) return;
   const int b = s / c.Hq, qh = s % c.Hq, h = qh / c.G;
   const int n = c.n_ctx[b];
   const int S = c.S, L = c.L, d = c.d;
   const int m = n - S;
-  if (lane == 0) c.counts[(size_t)s * CNT_N + CNT_BLOCKS] = 0;   // summed by k_select.cu
+  const int R = S + L;
+  if (tid == 0) c.counts[(size_t)s * CNT_N + CNT_BLOCKS] = 0;   // summed by k_select.cu
 
   double qv[kMaxPerLane];
   const uint16_t* qs = reinterpret_cast<const uint16_t*>(q + (size_t)s * d);
@@ -50,46 +58,63 @@ __global__ void __launch_bounds__(kWarps * 32, 6) lfps_gate_kernel(Ctx c, const 
     qv[e] = (j < d) ? (double)bf2f(qs[j]) : 0.0;
   }
   // logits: sinks [0, S), local rows [n - L, n)  (gate.py:92-94)
-  double sl_max = -INFINITY, ll_max = -INFINITY;
-  double sl[32];           // S <= 31
-  double ll[64];           // L <= 64
-  bool finite = true;
-  for (int i = 0; i < S; ++i) {
-    sl[i] = cdiv(row_dot(krow(c, b, h, i), qv, d, lane), c.sqrt_d);
-    finite &= isfinite(sl[i]);
-    sl_max = fmax(sl_max, sl[i]);
+  for (int r = warp; r < R; r += kGateWarps) {
+    const __nv_bfloat16* row = r < S ? krow(c, b, h, r) : krow(c, b, h, n - L + (r - S));
+    const double z = cdiv(row_dot(row, qv, d, lane), c.sqrt_d);
+    if (lane == 0) lg[r] = z;
   }
-  for (int i = 0; i < L; ++i) {
-    ll[i] = cdiv(row_dot(krow(c, b, h, n - L + i), qv, d, lane), c.sqrt_d);
-    finite &= isfinite(ll[i]);
-    ll_max = fmax(ll_max, ll[i]);
-  }
-  // global exponent (gate.py:77-81): q.Kbar / sqrt(d) + |q|^2 sigma^2 / 2
-  const double* kbar = c.mean_key + ((size_t)b * c.Hkv + h) * d;
-  double qk = 0.0, qq = 0.0;
+  // global exponent (gate.py:77-81): q.Kbar / sqrt(d) + |q|^2 sigma^2 / 2, by
+  // the warp with the fewest rows
+  if (warp == (R % kGateWarps)) {
+    const double* kbar = c.mean_key + ((size_t)b * c.Hkv + h) * d;
+    double qk = 0.0, qq = 0.0;
 #pragma unroll
-  for (int e = 0; e < kMaxPerLane; ++e) {
-    const int j = lane + 32 * e;
-    if (j < d) {
-      qk = cadd(qk, cmul(qv[e], kbar[j]));
-      qq = cadd(qq, cmul(qv[e], qv[e]));
+    for (int e = 0; e < kMaxPerLane; ++e) {
+      const int j = lane + 32 * e;
+      if (j < d) {
+        qk = cadd(qk, cmul(qv[e], kbar[j]));
+        qq = cadd(qq, cmul(qv[e], qv[e]));
+      }
     }
+    qk = warp_fold(qk);
+    qq = warp_fold(qq);
+    if (lane == 0) gsh = cadd(cdiv(qk, c.sqrt_d), cdiv(cmul(qq, c.sigma[s]), 2.0));
   }
-  qk = warp_fold(qk);
-  qq = warp_fold(qq);
-  const double g = cadd(cdiv(qk, c.sqrt_d), cdiv(cmul(qq, c.sigma[s]), 2.0));
-  finite &= isfinite(g);
+  __syncthreads();
+  if (warp != 0) return;
+  const double g = gsh;
+  bool finite = isfinite(g);
+  double sl_max = -INFINITY, ll_max = -INFINITY;
+  for (int r = lane; r < R; r += 32) {
+    const double z = lg[r];
+    finite &= isfinite(z);
+    if (r < S) sl_max = fmax(sl_max, z);
+    else ll_max = fmax(ll_max, z);
+  }
+  finite = __all_sync(LFPS_FULL, finite);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    sl_max = fmax(sl_max, __shfl_xor_sync(LFPS_FULL, sl_max, o));
+    ll_max = fmax(ll_max, __shfl_xor_sync(LFPS_FULL, ll_max, o));
+  }
   if (!finite) {
     if (lane == 0) { set_err(c, s, LFPS_ERR_NONFINITE_LOGITS); c.bypass[s] = 0; c.rho[s] = NAN; }
     return;
   }
-  // shared max shift and the three mass terms (gate.py:107-111)
+  // shared max shift and the three mass terms (gate.py:107-111): the
+  // exponentials in parallel, the two sums left to right
   const double shift = fmax(fmax(sl_max, ll_max), g);
-  double w_s = 0.0, w_l = 0.0;
-  for (int i = 0; i < S; ++i) w_s = cadd(w_s, cexp(csub(sl[i], shift)));
-  for (int i = 0; i < L; ++i) w_l = cadd(w_l, cexp(csub(ll[i], shift)));
-  const double w_g = cmul(cexp(csub(g, shift)), (double)m);
-  const double rho = cdiv(w_s, cadd(cadd(w_s, w_g), w_l));
+  for (int r = lane; r < R; r += 32) ev[r] = cexp(csub(lg[r], shift));
+  __syncwarp();
+  double rho = 0.0;
+  if (lane == 0) {
+    double w_s = 0.0, w_l = 0.0;
+    for (int i = 0; i < S; ++i) w_s = cadd(w_s, ev[i]);
+    for (int i = 0; i < L; ++i) w_l = cadd(w_l, ev[S + i]);
+    const double w_g = cmul(cexp(csub(g, shift)), (double)m);
+    rho = cdiv(w_s, cadd(cadd(w_s, w_g), w_l));
+  }
+  rho = __shfl_sync(LFPS_FULL, rho, 0);
   if (!isfinite(rho)) {
     if (lane == 0) { set_err(c, s, LFPS_ERR_NONFINITE_RHO); c.bypass[s] = 0; c.rho[s] = rho; }
     return;
@@ -108,12 +133,12 @@ __global__ void __launch_bounds__(kWarps * 32, 6) lfps_gate_kernel(Ctx c, const 
   // softmax over [sink logits..., g]: max, cexp, 256-thread canonical sum
   // (for <= 32 terms the warp fold is the block fold), divide.
   double mx = fmax(sl_max, g);
-  const double ev = (lane < S) ? cexp(csub(sl[lane < S ? lane : 0], mx))
-                               : (lane == S ? cexp(csub(g, mx)) : 0.0);
-  const double tot = warp_fold(ev);
+  const double evs = (lane < S) ? cexp(csub(lg[lane < S ? lane : 0], mx))
+                                : (lane == S ? cexp(csub(g, mx)) : 0.0);
+  const double tot = warp_fold(evs);
   double w[32];
   for (int i = 0; i <= S; ++i) {
-    const double ei = __shfl_sync(LFPS_FULL, ev, i);
+    const double ei = __shfl_sync(LFPS_FULL, evs, i);
     w[i] = cdiv(ei, tot);
   }
   for (int j = lane; j < d; j += 32) {
@@ -130,8 +155,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6) lfps_gate_kernel(Ctx c, const 
 }  // namespace
 
 cudaError_t launch_gate(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
-  const int blocks = (c.s_cnt + kWarps - 1) / kWarps;
-  lfps_gate_kernel<<<blocks, kWarps * 32, 0, st>>>(c, q);
+  lfps_gate_kernel<<<c.s_cnt, kGateWarps * 32, 0, st>>>(c, q);
   return cudaGetLastError();
 }
 

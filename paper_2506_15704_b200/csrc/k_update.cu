@@ -24,7 +24,13 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxDirtyWords = 32;
-constexpr int kUnroll = 2;               // C2 entries per thread in flight
+#ifndef LFPS_UPDATE_UNROLL
+#define LFPS_UPDATE_UNROLL 2
+#endif
+constexpr int kUnroll = LFPS_UPDATE_UNROLL;   // C2 entries per thread in flight
+#ifndef LFPS_UPDATE_CTAS
+#define LFPS_UPDATE_CTAS 6
+#endif
 
 __device__ __forceinline__ void mark(uint32_t (*dmark)[kMaxDirtyWords], int t, int blk) {
   atomicOr(&dmark[t][blk >> 5], 1u << (blk & 31));
@@ -33,18 +39,23 @@ __device__ __forceinline__ void mark(uint32_t (*dmark)[kMaxDirtyWords], int t, i
 // One CTA per session: the session's table update, the unit's KV append (by
 // the unit's first q-head), and -- in the last CTA to finish -- the context
 // count of every request (store.py:64-77 append, then engine.py:188-191).
-__global__ void __launch_bounds__(kThreads, 6) lfps_update_kernel(Ctx c, const __nv_bfloat16* k_new,
+__global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel(Ctx c, const __nv_bfloat16* k_new,
                                                                const __nv_bfloat16* v_new) {
   __shared__ uint32_t dmark[2][kMaxDirtyWords];
   __shared__ int clamp_red[kThreads / 32];
   const int s = blockIdx.x, tid = threadIdx.x;
-  if (c.err[0] != 0) return;                  // a failed step commits nothing
   const int b = s / c.Hq, qh = s % c.Hq;
+  // independent prologue loads, issued together
+  const int failed = c.err[0];
   const int n = c.n_ctx[b];
+  int base = c.sla_base[s];
+  const int byp = c.bypass[s];
+  const double sc0 = c.scale[s];
+  const int k2 = c.counts[(size_t)s * CNT_N + CNT_C2];
+  if (failed != 0) return;                    // a failed step commits nothing
   const int m = n - c.S;
   double* ver = ver_row(c, s);
   double* sla = sla_row(c, s);
-  int base = c.sla_base[s];
   const int dw = c.bw.dwords;
   uint32_t* dirty = c.bw.dirty + (size_t)(2 * s) * dw;
   // KV append of the unit's new row at position n (one session per unit)
@@ -57,7 +68,7 @@ __global__ void __launch_bounds__(kThreads, 6) lfps_update_kernel(Ctx c, const _
       vd[t] = v_new[(size_t)u * c.d + t];
     }
   }
-  if (c.bypass[s]) {
+  if (byp) {
     if (tid == 0) {                     // grow only (engine.py:133-137)
       ver[m] = 0.0;
       sla[base + m] = 0.0;              // no parked carry on a gated step
@@ -67,11 +78,10 @@ __global__ void __launch_bounds__(kThreads, 6) lfps_update_kernel(Ctx c, const _
     }
   } else {
     for (int i = tid; i < 2 * kMaxDirtyWords; i += kThreads) (&dmark[0][0])[i] = 0u;
-    const int k2 = c.counts[(size_t)s * CNT_N + CNT_C2];
     const int* idx = c.c2_idx + (size_t)s * c.list_cap;
     const double* uw = c.uw + (size_t)s * c.list_cap;
     // decay with renormalisation (tables.py:167-169, 240-244)
-    double sc = cmul(c.scale[s], c.r);
+    double sc = cmul(sc0, c.r);
     bool renorm = false;
     if (sc < 1e-120) {
       for (int i = tid; i < m; i += kThreads) ver[i] = cmul(ver[i], sc);
