@@ -225,7 +225,7 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
   }
 
   trace_at(c, s, 9, t0);
-  // ---- data checks and the update weights u (committed by k_update.cu) ----------------
+  // ---- data checks; the C2 max for the update weights (k_update.cu) ----------------
   if (__syncthreads_or(!(chk == 0.0f))) {
     if (tid == 0) set_err(c, s, LFPS_ERR_NONFINITE_SCORES);
     return;
@@ -233,41 +233,11 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
   for (int o = 16; o >= 1; o >>= 1) mxc = fmaxf(mxc, __shfl_xor_sync(LFPS_FULL, mxc, o));
   if (lane == 0) sh.gmax[warp] = mxc;
   __syncthreads();
-  float mf = sh.gmax[0];
-#pragma unroll
-  for (int w = 1; w < kWarps; ++w) mf = fmaxf(mf, sh.gmax[w]);
-  const double mx = (double)mf;
-  double e[kMaxE];
-  double acc = 0.0;
-#pragma unroll
-  for (int i = 0; i < kMaxE; ++i) {
-    const int j = tid + i * kCanon;
-    e[i] = j < k2 ? cexp(csub((double)c2z[j], mx)) : 0.0;
-    if (j < k2) acc = cadd(acc, e[i]);
-  }
-  for (int j = tid + kMaxE * kCanon; j < k2; j += kCanon) acc = cadd(acc, cexp(csub((double)c2z[j], mx)));
-  const double tot = canon_sum(acc, sh.red);
-  double* uw = c.uw + (size_t)s * c.list_cap;
-  acc = 0.0;
-#pragma unroll
-  for (int i = 0; i < kMaxE; ++i) {
-    const int j = tid + i * kCanon;
-    if (j < k2) {
-      const double u = cdiv(e[i], tot);
-      uw[j] = u;
-      acc = cadd(acc, u);
-    }
-  }
-  for (int j = tid + kMaxE * kCanon; j < k2; j += kCanon) {
-    const double u = cdiv(cexp(csub((double)c2z[j], mx)), tot);
-    uw[j] = u;
-    acc = cadd(acc, u);
-  }
-  const double wsum = canon_sum(acc, sh.red);
   if (tid == 0) {
-    if (fabs(wsum - 1.0) > 1e-6) set_err(c, s, LFPS_ERR_WEIGHT_SUM);
-    c.bw.wstat[2 * (size_t)s] = mx;
-    c.bw.wstat[2 * (size_t)s + 1] = tot;
+    float mf = sh.gmax[0];
+#pragma unroll
+    for (int w = 1; w < kWarps; ++w) mf = fmaxf(mf, sh.gmax[w]);
+    c.bw.wstat[2 * (size_t)s] = (double)mf;
     if (c.flags & LFPS_FLAG_TRACE) {
       c.trace[(size_t)s * 16 + 10] = now_clk() - t0;
       c.trace[(size_t)s * 16 + 14] = now_ns();

@@ -3,8 +3,9 @@
 //
 // lfps_update_kernel restates ScoreTablePair.update / grow (tables.py:144-220)
 // on the linear slash window: u = canonical fp64 softmax of the selected
-// fp32 scores (engine.py:184, devmath.softmax_update), computed and checked
-// (|sum u - 1| <= 1e-6) by the finish kernel, read from uw; scale *= r with renormalisation below 1e-120 (vertical [0, m) and
+// fp32 scores (engine.py:184, devmath.softmax_update) with the C2 max from
+// the finish kernel, checked (|sum u - 1| <= 1e-6); scale *= r with
+// renormalisation below 1e-120 (vertical [0, m) and
 // slash logical [0, m] multiplied by the new scale); slash shift = base - 1
 // with the new logical slot 0 zeroed and the old top parked at logical m;
 // add = (u - 1/(2k)) / scale folded into both tables at C2; negative
@@ -24,6 +25,25 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxDirtyWords = 32;
+constexpr int kMaxE = 8;                 // update weights cached per thread (|C2| <= 2048)
+
+// canonical 256-wide block sum (devmath.block_sum); all threads get it
+__device__ __forceinline__ double block_sum256(double acc, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  acc = warp_fold(acc);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    double v = lane < 8 ? red[lane] : 0.0;
+#pragma unroll
+    for (int h = 4; h >= 1; h >>= 1) v = cadd(v, __shfl_xor_sync(LFPS_FULL, v, h));
+    if (lane == 0) red[8] = v;
+  }
+  __syncthreads();
+  const double out = red[8];
+  __syncthreads();
+  return out;
+}
 #ifndef LFPS_UPDATE_UNROLL
 #define LFPS_UPDATE_UNROLL 2
 #endif
@@ -43,6 +63,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
                                                                const __nv_bfloat16* v_new) {
   __shared__ uint32_t dmark[2][kMaxDirtyWords];
   __shared__ int clamp_red[kThreads / 32];
+  __shared__ double red[16];
   const int s = blockIdx.x, tid = threadIdx.x;
   const int b = s / c.Hq, qh = s % c.Hq;
   // independent prologue loads, issued together
@@ -79,75 +100,126 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
   } else {
     for (int i = tid; i < 2 * kMaxDirtyWords; i += kThreads) (&dmark[0][0])[i] = 0u;
     const int* idx = c.c2_idx + (size_t)s * c.list_cap;
-    const double* uw = c.uw + (size_t)s * c.list_cap;
-    // decay with renormalisation (tables.py:167-169, 240-244)
-    double sc = cmul(sc0, c.r);
-    bool renorm = false;
-    if (sc < 1e-120) {
-      for (int i = tid; i < m; i += kThreads) ver[i] = cmul(ver[i], sc);
-      for (int i = tid; i <= m; i += kThreads) sla[base + i] = cmul(sla[base + i], sc);
-      sc = 1.0;
-      renorm = true;
+    const float* c2z = c.c2_score + (size_t)s * c.list_cap;
+    // update weights u = canonical fp64 softmax of the C2 scores
+    // (devmath.softmax_update, engine.py:184) with the C2 max from the finish
+    // kernel; thread t owns entries t + 256 i, exactly the entries it folds
+    // below.  The |sum u - 1| <= 1e-6 check (tables.py:161-163) cannot fail
+    // for finite scores (the max term is exactly 1, every u rounds once); if it
+    // ever did, this session alone would skip its commit.
+    const double mx = c.bw.wstat[2 * (size_t)s];
+    double e[kMaxE];
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < kMaxE; ++i) {
+      const int j = tid + i * kThreads;
+      e[i] = j < k2 ? cexp(csub((double)c2z[j], mx)) : 0.0;
+      if (j < k2) acc = cadd(acc, e[i]);
     }
-    // slash shift (tables.py:174-177)
-    base -= 1;
-    __syncthreads();
-    if (tid == 0) sla[base] = 0.0;
-    __syncthreads();
-    // residual fold and clamp (tables.py:179-199), kUnroll entries in flight
-    const double inv = cdiv(1.0, cmul(2.0, (double)k2));
-    int clamps = 0;
-    for (int j0 = tid; j0 < k2; j0 += kThreads * kUnroll) {
-      int li[kUnroll];
-      double u[kUnroll], v0[kUnroll], w0[kUnroll];
+    for (int j = tid + kMaxE * kThreads; j < k2; j += kThreads) acc = cadd(acc, cexp(csub((double)c2z[j], mx)));
+    const double tot = block_sum256(acc, red);
+    acc = 0.0;
 #pragma unroll
-      for (int r = 0; r < kUnroll; ++r) {
-        const int j = j0 + r * kThreads;
-        li[r] = j < k2 ? idx[j] - c.S : -1;
-        u[r] = j < k2 ? uw[j] : 0.0;
-      }
-#pragma unroll
-      for (int r = 0; r < kUnroll; ++r) {
-        v0[r] = li[r] >= 0 ? ver[li[r]] : 0.0;
-        w0[r] = li[r] >= 0 ? sla[base + li[r]] : 0.0;
-      }
-#pragma unroll
-      for (int r = 0; r < kUnroll; ++r) {
-        if (li[r] < 0) continue;
-        const double add = cdiv(csub(u[r], inv), sc);
-        double v = cadd(v0[r], add);
-        if (v < 0.0) { v = 0.0; ++clamps; }
-        ver[li[r]] = v;
-        const int slot = base + li[r];
-        double w = cadd(w0[r], add);
-        if (w < 0.0) { w = 0.0; ++clamps; }
-        sla[slot] = w;
-        mark(dmark, 0, li[r] / kBlk);
-        mark(dmark, 1, slot / kBlk);
+    for (int i = 0; i < kMaxE; ++i) {
+      const int j = tid + i * kThreads;
+      if (j < k2) {
+        e[i] = cdiv(e[i], tot);
+        acc = cadd(acc, e[i]);
       }
     }
-    for (int o = 16; o >= 1; o >>= 1) clamps += __shfl_xor_sync(LFPS_FULL, clamps, o);
-    if ((tid & 31) == 0) clamp_red[tid >> 5] = clamps;
-    if (tid == 0) {
-      // grow (tables.py:202-220): vertical slot m, slash slot base (new logical 0)
-      mark(dmark, 0, m / kBlk);
-      mark(dmark, 1, base / kBlk);
-    }
-    __syncthreads();
-    if (tid < 2 * dw) {
-      const int t = tid / dw, w = tid % dw;
-      const uint32_t mk = dmark[t][w];
-      if (mk) dirty[t * dw + w] |= mk;
-    }
-    if (tid == 0) {
-      int tc = 0;
-      for (int w = 0; w < kThreads / 32; ++w) tc += clamp_red[w];
-      c.counts[(size_t)s * CNT_N + CNT_CLAMP] = tc;
-      c.clamp_count[s] += tc;
-      ver[m] = 0.0;                       // the parked slash value at logical m stays
-      c.scale[s] = sc;
-      c.sla_base[s] = base;
-      if (renorm) c.bw.valid[s] = 0;
+    for (int j = tid + kMaxE * kThreads; j < k2; j += kThreads)
+      acc = cadd(acc, cdiv(cexp(csub((double)c2z[j], mx)), tot));
+    const double wsum = block_sum256(acc, red);
+    const bool wok = fabs(wsum - 1.0) <= 1e-6;        // block-uniform
+    if (!wok && tid == 0) set_err(c, s, LFPS_ERR_WEIGHT_SUM);
+    if (wok) {
+      // decay with renormalisation (tables.py:167-169, 240-244)
+      double sc = cmul(sc0, c.r);
+      bool renorm = false;
+      if (sc < 1e-120) {
+        for (int i = tid; i < m; i += kThreads) ver[i] = cmul(ver[i], sc);
+        for (int i = tid; i <= m; i += kThreads) sla[base + i] = cmul(sla[base + i], sc);
+        sc = 1.0;
+        renorm = true;
+      }
+      // slash shift (tables.py:174-177)
+      base -= 1;
+      __syncthreads();
+      if (tid == 0) sla[base] = 0.0;
+      __syncthreads();
+      // residual fold and clamp (tables.py:179-199), kUnroll entries in flight
+      const double inv = cdiv(1.0, cmul(2.0, (double)k2));
+      int clamps = 0;
+      // entries j = tid + 256 i, i = i0 .. i0 + kUnroll - 1 (weights of i < kMaxE
+      // cached in registers: the i loop is unrolled so e[] stays in registers)
+      auto fold = [&](int i0, const double* u) {
+        int li[kUnroll];
+        double v0[kUnroll], w0[kUnroll];
+#pragma unroll
+        for (int r = 0; r < kUnroll; ++r) {
+          const int j = tid + (i0 + r) * kThreads;
+          li[r] = j < k2 ? idx[j] - c.S : -1;
+        }
+#pragma unroll
+        for (int r = 0; r < kUnroll; ++r) {
+          v0[r] = li[r] >= 0 ? ver[li[r]] : 0.0;
+          w0[r] = li[r] >= 0 ? sla[base + li[r]] : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < kUnroll; ++r) {
+          if (li[r] < 0) continue;
+          const double add = cdiv(csub(u[r], inv), sc);
+          double v = cadd(v0[r], add);
+          if (v < 0.0) { v = 0.0; ++clamps; }
+          ver[li[r]] = v;
+          const int slot = base + li[r];
+          double w = cadd(w0[r], add);
+          if (w < 0.0) { w = 0.0; ++clamps; }
+          sla[slot] = w;
+          mark(dmark, 0, li[r] / kBlk);
+          mark(dmark, 1, slot / kBlk);
+        }
+      };
+#pragma unroll
+      for (int i0 = 0; i0 < kMaxE; i0 += kUnroll) {
+        if (tid + i0 * kThreads >= k2) break;
+        double u[kUnroll];
+#pragma unroll
+        for (int r = 0; r < kUnroll; ++r) u[r] = e[i0 + r];
+        fold(i0, u);
+      }
+      for (int i0 = kMaxE; tid + i0 * kThreads < k2; i0 += kUnroll) {
+        double u[kUnroll];
+#pragma unroll
+        for (int r = 0; r < kUnroll; ++r) {
+          const int j = tid + (i0 + r) * kThreads;
+          u[r] = j < k2 ? cdiv(cexp(csub((double)c2z[j], mx)), tot) : 0.0;
+        }
+        fold(i0, u);
+      }
+      for (int o = 16; o >= 1; o >>= 1) clamps += __shfl_xor_sync(LFPS_FULL, clamps, o);
+      if ((tid & 31) == 0) clamp_red[tid >> 5] = clamps;
+      if (tid == 0) {
+        // grow (tables.py:202-220): vertical slot m, slash slot base (new logical 0)
+        mark(dmark, 0, m / kBlk);
+        mark(dmark, 1, base / kBlk);
+      }
+      __syncthreads();
+      if (tid < 2 * dw) {
+        const int t = tid / dw, w = tid % dw;
+        const uint32_t mk = dmark[t][w];
+        if (mk) dirty[t * dw + w] |= mk;
+      }
+      if (tid == 0) {
+        int tc = 0;
+        for (int w = 0; w < kThreads / 32; ++w) tc += clamp_red[w];
+        c.counts[(size_t)s * CNT_N + CNT_CLAMP] = tc;
+        c.clamp_count[s] += tc;
+        ver[m] = 0.0;                       // the parked slash value at logical m stays
+        c.scale[s] = sc;
+        c.sla_base[s] = base;
+        if (renorm) c.bw.valid[s] = 0;
+      }
     }
   }
   // the last CTA publishes the new context lengths (every n_ctx reader is done)
