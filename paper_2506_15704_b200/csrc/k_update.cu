@@ -109,11 +109,19 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
     // ever did, this session alone would skip its commit.
     const double mx = c.bw.wstat[2 * (size_t)s];
     double e[kMaxE];
+    int lix[kMaxE];                       // logical C2 index of entry i (-1: none)
+    float zi[kMaxE];
+#pragma unroll
+    for (int i = 0; i < kMaxE; ++i) {     // one round trip for scores and indices
+      const int j = tid + i * kThreads;
+      zi[i] = j < k2 ? c2z[j] : 0.0f;
+      lix[i] = j < k2 ? idx[j] - c.S : -1;
+    }
     double acc = 0.0;
 #pragma unroll
     for (int i = 0; i < kMaxE; ++i) {
       const int j = tid + i * kThreads;
-      e[i] = j < k2 ? cexp(csub((double)c2z[j], mx)) : 0.0;
+      e[i] = j < k2 ? cexp(csub((double)zi[i], mx)) : 0.0;
       if (j < k2) acc = cadd(acc, e[i]);
     }
     for (int j = tid + kMaxE * kThreads; j < k2; j += kThreads) acc = cadd(acc, cexp(csub((double)c2z[j], mx)));
@@ -152,14 +160,8 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
       int clamps = 0;
       // entries j = tid + 256 i, i = i0 .. i0 + kUnroll - 1 (weights of i < kMaxE
       // cached in registers: the i loop is unrolled so e[] stays in registers)
-      auto fold = [&](int i0, const double* u) {
-        int li[kUnroll];
+      auto fold = [&](const int* li, const double* u) {
         double v0[kUnroll], w0[kUnroll];
-#pragma unroll
-        for (int r = 0; r < kUnroll; ++r) {
-          const int j = tid + (i0 + r) * kThreads;
-          li[r] = j < k2 ? idx[j] - c.S : -1;
-        }
 #pragma unroll
         for (int r = 0; r < kUnroll; ++r) {
           v0[r] = li[r] >= 0 ? ver[li[r]] : 0.0;
@@ -184,18 +186,24 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
       for (int i0 = 0; i0 < kMaxE; i0 += kUnroll) {
         if (tid + i0 * kThreads >= k2) break;
         double u[kUnroll];
+        int li[kUnroll];
 #pragma unroll
-        for (int r = 0; r < kUnroll; ++r) u[r] = e[i0 + r];
-        fold(i0, u);
+        for (int r = 0; r < kUnroll; ++r) {
+          u[r] = e[i0 + r];
+          li[r] = lix[i0 + r];
+        }
+        fold(li, u);
       }
       for (int i0 = kMaxE; tid + i0 * kThreads < k2; i0 += kUnroll) {
         double u[kUnroll];
+        int li[kUnroll];
 #pragma unroll
         for (int r = 0; r < kUnroll; ++r) {
           const int j = tid + (i0 + r) * kThreads;
           u[r] = j < k2 ? cdiv(cexp(csub((double)c2z[j], mx)), tot) : 0.0;
+          li[r] = j < k2 ? idx[j] - c.S : -1;
         }
-        fold(i0, u);
+        fold(li, u);
       }
       for (int o = 16; o >= 1; o >>= 1) clamps += __shfl_xor_sync(LFPS_FULL, clamps, o);
       if ((tid & 31) == 0) clamp_red[tid >> 5] = clamps;
