@@ -36,6 +36,7 @@ struct Ctx {
   float sqrt_d_f32;
   int s, S, L, bypass_mode, exhaustive, n_off, flags;
   int s_off, s_cnt;   // session range [s_off, s_off + s_cnt) of a per-session launch
+  int epoch;          // nonzero call stamp: err[0] == epoch <=> this call failed
   int off[16];
   // state
   const __nv_bfloat16* K;
@@ -82,7 +83,7 @@ __device__ __forceinline__ const __nv_bfloat16* vrow(const Ctx& c, int b, int h,
 
 __device__ __forceinline__ void set_err(const Ctx& c, int s, int code) {
   c.err[1 + s] = code;
-  atomicExch(c.err, 1);
+  atomicExch(c.err, c.epoch);
 }
 
 // phase timestamps (LFPS_FLAG_TRACE): slot k of session s = clock64() - t0;

@@ -15,7 +15,7 @@
 // renormalisation invalidates all of the session's block summaries.
 //
 // Nothing is committed if any session of the batch raised a data error
-// (err[0] != 0): the whole step is atomic (engine.py:8-9).
+// (err[0] == this call's stamp): the whole step is atomic (engine.py:8-9).
 #include "common.cuh"
 #include "canon.cuh"
 
@@ -67,13 +67,13 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
   const int s = blockIdx.x, tid = threadIdx.x;
   const int b = s / c.Hq, qh = s % c.Hq;
   // independent prologue loads, issued together
-  const int failed = c.err[0];
+  const int failed = c.err[0] == c.epoch;
   const int n = c.n_ctx[b];
   int base = c.sla_base[s];
   const int byp = c.bypass[s];
   const double sc0 = c.scale[s];
   const int k2 = c.counts[(size_t)s * CNT_N + CNT_C2];
-  if (failed != 0) return;                    // a failed step commits nothing
+  if (failed) return;                         // a failed step commits nothing
   const int m = n - c.S;
   double* ver = ver_row(c, s);
   double* sla = sla_row(c, s);
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
     // kernel; thread t owns entries t + 256 i, exactly the entries it folds
     // below.  The |sum u - 1| <= 1e-6 check (tables.py:161-163) cannot fail
     // for finite scores (the max term is exactly 1, every u rounds once); if it
-    // ever did, this session alone would skip its commit.
+    // ever did, this session alone would skip its commit (err[0] = -stamp).
     const double mx = c.bw.wstat[2 * (size_t)s];
     double e[kMaxE];
     int lix[kMaxE];                       // logical C2 index of entry i (-1: none)
@@ -139,7 +139,10 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
       acc = cadd(acc, cdiv(cexp(csub((double)c2z[j], mx)), tot));
     const double wsum = block_sum256(acc, red);
     const bool wok = fabs(wsum - 1.0) <= 1e-6;        // block-uniform
-    if (!wok && tid == 0) set_err(c, s, LFPS_ERR_WEIGHT_SUM);
+    if (!wok && tid == 0) {                  // reported, but not as a failed step:
+      c.err[1 + s] = LFPS_ERR_WEIGHT_SUM;    // the other sessions commit
+      atomicExch(c.err, -c.epoch);
+    }
     if (wok) {
       // decay with renormalisation (tables.py:167-169, 240-244)
       double sc = cmul(sc0, c.r);
@@ -239,6 +242,10 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
       __threadfence();
       for (int r = 0; r < c.B; ++r) c.n_ctx[r] += 1;
       *c.done = 0u;
+      // err[0] after a step: 0 = committed (a stale stamp of an earlier failed
+      // call is dropped here), this call's stamp = failed
+      const int e0 = atomicAdd(c.err, 0);
+      if (e0 != c.epoch && e0 != -c.epoch) c.err[0] = 0;
     }
   }
 }

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <cmath>
+#include <atomic>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -134,7 +135,7 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
     return fail(LFPS_E_INVALID, "workspace too small: %zu < %zu bytes", ws->bytes, L.total_bytes);
   memset(c, 0, sizeof(*c));
   c->B = d->batch; c->Hkv = d->kv_heads; c->G = d->group; c->Hq = d->kv_heads * d->group;
-  c->NS = c->B * c->Hq; c->s_off = 0; c->s_cnt = c->NS; c->d = d->d; c->n_max = d->n_max; c->m_cap = d->m_cap;
+  c->NS = c->B * c->Hq; c->s_off = 0; c->s_cnt = c->NS; c->epoch = 1; c->d = d->d; c->n_max = d->n_max; c->m_cap = d->m_cap;
   c->sla_cap = slash_cap(d->m_cap); c->sla_home = slash_home(d->m_cap);
   c->words = L.words; c->list_cap = L.list_cap;
   c->r = p->r; c->eps = p->epsilon; c->a = p->a; c->frac = p->k_fraction; c->sqrt_d = p->sqrt_d;
@@ -242,6 +243,15 @@ cudaEvent_t prof_event() {
   } while (0)
 
 // ---- internal streams for session-group concurrency (LFPS_FLAG_SPLIT) -------
+// call stamps for err[0] (Ctx::epoch): a decode step that fails leaves its
+// stamp in err[0]; the next step's kernels compare against their own stamp,
+// so no clearing kernel is needed (per-session codes are cleared by the gate)
+std::atomic<int> g_epoch{1};
+int next_epoch() {
+  int e = g_epoch.fetch_add(1) & 0x3fffffff;
+  return e ? e : next_epoch();
+}
+
 #ifndef LFPS_SPLIT_GROUPS
 #define LFPS_SPLIT_GROUPS 2
 #endif
@@ -293,8 +303,8 @@ int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out) {
 int lfps_decode_launches(const lfps_dims* dims, int32_t flags) {
   if (dims && (flags & LFPS_FLAG_SPLIT) &&
       (long long)dims->batch * dims->kv_heads * dims->group >= 256)
-    return 2 + 4 * kSplitGroups;
-  return 6;
+    return 1 + 4 * kSplitGroups;
+  return 5;
 }
 
 int lfps_slash_capacity(const lfps_dims* dims) {
@@ -377,7 +387,7 @@ int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_sta
   if (rc) return rc;
   cudaStream_t sm = static_cast<cudaStream_t>(stream);
   const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
-  LAUNCH_P("clear_err", sm, lfps::launch_clear_err(c, sm));
+  c.epoch = next_epoch();
   if ((c.flags & LFPS_FLAG_SPLIT) && !g_prof_on && c.NS >= 256) {
     // two session halves, each gate -> stats -> select -> finish on its own stream
     Pipe* pp = nullptr;

@@ -35,9 +35,9 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(lib, name), name
     assert set(_lib.EXPORTS) <= set(declared_functions())
     assert lib.lfps_abi_version() == _lib.ABI_VERSION
-    assert lib.lfps_decode_launches(None, 0) == 6 and lib.lfps_exact_launches() > 0
+    assert lib.lfps_decode_launches(None, 0) == 5 and lib.lfps_exact_launches() > 0
     big = _lib.Dims(64, 8, 4, 128, 4096, 4096)
-    assert lib.lfps_decode_launches(C.byref(big), _lib.FLAG_SPLIT) == 10
+    assert lib.lfps_decode_launches(C.byref(big), _lib.FLAG_SPLIT) == 9
 
 
 def test_struct_layouts_match_header(tmp_path):

@@ -233,3 +233,32 @@ def test_full_attention_matches_oracle():
             ref = w @ values
             got = out[0, h * pair.G + g]
             assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-5
+
+
+def test_failed_step_commits_nothing_then_recovers():
+    """A data error in one session (a non-finite query -> non-finite gate
+    logits, engine.py:8-9) fails the whole step: nothing is committed, the
+    error is reported; the next good step commits exactly as if the failed
+    call never happened (the err[0] call stamp needs no clearing kernel)."""
+    import gpu_drive
+    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, n0=900, steps=3, seed=29)
+    sess = pair.sess
+    n0 = pair.n0
+    res, outs = pair.step(Q[:, :, :, 0], K[:, :, n0], V[:, :, n0], 0.05)
+    pair.compare_step(res, outs)
+    before = [t.clone() for t in (sess.ver, sess.sla, sess.scale, sess.sla_base, sess.n_ctx)]
+    n_before = list(sess.n_host)
+    qbad = Q[:, :, :, 1].copy()
+    qbad[1, 0, 2, 5] = np.inf                      # session 1 * 8 + 0 * 4 + 2
+    with pytest.raises(ValueError, match="session 10"):
+        sess.decode_step(gpu_drive.bf16(qbad.reshape(2, -1, pair.d)).cuda(),
+                         gpu_drive.bf16(K[:, :, n0 + 1]).cuda(),
+                         gpu_drive.bf16(V[:, :, n0 + 1]).cuda(), 0.05, check=True)
+    assert list(sess.n_host) == n_before
+    after = (sess.ver, sess.sla, sess.scale, sess.sla_base, sess.n_ctx)
+    assert all(torch.equal(x, y) for x, y in zip(before, after))
+    # the good step (same new row) commits and matches the oracle
+    res, outs = pair.step(Q[:, :, :, 1], K[:, :, n0 + 1], V[:, :, n0 + 1], 0.05)
+    pair.compare_step(res, outs)
+    res, outs = pair.step(Q[:, :, :, 2], K[:, :, n0 + 2], V[:, :, n0 + 2], 0.05)
+    pair.compare_step(res, outs)
