@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--no-split", action="store_true",
                     help="disable LFPS_FLAG_SPLIT (two session halves on two streams)")
     ap.add_argument("--unit-finish", action="store_true", help="LFPS_FLAG_UNIT_FINISH")
+    ap.add_argument("--gather", action="store_true",
+                    help="N > 1: all-gather each e2e step's outputs and C2 counts to rank 0 (NCCL)")
     ap.add_argument("--profile-only", action="store_true",
                     help="short run for ncu: no e2e, recall or cpu legs")
     return ap.parse_args()
@@ -96,6 +98,11 @@ def dist_init(world, local):
             dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
+
+
+def dist_backend() -> str:
+    import torch.distributed as dist
+    return dist.get_backend() if dist.is_initialized() else "none"
 
 
 def barrier(world):
@@ -503,20 +510,43 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize(dev)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        # --gather (N > 1): every step ends with an NCCL all-gather of the
+        # batch's outputs and C2 counts (equal shards), read back on rank 0 --
+        # the north star's final gather, after the decode path.  Opt-in: it
+        # has not been run on more than one GPU yet.
+        gather = args.gather and world > 1 and dist_backend() == "nccl"
+        if gather:
+            import torch.distributed as dist
+            cnt_d = torch.empty(sess.counts.shape, dtype=torch.int32, device=dev)
+            g_out = torch.empty((world,) + tuple(sess.out.shape), dtype=torch.float32, device=dev)
+            g_cnt = torch.empty((world,) + tuple(sess.counts.shape), dtype=torch.int32, device=dev)
+            out_h = torch.empty(g_out.shape, dtype=torch.float32).pin_memory()
+            cnt_h = torch.empty(g_cnt.shape, dtype=torch.int32).pin_memory()
         base = args.warmup + args.steps + prof_steps
         e0.record(cuda_stream)
         for t in range(base, base + e2e_steps):
             ind.copy_(inh[t % T_in], non_blocking=True)
             sess.decode_step(qd, kd, vd, frac)
-            out_h.copy_(sess.out, non_blocking=True)
+            if gather:
+                cnt_d.copy_(sess.counts)
+                dist.all_gather_into_tensor(g_out, sess.out)
+                dist.all_gather_into_tensor(g_cnt, cnt_d)
+                if rank == 0:
+                    out_h.copy_(g_out, non_blocking=True)
+                    cnt_h.copy_(g_cnt, non_blocking=True)
+            else:
+                out_h.copy_(sess.out, non_blocking=True)
         e1.record(cuda_stream)
         torch.cuda.synchronize(dev)
         e2e_ms = allmax(world, e0.elapsed_time(e1) / e2e_steps)
         sess.check_errors("e2e steps")
+        d2h = out_h.numel() * 4 + (cnt_h.numel() * 4 if gather else 0)
         e2e = {"value": e2e_ms * 1e3, "unit": UNIT,
                "h2d_bytes_per_step": int(ind.numel() * ind.element_size()),
-               "d2h_bytes_per_step": int(out_h.numel() * 4),
-               "api": "BatchedSession.decode_step (pinned host q/k/v in, host output back)"}
+               "d2h_bytes_per_step": int(d2h if rank == 0 or not gather else 0),
+               "api": "BatchedSession.decode_step (pinned host q/k/v in, host output back)"
+                      + ("; outputs and C2 counts all-gathered over NCCL, read back on rank 0"
+                         if gather else "")}
 
     # ---- recall vs the exact full-scan path, and its device time ----
     recall = None
