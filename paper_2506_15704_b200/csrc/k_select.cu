@@ -326,9 +326,9 @@ __global__ void __launch_bounds__(kStatsThreads, LFPS_STATS_CTAS) lfps_stats_ker
 struct SelectShared {
   int nhot;
   int task[kMaxTasks];
-  uint16_t fbuf[kWarps][1024];   // a warp's candidate positions: lane << 5 | bit
-  int fword[kWarps][32];         // C0 word of each lane
-  uint32_t fc1[kWarps][32];      // C1 bits of each lane's word
+  uint16_t fbuf[kThreads * 32];  // the round's candidate slots: thread << 5 | bit
+  int fword[kThreads];           // C0 word of each thread
+  uint32_t fc1[kThreads];        // C1 bits of each thread's word
   double thr0[2], thrf[2];
   int deg[2];
   int wsum[kWarps];
@@ -476,33 +476,26 @@ __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel
       }
       uint32_t c1 = cand;
       if (!c.exhaustive) {
-        // F at the dilated positions.  The warp's candidates are flattened
-        // into one list and read 32 lanes x 4 deep, so a dense word (a band:
-        // 32 candidates) costs the warp no more round trips than a sparse one.
-        const int k = __popc(cand);
-        int off = k;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(LFPS_FULL, off, o);
-          if (lane >= o) off += y;
-        }
-        const int K = __shfl_sync(LFPS_FULL, off, 31);
-        off -= k;
-        uint16_t* buf = sh.fbuf[warp];
-        for (uint32_t x = cand; x; x &= x - 1) buf[off++] = (uint16_t)((lane << 5) | (__ffs(x) - 1));
-        sh.fword[warp][lane] = w;
-        sh.fc1[warp][lane] = 0u;
-        __syncwarp();
-        for (int g0 = lane; g0 < K; g0 += 128) {
+        // F at the dilated positions.  The round's candidates are flattened
+        // into one list and read by all 256 threads, 4 deep: a band of dense
+        // words (32 candidates each, all in one warp) costs no more round
+        // trips than scattered sparse words.
+        int K;
+        int off = block_scan(__popc(cand), sh.wsum, &K);
+        for (uint32_t x = cand; x; x &= x - 1) sh.fbuf[off++] = (uint16_t)((tid << 5) | (__ffs(x) - 1));
+        sh.fword[tid] = w;
+        sh.fc1[tid] = 0u;
+        __syncthreads();
+        for (int g0 = tid; g0 < K; g0 += 4 * kThreads) {
           int e[4];
           long long xv[4], xs[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) e[q] = g0 + 32 * q < K ? buf[g0 + 32 * q] : -1;
+          for (int q = 0; q < 4; ++q) e[q] = g0 + kThreads * q < K ? sh.fbuf[g0 + kThreads * q] : -1;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             xv[q] = xs[q] = -1ll;
             if (e[q] >= 0) {
-              const int i = sh.fword[warp][e[q] >> 5] * 32 + (e[q] & 31);
+              const int i = sh.fword[e[q] >> 5] * 32 + (e[q] & 31);
               xv[q] = __ldg(verb + i);
               xs[q] = __ldg(slab + i);
             }
@@ -510,10 +503,10 @@ __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             if (e[q] >= 0 && (xv[q] > tfv || xs[q] > tfs))
-              atomicOr(&sh.fc1[warp][e[q] >> 5], 1u << (e[q] & 31));
+              atomicOr(&sh.fc1[e[q] >> 5], 1u << (e[q] & 31));
         }
-        __syncwarp();
-        c1 = sh.fc1[warp][lane];
+        __syncthreads();
+        c1 = sh.fc1[tid];
       }
       uint32_t pr = 0u;
       if (w >= 0) {
