@@ -386,11 +386,12 @@ def phase_trace(sess, step, t, dev) -> dict:
         return float(col.mean()) / ghz / 1e3
 
     return {
-        # stats kernel (per session x table; table 0's CTA): A, A + B; select
-        # kernel (per session): C, C + D
+        # stats kernel (per session x table; table 0's CTA): A, A + B, A + B +
+        # C; select kernel (per session): C0 assembly, + D
         "select": {"A_rebuild": us(tr[:, 1]), "B_merge": us(tr[:, 2] - tr[:, 1]),
-                   "C_hot": us(tr[:, 3]), "D_probe": us(tr[:, 4] - tr[:, 3]),
-                   "cta_total": us(tr[:, 2] + tr[:, 4]),
+                   "C_hot": us(tr[:, 7] - tr[:, 2]), "C0_assemble": us(tr[:, 3]),
+                   "D_probe": us(tr[:, 4] - tr[:, 3]), "D_first_F_reads": us(tr[:, 6] - tr[:, 3]),
+                   "cta_total": us(tr[:, 7] + tr[:, 4]),
                    "span": float(tr[:, 12].max() - tr[:, 15].min()) / 1e3},
         "finish": {"union": us(tr[:, 11]), "rows": us(tr[:, 8]), "merge": us(tr[:, 9] - tr[:, 8]),
                    "checks": us(tr[:, 10] - tr[:, 9]), "cta_total": us(tr[:, 10]),

@@ -45,7 +45,7 @@ extern "C" {
 #define LFPS_API
 #endif
 
-#define LFPS_ABI_VERSION 2
+#define LFPS_ABI_VERSION 3
 
 #define LFPS_OK 0
 #define LFPS_E_INVALID -1   /* bad argument (shape, range, capacity) */
@@ -137,7 +137,8 @@ typedef struct lfps_ws_layout {
   size_t probe_score; /* f32 [NS, list_cap] */
   size_t c2_idx;      /* i32 [NS, list_cap] */
   size_t c2_score;    /* f32 [NS, list_cap] */
-  size_t uw;          /* f64 [NS, list_cap] update weights u of C2 */
+  size_t uw;          /* f64 [NS, list_cap] scratch: exact-path top-k overflow,
+                         per-unit finish update weights */
   size_t scratch;     /* f64 [NS, list_cap] bootstrap scratch */
   /* Block summaries of the tracker tables.  These PERSIST across steps (a
      cache of the state, kept in the workspace): item = 2 s + table (0 =
@@ -151,6 +152,9 @@ typedef struct lfps_ws_layout {
   size_t wstat;       /* f64 [NS, 2] max and normaliser of the update softmax */
   size_t trace;       /* i64 [NS, 16] phase timestamps (LFPS_FLAG_TRACE) */
   size_t done;        /* u32 commit-kernel completion counter (kept at 0) */
+  size_t hot;         /* i32x2 [2 NS, 16 nblk + 1] per-step C0 words of each
+                         table: (count, 0), then (logical index of the
+                         word's first slot, slot bits) */
   int32_t nblk;       /* blocks per item (slash_cap / 512) */
   int32_t dirty_words;
   int32_t words;      /* bitmap words per (session, table, kind) */

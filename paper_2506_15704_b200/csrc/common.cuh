@@ -64,9 +64,10 @@ struct Ctx {
   float* probe_score;
   int* c2_idx;
   float* c2_score;
-  double* uw;       // [NS, list_cap] update weights u of C2 (finish -> update)
+  double* uw;       // [NS, list_cap] scratch (exact top-k overflow, per-unit finish weights)
   long long* trace; // [NS, 16] phase timestamps (LFPS_FLAG_TRACE)
-  unsigned* done;   // [1] CTAs finished in the commit kernel (last one bumps n_ctx)
+  unsigned* done;     // [1] CTAs finished in the commit kernel (last one bumps n_ctx)
+  int2* hot;          // [2 NS][16 nblk + 1] per-step C0 words (k_select.cu)
   double* scratch;
   BlockWs bw;
 };

@@ -218,10 +218,20 @@ __device__ __forceinline__ long long warp_max64(long long x) {
 }
 
 struct StatsShared {
-  int ntask;
+  int ntask, nhot, npair;
   int task[kLeaves];
+  int hot[kLeaves];
   Mom part[4];
+  double thr0;
+  int deg;
 };
+
+// C0 words of one (session, table), written by lfps_stats_kernel for
+// lfps_select_kernel (ws.hot): entry 0 = (count, 0), then (logical index of
+// the word's first slot, 32 slot bits); at most 16 words per block
+__device__ __forceinline__ int2* hot_list(const Ctx& c, int s, int t) {
+  return c.hot + (size_t)(2 * s + t) * (16 * c.bw.nblk + 1);
+}
 
 #ifndef LFPS_STATS_CTAS
 #define LFPS_STATS_CTAS 8
@@ -318,14 +328,49 @@ __global__ void __launch_bounds__(kStatsThreads, LFPS_STATS_CTAS) lfps_stats_ker
     }
     double* thr = c.thr + (size_t)(2 * s + t) * 4;
     thr[0] = tau; thr[1] = mean; thr[2] = deg ? 1.0 : 0.0; thr[3] = kappa;
-    atomicAdd(c.counts + (size_t)s * CNT_N + CNT_BLOCKS, sh.ntask);
+    sh.deg = deg ? 1 : 0;
+    sh.thr0 = deg ? NAN : cdiv(tau, sc);
+    sh.nhot = 0;
+    sh.npair = 0;
     if (t == 0 && (c.flags & LFPS_FLAG_TRACE)) c.trace[(size_t)s * 16 + 2] = now_clk() - tclk0;
+  }
+  __syncthreads();
+
+  // ---- C: this table's part of C0 (select_initial): only blocks whose max is
+  // above tau / scale can hold members (the dirty ones were just read by A) ----
+  int2* hot = hot_list(c, s, t);
+  if (!sh.deg) {
+    const long long tb = thr_bits(sh.thr0);
+    const double* bm = c.bw.bmax + (size_t)(2 * s + t) * nb;
+    for (int i = tid; i < w.nseg; i += kStatsThreads)
+      if (__double_as_longlong(__ldcg(bm + w.first + i)) > tb) sh.hot[atomicAdd(&sh.nhot, 1)] = w.first + i;
+    __syncthreads();
+    for (int k = warp; k < sh.nhot; k += kStatsWarps) {
+      const int blk = sh.hot[k];
+      int a, vc;
+      segment(w, blk, a, vc);
+      double v[16];
+      load_seg(row, a, vc, lane, v);
+      const int L0 = a - w.lo;                         // logical index of element 0
+      uint32_t mine = 0;                               // lane e keeps ballot word e
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const uint32_t wd = __ballot_sync(LFPS_FULL, e * 32 + lane < vc &&
+                                                         __double_as_longlong(v[e]) > tb);
+        if (lane == e) mine = wd;
+      }
+      if (lane < 16 && mine) hot[1 + atomicAdd(&sh.npair, 1)] = make_int2(L0 + lane * 32, (int)mine);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    hot[0] = make_int2(sh.npair, 0);
+    atomicAdd(c.counts + (size_t)s * CNT_N + CNT_BLOCKS, sh.ntask + sh.nhot);
+    if (t == 0 && (c.flags & LFPS_FLAG_TRACE)) c.trace[(size_t)s * 16 + 7] = now_clk() - tclk0;
   }
 }
 
 struct SelectShared {
-  int nhot;
-  int task[kMaxTasks];
   uint16_t fbuf[kThreads * 32];  // the round's candidate slots: thread << 5 | bit
   int fword[kThreads];           // C0 word of each thread
   uint32_t fc1[kThreads];        // C1 bits of each thread's word
@@ -353,6 +398,18 @@ __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel
     tau = thr[0]; mean = thr[1]; degv = thr[2];
     sc = c.scale[s];
   }
+  // the tables' C0 words from lfps_stats_kernel: the counts and the first
+  // 256 words of each list in the same round trip
+  int2 hp[2] = {make_int2(0, 0), make_int2(0, 0)};
+  int hn[2] = {0, 0};
+  if (!c.exhaustive && !byp) {
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int2* hl = hot_list(c, s, t);
+      hn[t] = hl[0].x;
+      if (tid < 16 * c.bw.nblk) hp[t] = hl[1 + tid];
+    }
+  }
   if (byp) {
     if (tid < CNT_N) cnt[tid] = 0;
     return;
@@ -375,7 +432,6 @@ __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel
     c0w[w] = !c.exhaustive ? 0u : ((w == W - 1 && (m & 31)) ? ((1u << (m & 31)) - 1u) : LFPS_FULL);
   for (int w = tid; w < AW; w += kThreads)
     act[w] = !c.exhaustive ? 0u : ((w == AW - 1 && (W & 31)) ? ((1u << (W & 31)) - 1u) : LFPS_FULL);
-  if (tid == 0) sh.nhot = 0;
   if (tid < 2) {
     const int t = tid;
     double* thr = c.thr + (size_t)(2 * s + t) * 4;
@@ -393,40 +449,15 @@ __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel
     for (int w = max(0, m - c.L) >> 5; w < W; ++w) act[w >> 5] |= 1u << (w & 31);
     c.bw.valid[s] = 1;                   // both tables' summaries are current
   }
-  // ---- C: C0 from the hot blocks (select_initial) ----------------------------------
+  // ---- C: C0 = union of the tables' words (select_initial) ------------------------
   if (!c.exhaustive) {
-    for (int t = 0; t < 2; ++t) {
-      if (sh.deg[t]) continue;                       // a degenerate table contributes nothing
-      const long long tb = thr_bits(sh.thr0[t]);
-      const Window& w = t ? wsl : wv;
-      const double* bm = c.bw.bmax + (size_t)(2 * s + t) * nb;
-      for (int i = tid; i < w.nseg; i += kThreads) {
-        if (__double_as_longlong(__ldcg(bm + w.first + i)) > tb) {
-          const int pos = atomicAdd(&sh.nhot, 1);
-          sh.task[pos] = (t << 16) | (w.first + i);
-        }
-      }
-    }
-    __syncthreads();
-    for (int k = warp; k < sh.nhot; k += kWarps) {
-      const int task = sh.task[k];
-      const int t = task >> 16, blk = task & 0xffff;
-      const Window& w = t ? wsl : wv;
-      int a, vc;
-      segment(w, blk, a, vc);
-      double v[16];
-      load_seg(t ? sla_row(c, s) : ver, a, vc, lane, v);
-      const long long tb = thr_bits(sh.thr0[t]);
-      const int L0 = a - w.lo;                         // logical index of element 0
-      uint32_t mine = 0;                               // lane e keeps ballot word e
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const uint32_t wd = __ballot_sync(LFPS_FULL, e * 32 + lane < vc &&
-                                                         __double_as_longlong(v[e]) > tb);
-        if (lane == e) mine = wd;
-      }
-      if (lane < 16 && mine) {                         // 16 lanes publish in parallel
-        const int L = L0 + lane * 32;
+    for (int t = 0; t < 2; ++t) {
+      const int2* hl = hot_list(c, s, t);
+      for (int i = tid; i < hn[t]; i += kThreads) {
+        const int2 e = i == tid ? hp[t] : hl[1 + i];
+        const uint32_t mine = (uint32_t)e.y;
+        const int L = e.x;
         const int sft = L & 31, wi = L >> 5;
         atomicOr(&c0w[wi], mine << sft);
         const bool hi = sft && (mine >> (32 - sft));
@@ -506,6 +537,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel
               atomicOr(&sh.fc1[e[q] >> 5], 1u << (e[q] & 31));
         }
         __syncthreads();
+        if (r == 0) trace_at(c, s, 6, tclk0);         // first round's F reads done
         c1 = sh.fc1[tid];
       }
       uint32_t pr = 0u;
@@ -539,7 +571,6 @@ __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel
       cnt[CNT_C1] = t1;
       cnt[CNT_PROBE] = written;
       cnt[CNT_DROP] = t3;
-      cnt[CNT_BLOCKS] += sh.nhot;          // + the rebuilt blocks of lfps_stats_kernel
       if (c.flags & LFPS_FLAG_TRACE) {
         c.trace[(size_t)s * 16 + 4] = now_clk() - tclk0;
         c.trace[(size_t)s * 16 + 12] = now_ns();

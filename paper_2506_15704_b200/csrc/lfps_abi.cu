@@ -118,6 +118,7 @@ int layout(const lfps_dims* d, lfps_ws_layout* L) {
   L->wstat = take(NS * 2 * 8);
   L->trace = take(NS * 16 * 8);
   L->done = take(64);
+  L->hot = take(NI * (size_t)(16 * L->nblk + 1) * 8);
   L->total_bytes = o;
   return LFPS_OK;
 }
@@ -174,6 +175,7 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
   c->bw.wstat = reinterpret_cast<double*>(base + L.wstat);
   c->trace = reinterpret_cast<long long*>(base + L.trace);
   c->done = reinterpret_cast<unsigned*>(base + L.done);
+  c->hot = reinterpret_cast<int2*>(base + L.hot);
   c->bw.nblk = L.nblk;
   c->bw.dwords = L.dirty_words;
   return LFPS_OK;
