@@ -43,7 +43,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kLeaves = 512;                  // segments per window: m <= 511 * 512
-constexpr int kMaxTasks = 2 * kLeaves;
 
 struct Mom {
   double n, mu, m2, m3, m4;
@@ -237,7 +236,7 @@ __device__ __forceinline__ int2* hot_list(const Ctx& c, int s, int t) {
 #define LFPS_STATS_CTAS 8
 #endif
 #ifndef LFPS_SELECT_CTAS
-#define LFPS_SELECT_CTAS 4
+#define LFPS_SELECT_CTAS 5
 #endif
 constexpr int kStatsThreads = 128;
 constexpr int kStatsWarps = kStatsThreads / 32;
@@ -425,7 +424,6 @@ __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel
   const double* sla = sla_row(c, s) + base;   // logical view
   const Window wv = make_window(0, m);
   const Window wsl = make_window(base, m);
-  const int nb = c.bw.nblk;
   const long long tclk0 = now_clk();
 
   for (int w = tid; w < W; w += kThreads)
