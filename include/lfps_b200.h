@@ -26,7 +26,10 @@
  *    gate.py:104-113; weights not summing to 1, tables.py:161-163; kappa == 0,
  *    the ZeroDivisionError of tables.py:315) are detected on the device: the
  *    step then commits NO state for any session (tables, KV rows and n_ctx
- *    unchanged) and sets err[0]; per-session codes are in err[1 + s].
+ *    unchanged) and err[0] holds the call's nonzero stamp (0 after a
+ *    committed step); err[1 + s] = (stamp << 4) | code for the sessions that
+ *    raised in that call (codes with another stamp are stale).  A negative
+ *    err[0] marks a failure that only skipped its own sessions' commit.
  *  - Session index s = b * Hq + qh, q-head qh reads KV head qh / G (GQA).
  */
 #ifndef LFPS_B200_H
@@ -45,7 +48,7 @@ extern "C" {
 #define LFPS_API
 #endif
 
-#define LFPS_ABI_VERSION 3
+#define LFPS_ABI_VERSION 4
 
 #define LFPS_OK 0
 #define LFPS_E_INVALID -1   /* bad argument (shape, range, capacity) */
@@ -127,7 +130,8 @@ typedef struct lfps_ws_layout {
   size_t total_bytes;
   size_t rho;         /* f64 [NS] sink share */
   size_t bypass;      /* i32 [NS] 1 if gated */
-  size_t err;         /* i32 [1 + NS] err[0] = any, err[1+s] per session */
+  size_t err;         /* i32 [1 + NS] err[0] = failed call's stamp, err[1+s]
+                         = stamp << 4 | code per session */
   size_t out;         /* f32 [NS, d] attention output */
   size_t thr;         /* f64 [NS, 2, 4] tau, mean, degenerate, kappa per table */
   size_t counts;      /* i32 [NS, 8] |c0| |c1| |probe| c0_dropped k |c2| clamps
@@ -153,8 +157,10 @@ typedef struct lfps_ws_layout {
   size_t trace;       /* i64 [NS, 16] phase timestamps (LFPS_FLAG_TRACE) */
   size_t done;        /* u32 commit-kernel completion counter (kept at 0) */
   size_t hot;         /* i32x2 [2 NS, 16 nblk + 1] per-step C0 words of each
-                         table: (count, 0), then (logical index of the
-                         word's first slot, slot bits) */
+                         table: (count, table blocks read), then (logical
+                         index of the word's first slot, slot bits) */
+  size_t thr_next;    /* f64 [NS, 2, 4] thresholds computed for the select
+                         kernel (copied to thr for the non-gated sessions) */
   int32_t nblk;       /* blocks per item (slash_cap / 512) */
   int32_t dirty_words;
   int32_t words;      /* bitmap words per (session, table, kind) */
@@ -195,7 +201,8 @@ LFPS_API int lfps_bootstrap_stats(const lfps_dims* dims, const lfps_params* p,
  * Top-k, joint sink+selection attention, table update, then KV append of
  * k_new / v_new and n_ctx += 1.  Table updates, the append and n_ctx are
  * committed by the last kernels of the step, after every data check of
- * every session has passed (err[0] == 0), so a failed step changes nothing
+ * every session has passed (err[0] != this call's stamp), so a failed step
+ * changes nothing
  * but the block-summary cache (which stays consistent with the tables).
  * q: bf16 [B, Hq, d]; k_new, v_new: bf16 [B, Hkv, d]; all device.
  * n_host: the caller's host copy of n_ctx [B] (used for validation and

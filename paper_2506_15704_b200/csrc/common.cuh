@@ -36,7 +36,7 @@ struct Ctx {
   float sqrt_d_f32;
   int s, S, L, bypass_mode, exhaustive, n_off, flags;
   int s_off, s_cnt;   // session range [s_off, s_off + s_cnt) of a per-session launch
-  int epoch;          // nonzero call stamp: err[0] == epoch <=> this call failed
+  int epoch;          // call stamp in [1, 2^27): err[0] == epoch <=> this call failed
   int off[16];
   // state
   const __nv_bfloat16* K;
@@ -58,6 +58,7 @@ struct Ctx {
   int* err;
   float* out;
   double* thr;
+  double* thr_next;   // [NS, 2, 4] thresholds of the upcoming select (stats -> select)
   int* counts;
   uint32_t* bits;
   int* probe_idx;
@@ -82,8 +83,12 @@ __device__ __forceinline__ const __nv_bfloat16* vrow(const Ctx& c, int b, int h,
   return c.V + (((size_t)b * c.Hkv + h) * c.n_max + i) * c.d;
 }
 
+// err[1 + s] = (call stamp << 4) | code: a code counts only for the call whose
+// stamp err[0] holds, so no kernel has to clear the codes before the gate and
+// the stats kernel (which run concurrently) may raise them
+__device__ __forceinline__ int err_code(const Ctx& c, int code) { return (c.epoch << 4) | code; }
 __device__ __forceinline__ void set_err(const Ctx& c, int s, int code) {
-  c.err[1 + s] = code;
+  c.err[1 + s] = err_code(c, code);
   atomicExch(c.err, c.epoch);
 }
 

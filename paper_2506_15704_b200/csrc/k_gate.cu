@@ -48,10 +48,6 @@ __global__ void __launch_bounds__(kGateWarps * 32) lfps_gate_kernel(Ctx c, const
   const int S = c.S, L = c.L, d = c.d;
   const int m = n - S;
   const int R = S + L;
-  if (tid == 0) {
-    c.counts[(size_t)s * CNT_N + CNT_BLOCKS] = 0;   // summed by k_select.cu
-    c.err[1 + s] = 0;                              // this call's code (err[0]: Ctx::epoch)
-  }
 
   double qv[kMaxPerLane];
   const uint16_t* qs = reinterpret_cast<const uint16_t*>(q + (size_t)s * d);

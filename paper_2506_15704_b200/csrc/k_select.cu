@@ -241,8 +241,9 @@ __device__ __forceinline__ int2* hot_list(const Ctx& c, int s, int t) {
 constexpr int kStatsThreads = 128;
 constexpr int kStatsWarps = kStatsThreads / 32;
 
-// A + B of one (session, table): rebuild the dirty blocks, merge the
-// window's segment moments, write thr[(2 s + t) * 4 + {tau, mean, deg, kappa}].
+// A + B + C of one (session, table): rebuild the dirty blocks, merge the
+// window's segment moments into thr_next[(2 s + t) * 4 + {tau, mean, deg,
+// kappa}], and list the table's C0 words.
 __global__ void __launch_bounds__(kStatsThreads, LFPS_STATS_CTAS) lfps_stats_kernel(Ctx c) {
   __shared__ StatsShared sh;
   const int s = c.s_off + (blockIdx.x >> 1), t = blockIdx.x & 1;
@@ -250,14 +251,15 @@ __global__ void __launch_bounds__(kStatsThreads, LFPS_STATS_CTAS) lfps_stats_ker
   if (c.exhaustive) return;
   const int b = s / c.Hq;
   const int dw = c.bw.dwords;
-  // independent prologue loads, issued together (one round trip, not four)
-  const int byp = c.bypass[s];
+  // independent prologue loads, issued together (one round trip, not four).
+  // The stats kernel runs concurrently with the gate, so it works for every
+  // session, gated or not: a gated session's thresholds are simply not used
+  // (and not exported) by the select kernel.
   const int n = c.n_ctx[b];
   const int base = t ? c.sla_base[s] : 0;
   const bool valid = c.bw.valid[s] != 0;
   uint32_t* dp = c.bw.dirty + (size_t)(2 * s + t) * dw + tid;
   const uint32_t dbits = tid < dw ? *dp : 0u;
-  if (byp) return;
   const int m = n - c.S;
   const Window w = make_window(base, m);
   const int nb = c.bw.nblk;
@@ -321,11 +323,10 @@ __global__ void __launch_bounds__(kStatsThreads, LFPS_STATS_CTAS) lfps_stats_ker
     const bool deg = cmul(cmul(tot.m2, sc), sc) < 1e-12;
     double tau = NAN, kappa = NAN;
     if (!deg) {
-      kappa = cdiv(tot.m4, cmul(tot.m2, tot.m2));
-      if (kappa == 0.0) set_err(c, s, LFPS_ERR_KAPPA_ZERO);
+      kappa = cdiv(tot.m4, cmul(tot.m2, tot.m2));   // kappa == 0 is raised by select
       tau = cdiv(cmul(c.a, mean), kappa);
     }
-    double* thr = c.thr + (size_t)(2 * s + t) * 4;
+    double* thr = c.thr_next + (size_t)(2 * s + t) * 4;
     thr[0] = tau; thr[1] = mean; thr[2] = deg ? 1.0 : 0.0; thr[3] = kappa;
     sh.deg = deg ? 1 : 0;
     sh.thr0 = deg ? NAN : cdiv(tau, sc);
@@ -363,8 +364,7 @@ __global__ void __launch_bounds__(kStatsThreads, LFPS_STATS_CTAS) lfps_stats_ker
     __syncthreads();
   }
   if (tid == 0) {
-    hot[0] = make_int2(sh.npair, 0);
-    atomicAdd(c.counts + (size_t)s * CNT_N + CNT_BLOCKS, sh.ntask + sh.nhot);
+    hot[0] = make_int2(sh.npair, sh.ntask + sh.nhot);
     if (t == 0 && (c.flags & LFPS_FLAG_TRACE)) c.trace[(size_t)s * 16 + 7] = now_clk() - tclk0;
   }
 }
@@ -391,26 +391,29 @@ __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel
   const int byp = c.bypass[s];
   const int n = c.n_ctx[b];
   const int base = c.sla_base[s];
-  double tau = 0.0, mean = 0.0, degv = 0.0, sc = 1.0;
+  double tau = 0.0, mean = 0.0, degv = 0.0, kap = 0.0, sc = 1.0;
   if (tid < 2 && !c.exhaustive) {
-    const double* thr = c.thr + (size_t)(2 * s + tid) * 4;
-    tau = thr[0]; mean = thr[1]; degv = thr[2];
+    const double* thr = c.thr_next + (size_t)(2 * s + tid) * 4;
+    tau = thr[0]; mean = thr[1]; degv = thr[2]; kap = thr[3];
     sc = c.scale[s];
   }
   // the tables' C0 words from lfps_stats_kernel: the counts and the first
   // 256 words of each list in the same round trip
   int2 hp[2] = {make_int2(0, 0), make_int2(0, 0)};
-  int hn[2] = {0, 0};
-  if (!c.exhaustive && !byp) {
+  int hn[2] = {0, 0}, blocks = 0;
+  if (!c.exhaustive) {
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       const int2* hl = hot_list(c, s, t);
-      hn[t] = hl[0].x;
+      const int2 h0 = hl[0];
+      hn[t] = h0.x;
+      blocks += h0.y;
       if (tid < 16 * c.bw.nblk) hp[t] = hl[1 + tid];
     }
   }
+  if (tid == 0 && !c.exhaustive) c.bw.valid[s] = 1;   // both tables' summaries are current
   if (byp) {
-    if (tid < CNT_N) cnt[tid] = 0;
+    if (tid < CNT_N) cnt[tid] = tid == CNT_BLOCKS ? blocks : 0;
     return;
   }
   const int S = c.S;
@@ -440,12 +443,13 @@ __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel
       sh.deg[t] = degv != 0.0;
       sh.thr0[t] = sh.deg[t] ? NAN : cdiv(tau, sc);
       sh.thrf[t] = cdiv(mean, sc);
+      thr[0] = tau; thr[1] = mean; thr[2] = degv; thr[3] = kap;   // export
+      if (!sh.deg[t] && kap == 0.0) set_err(c, s, LFPS_ERR_KAPPA_ZERO);
     }
   }
   __syncthreads();
   if (tid == 0 && !c.exhaustive) {       // tail words are always active
     for (int w = max(0, m - c.L) >> 5; w < W; ++w) act[w >> 5] |= 1u << (w & 31);
-    c.bw.valid[s] = 1;                   // both tables' summaries are current
   }
   // ---- C: C0 = union of the tables' words (select_initial) ------------------------
   if (!c.exhaustive) {
@@ -569,6 +573,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel
       cnt[CNT_C1] = t1;
       cnt[CNT_PROBE] = written;
       cnt[CNT_DROP] = t3;
+      cnt[CNT_BLOCKS] = blocks;
       if (c.flags & LFPS_FLAG_TRACE) {
         c.trace[(size_t)s * 16 + 4] = now_clk() - tclk0;
         c.trace[(size_t)s * 16 + 12] = now_ns();

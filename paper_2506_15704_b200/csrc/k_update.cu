@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
     const double wsum = block_sum256(acc, red);
     const bool wok = fabs(wsum - 1.0) <= 1e-6;        // block-uniform
     if (!wok && tid == 0) {                  // reported, but not as a failed step:
-      c.err[1 + s] = LFPS_ERR_WEIGHT_SUM;    // the other sessions commit
+      c.err[1 + s] = err_code(c, LFPS_ERR_WEIGHT_SUM);   // the other sessions commit
       atomicExch(c.err, -c.epoch);
     }
     if (wok) {

@@ -119,6 +119,7 @@ int layout(const lfps_dims* d, lfps_ws_layout* L) {
   L->trace = take(NS * 16 * 8);
   L->done = take(64);
   L->hot = take(NI * (size_t)(16 * L->nblk + 1) * 8);
+  L->thr_next = take(NS * 8 * 8);
   L->total_bytes = o;
   return LFPS_OK;
 }
@@ -176,6 +177,7 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
   c->trace = reinterpret_cast<long long*>(base + L.trace);
   c->done = reinterpret_cast<unsigned*>(base + L.done);
   c->hot = reinterpret_cast<int2*>(base + L.hot);
+  c->thr_next = reinterpret_cast<double*>(base + L.thr_next);
   c->bw.nblk = L.nblk;
   c->bw.dwords = L.dirty_words;
   return LFPS_OK;
@@ -250,7 +252,7 @@ cudaEvent_t prof_event() {
 // so no clearing kernel is needed (per-session codes are cleared by the gate)
 std::atomic<int> g_epoch{1};
 int next_epoch() {
-  int e = g_epoch.fetch_add(1) & 0x3fffffff;
+  int e = g_epoch.fetch_add(1) & 0x7ffffff;          // stamp << 4 fits an int32
   return e ? e : next_epoch();
 }
 
@@ -261,7 +263,8 @@ constexpr int kSplitGroups = LFPS_SPLIT_GROUPS;   // session groups of LFPS_FLAG
 struct Pipe {
   int dev = -1;
   cudaStream_t st[kSplitGroups] = {};
-  cudaEvent_t fork = nullptr, join[kSplitGroups] = {};
+  cudaStream_t aux[kSplitGroups] = {};      // the stats kernel, concurrent with the gate
+  cudaEvent_t fork = nullptr, join[kSplitGroups] = {}, stats[kSplitGroups] = {};
 };
 std::mutex g_pipe_mu;
 Pipe g_pipe[16];
@@ -276,7 +279,9 @@ cudaError_t get_pipe(Pipe** out) {
   if (p.dev < 0) {
     for (int i = 0; i < kSplitGroups; ++i) {
       if ((e = cudaStreamCreateWithFlags(&p.st[i], cudaStreamNonBlocking)) != cudaSuccess) return e;
+      if ((e = cudaStreamCreateWithFlags(&p.aux[i], cudaStreamNonBlocking)) != cudaSuccess) return e;
       if ((e = cudaEventCreateWithFlags(&p.join[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+      if ((e = cudaEventCreateWithFlags(&p.stats[i], cudaEventDisableTiming)) != cudaSuccess) return e;
     }
     if ((e = cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
     p.dev = dev;
@@ -306,7 +311,7 @@ int lfps_decode_launches(const lfps_dims* dims, int32_t flags) {
   if (dims && (flags & LFPS_FLAG_SPLIT) &&
       (long long)dims->batch * dims->kv_heads * dims->group >= 256)
     return 1 + 4 * kSplitGroups;
-  return 5;
+  return 5;   // gate | stats, select, finish, update
 }
 
 int lfps_slash_capacity(const lfps_dims* dims) {
@@ -390,40 +395,54 @@ int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_sta
   cudaStream_t sm = static_cast<cudaStream_t>(stream);
   const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
   c.epoch = next_epoch();
-  if ((c.flags & LFPS_FLAG_SPLIT) && !g_prof_on && c.NS >= 256) {
-    // two session halves, each gate -> stats -> select -> finish on its own stream
-    Pipe* pp = nullptr;
+  // The stats kernel does not depend on the gate (it serves every session),
+  // so the two run concurrently: stats on an internal stream forked from
+  // the caller's, joined before select.  LFPS_FLAG_SPLIT additionally runs
+  // kSplitGroups session groups, each [gate | stats] -> select -> finish, on
+  // their own streams; the update (commit) joins them on the caller's
+  // stream.  Under lfps_profile_enable everything runs serially on the
+  // caller's stream so each kernel is timed alone.
+  if (g_prof_on) {
+    LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
+    LAUNCH_P("stats", sm, lfps::launch_stats(c, sm));
+    LAUNCH_P("select", sm, lfps::launch_select(c, m_max, sm));
+  }
+  Pipe* pp = nullptr;
+  if (!g_prof_on) {
     LAUNCH(get_pipe(&pp));
     LAUNCH(cudaEventRecord(pp->fork, sm));
-    const int per = (c.NS / kSplitGroups + 31) / 32 * 32;
-    for (int g = 0; g < kSplitGroups; ++g) {
-      lfps::Ctx cg = c;
-      cg.s_off = g * per;
-      cg.s_cnt = g == kSplitGroups - 1 ? c.NS - g * per : per;
-      cudaStream_t gs = pp->st[g];
-      LAUNCH(cudaStreamWaitEvent(gs, pp->fork, 0));
-      LAUNCH(lfps::launch_gate(cg, qb, gs));
-      LAUNCH(lfps::launch_stats(cg, gs));
-      LAUNCH(lfps::launch_select(cg, m_max, gs));
-      LAUNCH(lfps::launch_finish(cg, qb, gs));
-      LAUNCH(cudaEventRecord(pp->join[g], gs));
-      LAUNCH(cudaStreamWaitEvent(sm, pp->join[g], 0));
-    }
-    LAUNCH_P("update", sm, lfps::launch_update(c, static_cast<const __nv_bfloat16*>(k_new),
-                                                static_cast<const __nv_bfloat16*>(v_new), sm));
-    return LFPS_OK;
   }
-  LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
-  LAUNCH_P("stats", sm, lfps::launch_stats(c, sm));
-  LAUNCH_P("select", sm, lfps::launch_select(c, m_max, sm));
+  const bool split = (c.flags & LFPS_FLAG_SPLIT) && !g_prof_on && c.NS >= 256;
   // LFPS_FLAG_UNIT_FINISH: GQA units of <= 4 q-heads (d 128 / 256) finish per
   // unit over the union of their probe rows (tensor-core softmax.V); measured
   // slower than the per-session kernel at C4 (2 CTAs/SM), so
   // it is opt-in
-  const bool per_unit = (c.flags & LFPS_FLAG_UNIT_FINISH) && (c.G <= 4) &&
+  const bool per_unit = !split && (c.flags & LFPS_FLAG_UNIT_FINISH) && (c.G <= 4) &&
                         (c.d == 128 || c.d == 256);
-  if (per_unit) LAUNCH_P("finish", sm, lfps::launch_finish_unit(c, qb, sm));
-  else LAUNCH_P("finish", sm, lfps::launch_finish(c, qb, sm));
+  const int groups = split ? kSplitGroups : 1;
+  const int per = (c.NS / groups + 31) / 32 * 32;
+  for (int g = 0; g < groups; ++g) {
+    lfps::Ctx cg = c;
+    cg.s_off = g * per;
+    cg.s_cnt = g == groups - 1 ? c.NS - g * per : per;
+    cudaStream_t gs = split ? pp->st[g] : sm;
+    if (!g_prof_on) {
+      cudaStream_t as = pp->aux[g];
+      if (split) LAUNCH(cudaStreamWaitEvent(gs, pp->fork, 0));
+      LAUNCH(cudaStreamWaitEvent(as, pp->fork, 0));
+      LAUNCH(lfps::launch_stats(cg, as));
+      LAUNCH(cudaEventRecord(pp->stats[g], as));
+      LAUNCH(lfps::launch_gate(cg, qb, gs));
+      LAUNCH(cudaStreamWaitEvent(gs, pp->stats[g], 0));
+      LAUNCH(lfps::launch_select(cg, m_max, gs));
+    }
+    if (per_unit) LAUNCH_P("finish", gs, lfps::launch_finish_unit(cg, qb, gs));
+    else LAUNCH_P("finish", gs, lfps::launch_finish(cg, qb, gs));
+    if (split) {
+      LAUNCH(cudaEventRecord(pp->join[g], gs));
+      LAUNCH(cudaStreamWaitEvent(sm, pp->join[g], 0));
+    }
+  }
   LAUNCH_P("update", sm, lfps::launch_update(c, static_cast<const __nv_bfloat16*>(k_new),
                                               static_cast<const __nv_bfloat16*>(v_new), sm));
   return LFPS_OK;

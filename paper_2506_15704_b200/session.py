@@ -227,7 +227,12 @@ class BatchedSession:
         err = self.err.cpu()
         if int(err[0]) == 0:
             return
-        codes = err[1:]
+        # err[0] = the failed call's stamp (negated: a session-local failure),
+        # err[1 + s] = stamp << 4 | code (codes of other calls are stale)
+        stamp = abs(int(err[0]))
+        raw = err[1:]
+        live = (raw >> 4) == stamp
+        codes = torch.where(live, raw & 15, torch.zeros_like(raw))
         bad = torch.nonzero(codes).flatten()
         s = int(bad[0]) if bad.numel() else -1
         code = int(codes[s]) if s >= 0 else 0
