@@ -26,6 +26,10 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kMaxDirtyWords = 32;
 constexpr int kMaxE = 8;                 // update weights cached per thread (|C2| <= 2048)
+#ifndef LFPS_UPDATE_SPEC
+#define LFPS_UPDATE_SPEC 4
+#endif
+constexpr int kSpec = LFPS_UPDATE_SPEC;  // C2 entries per thread fetched with the prologue
 
 // canonical 256-wide block sum (devmath.block_sum); all threads get it
 __device__ __forceinline__ double block_sum256(double acc, double* red) {
@@ -73,6 +77,19 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
   const int byp = c.bypass[s];
   const double sc0 = c.scale[s];
   const int k2 = c.counts[(size_t)s * CNT_N + CNT_C2];
+  // the first kSpec C2 entries of this thread, fetched with the prologue
+  // (before k2 is known; entries at or beyond k2 are ignored below)
+  const int* idx = c.c2_idx + (size_t)s * c.list_cap;
+  const float* c2z = c.c2_score + (size_t)s * c.list_cap;
+  const double mx = c.bw.wstat[2 * (size_t)s];
+  float zs[kSpec];
+  int is[kSpec];
+#pragma unroll
+  for (int i = 0; i < kSpec; ++i) {
+    const int j = tid + i * kThreads;
+    zs[i] = j < c.list_cap ? c2z[j] : 0.0f;
+    is[i] = j < c.list_cap ? idx[j] : 0;
+  }
   if (failed) return;                         // a failed step commits nothing
   const int m = n - c.S;
   double* ver = ver_row(c, s);
@@ -99,23 +116,25 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
     }
   } else {
     for (int i = tid; i < 2 * kMaxDirtyWords; i += kThreads) (&dmark[0][0])[i] = 0u;
-    const int* idx = c.c2_idx + (size_t)s * c.list_cap;
-    const float* c2z = c.c2_score + (size_t)s * c.list_cap;
     // update weights u = canonical fp64 softmax of the C2 scores
     // (devmath.softmax_update, engine.py:184) with the C2 max from the finish
     // kernel; thread t owns entries t + 256 i, exactly the entries it folds
     // below.  The |sum u - 1| <= 1e-6 check (tables.py:161-163) cannot fail
     // for finite scores (the max term is exactly 1, every u rounds once); if it
     // ever did, this session alone would skip its commit (err[0] = -stamp).
-    const double mx = c.bw.wstat[2 * (size_t)s];
     double e[kMaxE];
     int lix[kMaxE];                       // logical C2 index of entry i (-1: none)
     float zi[kMaxE];
 #pragma unroll
     for (int i = 0; i < kMaxE; ++i) {     // one round trip for scores and indices
       const int j = tid + i * kThreads;
-      zi[i] = j < k2 ? c2z[j] : 0.0f;
-      lix[i] = j < k2 ? idx[j] - c.S : -1;
+      if (i < kSpec) {
+        zi[i] = j < k2 ? zs[i] : 0.0f;
+        lix[i] = j < k2 ? is[i] - c.S : -1;
+      } else {
+        zi[i] = j < k2 ? c2z[j] : 0.0f;
+        lix[i] = j < k2 ? idx[j] - c.S : -1;
+      }
     }
     double acc = 0.0;
 #pragma unroll
