@@ -309,7 +309,8 @@ __device__ __forceinline__ float2 score_rows(const RowsT& r, const Part<PQ>& q, 
 }
 
 // Stream rows [0, nrows) through shared memory, kStagesR tiles of
-// 32 x rows_per_group rows deep: every thread copies 16-byte chunks of its group's rows
+// 32 x rows_per_group rows deep (each 8-lane group stages and reads only its
+// own rows: warp barriers only): every thread copies 16-byte chunks of its group's rows
 // (cp.async, L2 only), 8 threads per row; row_of(rid) gives the cache row of
 // list entry rid.  visit(const Rows2&) is called by EVERY thread for every
 // tile, so visits may use full-warp shuffles; a row with ok = false has a
@@ -369,7 +370,11 @@ __device__ __forceinline__ void stream_rows(uint8_t* stages, const __nv_bfloat16
 #pragma unroll 1
   for (int tile = 0; tile < ntiles; ++tile) {
     cp_async_wait<kStagesR - 2>();                    // this thread's copies of `tile` landed
-    __syncthreads();                                  // everyone's; stage (tile - 1) is free
+    // A group's rows are copied by the group's own 8 lanes and read only by
+    // them, so a warp barrier suffices: it publishes the warp's copies and
+    // frees the warp's part of stage (tile - 1).  Warps run their tiles
+    // independently (no CTA barrier per tile).
+    __syncwarp();
     issue(ws, ahead);
     fetch(tile + kStagesR, ahead);
     ws = ws + 1 == kStagesR ? 0 : ws + 1;
