@@ -19,7 +19,10 @@ constexpr int kStages = 3;               // k_finish_unit.cu: stages
 constexpr int kR = 2;                    // stream_rows: max rows per 8-lane group per tile
 // rows per group per tile for d = 16 PQ: two (one tile = 64 rows), one for
 // d = 256 so that a stage stays at 32 KB
-__host__ __device__ constexpr int rows_per_group(int pq) { return pq >= 16 ? 1 : 2; }
+#ifndef LFPS_ROWS_R
+#define LFPS_ROWS_R 2
+#endif
+__host__ __device__ constexpr int rows_per_group(int pq) { return pq >= 16 ? 1 : LFPS_ROWS_R; }
 #ifndef LFPS_ROW_STAGES
 #define LFPS_ROW_STAGES 2
 #endif
