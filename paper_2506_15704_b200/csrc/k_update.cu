@@ -116,6 +116,9 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
     }
   } else {
     for (int i = tid; i < 2 * kMaxDirtyWords; i += kThreads) (&dmark[0][0])[i] = 0u;
+    // the slot below the window becomes the new logical slot 0 (it is outside
+    // the window until then, so zeroing it early commits nothing)
+    if (tid == 0) sla[base - 1] = 0.0;
     // update weights u = canonical fp64 softmax of the C2 scores
     // (devmath.softmax_update, engine.py:184) with the C2 max from the finish
     // kernel; thread t owns entries t + 256 i, exactly the entries it folds
@@ -172,11 +175,11 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
         sc = 1.0;
         renorm = true;
       }
-      // slash shift (tables.py:174-177)
+      // slash shift (tables.py:174-177): the new logical slot 0 (base - 1) was
+      // zeroed at the top of this branch; the weight sums' barriers order it
+      // before the fold
       base -= 1;
-      __syncthreads();
-      if (tid == 0) sla[base] = 0.0;
-      __syncthreads();
+      if (renorm) __syncthreads();                     // block-uniform
       // residual fold and clamp (tables.py:179-199), kUnroll entries in flight
       const double inv = cdiv(1.0, cmul(2.0, (double)k2));
       int clamps = 0;
