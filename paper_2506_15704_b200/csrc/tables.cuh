@@ -235,6 +235,16 @@ __device__ void maintain_table(const Ctx& c, int s, int t, const Window& w, doub
   worker_sync(bar);
   if (t == 0) trace_at(c, s, 1, tclk0);
 
+  // the window's block maxima (C's input, final after A) load during B
+  long long bmx[kLeaves / 128];
+  {
+    const double* bm = c.bw.bmax + (size_t)(2 * s + t) * nb + w.first;
+#pragma unroll
+    for (int k = 0; k < kLeaves / 128; ++k) {
+      const int i = tid4 + 128 * k;
+      bmx[k] = i < w.nseg ? __double_as_longlong(__ldcg(bm + i)) : 0ll;
+    }
+  }
   // ---- B: thresholds (compute_thresholds), one quarter of the tree per warp ----------
   const Mom q = quarter_merge(c.bw.bsum + (size_t)(2 * s + t) * nb * 4, w, warp, lane);
   if (lane == 0) sh.part[warp] = q;
@@ -263,9 +273,11 @@ __device__ void maintain_table(const Ctx& c, int s, int t, const Window& w, doub
   int2* hot = hot_list(c, s, t);
   if (!sh.deg) {
     const long long tb = thr_bits(sh.thr0);
-    const double* bm = c.bw.bmax + (size_t)(2 * s + t) * nb;
-    for (int i = tid4; i < w.nseg; i += 128)
-      if (__double_as_longlong(__ldcg(bm + w.first + i)) > tb) sh.hot[atomicAdd(&sh.nhot, 1)] = w.first + i;
+#pragma unroll
+    for (int k = 0; k < kLeaves / 128; ++k) {
+      const int i = tid4 + 128 * k;
+      if (i < w.nseg && bmx[k] > tb) sh.hot[atomicAdd(&sh.nhot, 1)] = w.first + i;
+    }
     worker_sync(bar);
     for (int k = warp; k < sh.nhot; k += 4) {
       const int blk = sh.hot[k];
