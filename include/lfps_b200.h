@@ -213,6 +213,17 @@ LFPS_API int lfps_decode_step(const lfps_dims* dims, const lfps_params* p,
                      const void* q, const void* k_new, const void* v_new,
                      const int32_t* n_host, void* stream);
 
+/* lfps_decode_step plus the step's attention output copied to out_host
+ * (f32 [B, Hq, d], host memory; pinned for an asynchronous copy) as soon as
+ * the output is final: the copy runs on an internal stream alongside the
+ * commit kernel, and the caller's stream waits for it, so out_host is
+ * filled when the caller's stream reaches the end of the call.  A step that
+ * fails a data check still copies its (partial) output. */
+LFPS_API int lfps_decode_step_host_out(const lfps_dims* dims, const lfps_params* p,
+                     const lfps_state* st, const lfps_workspace* ws,
+                     const void* q, const void* k_new, const void* v_new,
+                     const int32_t* n_host, void* out_host, void* stream);
+
 /* Exact full-scan Top-k comparison path (exact_topk_step, bench.py:73-80)
  * over the pre-append rows of every session: fp32 scores of all non-sink
  * rows, Top-k with lower-index ties, joint sink+selection output.  Read-only

@@ -37,7 +37,7 @@ ERR_NAMES = {
 
 EXPORTS = ("lfps_abi_version", "lfps_last_error", "lfps_workspace_layout",
            "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step",
-           "lfps_exact_topk_step", "lfps_overlap", "lfps_decode_launches", "lfps_slash_capacity",
+           "lfps_decode_step_host_out", "lfps_exact_topk_step", "lfps_overlap", "lfps_decode_launches", "lfps_slash_capacity",
            "lfps_exact_launches", "lfps_profile_enable", "lfps_profile_collect")
 
 
@@ -99,6 +99,9 @@ def _declare(lib):
                                          C.c_void_p]
     lib.lfps_decode_step.argtypes = [P(Dims), P(Params), P(State), P(Workspace), C.c_void_p,
                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.lfps_decode_step_host_out.argtypes = [P(Dims), P(Params), P(State), P(Workspace),
+                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.c_void_p, C.c_void_p]
     lib.lfps_exact_topk_step.argtypes = [P(Dims), P(Params), P(State), P(Workspace), C.c_void_p,
                                          C.c_void_p, C.c_void_p]
     lib.lfps_overlap.argtypes = [P(Dims), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -107,7 +110,8 @@ def _declare(lib):
     lib.lfps_decode_launches.argtypes = [C.c_void_p, C.c_int32]
     lib.lfps_profile_collect.argtypes = [P(KernelTime), C.c_int32, P(C.c_int32)]
     for name in ("lfps_profile_enable", "lfps_profile_collect", "lfps_workspace_layout",
-                 "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step", "lfps_exact_topk_step", "lfps_overlap",
+                 "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step",
+                 "lfps_decode_step_host_out", "lfps_exact_topk_step", "lfps_overlap",
                  "lfps_decode_launches", "lfps_exact_launches", "lfps_slash_capacity"):
         getattr(lib, name).restype = C.c_int
 

@@ -265,6 +265,8 @@ struct Pipe {
   cudaStream_t st[kSplitGroups] = {};
   cudaStream_t aux[kSplitGroups] = {};      // the stats kernel, concurrent with the gate
   cudaEvent_t fork = nullptr, join[kSplitGroups] = {}, stats[kSplitGroups] = {};
+  cudaStream_t copy = nullptr;              // host output copy beside the commit
+  cudaEvent_t out_ready = nullptr, out_done = nullptr;
 };
 std::mutex g_pipe_mu;
 Pipe g_pipe[16];
@@ -284,6 +286,9 @@ cudaError_t get_pipe(Pipe** out) {
       if ((e = cudaEventCreateWithFlags(&p.stats[i], cudaEventDisableTiming)) != cudaSuccess) return e;
     }
     if ((e = cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&p.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&p.out_ready, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&p.out_done, cudaEventDisableTiming)) != cudaSuccess) return e;
     p.dev = dev;
   }
   *out = &p;
@@ -382,9 +387,27 @@ int lfps_bootstrap_stats(const lfps_dims* dims, const lfps_params* p, const lfps
   return LFPS_OK;
 }
 
+static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
+                       const lfps_workspace* ws, const void* q, const void* k_new,
+                       const void* v_new, const int32_t* n_host, void* out_host, void* stream);
+
 int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
                      const lfps_workspace* ws, const void* q, const void* k_new,
                      const void* v_new, const int32_t* n_host, void* stream) {
+  return decode_impl(dims, p, st, ws, q, k_new, v_new, n_host, nullptr, stream);
+}
+
+int lfps_decode_step_host_out(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
+                              const lfps_workspace* ws, const void* q, const void* k_new,
+                              const void* v_new, const int32_t* n_host, void* out_host,
+                              void* stream) {
+  if (!out_host) return fail(LFPS_E_INVALID, "out_host is NULL");
+  return decode_impl(dims, p, st, ws, q, k_new, v_new, n_host, out_host, stream);
+}
+
+static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
+                       const lfps_workspace* ws, const void* q, const void* k_new,
+                       const void* v_new, const int32_t* n_host, void* out_host, void* stream) {
   lfps::Ctx c;
   int rc = make_ctx(dims, p, st, ws, &c);
   if (rc) return rc;
@@ -443,8 +466,18 @@ int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_sta
       LAUNCH(cudaStreamWaitEvent(sm, pp->join[g], 0));
     }
   }
+  // the output is final here (gate + finish); the commit does not touch it
+  if (out_host) {
+    if (!pp) LAUNCH(get_pipe(&pp));
+    LAUNCH(cudaEventRecord(pp->out_ready, sm));
+    LAUNCH(cudaStreamWaitEvent(pp->copy, pp->out_ready, 0));
+    LAUNCH(cudaMemcpyAsync(out_host, c.out, (size_t)c.NS * c.d * sizeof(float),
+                           cudaMemcpyDeviceToHost, pp->copy));
+    LAUNCH(cudaEventRecord(pp->out_done, pp->copy));
+  }
   LAUNCH_P("update", sm, lfps::launch_update(c, static_cast<const __nv_bfloat16*>(k_new),
                                               static_cast<const __nv_bfloat16*>(v_new), sm));
+  if (out_host) LAUNCH(cudaStreamWaitEvent(sm, pp->out_done, 0));
   return LFPS_OK;
 }
 

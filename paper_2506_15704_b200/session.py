@@ -243,12 +243,16 @@ class BatchedSession:
 
     # -- decode ---------------------------------------------------------------
     def decode_step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,
-                    k_fraction: float, check: bool = False) -> BatchedStepResult:
+                    k_fraction: float, check: bool = False,
+                    out_host: torch.Tensor | None = None) -> BatchedStepResult:
         """One LFPS decode step for all sessions (engine.py:97-201).
 
         q bf16 [B, Hq, d]; k_new, v_new bf16 [B, Hkv, d] (device).  On a
         data error no state is committed; ``check=True`` synchronises and
-        raises it."""
+        raises it.  ``out_host`` (f32 [B, Hq, d], pinned host memory) receives
+        the step's output as soon as it is final, copied beside the commit
+        kernel (lfps_decode_step_host_out); it is filled once the current
+        stream passes this call."""
         if not 0.0 < k_fraction <= 1.0:
             raise ValueError(f"k_fraction must be in (0, 1], got {k_fraction}")
         if self.tables_stale:
@@ -261,10 +265,21 @@ class BatchedSession:
             if t.dtype != torch.bfloat16 or t.device != self.device or not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous bf16 tensor on {self.device}")
         n_host = (C.c_int32 * self.B)(*self.n_host)
-        _lib.check(self.lib.lfps_decode_step(
-            C.byref(self.dims), C.byref(self._params(k_fraction)), C.byref(self.state),
-            C.byref(self.ws), C.c_void_p(q.data_ptr()), C.c_void_p(k_new.data_ptr()),
-            C.c_void_p(v_new.data_ptr()), n_host, self._stream()), "decode_step")
+        if out_host is None:
+            _lib.check(self.lib.lfps_decode_step(
+                C.byref(self.dims), C.byref(self._params(k_fraction)), C.byref(self.state),
+                C.byref(self.ws), C.c_void_p(q.data_ptr()), C.c_void_p(k_new.data_ptr()),
+                C.c_void_p(v_new.data_ptr()), n_host, self._stream()), "decode_step")
+        else:
+            if (tuple(out_host.shape) != tuple(self.out.shape) or out_host.dtype != torch.float32
+                    or out_host.device.type != "cpu" or not out_host.is_contiguous()):
+                raise ValueError(f"out_host must be a contiguous f32 CPU tensor of shape "
+                                 f"{tuple(self.out.shape)}")
+            _lib.check(self.lib.lfps_decode_step_host_out(
+                C.byref(self.dims), C.byref(self._params(k_fraction)), C.byref(self.state),
+                C.byref(self.ws), C.c_void_p(q.data_ptr()), C.c_void_p(k_new.data_ptr()),
+                C.c_void_p(v_new.data_ptr()), n_host, C.c_void_p(out_host.data_ptr()),
+                self._stream()), "decode_step")
         if check:
             torch.cuda.current_stream(self.device).synchronize()
             self.check_errors("decode_step")

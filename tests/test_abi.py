@@ -23,7 +23,8 @@ def test_header_declares_the_boundary():
     names = declared_functions()
     for want in ("lfps_abi_version", "lfps_last_error", "lfps_workspace_layout",
                  "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step",
-                 "lfps_exact_topk_step", "lfps_overlap", "lfps_profile_enable",
+                 "lfps_decode_step_host_out", "lfps_exact_topk_step", "lfps_overlap",
+                 "lfps_profile_enable",
                  "lfps_profile_collect", "lfps_decode_launches", "lfps_exact_launches",
                  "lfps_slash_capacity"):
         assert want in names

@@ -262,3 +262,29 @@ def test_failed_step_commits_nothing_then_recovers():
     pair.compare_step(res, outs)
     res, outs = pair.step(Q[:, :, :, 2], K[:, :, n0 + 2], V[:, :, n0 + 2], 0.05)
     pair.compare_step(res, outs)
+
+
+def test_decode_step_host_output():
+    """lfps_decode_step_host_out: the output lands in pinned host memory
+    (copied beside the commit kernel) bit-identical to the device output,
+    and the step is otherwise the same step (oracle parity)."""
+    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, n0=900, steps=2, seed=31)
+    import gpu_drive
+    sess = pair.sess
+    n0 = pair.n0
+    res, outs = pair.step(Q[:, :, :, 0], K[:, :, n0], V[:, :, n0], 0.05)
+    pair.compare_step(res, outs)
+    host = torch.empty(tuple(sess.out.shape), dtype=torch.float32).pin_memory()
+    host.fill_(float("nan"))
+    B, Hkv, G, d = pair.B, pair.Hkv, pair.G, pair.d
+    res = sess.decode_step(gpu_drive.bf16(Q[:, :, :, 1].reshape(B, Hkv * G, d)).cuda(),
+                           gpu_drive.bf16(K[:, :, n0 + 1]).cuda(),
+                           gpu_drive.bf16(V[:, :, n0 + 1]).cuda(), 0.05, out_host=host)
+    torch.cuda.current_stream().synchronize()
+    sess.check_errors("host-output step")
+    assert torch.equal(host, sess.out.cpu())
+    with pytest.raises(ValueError):
+        sess.decode_step(gpu_drive.bf16(Q[:, :, :, 1].reshape(B, Hkv * G, d)).cuda(),
+                         gpu_drive.bf16(K[:, :, n0 + 1]).cuda(),
+                         gpu_drive.bf16(V[:, :, n0 + 1]).cuda(), 0.05,
+                         out_host=torch.empty(3, dtype=torch.float32))
