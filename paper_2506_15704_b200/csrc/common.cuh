@@ -108,6 +108,25 @@ __device__ __forceinline__ double* ver_row(const Ctx& c, int s) { return c.ver +
 __device__ __forceinline__ double* sla_row(const Ctx& c, int s) { return c.sla + (size_t)s * c.sla_cap; }
 
 // ---- host-side launch wrappers (defined in the k_*.cu files) -------------
+// Launch with programmatic stream serialization (PDL): the kernel may be
+// scheduled while its predecessor in the stream drains; it calls pdl_wait()
+// before reading anything the predecessor wrote.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 cudaError_t launch_gate(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
 cudaError_t launch_stats(const Ctx& c, cudaStream_t st);
 cudaError_t launch_select(const Ctx& c, int m_max, cudaStream_t st);

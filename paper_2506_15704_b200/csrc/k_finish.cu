@@ -42,7 +42,9 @@ template <int PQ>
 __global__ void __launch_bounds__(kThreads, kRowCtas) lfps_finish_kernel(Ctx c, const __nv_bfloat16* q) {
   extern __shared__ __align__(128) uint8_t stages[];      // kStages x [K tile | V tile]
   __shared__ FinishShared sh;
+  pdl_wait();                                             // the select kernel's lists
   finish_session<PQ>(c, q, c.s_off + blockIdx.x, stages, sh);
+  pdl_trigger();
 }
 
 template <int PQ>
@@ -58,8 +60,7 @@ cudaError_t launch_finish_d(const Ctx& c, const __nv_bfloat16* q, cudaStream_t s
     if (e != cudaSuccess) return e;
     set = true;
   }
-  lfps_finish_kernel<PQ><<<c.s_cnt, kThreads, smem, st>>>(c, q);
-  return cudaGetLastError();
+  return launch_pdl(lfps_finish_kernel<PQ>, dim3(c.s_cnt), dim3(kThreads), smem, st, c, q);
 }
 
 }  // namespace

@@ -35,6 +35,7 @@
 // positive).  Table bytes read per step: dirty + hot blocks, not 2 m.
 #include "common.cuh"
 #include "canon.cuh"
+#include "ptx.cuh"
 #include "tables.cuh"
 
 namespace lfps {
@@ -324,6 +325,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel
       }
     }
   }
+  pdl_trigger();
 }
 
 }  // namespace

@@ -18,6 +18,7 @@
 // (err[0] == this call's stamp): the whole step is atomic (engine.py:8-9).
 #include "common.cuh"
 #include "canon.cuh"
+#include "ptx.cuh"
 
 namespace lfps {
 
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
   __shared__ double red[16];
   const int s = blockIdx.x, tid = threadIdx.x;
   const int b = s / c.Hq, qh = s % c.Hq;
+  pdl_wait();                                 // the finish kernel's lists and scores
   // independent prologue loads, issued together
   const int failed = c.err[0] == c.epoch;
   const int n = c.n_ctx[b];
@@ -281,8 +283,7 @@ __global__ void lfps_clear_err_kernel(Ctx c) {
 
 cudaError_t launch_update(const Ctx& c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new,
                           cudaStream_t st) {
-  lfps_update_kernel<<<c.NS, kThreads, 0, st>>>(c, k_new, v_new);
-  return cudaGetLastError();
+  return launch_pdl(lfps_update_kernel, dim3(c.NS), dim3(kThreads), 0, st, c, k_new, v_new);
 }
 
 cudaError_t launch_clear_err(const Ctx& c, cudaStream_t st) {
