@@ -7,7 +7,9 @@
 // exact and the LFPS selections compare like for like).  The K stream is the
 // HBM-bound part of the exact path: each row is read ONCE for the G heads
 // (the GQA GEMV); 8 lanes own a row (lane l: canonical partials l and l + 8,
-// two chains in one packed FFMA2 per element), R rows in flight per group.
+// two chains in one packed FFMA2 per element; the bf16 widening is shared
+// by the G heads).  K rows stream through shared memory with cp.async, 4
+// tiles of 64 rows in flight per CTA, each group staging its own rows.
 // Scores land in probe_score[s][j - S] (implicit index list).
 #include "rows.cuh"
 
@@ -17,7 +19,9 @@ namespace {
 
 using namespace rows;
 
-constexpr int kR = 3;                       // rows in flight per 8-lane group
+constexpr int kR = 2;                       // rows per 8-lane group per tile
+// tiles in flight (cp.async stages): 64 KiB of K per CTA
+__host__ __device__ constexpr int score_stages(int pq) { return pq >= 16 ? 2 : 4; }
 
 template <int PQ>
 __device__ __forceinline__ Part<PQ> ldg_part(const __nv_bfloat16* row, int l8) {
@@ -70,21 +74,51 @@ __global__ void __launch_bounds__(kThreads, 2) lfps_exact_score_kernel(Ctx c, co
   const __nv_bfloat16* kb = krow(c, b, h, S);
   const int gs = l8 % G;                              // the head this lane divides and writes
   float* out = c.probe_score + (size_t)(s0 + gs) * c.list_cap;
-  for (int base = r0; base < r1; base += kStep) {     // uniform trip count: full-warp shuffles
-    Part<PQ> kr[kR];
-    int rr[kR];
+  // K rows stream through shared memory, kScoreStages tiles of kStep rows:
+  // each 8-lane group copies (cp.async) and reads only its own rows, so the
+  // warps run independently with warp barriers only
+  extern __shared__ __align__(128) uint8_t kst[];
+  constexpr int kScoreStages = score_stages(PQ);
+  constexpr int kRowB = PQ * 32;                      // bytes per K row
+  constexpr int kChunks = kRowB / 16;
+  constexpr int kStageB = kStep * kRowB;
+  const uint32_t sb = smem_u32(kst) + grp * kRowB;
+  const uint8_t* kb8 = reinterpret_cast<const uint8_t*>(kb) + l8 * 16;
+  const int ntiles = (r1 - r0 + kStep - 1) / kStep;
+  auto issue = [&](int tile) {
+    if (tile < ntiles) {
+      const uint32_t st = sb + (tile % kScoreStages) * kStageB + l8 * 16;
 #pragma unroll
-    for (int i = 0; i < kR; ++i) {
-      rr[i] = base + grp + kGroups8 * i;
-      kr[i] = ldg_part<PQ>(kb + (size_t)(rr[i] < r1 ? rr[i] : r0) * c.d, l8);
+      for (int i = 0; i < kR; ++i) {
+        const int row = r0 + tile * kStep + grp + kGroups8 * i;
+        if (row < r1) {
+#pragma unroll
+          for (int ch = 0; ch < kChunks; ch += 8) {
+            if (kChunks % 8 != 0 && ch + l8 >= kChunks) continue;
+            cp_async16_s(st + i * kGroups8 * kRowB + ch * 16, kb8 + (size_t)row * kRowB + ch * 16);
+          }
+        }
+      }
     }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int t = 0; t < kScoreStages - 1; ++t) issue(t);
+#pragma unroll 1
+  for (int tile = 0; tile < ntiles; ++tile) {         // uniform trip count: full-warp shuffles
+    cp_async_wait<kScoreStages - 2>();
+    __syncwarp();
+    issue(tile + kScoreStages - 1);
+    const uint32_t st = sb + (tile % kScoreStages) * kStageB;
 #pragma unroll
     for (int i = 0; i < kR; ++i) {
+      const int rr = r0 + tile * kStep + grp + kGroups8 * i;
+      const Part<PQ> kr = ld_part_s<PQ>(st + i * kGroups8 * kRowB, l8);
       float2 kp[PQ];
 #pragma unroll
       for (int t = 0; t < PQ / 2; ++t) {
-        kp[2 * t] = make_float2(bf_lo(kr[i].a[t]), bf_lo(kr[i].b[t]));
-        kp[2 * t + 1] = make_float2(bf_hi(kr[i].a[t]), bf_hi(kr[i].b[t]));
+        kp[2 * t] = make_float2(bf_lo(kr.a[t]), bf_lo(kr.b[t]));
+        kp[2 * t + 1] = make_float2(bf_hi(kr.a[t]), bf_hi(kr.b[t]));
       }
       float mine = 0.0f;
 #pragma unroll
@@ -98,9 +132,10 @@ __global__ void __launch_bounds__(kThreads, 2) lfps_exact_score_kernel(Ctx c, co
         if (g == gs) mine = v;
       }
       const float z = __fdiv_rn(mine, c.sqrt_d_f32);
-      if (rr[i] < r1 && l8 < G) out[rr[i]] = z;
+      if (rr < r1 && l8 < G) out[rr] = z;
     }
   }
+  cp_async_wait<0>();
 }
 
 template <int PQ>
@@ -112,13 +147,22 @@ cudaError_t launch_exact_d(const Ctx& c, const __nv_bfloat16* q, int m_max, cuda
   if (per_unit > cap) per_unit = cap;
   if (per_unit < 1) per_unit = 1;
   const dim3 grid(per_unit, units);
+  const size_t smem = (size_t)score_stages(PQ) * kGroups8 * kR * PQ * 32;
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kThreads, smem, st>>>(c, q);
+    return cudaSuccess;
+  };
+  cudaError_t e;
   switch (c.G) {
-    case 1: lfps_exact_score_kernel<PQ, 1><<<grid, kThreads, 0, st>>>(c, q); break;
-    case 2: lfps_exact_score_kernel<PQ, 2><<<grid, kThreads, 0, st>>>(c, q); break;
-    case 4: lfps_exact_score_kernel<PQ, 4><<<grid, kThreads, 0, st>>>(c, q); break;
-    case 8: lfps_exact_score_kernel<PQ, 8><<<grid, kThreads, 0, st>>>(c, q); break;
+    case 1: e = go(lfps_exact_score_kernel<PQ, 1>); break;
+    case 2: e = go(lfps_exact_score_kernel<PQ, 2>); break;
+    case 4: e = go(lfps_exact_score_kernel<PQ, 4>); break;
+    case 8: e = go(lfps_exact_score_kernel<PQ, 8>); break;
     default: return cudaErrorInvalidValue;
   }
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
