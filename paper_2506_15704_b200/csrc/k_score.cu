@@ -20,6 +20,9 @@ namespace {
 using namespace rows;
 
 constexpr int kR = 2;                       // rows per 8-lane group per tile
+#ifndef LFPS_SCORE_CTAS
+#define LFPS_SCORE_CTAS 2
+#endif
 // tiles in flight (cp.async stages): 64 KiB of K per CTA
 __host__ __device__ constexpr int score_stages(int pq) { return pq >= 16 ? 2 : 4; }
 
@@ -46,7 +49,7 @@ __device__ __forceinline__ Part<PQ> ldg_part(const __nv_bfloat16* row, int l8) {
 }
 
 template <int PQ, int G>
-__global__ void __launch_bounds__(kThreads, 2) lfps_exact_score_kernel(Ctx c, const __nv_bfloat16* q) {
+__global__ void __launch_bounds__(kThreads, LFPS_SCORE_CTAS) lfps_exact_score_kernel(Ctx c, const __nv_bfloat16* q) {
   const int u = blockIdx.y;
   const int b = u / c.Hkv, h = u % c.Hkv;
   const int n = c.n_ctx[b];
