@@ -95,9 +95,10 @@ def test_exhaustive_and_mean_only_modes():
         pair.compare_step(res, outs)
 
 
-def test_exact_path_matches_oracle_and_overlap():
+@pytest.mark.parametrize("d,group", [(128, 4), (64, 8), (256, 2), (32, 1)])
+def test_exact_path_matches_oracle_and_overlap(d, group):
     from oracle import lfps_oracle as lo
-    pair, K, V, Q = _gqa_pair(batch=1, kv_heads=2, n0=4000, steps=2)
+    pair, K, V, Q = _gqa_pair(batch=1, kv_heads=2, group=group, n0=4000, steps=2, d=d)
     sess = pair.sess
     frac = 0.05
     q = Q[:, :, :, 0]
