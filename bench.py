@@ -686,6 +686,8 @@ def run_c3(args, world, rank, local):
                              kv_cache=(sess[0].k_cache, sess[0].v_cache))
         s_l.copy_tracker_from(sess[0])
         sess.append(s_l)
+    for s_l in sess:
+        s_l.split = not args.no_split
     setup_s = time.time() - t_setup
 
     def token_step(t):
