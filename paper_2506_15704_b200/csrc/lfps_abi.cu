@@ -260,6 +260,10 @@ int next_epoch() {
 #define LFPS_SPLIT_GROUPS 2
 #endif
 constexpr int kSplitGroups = LFPS_SPLIT_GROUPS;   // session groups of LFPS_FLAG_SPLIT
+#ifndef LFPS_SPLIT_MIN
+#define LFPS_SPLIT_MIN 256
+#endif
+constexpr int kSplitMin = LFPS_SPLIT_MIN;         // sessions below which the split is off
 struct Pipe {
   int dev = -1;
   cudaStream_t st[kSplitGroups] = {};
@@ -314,7 +318,7 @@ int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out) {
 // LFPS_FLAG_SPLIT (and >= 256 sessions) gate/select/finish run per half
 int lfps_decode_launches(const lfps_dims* dims, int32_t flags) {
   if (dims && (flags & LFPS_FLAG_SPLIT) &&
-      (long long)dims->batch * dims->kv_heads * dims->group >= 256)
+      (long long)dims->batch * dims->kv_heads * dims->group >= kSplitMin)
     return 1 + 4 * kSplitGroups;
   return 5;   // gate | stats, select, finish, update
 }
@@ -435,7 +439,7 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
     LAUNCH(get_pipe(&pp));
     LAUNCH(cudaEventRecord(pp->fork, sm));
   }
-  const bool split = (c.flags & LFPS_FLAG_SPLIT) && !g_prof_on && c.NS >= 256;
+  const bool split = (c.flags & LFPS_FLAG_SPLIT) && !g_prof_on && c.NS >= kSplitMin;
   // LFPS_FLAG_UNIT_FINISH: GQA units of <= 4 q-heads (d 128 / 256) finish per
   // unit over the union of their probe rows (tensor-core softmax.V); measured
   // slower than the per-session kernel at C4 (2 CTAs/SM), so
