@@ -204,16 +204,18 @@ def test_long_trajectory_crosses_slash_blocks():
         pair.compare_step(res, outs, tables=(t % 10 == 0))
 
 
-@pytest.mark.parametrize("split", [True, False])
-def test_split_streams_bit_exact(split):
-    """256 sessions (8 requests x 8 KV heads x 4): LFPS_FLAG_SPLIT runs the two
-    session halves on two internal streams; results are identical."""
-    pair, K, V, Q = _gqa_pair(batch=8, kv_heads=8, group=4, d=64, n0=700, steps=2, seed=41)
+@pytest.mark.parametrize("split,steps", [(True, 2), (False, 2), (True, 24)])
+def test_split_streams_bit_exact(split, steps):
+    """256 sessions (8 requests x 8 KV heads x 4): LFPS_FLAG_SPLIT runs two
+    session groups on internal streams, each with its stats kernel beside its
+    gate, and PDL between the later kernels; results are identical to the
+    oracle over many steps (no cross-step or cross-stream races)."""
+    pair, K, V, Q = _gqa_pair(batch=8, kv_heads=8, group=4, d=64, n0=700, steps=steps, seed=41)
     pair.sess.split = split
     n0 = pair.n0
-    for t in range(2):
+    for t in range(steps):
         res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], 0.05)
-        pair.compare_step(res, outs, tables=(t == 1))
+        pair.compare_step(res, outs, tables=(t % 8 == 1 or t == steps - 1))
 
 
 def test_full_attention_matches_oracle():
