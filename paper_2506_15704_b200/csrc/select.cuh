@@ -16,10 +16,6 @@ using namespace tbl;
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-#ifndef LFPS_SELECT_FLAT
-#define LFPS_SELECT_FLAT 4096
-#endif
-constexpr int kFlat = LFPS_SELECT_FLAT;     // candidate slots flattened per chunk
 
 // exclusive scan over the 256 threads of the block; total in *total
 __device__ __forceinline__ int block_scan(int v, int* warp_sums, int* total) {
@@ -61,12 +57,12 @@ struct SelectShared {
 
 // dynamic shared memory of select_session for W = ceil(m / 32) C0 words:
 // C0 bitmap [W], active-word list [W] u16, active words [ceil(W / 32)],
-// then the flattening buffers (u16 [kFlat], int [256], u32 [256])
+// then the flattening buffers (u16 [256 * 32], int [256], u32 [256])
 __host__ __device__ constexpr size_t select_bitmap_bytes(int W) {
   return ((size_t)W * 4 + (size_t)(W + 1) / 2 * 4 + (size_t)(W + 31) / 32 * 4 + 15) / 16 * 16;
 }
 __host__ __device__ constexpr size_t select_smem(int m_max) {
-  return select_bitmap_bytes((m_max + 31) / 32) + kFlat * 2 + kThreads * 4 * 2;
+  return select_bitmap_bytes((m_max + 31) / 32) + kThreads * 32 * 2 + kThreads * 4 * 2;
 }
 
 // C + D of session s from the thresholds and C0 words of lfps_stats_kernel;
@@ -114,8 +110,8 @@ __device__ __forceinline__ void select_session(const Ctx& c, int s, uint32_t* sm
   const int AW = (W + 31) / 32;
   // candidate flattening buffers behind the bitmaps (16-B aligned)
   uint8_t* fb = reinterpret_cast<uint8_t*>(smem) + select_bitmap_bytes(W);
-  uint16_t* fbuf = reinterpret_cast<uint16_t*>(fb);          // [kFlat]
-  int* fword = reinterpret_cast<int*>(fb + kFlat * 2);            // [kThreads]
+  uint16_t* fbuf = reinterpret_cast<uint16_t*>(fb);          // [kThreads * 32]
+  int* fword = reinterpret_cast<int*>(fb + kThreads * 32 * 2);   // [kThreads]
   uint32_t* fc1 = reinterpret_cast<uint32_t*>(fword + kThreads); // [kThreads]
   const double* ver = ver_row(c, s);
   const double* sla = sla_row(c, s) + base;   // logical view
@@ -208,22 +204,16 @@ __device__ __forceinline__ void select_session(const Ctx& c, int s, uint32_t* sm
         // words (32 candidates each, all in one warp) costs no more round
         // trips than scattered sparse words.
         int K;
-        const int off = block_scan(__popc(cand), sh.wsum, &K);
+        int off = block_scan(__popc(cand), sh.wsum, &K);
+        for (uint32_t x = cand; x; x &= x - 1) fbuf[off++] = (uint16_t)((tid << 5) | (__ffs(x) - 1));
         fword[tid] = w;
         fc1[tid] = 0u;
-        // chunks of kFlat candidates (one chunk unless the round is dense)
-        for (int c0 = 0; c0 < K; c0 += kFlat) {
-          if (c0) __syncthreads();                    // the previous chunk is consumed
-          int o = off;
-          for (uint32_t x = cand; x; x &= x - 1, ++o)
-            if (o >= c0 && o < c0 + kFlat) fbuf[o - c0] = (uint16_t)((tid << 5) | (__ffs(x) - 1));
-          __syncthreads();
-          const int kc = min(K - c0, kFlat);
-        for (int g0 = tid; g0 < kc; g0 += 4 * kThreads) {
+        __syncthreads();
+        for (int g0 = tid; g0 < K; g0 += 4 * kThreads) {
           int e[4];
           long long xv[4], xs[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) e[q] = g0 + kThreads * q < kc ? fbuf[g0 + kThreads * q] : -1;
+          for (int q = 0; q < 4; ++q) e[q] = g0 + kThreads * q < K ? fbuf[g0 + kThreads * q] : -1;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             xv[q] = xs[q] = -1ll;
@@ -237,7 +227,6 @@ __device__ __forceinline__ void select_session(const Ctx& c, int s, uint32_t* sm
           for (int q = 0; q < 4; ++q)
             if (e[q] >= 0 && (xv[q] > tfv || xs[q] > tfs))
               atomicOr(&fc1[e[q] >> 5], 1u << (e[q] & 31));
-        }
         }
         __syncthreads();
         if (r == 0) trace_at(c, s, 6, tclk0);         // first round's F reads done

@@ -248,62 +248,55 @@ __device__ void maintain_table(const Ctx& c, int s, int t, const Window& w, doub
   // ---- B: thresholds (compute_thresholds), one quarter of the tree per warp ----------
   const Mom q = quarter_merge(c.bw.bsum + (size_t)(2 * s + t) * nb * 4, w, warp, lane);
   if (lane == 0) sh.part[warp] = q;
-  if (tid4 == 0) { sh.nhot = 0; sh.npair = 0; }
   worker_sync(bar);
-  // every warp finishes the tree itself (lane 0, identical arithmetic), so
-  // no second barrier is needed before C
-  double thr0 = 0.0;
-  int deg = 0;
-  if (lane == 0) {
+  if (tid4 == 0) {
     const Mom tot = merge(merge(sh.part[0], sh.part[1]), merge(sh.part[2], sh.part[3]));
     const double mean = cmul(tot.mu, sc);
-    deg = cmul(cmul(tot.m2, sc), sc) < 1e-12;
+    const bool deg = cmul(cmul(tot.m2, sc), sc) < 1e-12;
     double tau = NAN, kappa = NAN;
     if (!deg) {
       kappa = cdiv(tot.m4, cmul(tot.m2, tot.m2));
       tau = cdiv(cmul(c.a, mean), kappa);
     }
-    thr0 = deg ? NAN : cdiv(tau, sc);
-    if (warp == 0) {
-      double* thr = c.thr_next + (size_t)(2 * s + t) * 4;
-      thr[0] = tau; thr[1] = mean; thr[2] = deg ? 1.0 : 0.0; thr[3] = kappa;
-      if (t == 0 && (c.flags & LFPS_FLAG_TRACE)) c.trace[(size_t)s * 16 + 2] = now_clk() - tclk0;
-    }
+    double* thr = c.thr_next + (size_t)(2 * s + t) * 4;
+    thr[0] = tau; thr[1] = mean; thr[2] = deg ? 1.0 : 0.0; thr[3] = kappa;
+    sh.deg = deg ? 1 : 0;
+    sh.thr0 = deg ? NAN : cdiv(tau, sc);
+    sh.nhot = 0;
+    sh.npair = 0;
+    if (t == 0 && (c.flags & LFPS_FLAG_TRACE)) c.trace[(size_t)s * 16 + 2] = now_clk() - tclk0;
   }
-  thr0 = __shfl_sync(LFPS_FULL, thr0, 0);
-  deg = __shfl_sync(LFPS_FULL, deg, 0);
+  worker_sync(bar);
 
   // ---- C: this table's part of C0 (select_initial): only blocks whose max is
-  // above tau / scale can hold members (the dirty ones were just read by A).
-  // A warp reduces the hot blocks whose maxima its own lanes hold. ----
+  // above tau / scale can hold members (the dirty ones were just read by A) ----
   int2* hot = hot_list(c, s, t);
-  if (!deg) {
-    const long long tb = thr_bits(thr0);
+  if (!sh.deg) {
+    const long long tb = thr_bits(sh.thr0);
 #pragma unroll
     for (int k = 0; k < kLeaves / 128; ++k) {
       const int i = tid4 + 128 * k;
-      uint32_t hb = __ballot_sync(LFPS_FULL, i < w.nseg && bmx[k] > tb);
-      if (lane == 0 && hb) atomicAdd(&sh.nhot, __popc(hb));
-      while (hb) {
-        const int blk = w.first + 128 * k + 32 * warp + __ffs(hb) - 1;
-        hb &= hb - 1;
-        int a, vc;
-        segment(w, blk, a, vc);
-        double v[16];
-        load_seg(row, a, vc, lane, v);
-        const int L0 = a - w.lo;                       // logical index of element 0
-        uint32_t mine = 0;                             // lane e keeps ballot word e
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const uint32_t wd = __ballot_sync(LFPS_FULL, e * 32 + lane < vc &&
-                                                           __double_as_longlong(v[e]) > tb);
-          if (lane == e) mine = wd;
-        }
-        if (lane < 16 && mine) hot[1 + atomicAdd(&sh.npair, 1)] = make_int2(L0 + lane * 32, (int)mine);
-      }
+      if (i < w.nseg && bmx[k] > tb) sh.hot[atomicAdd(&sh.nhot, 1)] = w.first + i;
     }
+    worker_sync(bar);
+    for (int k = warp; k < sh.nhot; k += 4) {
+      const int blk = sh.hot[k];
+      int a, vc;
+      segment(w, blk, a, vc);
+      double v[16];
+      load_seg(row, a, vc, lane, v);
+      const int L0 = a - w.lo;                         // logical index of element 0
+      uint32_t mine = 0;                               // lane e keeps ballot word e
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const uint32_t wd = __ballot_sync(LFPS_FULL, e * 32 + lane < vc &&
+                                                         __double_as_longlong(v[e]) > tb);
+        if (lane == e) mine = wd;
+      }
+      if (lane < 16 && mine) hot[1 + atomicAdd(&sh.npair, 1)] = make_int2(L0 + lane * 32, (int)mine);
+    }
+    worker_sync(bar);
   }
-  worker_sync(bar);
   if (tid4 == 0) {
     hot[0] = make_int2(sh.npair, sh.ntask + sh.nhot);
     if (t == 0 && (c.flags & LFPS_FLAG_TRACE)) c.trace[(size_t)s * 16 + 7] = now_clk() - tclk0;
