@@ -8,6 +8,7 @@
 // cache and the fp64 prior buffers.
 #include "common.cuh"
 #include "canon.cuh"
+#include "ptx.cuh"
 
 namespace lfps {
 
@@ -42,6 +43,7 @@ __global__ void __launch_bounds__(kGateWarps * 32) lfps_gate_kernel(Ctx c, const
   __shared__ double gsh;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int s = c.s_off + blockIdx.x;
+  pdl_wait();                                  // the previous step's commit (n_ctx, K rows)
   if (s >= c.NS) return;
   const int b = s / c.Hq, qh = s % c.Hq, h = qh / c.G;
   const int n = c.n_ctx[b];
@@ -154,8 +156,7 @@ __global__ void __launch_bounds__(kGateWarps * 32) lfps_gate_kernel(Ctx c, const
 }  // namespace
 
 cudaError_t launch_gate(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
-  lfps_gate_kernel<<<c.s_cnt, kGateWarps * 32, 0, st>>>(c, q);
-  return cudaGetLastError();
+  return launch_pdl(lfps_gate_kernel, dim3(c.s_cnt), dim3(kGateWarps * 32), 0, st, c, q);
 }
 
 }  // namespace lfps

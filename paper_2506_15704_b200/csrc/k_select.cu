@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kStatsThreads, LFPS_STATS_CTAS) lfps_stats_ker
 __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel(Ctx c) {
   extern __shared__ __align__(16) uint32_t smem[];
   __shared__ SelectShared sh;
+  pdl_wait();                                  // the gate's bypass decisions
   select_session(c, c.s_off + blockIdx.x, smem, sh);
   pdl_trigger();
 }
@@ -109,8 +110,7 @@ cudaError_t launch_select(const Ctx& c, int m_max, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     set = true;
   }
-  lfps_select_kernel<<<c.s_cnt, kThreads, smem, st>>>(c);
-  return cudaGetLastError();
+  return launch_pdl(lfps_select_kernel, dim3(c.s_cnt), dim3(kThreads), smem, st, c);
 }
 
 }  // namespace lfps

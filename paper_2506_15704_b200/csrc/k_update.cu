@@ -272,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
       if (e0 != c.epoch && e0 != -c.epoch) c.err[0] = 0;
     }
   }
+  pdl_trigger();
 }
 
 __global__ void lfps_clear_err_kernel(Ctx c) {
