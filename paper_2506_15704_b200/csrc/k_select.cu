@@ -1,8 +1,10 @@
 // k_select.cu -- thresholds and candidate construction (K1 + K2) from
 // PERSISTENT block summaries, as two kernels:
 //
-//   lfps_stats_kernel   one 128-thread CTA per (session, table): A + B
-//   lfps_select_kernel  one 256-thread CTA per session: C + D
+//   lfps_stats_kernel   one 128-thread CTA per (session, table): A + B + C
+//                       (tables.cuh maintain_table); runs beside the gate
+//   lfps_select_kernel  one 256-thread CTA per session: C0 assembly + D
+//                       (select.cuh select_session)
 //
 // Restates compute_thresholds (tables.py:295-317, _phys_moments :127-140),
 // select_initial (candidates.py:45-58), expand (:61-82) and
@@ -20,16 +22,18 @@
 //   A  rebuilds the dirty blocks (every block when the session's summaries
 //      are not valid: first step, after a renormalisation);
 //   B  merges the window's segment moments in the canonical pairwise tree
-//      (devmath.table_moments) -> tau, mean, degenerate, kappa in thr[];
+//      (devmath.table_moments) -> tau, mean, degenerate, kappa in thr_next[];
 //      exactly the same arithmetic as rebuilding every block;
-//   C  C0 = {slots with phys > tau / scale}: only "hot" blocks (max above
-//      the threshold) can hold members, and only those are read;
+//   C  the table's part of C0 = {slots with phys > tau / scale}: only "hot"
+//      blocks (max above the threshold) can hold members, and only those are
+//      read; their C0 words are listed in ws.hot, and the select kernel ORs
+//      both tables' words into its bitmap;
 //   D  C1 = F & dilate(C0, offsets), F read at dilated slots only;
 //      probe = C1 | local tail, compacted into a sorted absolute index list.
 //
-// A + B are fp64 latency chains per table: running them per (session, table)
-// in 128-thread CTAs (8 per SM) doubles the sessions in flight over one
-// 256-thread CTA per session doing both tables.
+// A, B and C are fp64 latency chains per table: running them per (session,
+// table) in 128-thread CTAs (8 per SM) doubles the sessions in flight over
+// one 256-thread CTA per session doing both tables.
 //
 // All comparisons are exact fp64 (on bit patterns: phys values are +0 or
 // positive).  Table bytes read per step: dirty + hot blocks, not 2 m.
