@@ -9,8 +9,9 @@
 // canonicalised to +0.0 (canon.cuh score_key).  One 512-thread CTA per
 // session; the m scores (512 KiB at 128k) are streamed twice:
 //
-//   0  a strided sample of 4096 keys is sorted in shared memory; the sample
-//      ranks around k m / 4096 (+- 4 sqrt(rank) + 16) bound a key window
+//   0  a strided sample of 4096 keys; its order statistics at ranks around
+//      k m / 4096 (+- 4 sqrt(rank) + 16), found by two radix selects in
+//      shared memory (not a full sort), bound a key window
 //      [lo, hi] that holds the k-th largest key with overwhelming probability;
 //   1  one pass counts the keys above hi per warp chunk and collects the
 //      window's (key, index) pairs in shared memory;
@@ -37,7 +38,7 @@ constexpr int kShift = 21;
 constexpr int kCand = 6144;                 // window candidates kept in shared memory
 
 struct TopkShared {
-  unsigned samp[kSample];                   // sample keys, sorted descending (also histogram)
+  unsigned samp[kSample];                   // fallback histogram (kBins <= kSample)
   uint2 cand[kCand];                        // (key, index)
   int wsum[kWarps];
   int above[kWarps];                        // keys above the window, per warp chunk
@@ -133,27 +134,18 @@ __global__ void __launch_bounds__(kThreads) lfps_exact_topk_kernel(Ctx c) {
   uint32_t lo = 0, hi = 0xffffffffu;
   bool use_window = p > 4 * kSample;
   if (use_window) {
+    // the two sample order statistics by radix select (the sample is staged
+    // as (key, i) in the candidate buffer, idle until pass 1)
     for (int i = tid; i < kSample; i += kThreads)
-      sh.samp[i] = key_at(z, (int)(((long long)i * p) / kSample));
+      sh.cand[i] = make_uint2(key_at(z, (int)(((long long)i * p) / kSample)), (uint32_t)i);
     __syncthreads();
-    // bitonic sort, descending
-    for (int size = 2; size <= kSample; size <<= 1) {
-      for (int stride = size >> 1; stride > 0; stride >>= 1) {
-        for (int i = tid; i < kSample / 2; i += kThreads) {
-          const int a = 2 * i - (i & (stride - 1));
-          const int bb = a + stride;
-          const bool desc = ((a & size) == 0);
-          const unsigned x = sh.samp[a], y = sh.samp[bb];
-          if ((x < y) == desc) { sh.samp[a] = y; sh.samp[bb] = x; }
-        }
-        __syncthreads();
-      }
-    }
     const int r = (int)(((long long)k * kSample) / p);
     const int delta = 4 * (int)sqrtf((float)r + 1.0f) + 16;
     const int rh = r - delta, rl = r + delta;
-    hi = rh <= 0 ? 0xffffffffu : sh.samp[rh];
-    lo = rl >= kSample ? 0u : sh.samp[rl];
+    int dummy;
+    // (sorted descending, sample entry q would be the (q + 1)-th largest key)
+    hi = rh <= 0 ? 0xffffffffu : radix_select(sh, sh.cand, kSample, 0u, 0u, 24, rh + 1, &dummy);
+    lo = rl >= kSample ? 0u : radix_select(sh, sh.cand, kSample, 0u, 0u, 24, rl + 1, &dummy);
     if (tid == 0) { sh.ncand = 0; sh.over = 0; }
     __syncthreads();
   }
