@@ -279,12 +279,18 @@ __global__ void __launch_bounds__(kThreads) lfps_exact_topk_kernel(Ctx c) {
     out_at += sh.above[w] + sh.gtc[w] + max(0, min(eq, need_eq - eq_at));
     eq_at += eq;
   }
+  // the next chunk's float4 is loaded while this one is emitted
+  float4 nxt = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (vec_ok && j0 + 4 * lane + 3 < j1) nxt = __ldg(reinterpret_cast<const float4*>(z + j0 + 4 * lane));
   for (int base = j0; base < j1; base += 128) {
     // lane owns 4 consecutive keys: j = base + 4 lane + e
     uint32_t keys[4];
     int ntake = 0, neq = 0;
+    const float4 cur = nxt;
+    if (vec_ok && base + 128 + 4 * lane + 3 < j1)
+      nxt = __ldg(reinterpret_cast<const float4*>(z + base + 128 + 4 * lane));
     if (vec_ok && base + 4 * lane + 3 < j1) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(z + base + 4 * lane));
+      const float4 v = cur;
       keys[0] = score_key(v.x); keys[1] = score_key(v.y);
       keys[2] = score_key(v.z); keys[3] = score_key(v.w);
     } else {
