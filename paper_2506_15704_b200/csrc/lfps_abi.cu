@@ -124,6 +124,10 @@ int layout(const lfps_dims* d, lfps_ws_layout* L) {
   return LFPS_OK;
 }
 
+// the error stamp of every call other than a decode step (bootstrap, exact
+// path); decode steps draw distinct stamps from next_epoch()
+constexpr int kOtherStamp = 0x7ffffff;
+
 int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
              const lfps_workspace* ws, lfps::Ctx* c) {
   int rc = check_dims(d);
@@ -137,7 +141,7 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
     return fail(LFPS_E_INVALID, "workspace too small: %zu < %zu bytes", ws->bytes, L.total_bytes);
   memset(c, 0, sizeof(*c));
   c->B = d->batch; c->Hkv = d->kv_heads; c->G = d->group; c->Hq = d->kv_heads * d->group;
-  c->NS = c->B * c->Hq; c->s_off = 0; c->s_cnt = c->NS; c->epoch = 1; c->d = d->d; c->n_max = d->n_max; c->m_cap = d->m_cap;
+  c->NS = c->B * c->Hq; c->s_off = 0; c->s_cnt = c->NS; c->epoch = kOtherStamp; c->d = d->d; c->n_max = d->n_max; c->m_cap = d->m_cap;
   c->sla_cap = slash_cap(d->m_cap); c->sla_home = slash_home(d->m_cap);
   c->words = L.words; c->list_cap = L.list_cap;
   c->r = p->r; c->eps = p->epsilon; c->a = p->a; c->frac = p->k_fraction; c->sqrt_d = p->sqrt_d;
@@ -253,7 +257,7 @@ cudaEvent_t prof_event() {
 std::atomic<int> g_epoch{1};
 int next_epoch() {
   int e = g_epoch.fetch_add(1) & 0x7ffffff;          // stamp << 4 fits an int32
-  return e ? e : next_epoch();
+  return (e && e != kOtherStamp) ? e : next_epoch();
 }
 
 #ifndef LFPS_SPLIT_GROUPS
