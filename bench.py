@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--no-split", action="store_true",
                     help="disable LFPS_FLAG_SPLIT (two session halves on two streams)")
     ap.add_argument("--unit-finish", action="store_true", help="LFPS_FLAG_UNIT_FINISH")
+    ap.add_argument("--pair-finish", action="store_true",
+                    help="LFPS_FLAG_PAIR_FINISH: two q-heads per finish CTA over their probe union")
     ap.add_argument("--gather", action="store_true",
                     help="N > 1: all-gather each e2e step's outputs and C2 counts to rank 0 (NCCL)")
     ap.add_argument("--profile-only", action="store_true",
@@ -424,6 +426,7 @@ def run_ours(args, world, rank, local):
     sess = BatchedSession(cfg, b_local, hkv, group, n_max=ctx + T + 8, device=dev)
     stream = populate(sess, spec)
     sess.split = not args.no_split
+    sess.pair_finish = args.pair_finish
     sess.unit_finish = args.unit_finish
     setup_s = time.time() - t_setup
     cuda_stream = torch.cuda.current_stream(dev)

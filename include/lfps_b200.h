@@ -94,6 +94,8 @@ typedef struct lfps_params {
 } lfps_params;
 
 /* lfps_params.flags */
+#define LFPS_FLAG_PAIR_FINISH 16 /* finish two q-heads of a unit per CTA over the union
+                                    of their probe rows (k_finish_pair.cu) */
 #define LFPS_FLAG_SPLIT 8        /* run two session halves' gate/select/finish on two
                                     internal streams (fork/join on the caller's) */
 #define LFPS_FLAG_UNIT_FINISH 4  /* finish GQA units (G <= 4, d 128/256) over the

@@ -23,6 +23,7 @@ FLAG_EXPORT_SETS = 1
 FLAG_TRACE = 2
 FLAG_UNIT_FINISH = 4
 FLAG_SPLIT = 8
+FLAG_PAIR_FINISH = 16
 
 # per-session device error codes (include/lfps_b200.h)
 ERR_NAMES = {

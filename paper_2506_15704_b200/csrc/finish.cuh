@@ -21,6 +21,77 @@ struct FinishShared {
   int sel_want;
 };
 
+// Merge the 32 group states of `at` into out[s], then the data checks (chk:
+// NaN once a score was not finite) and the C2 max for the update weights.
+// stages: scratch (>= 2 * 32 * d floats).
+template <int PQ>
+__device__ __forceinline__ void finish_tail(const Ctx& c, int s, uint8_t* stages, FinishShared& sh,
+                                            const Attn<PQ>& at, float chk, float mxc, long long t0) {
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5, l8 = tid & 7, grp = tid >> 3;
+  trace_at(c, s, 8, t0);
+  // ---- merge the 32 group states into the output (stages reused as scratch) ----------
+  {
+    constexpr int D = PQ * 16;
+    constexpr int kG = kThreads / D;                    // threads per output element
+    constexpr int kPer = kGroups8 / kG;                 // groups each of them merges
+    float* part = reinterpret_cast<float*>(stages);     // [kGroups8][D]
+#pragma unroll
+    for (int e = 0; e < PQ; ++e) {
+      part[grp * D + l8 * PQ + e] = at.acc[e].x;
+      part[grp * D + (l8 + 8) * PQ + e] = at.acc[e].y;
+    }
+    if (l8 == 0) { sh.part_m[grp] = at.m; sh.part_s[grp] = at.s; }
+    __syncthreads();
+    float M = -INFINITY;
+#pragma unroll 8
+    for (int x = 0; x < kGroups8; ++x) M = fmaxf(M, sh.part_m[x]);
+    const int t = tid % D, g = tid / D;
+    float num = 0.0f, den = 0.0f;
+#pragma unroll
+    for (int xi = 0; xi < kPer; ++xi) {
+      const int x = g * kPer + xi;
+      if (sh.part_m[x] == -INFINITY) continue;
+      const float f = ex2(sh.part_m[x] - M);
+      num = fmaf(f, part[x * D + t], num);
+      den = fmaf(f, sh.part_s[x], den);
+    }
+    __syncthreads();                                     // part is reused below
+    part[g * D + t] = num;
+    part[kG * D + g * D + t] = den;
+    __syncthreads();
+    if (tid < D) {
+      float nsum = 0.0f, dsum = 0.0f;
+#pragma unroll
+      for (int x = 0; x < kG; ++x) {
+        nsum += part[x * D + tid];
+        dsum += part[kG * D + x * D + tid];
+      }
+      c.out[(size_t)s * c.d + tid] = nsum / dsum;
+    }
+  }
+
+  trace_at(c, s, 9, t0);
+  // ---- data checks; the C2 max for the update weights (k_update.cu) ----------------
+  if (__syncthreads_or(!(chk == 0.0f))) {
+    if (tid == 0) set_err(c, s, LFPS_ERR_NONFINITE_SCORES);
+    return;
+  }
+  for (int o = 16; o >= 1; o >>= 1) mxc = fmaxf(mxc, __shfl_xor_sync(LFPS_FULL, mxc, o));
+  if (lane == 0) sh.gmax[warp] = mxc;
+  __syncthreads();
+  if (tid == 0) {
+    float mf = sh.gmax[0];
+#pragma unroll
+    for (int w = 1; w < kWarps; ++w) mf = fmaxf(mf, sh.gmax[w]);
+    c.bw.wstat[2 * (size_t)s] = (double)mf;
+    if (c.flags & LFPS_FLAG_TRACE) {
+      c.trace[(size_t)s * 16 + 10] = now_clk() - t0;
+      c.trace[(size_t)s * 16 + 14] = now_ns();
+    }
+  }
+}
+
 // The whole back half of one session's step, run by a 256-thread CTA.
 // `stages` is kStages x [K tile | V tile] of dynamic shared memory.
 template <int PQ>
@@ -182,67 +253,7 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
         });
   }
 
-  trace_at(c, s, 8, t0);
-  // ---- merge the 32 group states into the output (stages reused as scratch) ----------
-  {
-    constexpr int D = PQ * 16;
-    constexpr int kG = kThreads / D;                    // threads per output element
-    constexpr int kPer = kGroups8 / kG;                 // groups each of them merges
-    float* part = reinterpret_cast<float*>(stages);     // [kGroups8][D]
-#pragma unroll
-    for (int e = 0; e < PQ; ++e) {
-      part[grp * D + l8 * PQ + e] = at.acc[e].x;
-      part[grp * D + (l8 + 8) * PQ + e] = at.acc[e].y;
-    }
-    if (l8 == 0) { sh.part_m[grp] = at.m; sh.part_s[grp] = at.s; }
-    __syncthreads();
-    float M = -INFINITY;
-#pragma unroll 8
-    for (int x = 0; x < kGroups8; ++x) M = fmaxf(M, sh.part_m[x]);
-    const int t = tid % D, g = tid / D;
-    float num = 0.0f, den = 0.0f;
-#pragma unroll
-    for (int xi = 0; xi < kPer; ++xi) {
-      const int x = g * kPer + xi;
-      if (sh.part_m[x] == -INFINITY) continue;
-      const float f = ex2(sh.part_m[x] - M);
-      num = fmaf(f, part[x * D + t], num);
-      den = fmaf(f, sh.part_s[x], den);
-    }
-    __syncthreads();                                     // part is reused below
-    part[g * D + t] = num;
-    part[kG * D + g * D + t] = den;
-    __syncthreads();
-    if (tid < D) {
-      float nsum = 0.0f, dsum = 0.0f;
-#pragma unroll
-      for (int x = 0; x < kG; ++x) {
-        nsum += part[x * D + tid];
-        dsum += part[kG * D + x * D + tid];
-      }
-      c.out[(size_t)s * c.d + tid] = nsum / dsum;
-    }
-  }
-
-  trace_at(c, s, 9, t0);
-  // ---- data checks; the C2 max for the update weights (k_update.cu) ----------------
-  if (__syncthreads_or(!(chk == 0.0f))) {
-    if (tid == 0) set_err(c, s, LFPS_ERR_NONFINITE_SCORES);
-    return;
-  }
-  for (int o = 16; o >= 1; o >>= 1) mxc = fmaxf(mxc, __shfl_xor_sync(LFPS_FULL, mxc, o));
-  if (lane == 0) sh.gmax[warp] = mxc;
-  __syncthreads();
-  if (tid == 0) {
-    float mf = sh.gmax[0];
-#pragma unroll
-    for (int w = 1; w < kWarps; ++w) mf = fmaxf(mf, sh.gmax[w]);
-    c.bw.wstat[2 * (size_t)s] = (double)mf;
-    if (c.flags & LFPS_FLAG_TRACE) {
-      c.trace[(size_t)s * 16 + 10] = now_clk() - t0;
-      c.trace[(size_t)s * 16 + 14] = now_ns();
-    }
-  }
+  finish_tail<PQ>(c, s, stages, sh, at, chk, mxc, t0);
 }
 
 }  // namespace fin

@@ -467,8 +467,14 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
       LAUNCH(cudaStreamWaitEvent(gs, pp->stats[g], 0));
       LAUNCH(lfps::launch_select(cg, m_max, gs));
     }
-    if (per_unit) LAUNCH_P("finish", gs, lfps::launch_finish_unit(cg, qb, gs));
-    else LAUNCH_P("finish", gs, lfps::launch_finish(cg, qb, gs));
+    if (per_unit) {
+      LAUNCH_P("finish", gs, lfps::launch_finish_unit(cg, qb, gs));
+    } else if ((c.flags & LFPS_FLAG_PAIR_FINISH) && c.G % 2 == 0 && cg.s_off % 2 == 0 &&
+               cg.s_cnt % 2 == 0) {
+      LAUNCH_P("finish", gs, lfps::launch_finish_pair(cg, qb, gs));
+    } else {
+      LAUNCH_P("finish", gs, lfps::launch_finish(cg, qb, gs));
+    }
     if (split) {
       LAUNCH(cudaEventRecord(pp->join[g], gs));
       LAUNCH(cudaStreamWaitEvent(sm, pp->join[g], 0));

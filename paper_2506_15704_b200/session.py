@@ -33,7 +33,7 @@ CNT_C0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_BLOCKS = rang
 
 def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False,
                 trace: bool = False, unit_finish: bool = False,
-                split: bool = False) -> _lib.Params:
+                split: bool = False, pair_finish: bool = False) -> _lib.Params:
     err = cfg.device_limits_error()
     if err:
         raise ValueError(err)
@@ -50,7 +50,8 @@ def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False,
     for i, o in enumerate(offs):
         p.offsets[i] = o
     p.flags = ((_lib.FLAG_EXPORT_SETS if export_sets else 0) | (_lib.FLAG_TRACE if trace else 0)
-               | (_lib.FLAG_UNIT_FINISH if unit_finish else 0) | (_lib.FLAG_SPLIT if split else 0))
+               | (_lib.FLAG_UNIT_FINISH if unit_finish else 0) | (_lib.FLAG_SPLIT if split else 0)
+               | (_lib.FLAG_PAIR_FINISH if pair_finish else 0))
     return p
 
 
@@ -94,6 +95,7 @@ class BatchedSession:
         self.trace = False          # LFPS_FLAG_TRACE: per-session phase timestamps
         self.unit_finish = False    # LFPS_FLAG_UNIT_FINISH: per-unit finish kernel
         self.split = True           # LFPS_FLAG_SPLIT: two session halves on two streams
+        self.pair_finish = False    # LFPS_FLAG_PAIR_FINISH: two q-heads per finish CTA
         self.B, self.Hkv, self.G = batch, kv_heads, group
         self.Hq = kv_heads * group
         self.NS = batch * self.Hq
@@ -169,7 +171,7 @@ class BatchedSession:
 
     def _params(self, k_fraction: float = 1.0) -> _lib.Params:
         return make_params(self.cfg, k_fraction, self.export_sets, self.trace, self.unit_finish,
-                           self.split)
+                           self.split, self.pair_finish)
 
     # -- bootstrap ----------------------------------------------------------
     def load_prefill(self, b: int, keys: torch.Tensor, values: torch.Tensor):

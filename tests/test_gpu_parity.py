@@ -291,3 +291,16 @@ def test_decode_step_host_output():
                          gpu_drive.bf16(K[:, :, n0 + 1]).cuda(),
                          gpu_drive.bf16(V[:, :, n0 + 1]).cuda(), 0.05,
                          out_host=torch.empty(3, dtype=torch.float32))
+
+
+@pytest.mark.parametrize("frac,d", [(0.05, 128), (0.01, 128), (0.05, 64)])
+def test_pair_finish_bit_exact(frac, d):
+    """LFPS_FLAG_PAIR_FINISH: two q-heads of a unit per finish CTA over the
+    union of their probe rows -- identical to the oracle (and so to the
+    per-session kernel); at 1% (k < |probe|) it falls back per session."""
+    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, n0=3000, steps=3, d=d, seed=17)
+    pair.sess.pair_finish = True
+    n0 = pair.n0
+    for t in range(3):
+        res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], frac)
+        pair.compare_step(res, outs)
