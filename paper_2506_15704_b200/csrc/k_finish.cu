@@ -1,8 +1,8 @@
 // k_finish.cu -- the per-session back half of a decode step in ONE kernel:
 // candidate scoring (K3), Top-k (K4), sparse attention (K5) and the data
-// checks + update weights of the tracker update (K6; the update itself is
-// committed by k_update.cu once every session has passed).  One 256-thread
-// CTA per (request, q-head) session.
+// checks feeding the tracker update (K6; the weights are computed and the
+// update committed by k_update.cu once every session has passed).  One
+// 256-thread CTA per (request, q-head) session.
 //
 //   rows     K / V rows stream through shared memory in tiles of 64 rows
 //            (two per 8-lane group), 2 stages deep, gathered with cp.async
@@ -27,9 +27,10 @@
 //            packed fp32x2 FMAs), the 32 group states are merged at the end
 //            (fp32)
 //   checks   sinks and C2 scores finite (softmax_weights, numerics.py:61-62,
-//            called at engine.py:177 and :184); u = canonical fp64 softmax
-//            of the C2 scores (devmath.softmax_update) written to uw for the
-//            update, and |sum u - 1| <= 1e-6 (tables.py:161-163)
+//            called at engine.py:177 and :184); the C2 max goes to wstat,
+//            from which k_update.cu forms u = canonical fp64 softmax of the
+//            C2 scores (devmath.softmax_update) and checks |sum u - 1| <=
+//            1e-6 (tables.py:161-163)
 #include "finish.cuh"
 
 namespace lfps {
