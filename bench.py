@@ -498,8 +498,8 @@ def run_ours(args, world, rank, local):
     # ---- e2e through the public API with host buffers ----
     e2e = None
     if e2e_steps:
-        # each step's q | k_new | v_new packed in one pinned host buffer: one
-        # H2D copy per step into one device buffer the three inputs view
+        # each step's q | k_new | v_new packed in one pinned host buffer
+        # (BatchedSession.pack_step_inputs' layout): one H2D copy per step
         nq, nk = stream.q[0].numel(), stream.k_new[0].numel()
         packed = torch.cat([stream.q.reshape(T_in, -1), stream.k_new.reshape(T_in, -1),
                             stream.v_new.reshape(T_in, -1)], dim=1)
@@ -529,15 +529,20 @@ def run_ours(args, world, rank, local):
         base = args.warmup + args.steps + prof_steps
         e0.record(cuda_stream)
         for t in range(base, base + e2e_steps):
+            if not gather:
+                # lfps_decode_step_host_io: the library copies the packed
+                # inputs on its own stream beside the stats kernels and the
+                # output back beside the commit kernel
+                sess.decode_step_host(inh[t % T_in], frac, out_host=out_h)
+                continue
             ind.copy_(inh[t % T_in], non_blocking=True)
-            sess.decode_step(qd, kd, vd, frac, out_host=None if gather else out_h)
-            if gather:                  # else out_h was filled by decode_step itself
-                cnt_d.copy_(sess.counts)
-                dist.all_gather_into_tensor(g_out, sess.out)
-                dist.all_gather_into_tensor(g_cnt, cnt_d)
-                if rank == 0:
-                    out_h.copy_(g_out, non_blocking=True)
-                    cnt_h.copy_(g_cnt, non_blocking=True)
+            sess.decode_step(qd, kd, vd, frac)
+            cnt_d.copy_(sess.counts)
+            dist.all_gather_into_tensor(g_out, sess.out)
+            dist.all_gather_into_tensor(g_cnt, cnt_d)
+            if rank == 0:
+                out_h.copy_(g_out, non_blocking=True)
+                cnt_h.copy_(g_cnt, non_blocking=True)
         e1.record(cuda_stream)
         torch.cuda.synchronize(dev)
         e2e_ms = allmax(world, e0.elapsed_time(e1) / e2e_steps)
@@ -546,10 +551,11 @@ def run_ours(args, world, rank, local):
         e2e = {"value": e2e_ms * 1e3, "unit": UNIT,
                "h2d_bytes_per_step": int(ind.numel() * ind.element_size()),
                "d2h_bytes_per_step": int(d2h if rank == 0 or not gather else 0),
-               "api": "BatchedSession.decode_step (pinned host q/k/v in; the output copied to "
-                      "pinned host memory by the call, beside the commit kernel)"
-                      + ("; outputs and C2 counts all-gathered over NCCL, read back on rank 0"
-                         if gather else "")}
+               "api": ("BatchedSession.decode_step (pinned host q/k/v copied in; outputs and C2 "
+                       "counts all-gathered over NCCL, read back on rank 0)" if gather else
+                       "BatchedSession.decode_step_host = lfps_decode_step_host_io (pinned "
+                       "packed q|k_new|v_new in, copied by the call beside the stats kernels; "
+                       "the output copied to pinned host memory beside the commit kernel)")}
 
     # ---- recall vs the exact full-scan path, and its device time ----
     recall = None

@@ -48,7 +48,7 @@ extern "C" {
 #define LFPS_API
 #endif
 
-#define LFPS_ABI_VERSION 4
+#define LFPS_ABI_VERSION 5
 
 #define LFPS_OK 0
 #define LFPS_E_INVALID -1   /* bad argument (shape, range, capacity) */
@@ -225,6 +225,24 @@ LFPS_API int lfps_decode_step_host_out(const lfps_dims* dims, const lfps_params*
                      const lfps_state* st, const lfps_workspace* ws,
                      const void* q, const void* k_new, const void* v_new,
                      const int32_t* n_host, void* out_host, void* stream);
+
+/* The step with host inputs AND host output: in_host (host memory, pinned
+ * for an asynchronous copy) holds the step's inputs packed as bf16
+ * [q (B*Hq*d) | k_new (B*Hkv*d) | v_new (B*Hkv*d)]; they are copied to
+ * in_dev (a device buffer of lfps_step_input_bytes(dims)) on an internal
+ * stream that starts with the call, so the copy overlaps the step's table
+ * statistics (which do not read the inputs) and only the gate waits for it.
+ * in_dev must not be touched by other work until the caller's stream
+ * reaches the end of the call.  out_host as lfps_decode_step_host_out, or
+ * NULL for no output copy. */
+LFPS_API int lfps_decode_step_host_io(const lfps_dims* dims, const lfps_params* p,
+                     const lfps_state* st, const lfps_workspace* ws,
+                     const void* in_host, void* in_dev, const int32_t* n_host,
+                     void* out_host, void* stream);
+
+/* Bytes of the packed step input of lfps_decode_step_host_io (< 0: invalid
+ * dims). */
+LFPS_API int64_t lfps_step_input_bytes(const lfps_dims* dims);
 
 /* Exact full-scan Top-k comparison path (exact_topk_step, bench.py:73-80)
  * over the pre-append rows of every session: fp32 scores of all non-sink

@@ -18,7 +18,7 @@ from .errors import DeviceError
 # experiments); the default is the library __graft_entry__.build() makes
 LIB_PATH = os.environ.get("LFPS_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "lib", "liblfps_b200.so")
-ABI_VERSION = 4
+ABI_VERSION = 5
 FLAG_EXPORT_SETS = 1
 FLAG_TRACE = 2
 FLAG_UNIT_FINISH = 4
@@ -38,7 +38,8 @@ ERR_NAMES = {
 
 EXPORTS = ("lfps_abi_version", "lfps_last_error", "lfps_workspace_layout",
            "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step",
-           "lfps_decode_step_host_out", "lfps_exact_topk_step", "lfps_overlap", "lfps_decode_launches", "lfps_slash_capacity",
+           "lfps_decode_step_host_out", "lfps_decode_step_host_io", "lfps_step_input_bytes",
+           "lfps_exact_topk_step", "lfps_overlap", "lfps_decode_launches", "lfps_slash_capacity",
            "lfps_exact_launches", "lfps_profile_enable", "lfps_profile_collect")
 
 
@@ -103,6 +104,11 @@ def _declare(lib):
     lib.lfps_decode_step_host_out.argtypes = [P(Dims), P(Params), P(State), P(Workspace),
                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                               C.c_void_p, C.c_void_p]
+    lib.lfps_decode_step_host_io.argtypes = [P(Dims), P(Params), P(State), P(Workspace),
+                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.c_void_p]
+    lib.lfps_step_input_bytes.argtypes = [P(Dims)]
+    lib.lfps_step_input_bytes.restype = C.c_int64
     lib.lfps_exact_topk_step.argtypes = [P(Dims), P(Params), P(State), P(Workspace), C.c_void_p,
                                          C.c_void_p, C.c_void_p]
     lib.lfps_overlap.argtypes = [P(Dims), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -112,7 +118,8 @@ def _declare(lib):
     lib.lfps_profile_collect.argtypes = [P(KernelTime), C.c_int32, P(C.c_int32)]
     for name in ("lfps_profile_enable", "lfps_profile_collect", "lfps_workspace_layout",
                  "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step",
-                 "lfps_decode_step_host_out", "lfps_exact_topk_step", "lfps_overlap",
+                 "lfps_decode_step_host_out", "lfps_decode_step_host_io", "lfps_exact_topk_step",
+                 "lfps_overlap",
                  "lfps_decode_launches", "lfps_exact_launches", "lfps_slash_capacity"):
         getattr(lib, name).restype = C.c_int
 

@@ -275,6 +275,8 @@ struct Pipe {
   cudaEvent_t fork = nullptr, join[kSplitGroups] = {}, stats[kSplitGroups] = {};
   cudaStream_t copy = nullptr;              // host output copy beside the commit
   cudaEvent_t out_ready = nullptr, out_done = nullptr;
+  cudaStream_t in = nullptr;                // host input copy beside the stats kernel
+  cudaEvent_t in_ready = nullptr;
 };
 std::mutex g_pipe_mu;
 Pipe g_pipe[16];
@@ -297,6 +299,8 @@ cudaError_t get_pipe(Pipe** out) {
     if ((e = cudaStreamCreateWithFlags(&p.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&p.out_ready, cudaEventDisableTiming)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&p.out_done, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&p.in_ready, cudaEventDisableTiming)) != cudaSuccess) return e;
     p.dev = dev;
   }
   *out = &p;
@@ -397,12 +401,13 @@ int lfps_bootstrap_stats(const lfps_dims* dims, const lfps_params* p, const lfps
 
 static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
                        const lfps_workspace* ws, const void* q, const void* k_new,
-                       const void* v_new, const int32_t* n_host, void* out_host, void* stream);
+                       const void* v_new, const int32_t* n_host, void* out_host,
+                       const void* in_host, void* stream);
 
 int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
                      const lfps_workspace* ws, const void* q, const void* k_new,
                      const void* v_new, const int32_t* n_host, void* stream) {
-  return decode_impl(dims, p, st, ws, q, k_new, v_new, n_host, nullptr, stream);
+  return decode_impl(dims, p, st, ws, q, k_new, v_new, n_host, nullptr, nullptr, stream);
 }
 
 int lfps_decode_step_host_out(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
@@ -410,12 +415,32 @@ int lfps_decode_step_host_out(const lfps_dims* dims, const lfps_params* p, const
                               const void* v_new, const int32_t* n_host, void* out_host,
                               void* stream) {
   if (!out_host) return fail(LFPS_E_INVALID, "out_host is NULL");
-  return decode_impl(dims, p, st, ws, q, k_new, v_new, n_host, out_host, stream);
+  return decode_impl(dims, p, st, ws, q, k_new, v_new, n_host, out_host, nullptr, stream);
+}
+
+int64_t lfps_step_input_bytes(const lfps_dims* dims) {
+  if (check_dims(dims)) return LFPS_E_INVALID;
+  const int64_t units = (int64_t)dims->batch * dims->kv_heads;
+  return (units * dims->group + 2 * units) * dims->d * 2;
+}
+
+int lfps_decode_step_host_io(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
+                             const lfps_workspace* ws, const void* in_host, void* in_dev,
+                             const int32_t* n_host, void* out_host, void* stream) {
+  int rc = check_dims(dims);
+  if (rc) return rc;
+  if (!in_host || !in_dev) return fail(LFPS_E_INVALID, "in_host/in_dev is NULL");
+  const size_t units = (size_t)dims->batch * dims->kv_heads;
+  const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(in_dev);
+  const __nv_bfloat16* k_new = q + units * dims->group * dims->d;
+  const __nv_bfloat16* v_new = k_new + units * dims->d;
+  return decode_impl(dims, p, st, ws, q, k_new, v_new, n_host, out_host, in_host, stream);
 }
 
 static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
                        const lfps_workspace* ws, const void* q, const void* k_new,
-                       const void* v_new, const int32_t* n_host, void* out_host, void* stream) {
+                       const void* v_new, const int32_t* n_host, void* out_host,
+                       const void* in_host, void* stream) {
   lfps::Ctx c;
   int rc = make_ctx(dims, p, st, ws, &c);
   if (rc) return rc;
@@ -433,6 +458,13 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
   // their own streams; the update (commit) joins them on the caller's
   // stream.  Under lfps_profile_enable everything runs serially on the
   // caller's stream so each kernel is timed alone.
+  // host inputs (lfps_decode_step_host_io): q | k_new | v_new are contiguous
+  // from q on; the copy starts with the call on its own stream (after the
+  // caller's previous work, which may still read the buffer) and only the
+  // gate waits for it -- the stats kernel does not read the inputs
+  const size_t in_bytes = ((size_t)c.NS + 2 * (size_t)c.B * c.Hkv) * c.d * sizeof(__nv_bfloat16);
+  if (in_host && g_prof_on)
+    LAUNCH(cudaMemcpyAsync(const_cast<void*>(q), in_host, in_bytes, cudaMemcpyHostToDevice, sm));
   if (g_prof_on) {
     LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
     LAUNCH_P("stats", sm, lfps::launch_stats(c, sm));
@@ -442,6 +474,11 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
   if (!g_prof_on) {
     LAUNCH(get_pipe(&pp));
     LAUNCH(cudaEventRecord(pp->fork, sm));
+    if (in_host) {
+      LAUNCH(cudaStreamWaitEvent(pp->in, pp->fork, 0));
+      LAUNCH(cudaMemcpyAsync(const_cast<void*>(q), in_host, in_bytes, cudaMemcpyHostToDevice, pp->in));
+      LAUNCH(cudaEventRecord(pp->in_ready, pp->in));
+    }
   }
   const bool split = (c.flags & LFPS_FLAG_SPLIT) && !g_prof_on && c.NS >= kSplitMin;
   // LFPS_FLAG_UNIT_FINISH: GQA units of <= 4 q-heads (d 128 / 256) finish per
@@ -463,6 +500,7 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
       LAUNCH(cudaStreamWaitEvent(as, pp->fork, 0));
       LAUNCH(lfps::launch_stats(cg, as));
       LAUNCH(cudaEventRecord(pp->stats[g], as));
+      if (in_host) LAUNCH(cudaStreamWaitEvent(gs, pp->in_ready, 0));
       LAUNCH(lfps::launch_gate(cg, qb, gs));
       LAUNCH(cudaStreamWaitEvent(gs, pp->stats[g], 0));
       LAUNCH(lfps::launch_select(cg, m_max, gs));

@@ -141,6 +141,7 @@ class BatchedSession:
         self._views()
         self.step_count = 0
         self.tables_stale = False
+        self._in_dev = None        # decode_step_host's device staging buffer
 
     # -- workspace views ----------------------------------------------------
     def _region(self, off: int, dtype, shape):
@@ -282,6 +283,61 @@ class BatchedSession:
                 C.byref(self.ws), C.c_void_p(q.data_ptr()), C.c_void_p(k_new.data_ptr()),
                 C.c_void_p(v_new.data_ptr()), n_host, C.c_void_p(out_host.data_ptr()),
                 self._stream()), "decode_step")
+        if check:
+            torch.cuda.current_stream(self.device).synchronize()
+            self.check_errors("decode_step")
+        self.n_host = [n + 1 for n in self.n_host]
+        self.step_count += 1
+        return self.result()
+
+    def step_input_bytes(self) -> int:
+        """Bytes of one step's packed host input (lfps_step_input_bytes)."""
+        n = int(self.lib.lfps_step_input_bytes(C.byref(self.dims)))
+        if n < 0:
+            raise ValueError("invalid dims")
+        return n
+
+    def pack_step_inputs(self, q: torch.Tensor, k_new: torch.Tensor,
+                         v_new: torch.Tensor) -> torch.Tensor:
+        """Pinned host bf16 buffer [q | k_new | v_new] for decode_step_host."""
+        parts = [t.detach().to("cpu", torch.bfloat16).reshape(-1) for t in (q, k_new, v_new)]
+        packed = torch.cat(parts).pin_memory()
+        if packed.numel() * 2 != self.step_input_bytes():
+            raise ValueError("q / k_new / v_new do not have the session's shapes")
+        return packed
+
+    def decode_step_host(self, inputs_host: torch.Tensor, k_fraction: float,
+                         out_host: torch.Tensor | None = None,
+                         check: bool = False) -> BatchedStepResult:
+        """decode_step with host inputs (lfps_decode_step_host_io):
+        ``inputs_host`` is a contiguous CPU bf16 tensor packed as
+        [q | k_new | v_new] (``pack_step_inputs``; pinned for an asynchronous
+        copy).  The library copies it into the session's device staging
+        buffer on an internal stream that overlaps the step's table
+        statistics; ``out_host`` as in decode_step."""
+        if not 0.0 < k_fraction <= 1.0:
+            raise ValueError(f"k_fraction must be in (0, 1], got {k_fraction}")
+        if self.tables_stale:
+            raise ValueError("tables out of sync with the KV store (append_rows was used)")
+        nbytes = self.step_input_bytes()
+        if (inputs_host.device.type != "cpu" or inputs_host.dtype != torch.bfloat16
+                or not inputs_host.is_contiguous() or inputs_host.numel() * 2 != nbytes):
+            raise ValueError(f"inputs_host must be a contiguous bf16 CPU tensor of "
+                             f"{nbytes // 2} elements")
+        if out_host is not None and (
+                tuple(out_host.shape) != tuple(self.out.shape) or out_host.dtype != torch.float32
+                or out_host.device.type != "cpu" or not out_host.is_contiguous()):
+            raise ValueError(f"out_host must be a contiguous f32 CPU tensor of shape "
+                             f"{tuple(self.out.shape)}")
+        if self._in_dev is None:
+            self._in_dev = torch.empty(nbytes // 2, dtype=torch.bfloat16, device=self.device)
+        n_host = (C.c_int32 * self.B)(*self.n_host)
+        _lib.check(self.lib.lfps_decode_step_host_io(
+            C.byref(self.dims), C.byref(self._params(k_fraction)), C.byref(self.state),
+            C.byref(self.ws), C.c_void_p(inputs_host.data_ptr()),
+            C.c_void_p(self._in_dev.data_ptr()), n_host,
+            C.c_void_p(out_host.data_ptr() if out_host is not None else None),
+            self._stream()), "decode_step")
         if check:
             torch.cuda.current_stream(self.device).synchronize()
             self.check_errors("decode_step")

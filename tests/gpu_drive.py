@@ -24,6 +24,7 @@ class Pair:
         B, Hkv, _, d = keys.shape
         G = weights.shape[2]
         self.cfg, self.B, self.Hkv, self.G, self.d, self.n0 = cfg, B, Hkv, G, d, n0
+        self.host_io = False
         self.weights, self.finals = weights, finals
         self.sess = BatchedSession(cfg, B, Hkv, G, n_max=n_max or keys.shape[2] + 8,
                                    m_cap=m_cap, device="cuda", export_sets=True)
@@ -44,8 +45,15 @@ class Pair:
     def step(self, q, k_new, v_new, frac):
         """q [B, Hkv, G, d]; k_new/v_new [B, Hkv, d] (f32 bf16-valued)."""
         B, Hkv, G, d = self.B, self.Hkv, self.G, self.d
-        res = self.sess.decode_step(bf16(q.reshape(B, Hkv * G, d)).cuda(),
-                                    bf16(k_new).cuda(), bf16(v_new).cuda(), frac, check=True)
+        if self.host_io:          # lfps_decode_step_host_io: packed pinned inputs, host output
+            packed = self.sess.pack_step_inputs(bf16(q.reshape(B, Hkv * G, d)), bf16(k_new),
+                                                bf16(v_new))
+            host = torch.full(tuple(self.sess.out.shape), float("nan")).pin_memory()
+            res = self.sess.decode_step_host(packed, frac, out_host=host, check=True)
+            assert torch.equal(host, self.sess.out.cpu())
+        else:
+            res = self.sess.decode_step(bf16(q.reshape(B, Hkv * G, d)).cuda(),
+                                        bf16(k_new).cuda(), bf16(v_new).cuda(), frac, check=True)
         outs = []
         for b in range(B):
             for h in range(Hkv):

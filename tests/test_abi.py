@@ -23,7 +23,8 @@ def test_header_declares_the_boundary():
     names = declared_functions()
     for want in ("lfps_abi_version", "lfps_last_error", "lfps_workspace_layout",
                  "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step",
-                 "lfps_decode_step_host_out", "lfps_exact_topk_step", "lfps_overlap",
+                 "lfps_decode_step_host_out", "lfps_decode_step_host_io",
+                 "lfps_step_input_bytes", "lfps_exact_topk_step", "lfps_overlap",
                  "lfps_profile_enable",
                  "lfps_profile_collect", "lfps_decode_launches", "lfps_exact_launches",
                  "lfps_slash_capacity"):
@@ -39,6 +40,8 @@ def test_library_exports_every_declared_symbol():
     assert lib.lfps_decode_launches(None, 0) == 5 and lib.lfps_exact_launches() > 0
     big = _lib.Dims(64, 8, 4, 128, 4096, 4096)
     assert lib.lfps_decode_launches(C.byref(big), _lib.FLAG_SPLIT) == 9
+    assert lib.lfps_step_input_bytes(C.byref(big)) == (64 * 8 * 4 + 2 * 64 * 8) * 128 * 2
+    assert lib.lfps_step_input_bytes(C.byref(_lib.Dims(0, 8, 4, 128, 4096, 4096))) < 0
 
 
 def test_struct_layouts_match_header(tmp_path):

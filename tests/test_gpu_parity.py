@@ -204,14 +204,20 @@ def test_long_trajectory_crosses_slash_blocks():
         pair.compare_step(res, outs, tables=(t % 10 == 0))
 
 
-@pytest.mark.parametrize("split,steps", [(True, 2), (False, 2), (True, 24)])
-def test_split_streams_bit_exact(split, steps):
+@pytest.mark.parametrize("split,steps,host_io", [(True, 2, False), (False, 2, False),
+                                                 (True, 24, False), (True, 12, True),
+                                                 (False, 4, True)])
+def test_split_streams_bit_exact(split, steps, host_io):
     """256 sessions (8 requests x 8 KV heads x 4): LFPS_FLAG_SPLIT runs two
     session groups on internal streams, each with its stats kernel beside its
     gate, and PDL between the later kernels; results are identical to the
-    oracle over many steps (no cross-step or cross-stream races)."""
+    oracle over many steps (no cross-step or cross-stream races).  host_io:
+    every step through lfps_decode_step_host_io (the input copy on its own
+    stream beside the stats kernels, the output copied back to pinned host
+    memory, bit-identical to the device output)."""
     pair, K, V, Q = _gqa_pair(batch=8, kv_heads=8, group=4, d=64, n0=700, steps=steps, seed=41)
     pair.sess.split = split
+    pair.host_io = host_io
     n0 = pair.n0
     for t in range(steps):
         res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], 0.05)
@@ -291,6 +297,27 @@ def test_decode_step_host_output():
                          gpu_drive.bf16(K[:, :, n0 + 1]).cuda(),
                          gpu_drive.bf16(V[:, :, n0 + 1]).cuda(), 0.05,
                          out_host=torch.empty(3, dtype=torch.float32))
+
+
+def test_decode_step_host_io_small_and_rejects():
+    """lfps_decode_step_host_io on a small batch (oracle parity for several
+    steps, output bit-identical in host memory) and its argument checks."""
+    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, n0=900, steps=3, seed=37)
+    pair.host_io = True
+    n0 = pair.n0
+    for t in range(3):
+        res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], 0.05)
+        pair.compare_step(res, outs)
+    sess = pair.sess
+    nb = sess.step_input_bytes()
+    assert nb == (sess.B * sess.Hq + 2 * sess.B * sess.Hkv) * sess.d * 2
+    with pytest.raises(ValueError):       # wrong size
+        sess.decode_step_host(torch.zeros(nb // 2 - 1, dtype=torch.bfloat16), 0.05)
+    with pytest.raises(ValueError):       # wrong dtype
+        sess.decode_step_host(torch.zeros(nb // 2, dtype=torch.float16), 0.05)
+    with pytest.raises(ValueError):       # bad output buffer
+        sess.decode_step_host(torch.zeros(nb // 2, dtype=torch.bfloat16), 0.05,
+                              out_host=torch.empty(3, dtype=torch.float32))
 
 
 @pytest.mark.parametrize("frac,d", [(0.05, 128), (0.01, 128), (0.05, 64)])
