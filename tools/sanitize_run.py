@@ -2,7 +2,8 @@
 decode steps through the per-session and the per-unit finish, a Top-k (1%)
 step, and the exact path, on a B=1, 2 KV-head, G=4, n=2048 batch; then two
 steps of a 256-session batch (8 x 8 KV heads x 4, d=64) through the
-two-group stream split."""
+two-group stream split, the second with host inputs and output
+(lfps_decode_step_host_io)."""
 import os
 import sys
 
@@ -48,6 +49,7 @@ K, V, W, F, Q = (np.asarray(x) for x in (K, V, W, F, Q))
 pair = Pair(LfpsConfig(d=64), K, V, W, F, 700)
 pair.sess.split = True
 for t in range(2):
+    pair.host_io = t == 1           # lfps_decode_step_host_io: input copy beside stats
     res, outs = pair.step(Q[:, :, :, t], K[:, :, 700 + t], V[:, :, 700 + t], 0.05)
     pair.compare_step(res, outs, tables=(t == 1))
 torch.cuda.synchronize()
