@@ -101,6 +101,22 @@ def test_decode_step_validation_happens_before_launch():
         or b"must" in lib.lfps_last_error()
 
 
+def test_host_io_validation_happens_before_launch():
+    lib = _lib.load_library()
+    dims = _lib.Dims(1, 1, 1, 64, 4096, 4096)
+    p = _lib.Params()
+    buf = (C.c_uint8 * 64)()
+    rc = lib.lfps_decode_step_host_io(C.byref(dims), C.byref(p), C.byref(_lib.State()),
+                                      C.byref(_lib.Workspace()), None, C.byref(buf), None,
+                                      None, None)
+    assert rc == -1 and b"in_host" in lib.lfps_last_error()
+    bad = _lib.Dims(1, 1, 1, 60, 4096, 4096)                      # d not a multiple of 16
+    rc = lib.lfps_decode_step_host_io(C.byref(bad), C.byref(p), C.byref(_lib.State()),
+                                      C.byref(_lib.Workspace()), C.byref(buf), C.byref(buf),
+                                      None, None, None)
+    assert rc < 0 and lib.lfps_step_input_bytes(C.byref(bad)) < 0
+
+
 def test_library_refuses_to_pretend_without_gpu():
     """No CPU fallback: constructing a device session off-GPU raises."""
     import torch
