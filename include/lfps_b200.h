@@ -277,6 +277,28 @@ LFPS_API int lfps_profile_collect(lfps_kernel_time* out, int32_t cap, int32_t* n
 LFPS_API int lfps_decode_launches(const lfps_dims* dims, int32_t flags);
 LFPS_API int lfps_exact_launches(void);
 
+/* Paged KV store (a paged-KV caller).  The kernels address
+ * K/V as lfps_state.k_cache / v_cache [B, Hkv, n_max, d]; the pool reserves
+ * that range as VIRTUAL address space on the current device and backs it
+ * with physical pages (the device's allocation granularity, 2 MiB) only
+ * where a (request, KV head) has rows, so the decode kernels see the
+ * contiguous layout with no page table while memory follows the live
+ * contexts.  Every (request, KV head) span n_max * d * 2 bytes must be a
+ * multiple of the page size: lfps_kv_pool_page_bytes() gives it.
+ * lfps_kv_pool_reserve backs rows [0, rows + 64) of one (request, KV head)
+ * (the 64-row slack covers the last row tile of any kernel), mapping pages
+ * as the context grows; lfps_kv_pool_release unmaps all of request b's
+ * pages (a finished request).  The reference keeps one in-memory array per
+ * head (kv.py); this is the B200 equivalent for a serving caller. */
+typedef struct lfps_kv_pool lfps_kv_pool;
+LFPS_API int64_t lfps_kv_pool_page_bytes(void);
+LFPS_API int lfps_kv_pool_create(const lfps_dims* dims, lfps_kv_pool** pool,
+                                 void** k_cache, void** v_cache);
+LFPS_API int lfps_kv_pool_reserve(lfps_kv_pool* pool, int32_t b, int32_t h, int64_t rows);
+LFPS_API int lfps_kv_pool_release(lfps_kv_pool* pool, int32_t b);
+LFPS_API int64_t lfps_kv_pool_mapped_bytes(const lfps_kv_pool* pool);
+LFPS_API int lfps_kv_pool_destroy(lfps_kv_pool* pool);
+
 #ifdef __cplusplus
 }
 #endif

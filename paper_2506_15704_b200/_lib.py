@@ -40,7 +40,9 @@ EXPORTS = ("lfps_abi_version", "lfps_last_error", "lfps_workspace_layout",
            "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step",
            "lfps_decode_step_host_out", "lfps_decode_step_host_io", "lfps_step_input_bytes",
            "lfps_exact_topk_step", "lfps_overlap", "lfps_decode_launches", "lfps_slash_capacity",
-           "lfps_exact_launches", "lfps_profile_enable", "lfps_profile_collect")
+           "lfps_exact_launches", "lfps_kv_pool_page_bytes", "lfps_kv_pool_create",
+           "lfps_kv_pool_reserve", "lfps_kv_pool_release", "lfps_kv_pool_mapped_bytes",
+           "lfps_kv_pool_destroy", "lfps_profile_enable", "lfps_profile_collect")
 
 
 class Dims(C.Structure):
@@ -109,6 +111,17 @@ def _declare(lib):
                                              C.c_void_p]
     lib.lfps_step_input_bytes.argtypes = [P(Dims)]
     lib.lfps_step_input_bytes.restype = C.c_int64
+    lib.lfps_kv_pool_page_bytes.argtypes = []
+    lib.lfps_kv_pool_page_bytes.restype = C.c_int64
+    lib.lfps_kv_pool_create.argtypes = [P(Dims), P(C.c_void_p), P(C.c_void_p), P(C.c_void_p)]
+    lib.lfps_kv_pool_reserve.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int64]
+    lib.lfps_kv_pool_release.argtypes = [C.c_void_p, C.c_int32]
+    lib.lfps_kv_pool_mapped_bytes.argtypes = [C.c_void_p]
+    lib.lfps_kv_pool_mapped_bytes.restype = C.c_int64
+    lib.lfps_kv_pool_destroy.argtypes = [C.c_void_p]
+    for name in ("lfps_kv_pool_create", "lfps_kv_pool_reserve", "lfps_kv_pool_release",
+                 "lfps_kv_pool_destroy"):
+        getattr(lib, name).restype = C.c_int
     lib.lfps_exact_topk_step.argtypes = [P(Dims), P(Params), P(State), P(Workspace), C.c_void_p,
                                          C.c_void_p, C.c_void_p]
     lib.lfps_overlap.argtypes = [P(Dims), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

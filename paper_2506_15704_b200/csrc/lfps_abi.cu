@@ -32,6 +32,14 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(LFPS_E_CUDA, "%s: %s", where, cudaGetErrorString(e));
 }
 
+}  // namespace
+
+// error reporting for the other host-side translation units (kv_pool.cu)
+int lfps_abi_fail(int code, const char* msg) { return fail(code, "%s", msg); }
+int lfps_check_dims(const lfps_dims* d);
+
+namespace {
+
 constexpr int kMaxMcap = 510 * 512;     // slash table <= 1022 blocks (32 dirty words)
 constexpr int kMaxM = kMaxMcap - 2;     // k_select.cu: a window spans <= 512 blocks
 
@@ -569,3 +577,5 @@ int lfps_overlap(const lfps_dims* dims, const int32_t* sel, const int32_t* sel_c
 }
 
 }  // extern "C"
+
+int lfps_check_dims(const lfps_dims* d) { return check_dims(d); }

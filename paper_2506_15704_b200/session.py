@@ -77,7 +77,8 @@ class BatchedSession:
 
     def __init__(self, cfg: LfpsConfig, batch: int, kv_heads: int, group: int, n_max: int,
                  m_cap: int | None = None, device: torch.device | str | None = None,
-                 export_sets: bool = False, kv_cache: tuple | None = None):
+                 export_sets: bool = False, kv_cache: tuple | None = None,
+                 paged: bool = False):
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
         device = torch.device(device)
@@ -101,6 +102,12 @@ class BatchedSession:
         self.NS = batch * self.Hq
         self.d = cfg.d
         self.n_max = int(n_max)
+        if paged:
+            # whole pages per (request, KV head): round n_max up
+            from .kv_pool import page_rows
+            with torch.cuda.device(device):
+                pr = page_rows(cfg.d)
+            self.n_max = -(-self.n_max // pr) * pr
         m_cap = int(m_cap if m_cap is not None else n_max - cfg.sink_count + 2)
         m_cap += m_cap & 1
         self.m_cap = m_cap
@@ -109,7 +116,14 @@ class BatchedSession:
         self.sla_cap = _lib.slash_capacity(self.dims)
         dev = self.device
         f64, i32 = torch.float64, torch.int32
-        if kv_cache is not None:
+        self.kv_pool = None
+        if paged:
+            if kv_cache is not None:
+                raise ValueError("paged=True allocates its own KV pool")
+            from .kv_pool import KvPool
+            self.kv_pool = KvPool(self.dims, dev)
+            self.k_cache, self.v_cache = self.kv_pool.k, self.kv_pool.v
+        elif kv_cache is not None:
             # an existing cache (e.g. one layer's rows reused by other layers'
             # trackers): bf16 [batch, kv_heads, n_max, d] pair on this device
             self.k_cache, self.v_cache = kv_cache
@@ -142,6 +156,7 @@ class BatchedSession:
         self.step_count = 0
         self.tables_stale = False
         self._in_dev = None        # decode_step_host's device staging buffer
+        self._released = set()     # paged: requests whose pages were returned
 
     # -- workspace views ----------------------------------------------------
     def _region(self, off: int, dtype, shape):
@@ -183,6 +198,7 @@ class BatchedSession:
         if n0 <= self.cfg.sink_count + self.cfg.s:
             raise ValueError(
                 f"prefill needs more than sink_count + s = {self.cfg.sink_count + self.cfg.s} rows")
+        self._back(b, n0 + 1, reload=True)
         self.k_cache[b, :, :n0].copy_(keys)
         self.v_cache[b, :, :n0].copy_(values)
         self.n_host[b] = n0
@@ -197,6 +213,7 @@ class BatchedSession:
         if n0 <= self.cfg.sink_count + self.cfg.s:
             raise ValueError(
                 f"prefill needs more than sink_count + s = {self.cfg.sink_count + self.cfg.s} rows")
+        self._back(b, n0 + 1, reload=True)
         self.k_cache[b, h, :n0].copy_(keys)
         self.v_cache[b, h, :n0].copy_(values)
         self.n_host[b] = n0
@@ -267,6 +284,7 @@ class BatchedSession:
                 raise ValueError(f"{name} must have shape {shape}, got {tuple(t.shape)}")
             if t.dtype != torch.bfloat16 or t.device != self.device or not t.is_contiguous():
                 raise ValueError(f"{name} must be a contiguous bf16 tensor on {self.device}")
+        self._back_step()
         n_host = (C.c_int32 * self.B)(*self.n_host)
         if out_host is None:
             _lib.check(self.lib.lfps_decode_step(
@@ -289,6 +307,37 @@ class BatchedSession:
         self.n_host = [n + 1 for n in self.n_host]
         self.step_count += 1
         return self.result()
+
+    # -- paged KV (kv_pool.py) ------------------------------------------------
+    def _back(self, b: int, rows: int, reload: bool = False):
+        """Paged caches: back rows [0, rows) of request b before they are
+        written or read (the append of a step writes row n)."""
+        if self.kv_pool is None:
+            return
+        if b in self._released and not reload:
+            raise ValueError(f"request {b} was released; load_prefill it again first")
+        self._released.discard(b)
+        self.kv_pool.reserve(b, rows)
+
+    def _back_step(self):
+        if self.kv_pool is not None:
+            for b in range(self.B):
+                self._back(b, min(self.n_host[b] + 1, self.n_max))
+
+    def release_request(self, b: int):
+        """Paged caches: return request b's KV pages (a finished request).
+        Its rows are gone; decoding the batch again needs a new prefill for b
+        (load_prefill / load_unit + bootstrap)."""
+        if self.kv_pool is None:
+            raise ValueError("release_request needs paged=True")
+        self.kv_pool.release(b)
+        self._released.add(b)
+
+    def kv_mapped_bytes(self) -> int:
+        """Bytes of device memory behind the K and V caches."""
+        if self.kv_pool is not None:
+            return self.kv_pool.mapped_bytes()
+        return 2 * self.k_cache.numel() * self.k_cache.element_size()
 
     def step_input_bytes(self) -> int:
         """Bytes of one step's packed host input (lfps_step_input_bytes)."""
@@ -329,6 +378,7 @@ class BatchedSession:
                 or out_host.device.type != "cpu" or not out_host.is_contiguous()):
             raise ValueError(f"out_host must be a contiguous f32 CPU tensor of shape "
                              f"{tuple(self.out.shape)}")
+        self._back_step()
         if self._in_dev is None:
             self._in_dev = torch.empty(nbytes // 2, dtype=torch.bfloat16, device=self.device)
         n_host = (C.c_int32 * self.B)(*self.n_host)
@@ -353,6 +403,9 @@ class BatchedSession:
         if (self.B, self.Hkv, self.G, self.m_cap, self.sla_cap) != \
                 (other.B, other.Hkv, other.G, other.m_cap, other.sla_cap):
             raise ValueError("sessions differ in shape")
+        if self.kv_pool is not None:
+            raise ValueError("copy_tracker_from shares another session's KV rows: not with "
+                             "paged=True (pass kv_cache instead)")
         for name in ("ver", "sla", "scale", "sla_base", "clamp_count", "mean_key", "mean_value",
                      "sigma_hat_sq", "n_ctx"):
             getattr(self, name).copy_(getattr(other, name))
@@ -367,6 +420,7 @@ class BatchedSession:
         for name, t in (("new_key", k_new), ("new_value", v_new)):
             if tuple(t.shape) != (self.B, self.Hkv, self.d) or t.dtype != torch.bfloat16:
                 raise ValueError(f"{name} must be bf16 [{self.B}, {self.Hkv}, {self.d}]")
+        self._back_step()
         for b in range(self.B):
             n = self.n_host[b]
             if n >= self.n_max:

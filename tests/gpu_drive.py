@@ -20,14 +20,15 @@ class Pair:
     keys/values: f32 (bf16 values) [B, Hkv, n_total, d]; weights f32
     [B, Hkv, G, s, n0 - S]; finals [B, Hkv, G, d]."""
 
-    def __init__(self, cfg, keys, values, weights, finals, n0, n_max=None, m_cap=None):
+    def __init__(self, cfg, keys, values, weights, finals, n0, n_max=None, m_cap=None,
+                 paged=False):
         B, Hkv, _, d = keys.shape
         G = weights.shape[2]
         self.cfg, self.B, self.Hkv, self.G, self.d, self.n0 = cfg, B, Hkv, G, d, n0
         self.host_io = False
         self.weights, self.finals = weights, finals
         self.sess = BatchedSession(cfg, B, Hkv, G, n_max=n_max or keys.shape[2] + 8,
-                                   m_cap=m_cap, device="cuda", export_sets=True)
+                                   m_cap=m_cap, device="cuda", export_sets=True, paged=paged)
         for b in range(B):
             self.sess.load_prefill(b, bf16(keys[b, :, :n0]).cuda(), bf16(values[b, :, :n0]).cuda())
         w = torch.as_tensor(np.ascontiguousarray(weights, dtype=np.float32))

@@ -117,6 +117,19 @@ def test_host_io_validation_happens_before_launch():
     assert rc < 0 and lib.lfps_step_input_bytes(C.byref(bad)) < 0
 
 
+def test_kv_pool_validation_on_host():
+    import torch
+    lib = _lib.load_library()
+    pool, kp, vp = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    bad = _lib.Dims(0, 1, 1, 64, 4096, 4096)
+    assert lib.lfps_kv_pool_create(C.byref(bad), C.byref(pool), C.byref(kp), C.byref(vp)) < 0
+    assert lib.lfps_kv_pool_reserve(None, 0, 0, 1) == -1
+    assert lib.lfps_kv_pool_release(None, 0) == -1
+    assert lib.lfps_kv_pool_destroy(None) == 0
+    if not torch.cuda.is_available():       # no driver: the VM API is reported missing
+        assert lib.lfps_kv_pool_page_bytes() < 0
+
+
 def test_library_refuses_to_pretend_without_gpu():
     """No CPU fallback: constructing a device session off-GPU raises."""
     import torch

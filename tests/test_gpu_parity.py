@@ -57,7 +57,7 @@ def test_golden_trajectory_bit_exact(name):
 
 
 def _gqa_pair(batch=2, kv_heads=2, group=4, n0=3000, steps=8, d=128, seed=3, spec_kw=None,
-              **cfg_kw):
+              paged=False, **cfg_kw):
     from paper_2506_15704_b200.config import LfpsConfig
     from paper_2506_15704_b200.workload import GqaSpec, gen_unit
     spec = GqaSpec(batch=batch, kv_heads=kv_heads, group=group, d=d, n_prefill=n0, steps=steps,
@@ -75,7 +75,7 @@ def _gqa_pair(batch=2, kv_heads=2, group=4, n0=3000, steps=8, d=128, seed=3, spe
             qr.append(u.queries.float().numpy())
         K.append(kr); V.append(vr); W.append(wr); F.append(fr); Q.append(qr)
     K, V, W, F, Q = (np.asarray(x) for x in (K, V, W, F, Q))
-    return Pair(cfg, K, V, W, F, n0), K, V, Q
+    return Pair(cfg, K, V, W, F, n0, paged=paged), K, V, Q
 
 
 @pytest.mark.parametrize("frac", [0.05, 0.01])
@@ -318,6 +318,38 @@ def test_decode_step_host_io_small_and_rejects():
     with pytest.raises(ValueError):       # bad output buffer
         sess.decode_step_host(torch.zeros(nb // 2, dtype=torch.bfloat16), 0.05,
                               out_host=torch.empty(3, dtype=torch.float32))
+
+
+def test_paged_kv_pool_bit_exact_across_a_page():
+    """N4 paged-KV caller: K/V in a KvPool (virtual [B, Hkv, n_max, d], 2 MiB
+    pages mapped as contexts grow).  The context crosses a page boundary
+    during the run (8192 rows per page at d=128, incl. the 64-row slack);
+    every step matches the oracle, through decode_step and the host-io entry
+    point; the exact path reads the paged rows; releasing a request returns
+    its pages and blocks further steps until it is reloaded."""
+    from paper_2506_15704_b200 import kv_pool
+    rows = kv_pool.page_rows(128)
+    n0 = rows - kv_pool.SLACK_ROWS - 3
+    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, n0=n0, steps=6, seed=53, paged=True)
+    sess = pair.sess
+    assert sess.kv_pool is not None and sess.n_max % rows == 0
+    page = kv_pool.page_bytes()
+    assert sess.kv_mapped_bytes() == 2 * 2 * 2 * page            # K+V x B x Hkv, one page
+    for t in range(6):
+        pair.host_io = t % 2 == 1
+        res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], 0.05)
+        pair.compare_step(res, outs)
+    assert sess.kv_mapped_bytes() == 2 * 2 * 2 * 2 * page        # the second page
+    import gpu_drive
+    q = gpu_drive.bf16(Q[:, :, :, 6 - 1].reshape(2, -1, 128)).cuda()
+    sess.exact_topk_step(q, 0.05)
+    torch.cuda.synchronize()
+    sess.check_errors("exact on paged rows")
+    sess.release_request(1)
+    assert sess.kv_mapped_bytes() == 2 * 2 * 2 * page
+    with pytest.raises(ValueError):
+        sess.decode_step(q, gpu_drive.bf16(K[:, :, n0]).cuda(), gpu_drive.bf16(V[:, :, n0]).cuda(),
+                         0.05)
 
 
 @pytest.mark.parametrize("frac,d", [(0.05, 128), (0.01, 128), (0.05, 64)])
