@@ -57,7 +57,7 @@ def test_golden_trajectory_bit_exact(name):
 
 
 def _gqa_pair(batch=2, kv_heads=2, group=4, n0=3000, steps=8, d=128, seed=3, spec_kw=None,
-              paged=False, **cfg_kw):
+              paged=False, n_max=None, **cfg_kw):
     from paper_2506_15704_b200.config import LfpsConfig
     from paper_2506_15704_b200.workload import GqaSpec, gen_unit
     spec = GqaSpec(batch=batch, kv_heads=kv_heads, group=group, d=d, n_prefill=n0, steps=steps,
@@ -75,7 +75,7 @@ def _gqa_pair(batch=2, kv_heads=2, group=4, n0=3000, steps=8, d=128, seed=3, spe
             qr.append(u.queries.float().numpy())
         K.append(kr); V.append(vr); W.append(wr); F.append(fr); Q.append(qr)
     K, V, W, F, Q = (np.asarray(x) for x in (K, V, W, F, Q))
-    return Pair(cfg, K, V, W, F, n0, paged=paged), K, V, Q
+    return Pair(cfg, K, V, W, F, n0, paged=paged, n_max=n_max), K, V, Q
 
 
 @pytest.mark.parametrize("frac", [0.05, 0.01])
@@ -330,9 +330,10 @@ def test_paged_kv_pool_bit_exact_across_a_page():
     from paper_2506_15704_b200 import kv_pool
     rows = kv_pool.page_rows(128)
     n0 = rows - kv_pool.SLACK_ROWS - 3
-    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, n0=n0, steps=6, seed=53, paged=True)
+    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, n0=n0, steps=6, seed=53, paged=True,
+                              n_max=2 * rows)
     sess = pair.sess
-    assert sess.kv_pool is not None and sess.n_max % rows == 0
+    assert sess.kv_pool is not None and sess.n_max == 2 * rows
     page = kv_pool.page_bytes()
     assert sess.kv_mapped_bytes() == 2 * 2 * 2 * page            # K+V x B x Hkv, one page
     for t in range(6):
