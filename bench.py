@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-split", action="store_true",
                     help="disable LFPS_FLAG_SPLIT (two session halves on two streams)")
+    ap.add_argument("--paged", action="store_true",
+                    help="K/V in a KvPool (2 MiB pages mapped as contexts grow; kv_pool.py)")
     ap.add_argument("--unit-finish", action="store_true", help="LFPS_FLAG_UNIT_FINISH")
     ap.add_argument("--pair-finish", action="store_true",
                     help="LFPS_FLAG_PAIR_FINISH: two q-heads per finish CTA over their probe union")
@@ -423,7 +425,8 @@ def run_ours(args, world, rank, local):
                    seed=42 + 7919 * b0)
     dev = torch.device("cuda", torch.cuda.current_device())
     t_setup = time.time()
-    sess = BatchedSession(cfg, b_local, hkv, group, n_max=ctx + T + 8, device=dev)
+    sess = BatchedSession(cfg, b_local, hkv, group, n_max=ctx + T + 8, device=dev,
+                          paged=args.paged)
     stream = populate(sess, spec)
     sess.split = not args.no_split
     sess.pair_finish = args.pair_finish
@@ -630,7 +633,9 @@ def run_ours(args, world, rank, local):
                    "q_heads": hkv * group, "kv_heads": hkv, "d": d, "topk_fraction": frac,
                    "sharding": "requests across ranks, no collective on the decode path",
                    "l2": "flushed before every timed step (512 MiB write); each step timed "
-                         "by its own CUDA events"},
+                         "by its own CUDA events",
+                   "kv": ("paged (KvPool, %d MiB mapped)" % (sess.kv_mapped_bytes() >> 20)
+                          if args.paged else "contiguous")},
         "gpu_launches": args.steps * _lib.load_library().lfps_decode_launches(
             C.byref(sess.dims), sess._params(frac).flags),
         "roofline": {"bound": "hbm", "kernel": dominant,
