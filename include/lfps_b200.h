@@ -288,8 +288,9 @@ LFPS_API int lfps_exact_launches(void);
  * lfps_kv_pool_reserve backs rows [0, rows + 64) of one (request, KV head)
  * (the 64-row slack covers the last row tile of any kernel), mapping pages
  * as the context grows; lfps_kv_pool_release unmaps all of request b's
- * pages (a finished request).  The reference keeps one in-memory array per
- * head (kv.py); this is the B200 equivalent for a serving caller. */
+ * pages (a finished request).  The reference keeps one KvStore per head
+ * that doubles and copies when full (store.py:8-90, _grow at :79-90); here
+ * growth maps one more page, without a copy. */
 typedef struct lfps_kv_pool lfps_kv_pool;
 LFPS_API int64_t lfps_kv_pool_page_bytes(void);
 LFPS_API int lfps_kv_pool_create(const lfps_dims* dims, lfps_kv_pool** pool,

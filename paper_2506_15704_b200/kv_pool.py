@@ -5,9 +5,10 @@ bf16 ``[B, Hkv, n_max, d]``.  ``KvPool`` reserves that range as virtual
 address space and maps physical pages (the device's allocation granularity,
 2 MiB) per (request, KV head) only as its context grows -- the GPU's MMU is
 the page table, so the hot path is unchanged -- and unmaps a finished
-request's pages.  The reference keeps one growing in-memory array per head
-(``kv.py``); this is what that becomes for a batch of long-context requests
-on one 180 GB device.
+request's pages.  The reference keeps one KvStore per head whose arrays
+double and copy when full (``store.py:8-90``, ``_grow`` at :79-90); here a
+context grows by mapping one more page, with no copy and no re-pointing of
+the kernels, for a batch of long-context requests on one 180 GB device.
 """
 from __future__ import annotations
 
