@@ -16,7 +16,8 @@
  * Conventions
  *  - Plain pointers and sizes only.  Every pointer in lfps_state /
  *    lfps_workspace is a DEVICE pointer owned by the caller; the library
- *    never allocates.  `stream` is a cudaStream_t passed as void*.
+ *    never allocates, except the optional paged KV store (lfps_kv_pool_*),
+ *    which owns its pages.  `stream` is a cudaStream_t passed as void*.
  *  - Return 0 on success or a negative LFPS_E_* code; lfps_last_error()
  *    returns a thread-local message for the last failure.  All argument
  *    validation happens on the host before any launch, so a rejected call
