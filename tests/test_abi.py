@@ -139,3 +139,37 @@ def test_library_refuses_to_pretend_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises((DeviceError, RuntimeError, AssertionError)):
         BatchedSession(LfpsConfig(d=64), 1, 1, 1, n_max=1024, device="cuda")
+
+
+def test_kv_pool_backed_rows_bookkeeping():
+    """KvPool.reserve's host bookkeeping (no device): the rows usable without
+    another map call follow the C side's page rounding with the 64-row
+    slack, the last page of a span backs up to n_max, and release resets."""
+    from paper_2506_15704_b200 import kv_pool
+
+    calls = []
+
+    class FakeLib:
+        def lfps_kv_pool_reserve(self, h, b, kv, rows):
+            calls.append((b, kv, rows))
+            return 0
+
+        def lfps_kv_pool_release(self, h, b):
+            return 0
+
+    pool = kv_pool.KvPool.__new__(kv_pool.KvPool)
+    pool.lib, pool._h = FakeLib(), C.c_void_p(1)
+    pool.dims = _lib.Dims(2, 2, 4, 128, 3 * 8192, 3 * 8192)
+    pool.rows_per_page = 8192
+    pool.backed = [0, 0]
+    pool.reserve(0, 100)
+    assert pool.backed[0] == 8192 - kv_pool.SLACK_ROWS and len(calls) == 2   # one call per head
+    pool.reserve(0, 8128)                       # still inside the first page's usable rows
+    assert len(calls) == 2
+    pool.reserve(0, 8129)                       # crosses: two pages
+    assert pool.backed[0] == 2 * 8192 - kv_pool.SLACK_ROWS and len(calls) == 4
+    pool.reserve(0, 3 * 8192 - 10)              # the span's last page: everything backed
+    assert pool.backed[0] == 3 * 8192
+    pool.release(0)
+    assert pool.backed[0] == 0 and pool.backed[1] == 0
+    pool._h = C.c_void_p()                      # nothing to destroy
