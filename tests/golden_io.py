@@ -58,3 +58,51 @@ def load(name: str) -> Golden:
 def names():
     return sorted(os.path.splitext(os.path.basename(p))[0]
                   for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz")))
+
+
+# ---------------------------------------------------------------------------
+# seeded goldens (tests/golden/make_golden_seeded.py): reference outputs for
+# inputs regenerated from a workload spec, pinned by a SHA-256
+# ---------------------------------------------------------------------------
+
+SEEDED_DIR = os.path.join(GOLDEN_DIR, "seeded")
+
+
+@dataclass
+class Seeded:
+    name: str
+    spec: object           # workload.GqaSpec
+    cfg: dict
+    fracs: np.ndarray      # per step
+    K: np.ndarray          # f32 [Hkv, n0 + T, d]
+    V: np.ndarray
+    W: np.ndarray          # f32 [Hkv, G, s, m0]
+    F: np.ndarray          # [Hkv, G, d]
+    Q: np.ndarray          # [Hkv, G, T, d]
+    raw: dict
+
+    def sets(self, key: str):
+        lens = self.raw[key + "_len"]
+        cat = self.raw[key + "_cat"].astype(np.int64)
+        offs = np.concatenate([[0], np.cumsum(lens)])
+        return [cat[offs[i]: offs[i + 1]] for i in range(lens.size)]
+
+
+def seeded_names():
+    return sorted(os.path.splitext(os.path.basename(p))[0]
+                  for p in glob.glob(os.path.join(SEEDED_DIR, "*.npz")))
+
+
+def load_seeded(name: str) -> Seeded:
+    import sys
+    sys.path.insert(0, GOLDEN_DIR)
+    from make_golden_seeded import case_inputs
+    z = dict(np.load(os.path.join(SEEDED_DIR, name + ".npz")))
+    case = {"spec": ast.literal_eval(str(z["spec"]))}
+    spec, (K, V, W, F, Q), digest = case_inputs(case)
+    if digest != str(z["sha256"]):
+        raise AssertionError(
+            f"seeded golden {name}: the regenerated inputs hash to {digest}, the fixture "
+            f"was made from {z['sha256']} (torch CPU RNG / BLAS differ on this host)")
+    return Seeded(name=name, spec=spec, cfg=ast.literal_eval(str(z["cfg_json"])),
+                  fracs=z["fracs"], K=K, V=V, W=W, F=F, Q=Q, raw=z)

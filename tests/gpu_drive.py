@@ -43,8 +43,26 @@ class Pair:
                                                  weights[b, h], finals[b, h], cfg, lo.DevArith)
                 self.units.append((kv, trs, prs))
 
-    def step(self, q, k_new, v_new, frac):
-        """q [B, Hkv, G, d]; k_new/v_new [B, Hkv, d] (f32 bf16-valued)."""
+    def step(self, q, k_new, v_new, frac, cfg=None):
+        """q [B, Hkv, G, d]; k_new/v_new [B, Hkv, d] (f32 bf16-valued).
+        ``cfg`` overrides the configuration for this step only (the
+        reference's decode_step takes a config per call, engine.py:97)."""
+        B, Hkv, G, d = self.B, self.Hkv, self.G, self.d
+        cfg = cfg or self.cfg
+        saved, self.sess.cfg = self.sess.cfg, cfg
+        try:
+            res = self._device_step(q, k_new, v_new, frac)
+        finally:
+            self.sess.cfg = saved
+        outs = []
+        for b in range(B):
+            for h in range(Hkv):
+                kv, trs, prs = self.units[b * Hkv + h]
+                outs.append(lo.unit_step(kv, trs, prs, q[b, h], k_new[b, h], v_new[b, h], frac,
+                                         cfg, lo.DevArith, "fp32"))
+        return res, outs
+
+    def _device_step(self, q, k_new, v_new, frac):
         B, Hkv, G, d = self.B, self.Hkv, self.G, self.d
         if self.host_io:          # lfps_decode_step_host_io: packed pinned inputs, host output
             packed = self.sess.pack_step_inputs(bf16(q.reshape(B, Hkv * G, d)), bf16(k_new),
@@ -55,13 +73,7 @@ class Pair:
         else:
             res = self.sess.decode_step(bf16(q.reshape(B, Hkv * G, d)).cuda(),
                                         bf16(k_new).cuda(), bf16(v_new).cuda(), frac, check=True)
-        outs = []
-        for b in range(B):
-            for h in range(Hkv):
-                kv, trs, prs = self.units[b * Hkv + h]
-                outs.append(lo.unit_step(kv, trs, prs, q[b, h], k_new[b, h], v_new[b, h], frac,
-                                         self.cfg, lo.DevArith, "fp32"))
-        return res, outs
+        return res
 
     def compare_step(self, res, outs, out_tol=1e-5, tables=True):
         """Assert bit-exact sets/scalars/tables and toleranced outputs."""
@@ -104,3 +116,27 @@ class Pair:
                     np.testing.assert_array_equal(ver, tr.ver_view(), err_msg=tag + " ver")
                     np.testing.assert_array_equal(sla, tr.sla_view(), err_msg=tag + " sla")
         return worst
+
+
+def gqa_pair(batch=2, kv_heads=2, group=4, n0=3000, steps=8, d=128, seed=3, spec_kw=None,
+              paged=False, n_max=None, **cfg_kw):
+    from paper_2506_15704_b200.config import LfpsConfig
+    from paper_2506_15704_b200.workload import GqaSpec, gen_unit
+    kw = dict(slash_offsets=(64, 65), band_width=6)
+    kw.update(spec_kw or {})
+    spec = GqaSpec(batch=batch, kv_heads=kv_heads, group=group, d=d, n_prefill=n0, steps=steps,
+                   seed=seed, **kw)
+    cfg = LfpsConfig(d=d, **cfg_kw)
+    K, V, W, F, Q = [], [], [], [], []
+    for b in range(batch):
+        kr, vr, wr, fr, qr = [], [], [], [], []
+        for h in range(kv_heads):
+            u = gen_unit(spec, b, h, device="cpu")
+            kr.append(u.keys.float().numpy())
+            vr.append(u.values.float().numpy())
+            wr.append(u.weights.numpy())
+            fr.append(u.final_query.float().numpy())
+            qr.append(u.queries.float().numpy())
+        K.append(kr); V.append(vr); W.append(wr); F.append(fr); Q.append(qr)
+    K, V, W, F, Q = (np.asarray(x) for x in (K, V, W, F, Q))
+    return Pair(cfg, K, V, W, F, n0, paged=paged, n_max=n_max), K, V, Q

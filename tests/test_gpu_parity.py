@@ -56,26 +56,7 @@ def test_golden_trajectory_bit_exact(name):
                 np.testing.assert_array_equal(pair.sess.probe_list(0, gi), ref_probe[rec])
 
 
-def _gqa_pair(batch=2, kv_heads=2, group=4, n0=3000, steps=8, d=128, seed=3, spec_kw=None,
-              paged=False, n_max=None, **cfg_kw):
-    from paper_2506_15704_b200.config import LfpsConfig
-    from paper_2506_15704_b200.workload import GqaSpec, gen_unit
-    spec = GqaSpec(batch=batch, kv_heads=kv_heads, group=group, d=d, n_prefill=n0, steps=steps,
-                   seed=seed, slash_offsets=(64, 65), band_width=6, **(spec_kw or {}))
-    cfg = LfpsConfig(d=d, **cfg_kw)
-    K, V, W, F, Q = [], [], [], [], []
-    for b in range(batch):
-        kr, vr, wr, fr, qr = [], [], [], [], []
-        for h in range(kv_heads):
-            u = gen_unit(spec, b, h, device="cpu")
-            kr.append(u.keys.float().numpy())
-            vr.append(u.values.float().numpy())
-            wr.append(u.weights.numpy())
-            fr.append(u.final_query.float().numpy())
-            qr.append(u.queries.float().numpy())
-        K.append(kr); V.append(vr); W.append(wr); F.append(fr); Q.append(qr)
-    K, V, W, F, Q = (np.asarray(x) for x in (K, V, W, F, Q))
-    return Pair(cfg, K, V, W, F, n0, paged=paged, n_max=n_max), K, V, Q
+from gpu_drive import gqa_pair as _gqa_pair  # noqa: E402
 
 
 @pytest.mark.parametrize("frac", [0.05, 0.01])
