@@ -169,3 +169,37 @@ def test_moment_overflow_regime_matches_the_reference(group):
             assert float(sess.scale[0]) < 1e-80              # deep in the overflow regime
         assert failed == _reference_fate(pair, K, V, Q, n0, steps)
     assert (failed is not None) == (group == 1)
+
+
+def test_seeded_reference_golden_c1_16k():
+    """The C1 shape against the reference's OWN outputs (tests/golden/seeded/
+    c1_16k.npz, made by make_golden_seeded.py from the reference's
+    prefill_bootstrap / decode_step): every device C0 / C1 / probe / C2 set
+    equals the reference's, and the device matches the canonical oracle
+    bit for bit on the way (tables after the last step)."""
+    from gpu_drive import Pair
+    from golden_io import load_seeded
+    from paper_2506_15704_b200.config import LfpsConfig
+    g = load_seeded("c1_16k")
+    sp = g.spec
+    n0, T, Hkv, G = sp.n_prefill, sp.steps, sp.kv_heads, sp.group
+    pair = Pair(LfpsConfig(d=sp.d, **g.cfg), g.K[None], g.V[None], g.W[None], g.F[None], n0)
+    ref = {k: g.sets(k) for k in ("c0", "c1", "probe", "c2")}
+    for t in range(T):
+        res, outs = pair.step(g.Q[None, :, :, t], g.K[None, :, n0 + t], g.V[None, :, n0 + t],
+                              float(g.fracs[t]))
+        pair.compare_step(res, outs, tables=(t == T - 1))
+        byp = res.bypassed.cpu().numpy()
+        for qh in range(Hkv * G):
+            rec = t * Hkv * G + qh
+            assert bool(byp[0, qh]) == bool(g.raw["bypassed"][rec])
+            if byp[0, qh]:
+                continue
+            np.testing.assert_array_equal(pair.sess.c0_list(0, qh), ref["c0"][rec])
+            np.testing.assert_array_equal(pair.sess.c1_list(0, qh), ref["c1"][rec])
+            np.testing.assert_array_equal(pair.sess.probe_list(0, qh), ref["probe"][rec])
+            np.testing.assert_array_equal(pair.sess.c2_list(0, qh), ref["c2"][rec])
+        out = res.output.cpu().numpy()[0]
+        want = g.raw["outputs"][t * Hkv * G:(t + 1) * Hkv * G]
+        err = np.linalg.norm(out - want, axis=1) / np.linalg.norm(want, axis=1)
+        assert err.max() <= 1e-5, err.max()
