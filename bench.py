@@ -53,7 +53,7 @@ UNIT = "us/step"
 def parse():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=tuple(CONFIGS), default="c4")
@@ -65,11 +65,11 @@ def parse():
                     help="disable LFPS_FLAG_SPLIT (two session halves on two streams)")
     ap.add_argument("--paged", action="store_true",
                     help="K/V in a KvPool (2 MiB pages mapped as contexts grow; kv_pool.py)")
-    ap.add_argument("--unit-finish", action="store_true", help="LFPS_FLAG_UNIT_FINISH")
-    ap.add_argument("--pair-finish", action="store_true",
-                    help="LFPS_FLAG_PAIR_FINISH: two q-heads per finish CTA over their probe union")
     ap.add_argument("--gather", action="store_true",
                     help="N > 1: all-gather each e2e step's outputs and C2 counts to rank 0 (NCCL)")
+    ap.add_argument("--verify", type=int, default=2,
+                    help="after the run, replay this many (request, KV-head) units of rank 0 "
+                         "through the CPU oracle and require bit-exact tables and sets")
     ap.add_argument("--profile-only", action="store_true",
                     help="short run for ncu: no e2e, recall or cpu legs")
     return ap.parse_args()
@@ -213,56 +213,118 @@ def measured_peaks():
 
 
 # ---------------------------------------------------------------------------
-# CPU leg: the reference algorithm (oracle port, reference arithmetic) on host
-# cores, one process per core, BLAS pinned before the interpreter starts.
+# CPU leg: the UNMODIFIED reference package (pkg/src/lfps, installed into
+# baseline/_ref by tools/install_reference.sh) on the host's physical cores,
+# one process per core, BLAS pinned to one thread before numpy loads.
 # ---------------------------------------------------------------------------
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+_BLAS_VARS = ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS",
+              "NUMEXPR_NUM_THREADS", "VECLIB_MAXIMUM_THREADS")
+
+
+def reference_available() -> bool:
+    return os.path.exists(os.path.join(REF_DIR, "lfps", "engine.py"))
+
+
 def _cpu_worker(job):
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    """One host core: one (request, KV-head) unit of the workload as the
+    reference runs it -- G independent HeadSessions over identical bf16-valued
+    K/V (the reference has no GQA) -- stepping the stock
+    lfps.decode_step (engine.py:97-201) and timing lfps.bench.exact_topk_step
+    (bench.py:73-80) on the same pre-append rows.  Inputs are generated before
+    any timing; nothing of this repo runs inside the timed calls."""
+    for var in _BLAS_VARS:
+        os.environ[var] = "1"
     import numpy as np
     import torch
     torch.set_num_threads(1)
-    from oracle import lfps_oracle as lo
-    from paper_2506_15704_b200.config import LfpsConfig
     from paper_2506_15704_b200.workload import GqaSpec, gen_unit
     spec = GqaSpec(**job["spec"])
     b, h, steps, warm, frac = job["b"], job["h"], job["steps"], job["warmup"], job["frac"]
-    cfg = LfpsConfig(d=spec.d)
+    G, n0 = job["sessions"], spec.n_prefill
     u = gen_unit(spec, b, h, device="cpu")
-    n0 = spec.n_prefill
     keys = u.keys.double().numpy()
     values = u.values.double().numpy()
-    kv, trs, prs = lo.bootstrap_unit(keys[:n0], values[:n0], u.weights.double().numpy(),
-                                     u.final_query.double().numpy(), cfg, lo.RefArith)
+    weights = u.weights.double().numpy()
+    finals = u.final_query.double().numpy()
     qs = u.queries.double().numpy()              # [G, steps, d]
+    del u
+    if job["kind"] == "reference":
+        sys.path.insert(0, REF_DIR)
+        import lfps
+        from lfps.bench import exact_topk_step
+        cfg = lfps.LfpsConfig(d=spec.d)
+        sessions = [lfps.prefill_bootstrap(keys[:n0], values[:n0], weights[g], finals[g], cfg)
+                    for g in range(G)]
+
+        def lfps_step(g, q, t):
+            lfps.decode_step(sessions[g], q, keys[n0 + t], values[n0 + t], frac, cfg)
+
+        def exact_step(g, q):
+            st = sessions[g].store
+            exact_topk_step(q, st, max(1, round(frac * st.n)), cfg.sink_count)
+    else:                                        # the oracle port (reference arithmetic)
+        from oracle import lfps_oracle as lo
+        from paper_2506_15704_b200.config import LfpsConfig
+        cfg = LfpsConfig(d=spec.d)
+        kv, trs, prs = lo.bootstrap_unit(keys[:n0], values[:n0], weights[:G], finals[:G], cfg,
+                                         lo.RefArith)
+        kvs = [kv] + [lo.UnitKV(kv.keys.copy(), kv.values.copy(), kv.n) for _ in range(G - 1)]
+
+        def lfps_step(g, q, t):
+            lo.session_step(kvs[g], trs[g], prs[g], q, frac, cfg, lo.RefArith, "fp64")
+            kvs[g].append(keys[n0 + t], values[n0 + t])
+
+        def exact_step(g, q):
+            lo.exact_topk_step(kvs[g], q, lo.budget_k(frac, kvs[g].n), cfg, "fp64")
     lfps_ns, exact_ns = [], []
     for t in range(warm + steps):
-        for g in range(spec.group):
+        for g in range(G):
             q = qs[g, t]
             t0 = time.perf_counter_ns()
-            lo.exact_topk_step(kv, q, lo.budget_k(frac, kv.n), cfg, "fp64")
+            exact_step(g, q)
             t1 = time.perf_counter_ns()
-            lo.session_step(kv, trs[g], prs[g], q, frac, cfg, lo.RefArith, "fp64")
+            lfps_step(g, q, t)
             t2 = time.perf_counter_ns()
             if t >= warm:
                 exact_ns.append(t1 - t0)
                 lfps_ns.append(t2 - t1)
-        kv.append(keys[n0 + t], values[n0 + t])
     return {"lfps_ns": lfps_ns, "exact_ns": exact_ns}
 
 
-def cpu_leg(cfg_name: str, steps: int, warmup: int, workers: int):
-    """Time the reference algorithm on host cores; returns a dict."""
+def physical_cores() -> int:
+    """Physical cores available to this process (lscpu cores x sockets,
+    capped by the affinity mask)."""
+    avail = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        f = {k.strip(): v.strip() for k, v in (ln.split(":", 1) for ln in out.splitlines()
+                                              if ":" in ln)}
+        phys = int(f["Core(s) per socket"]) * int(f["Socket(s)"])
+        return max(1, min(phys, avail or phys))
+    except Exception:  # noqa: BLE001
+        return max(1, avail or 1)
+
+
+def cpu_leg(cfg_name: str, steps: int, warmup: int, workers: int, sessions: int = 2):
+    """Time the reference's CPU path on the host cores; returns a dict.
+
+    Bounded sample: each worker process steps `sessions` reference sessions
+    of one unit for `steps` timed steps (+ warm-up); the per-layer-step time
+    is extrapolated from the median session-step over all of a layer's
+    sessions spread over the cores."""
     import multiprocessing as mp
     batch, ctx, hkv, group, d, frac, _ = CONFIGS[cfg_name]
-    for var in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS",
-                "NUMEXPR_NUM_THREADS", "VECLIB_MAXIMUM_THREADS"):
+    for var in _BLAS_VARS:
         os.environ[var] = "1"
-    cores = workers or (os.cpu_count() or 1)
+    cores = workers or physical_cores()
+    kind = "reference" if reference_available() else "port"
+    sessions = min(sessions, group)
     spec = dict(batch=batch, kv_heads=hkv, group=group, d=d, n_prefill=ctx,
                 steps=warmup + steps, seed=42)
-    jobs = [dict(spec=spec, b=i // hkv, h=i % hkv, steps=steps, warmup=warmup, frac=frac)
-            for i in range(cores)]
+    jobs = [dict(spec=spec, b=(i // hkv) % batch, h=i % hkv, steps=steps, warmup=warmup,
+                 frac=frac, sessions=sessions, kind=kind) for i in range(cores)]
     ctxm = mp.get_context("spawn")
     t0 = time.time()
     with ctxm.Pool(cores) as pool:
@@ -274,7 +336,11 @@ def cpu_leg(cfg_name: str, steps: int, warmup: int, workers: int):
     med_l = statistics.median(lfps) / 1e3
     med_e = statistics.median(exact) / 1e3
     per_worker = math.ceil(ns_total / cores)
+    what = ("the unmodified reference package (baseline/_ref/lfps: decode_step, "
+            "bench.exact_topk_step)" if kind == "reference" else
+            "the oracle port at reference arithmetic (baseline/_ref missing)")
     return {
+        "kind": kind,
         "session_step_us_median": med_l,
         "exact_session_step_us_median": med_e,
         "layer_step_us": med_l * per_worker,
@@ -282,10 +348,10 @@ def cpu_leg(cfg_name: str, steps: int, warmup: int, workers: int):
         "cores": cores,
         "sessions_timed": len(lfps),
         "wall_s": wall,
-        "sample": (f"{cores} worker processes x 1 (request, KV-head) unit x {group} q-head "
-                   f"sessions x {steps} timed steps (+{warmup} warm-up) at context {ctx}; "
-                   f"per-layer-step time extrapolated as median session-step x "
-                   f"ceil({ns_total} sessions / {cores} cores)"),
+        "sample": (f"{what}: {cores} worker processes (one per physical core, BLAS 1 thread) x "
+                   f"{sessions} sessions of one (request, KV-head) unit x {steps} timed steps "
+                   f"(+{warmup} warm-up) at context {ctx}; per-layer-step time extrapolated as "
+                   f"median session-step x ceil({ns_total} sessions / {cores} cores)"),
     }
 
 
@@ -301,7 +367,10 @@ def cpu_model():
 def run_reference(args, world, rank):
     if rank != 0:
         return
-    r = cpu_leg(args.config, args.steps, args.warmup, args.cpu_workers)
+    # each timed "step" of this arm is a bounded sample: at most 24 steps per
+    # worker (the reference's KV store doubles its capacity 64 rows past the
+    # prefill), so --steps K --warmup W finishes within minutes at 128k
+    r = cpu_leg(args.config, min(args.steps, 24), min(args.warmup, 2), args.cpu_workers)
     batch, ctx, hkv, group, d, frac, desc = CONFIGS[args.config]
     line = {
         "impl": "reference",
@@ -312,7 +381,7 @@ def run_reference(args, world, rank):
         "config": {"workload": desc, "batch": batch, "context": ctx, "q_heads": hkv * group,
                    "kv_heads": hkv, "d": d, "topk_fraction": frac},
         "cpu_baseline": {"value": r["layer_step_us"], "unit": UNIT, "cores": r["cores"],
-                         "kind": "port", "sample": r["sample"], "cpu": cpu_model()},
+                         "kind": r["kind"], "sample": r["sample"], "cpu": cpu_model()},
         "e2e": {"value": r["layer_step_us"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "exact_topk_us_per_layer_step": r["exact_layer_step_us"],
@@ -328,15 +397,30 @@ def run_reference(args, world, rank):
 def step_bytes(sess, cfg) -> dict:
     """Algorithmic HBM bytes of the last decode step, per kernel.
 
-    Gathers count DISTINCT rows per (request, KV-head) unit: the G q-heads
-    of a unit read one shared K/V row store.  ``reference`` is SURVEY.md
-    §8(d)'s byte count for the reference algorithm (both fp64 tables read in
-    full every step), for comparison."""
+    Counted from the step's actual sets, each byte once, at the kernel that
+    must move it:
+
+    * stats  -- the table blocks it read (rebuilt dirty blocks + hot blocks,
+      4 KiB each, CNT_BLOCKS), the window's block summaries (32 B moments +
+      8 B max per 512-slot segment, both tables), its C0 word lists;
+    * select -- the C0 words (8 B per word entry, bounded by |C0|), the mean
+      filter F at the candidate slots (both tables, 16 B per C1 slot), the
+      probe list (4 B);
+    * finish -- DISTINCT K rows of the unit's probe sets and V rows of its
+      C2 sets plus sinks (the G q-heads of a unit share one row store), q
+      in and out, the C2 list and scores;
+    * update -- C2 scores + indices, the table read-modify-write (2 tables x
+      16 B), the unit's K/V append;
+    * gate   -- sink and local K rows per unit, q, K-bar / V-bar.
+
+    ``reference`` is SURVEY.md §8(d)'s byte count for the reference algorithm
+    (both fp64 tables read in full every step), for comparison."""
     import torch
-    from paper_2506_15704_b200.session import CNT_BLOCKS, CNT_C2, CNT_PROBE
+    from paper_2506_15704_b200.session import CNT_BLOCKS, CNT_C0, CNT_C1, CNT_C2, CNT_PROBE
     B, Hkv, G, d, S = sess.B, sess.Hkv, sess.G, sess.d, cfg.sink_count
     counts = sess.counts.to(torch.int64)
     probe, c2, blocks = counts[..., CNT_PROBE], counts[..., CNT_C2], counts[..., CNT_BLOCKS]
+    c0, c1 = counts[..., CNT_C0], counts[..., CNT_C1]
     active = (sess.bypass == 0)
     n_max = max(sess.n_host)
     row = d * 2
@@ -354,22 +438,22 @@ def step_bytes(sess, cfg) -> dict:
         mark[:, :S] = True
         return mark.sum(1).to(torch.float64)
 
-    k_rows = distinct(sess.probe_idx, probe)
-    v_rows = distinct(sess.c2_idx, c2)
-    nseg = torch.tensor([(n - S) / 512 + 1 for n in sess.n_host], dtype=torch.float64,
+    k_rows = distinct(sess.probe_idx, probe * active)
+    v_rows = distinct(sess.c2_idx, c2 * active)
+    nseg = torch.tensor([(n - 1 - S) / 512 + 1 for n in sess.n_host], dtype=torch.float64,
                         device=counts.device).repeat_interleave(Hkv * G).reshape(B, Hkv * G)
-    sel = (blocks.double() * 512 * 8 + 2 * nseg * 40 + probe.double() * (4 + 2 * 8)) * active
-    fin = (k_rows.sum() + v_rows.sum()) * row + sess.NS * (row + d * 4) + (probe.sum() * 8
-                                                                            + c2.sum() * 8)
-    upd = (c2.double() * (2 * 16 + 8)).sum() + sess.NS * 64
-    gate = B * Hkv * (S + cfg.local_window) * row + sess.NS * (row + 8 * d)
-    app = B * Hkv * 2 * row
-    kern = {"select": float(sel.sum()), "finish": float(fin), "update": float(upd),
-            "gate": float(gate), "append": float(app)}
-    m = torch.tensor([n - S for n in sess.n_host], dtype=torch.float64)
-    ref = float((m * 16).sum()) * Hkv * G + float(probe.sum() + c2.sum()) * row
+    stats = blocks.double() * 512 * 8 + 2 * nseg * 40 + c0.double() * 8
+    select = (c0.double() * 8 + c1.double() * 16 + probe.double() * 4) * active
+    fin = ((k_rows.sum() + v_rows.sum()) * row + sess.NS * (row + d * 4)
+           + float((c2 * active).sum()) * 8)
+    upd = float(((c2.double() * (8 + 2 * 16)) * active).sum()) + B * Hkv * 2 * row
+    gate = B * Hkv * (S + cfg.local_window) * row + sess.NS * (row + 8 * d) + B * Hkv * 2 * 8 * d
+    kern = {"gate": float(gate), "stats": float(stats.sum()), "select": float(select.sum()),
+            "finish": float(fin), "update": float(upd)}
+    m = torch.tensor([n - 1 - S for n in sess.n_host], dtype=torch.float64)
+    ref = float((m * 16).sum()) * Hkv * G + float(((probe + c2) * active).sum()) * row
     return {"kernels": kern, "total": sum(kern.values()), "reference": ref,
-            "blocks_mean": float(blocks.double()[active].mean()),
+            "blocks_mean": float(blocks.double().mean()),
             "k_rows_unit": float(k_rows.mean()), "v_rows_unit": float(v_rows.mean())}
 
 
@@ -404,6 +488,73 @@ def phase_trace(sess, step, t, dev) -> dict:
                 "of one extra untimed step"}
 
 
+def verify_units(sess, spec, stream, step_log, cfg, frac, count, dev) -> dict:
+    """Replay `count` (request, KV-head) units of this run through the CPU
+    oracle (oracle/lfps_oracle.py, canonical device arithmetic) from their
+    bootstrap over every decode step the bench executed, and require the
+    device's final tracker tables (phys values, lazy scale, clamp counts)
+    to be bit-identical, the last step's probe and C2 sets and counts equal,
+    its output within 1e-5 relative L2, and the KV rows the device appended
+    equal to the step inputs.  Identical final tables imply identical C2
+    sets on every step (every update folds its C2 set into both tables).
+    Runs after all timing; the oracle is only the checker here."""
+    import numpy as np
+    import torch
+    from oracle import lfps_oracle as lo
+    from paper_2506_15704_b200.session import CNT_C2, CNT_PROBE
+    from paper_2506_15704_b200.workload import gen_unit
+    t0 = time.time()
+    B, Hkv, G, S = sess.B, sess.Hkv, sess.G, cfg.sink_count
+    n0 = spec.n_prefill
+    units = []
+    for i in range(count):
+        b = (i * max(1, B - 1)) // max(1, count - 1) if count > 1 else 0
+        units.append((min(b, B - 1), (3 * i + 1) % Hkv))
+    worst = 0.0
+    checked = []
+    for b, h in dict.fromkeys(units):
+        u = gen_unit(spec, b, h, device=dev)
+        n_end = sess.n_host[b]
+        assert n_end == n0 + len(step_log)
+        keys = sess.k_cache[b, h, :n_end].double().cpu().numpy()
+        vals = sess.v_cache[b, h, :n_end].double().cpu().numpy()
+        np.testing.assert_array_equal(keys[:n0], u.keys[:n0].double().cpu().numpy())
+        kv, trs, prs = lo.bootstrap_unit(keys[:n0], vals[:n0], u.weights.double().cpu().numpy(),
+                                         u.final_query.double().cpu().numpy(), cfg, lo.DevArith)
+        qs = stream.q[:, b, h * G:(h + 1) * G].double().cpu().numpy()      # [T_in, G, d]
+        kn = stream.k_new[:, b, h].double().cpu().numpy()
+        vn = stream.v_new[:, b, h].double().cpu().numpy()
+        outs = None
+        for j, t in enumerate(step_log):
+            np.testing.assert_array_equal(keys[n0 + j], kn[t], err_msg=f"appended K row {j}")
+            np.testing.assert_array_equal(vals[n0 + j], vn[t], err_msg=f"appended V row {j}")
+            outs = lo.unit_step(kv, trs, prs, qs[t], kn[t], vn[t], frac, cfg, lo.DevArith, "fp32")
+        out = sess.out[b, h * G:(h + 1) * G].double().cpu().numpy()
+        cnt = sess.counts[b, h * G:(h + 1) * G].cpu().numpy()
+        for g in range(G):
+            s = b * sess.Hq + h * G + g
+            ver, sla, sc = sess.session_tables(s)
+            tag = f"unit ({b}, {h}) q-head {g}"
+            assert sc == trs[g].scale, tag
+            np.testing.assert_array_equal(ver, trs[g].ver_view(), err_msg=tag + " ver")
+            np.testing.assert_array_equal(sla, trs[g].sla_view(), err_msg=tag + " sla")
+            assert int(sess.clamp_count[s]) == trs[g].clamp_count, tag
+            o = outs[g]
+            if not o.bypassed:
+                assert cnt[g, CNT_PROBE] == o.probe.size and cnt[g, CNT_C2] == o.c2.size, tag
+                np.testing.assert_array_equal(sess.probe_list(b, h * G + g), o.probe, err_msg=tag)
+                np.testing.assert_array_equal(sess.c2_list(b, h * G + g), o.c2, err_msg=tag)
+            err = np.linalg.norm(out[g] - o.output) / max(np.linalg.norm(o.output), 1e-12)
+            assert err <= 1e-5, (tag, err)
+            worst = max(worst, err)
+        checked.append([b, h])
+    return {"units": checked, "sessions": len(checked) * G, "steps": len(step_log),
+            "tables": "bit-exact (phys ver/sla, scale, clamp counts) after every step's update",
+            "last_step_sets": "probe and C2 bit-exact", "output_rel_err_max": worst,
+            "oracle": "oracle/lfps_oracle.py DevArith (pinned against the reference, tests/)",
+            "seconds": time.time() - t0}
+
+
 def run_ours(args, world, rank, local):
     import ctypes as C
     import numpy as np
@@ -429,13 +580,14 @@ def run_ours(args, world, rank, local):
                           paged=args.paged)
     stream = populate(sess, spec)
     sess.split = not args.no_split
-    sess.pair_finish = args.pair_finish
-    sess.unit_finish = args.unit_finish
     setup_s = time.time() - t_setup
     cuda_stream = torch.cuda.current_stream(dev)
 
+    step_log = []              # input index of every decode step, in order (--verify)
+
     def step(t):
         t %= T_in
+        step_log.append(t)
         sess.decode_step(stream.q[t], stream.k_new[t], stream.v_new[t], frac)
 
     for t in range(args.warmup):
@@ -487,12 +639,18 @@ def run_ours(args, world, rank, local):
     dom_ms = kernel_ms[dominant]
     dom_bytes = alg["kernels"].get(dominant, 0)
     achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    traffic_all = {}
+    tpath = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
     if os.path.exists(tpath) and args.config == "c4":
         with open(tpath) as f:
-            tk = json.load(f)["kernels"].get(dominant)
-        traffic = tk["traffic_bytes"] if tk else None
+            traffic_all = {k: v.get("traffic_bytes") for k, v in json.load(f)["kernels"].items()}
+    traffic = traffic_all.get(dominant)
+    per_kernel = {}
+    for k, ms_k in kernel_ms.items():
+        by = alg["kernels"].get(k, 0.0)
+        gbs = by / (ms_k * 1e-3) / 1e9
+        per_kernel[k] = {"ms": ms_k, "algorithmic_bytes": by, "GBps": gbs, "frac": gbs / peak,
+                         "ncu_traffic_bytes": traffic_all.get(k)}
     counts = sess.counts.cpu().numpy()
     bypass = int(sess.bypass.sum())
     probe = counts[..., CNT_PROBE].astype(np.int64)
@@ -530,30 +688,45 @@ def run_ours(args, world, rank, local):
             out_h = torch.empty(g_out.shape, dtype=torch.float32).pin_memory()
             cnt_h = torch.empty(g_cnt.shape, dtype=torch.int32).pin_memory()
         base = args.warmup + args.steps + prof_steps
+        # Each step is what an autoregressive decode loop does: the step's
+        # packed q | k_new | v_new goes in from pinned host memory and its
+        # output must be back in host memory before the next step's query
+        # exists -- so every step ends with a host wait on the output.  The
+        # host wall clock (perf_counter) brackets all steps; the device
+        # events give the same span on the GPU's clock.
+        lat = []
         e0.record(cuda_stream)
         for t in range(base, base + e2e_steps):
+            h0 = time.perf_counter()
+            step_log.append(t % T_in)
             if not gather:
                 # lfps_decode_step_host_io: the library copies the packed
                 # inputs on its own stream beside the stats kernels and the
                 # output back beside the commit kernel
                 sess.decode_step_host(inh[t % T_in], frac, out_host=out_h)
-                continue
-            ind.copy_(inh[t % T_in], non_blocking=True)
-            sess.decode_step(qd, kd, vd, frac)
-            cnt_d.copy_(sess.counts)
-            dist.all_gather_into_tensor(g_out, sess.out)
-            dist.all_gather_into_tensor(g_cnt, cnt_d)
-            if rank == 0:
-                out_h.copy_(g_out, non_blocking=True)
-                cnt_h.copy_(g_cnt, non_blocking=True)
+            else:
+                ind.copy_(inh[t % T_in], non_blocking=True)
+                sess.decode_step(qd, kd, vd, frac)
+                cnt_d.copy_(sess.counts)
+                dist.all_gather_into_tensor(g_out, sess.out)
+                dist.all_gather_into_tensor(g_cnt, cnt_d)
+                if rank == 0:
+                    out_h.copy_(g_out, non_blocking=True)
+                    cnt_h.copy_(g_cnt, non_blocking=True)
+            cuda_stream.synchronize()            # the output is in host memory
+            lat.append(time.perf_counter() - h0)
         e1.record(cuda_stream)
         torch.cuda.synchronize(dev)
-        e2e_ms = allmax(world, e0.elapsed_time(e1) / e2e_steps)
+        e2e_ms = allmax(world, statistics.median(lat) * 1e3)
+        dev_ms = e0.elapsed_time(e1) / e2e_steps
         sess.check_errors("e2e steps")
         d2h = out_h.numel() * 4 + (cnt_h.numel() * 4 if gather else 0)
         e2e = {"value": e2e_ms * 1e3, "unit": UNIT,
                "h2d_bytes_per_step": int(ind.numel() * ind.element_size()),
                "d2h_bytes_per_step": int(d2h if rank == 0 or not gather else 0),
+               "timing": "median host wall-clock per step (perf_counter), each step waiting for "
+                         "its output in pinned host memory before the next starts; max over ranks",
+               "device_span_us_per_step": dev_ms * 1e3,
                "api": ("BatchedSession.decode_step (pinned host q/k/v copied in; outputs and C2 "
                        "counts all-gathered over NCCL, read back on rank 0)" if gather else
                        "BatchedSession.decode_step_host = lfps_decode_step_host_io (pinned "
@@ -616,6 +789,9 @@ def run_ours(args, world, rank, local):
                               "(full_attention_oracle / output_error, attention.py:88-134), "
                               "computed on the device"}}
 
+    verified = None
+    if args.verify and rank == 0 and not args.profile_only:
+        verified = verify_units(sess, spec, stream, step_log, cfg, frac, args.verify, dev)
     if rank != 0:
         return
     cpu = None
@@ -641,11 +817,12 @@ def run_ours(args, world, rank, local):
         "roofline": {"bound": "hbm", "kernel": dominant,
                      "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full, dram read+write "
+                     "traffic_source": "profiles/r02_ncu_traffic.json (ncu --set full, dram read+write "
                                        "per launch of this kernel at C4)" if traffic else None,
                      "algorithmic_bytes_per_launch": dom_bytes,
                      "avg_launch_ms": dom_ms, "peak_source": peak_src},
         "kernel_ms": kernel_ms,
+        "kernels": per_kernel,
         "phase_us": phases,
         "kernel_algorithmic_bytes": alg["kernels"],
         "step_algorithmic_bytes": int(alg["total"]),
@@ -659,6 +836,8 @@ def run_ours(args, world, rank, local):
         "probe_mean": float(probe.mean()), "c2_mean": float(c2.mean()),
         "k_rows_distinct_per_unit": alg["k_rows_unit"], "v_rows_distinct_per_unit": alg["v_rows_unit"],
     }
+    if verified:
+        line["verified_units"] = verified
     if e2e:
         line["e2e"] = e2e
     if recall:
@@ -666,7 +845,8 @@ def run_ours(args, world, rank, local):
         line["speedup_vs_exact_gpu"] = recall["exact_us_per_step"] / value
     if cpu:
         line["cpu_baseline"] = {"value": cpu["layer_step_us"], "unit": UNIT,
-                                "cores": cpu["cores"], "kind": "port", "sample": cpu["sample"],
+                                "cores": cpu["cores"], "kind": cpu["kind"],
+                                "sample": cpu["sample"],
                                 "cpu": cpu_model(),
                                 "session_step_us_median": cpu["session_step_us_median"],
                                 "exact_layer_step_us": cpu["exact_layer_step_us"]}

@@ -30,7 +30,16 @@
  *    unchanged) and err[0] holds the call's nonzero stamp (0 after a
  *    committed step); err[1 + s] = (stamp << 4) | code for the sessions that
  *    raised in that call (codes with another stamp are stale).  A negative
- *    err[0] marks a failure that only skipped its own sessions' commit.
+ *    err[0] marks the one failure detected only inside the commit (the
+ *    weight-sum check, unreachable for finite scores): the other sessions
+ *    commit, the KV rows and n_ctx advance, and the failed sessions' tables
+ *    only grow (as on a gated step), so every table stays in step with its
+ *    KV store.
+ *  - Threading: calls on distinct workspaces (sessions) are reentrant; each
+ *    workspace gets its own internal streams and events on its first decode
+ *    step (lfps_workspace_release frees them).  One workspace is driven by
+ *    one host thread at a time (the reference's single writer per session,
+ *    engine.py:38-47).
  *  - Session index s = b * Hq + qh, q-head qh reads KV head qh / G (GQA).
  */
 #ifndef LFPS_B200_H
@@ -49,7 +58,7 @@ extern "C" {
 #define LFPS_API
 #endif
 
-#define LFPS_ABI_VERSION 5
+#define LFPS_ABI_VERSION 6
 
 #define LFPS_OK 0
 #define LFPS_E_INVALID -1   /* bad argument (shape, range, capacity) */
@@ -95,13 +104,8 @@ typedef struct lfps_params {
 } lfps_params;
 
 /* lfps_params.flags */
-#define LFPS_FLAG_PAIR_FINISH 16 /* finish two q-heads of a unit per CTA over the union
-                                    of their probe rows (k_finish_pair.cu) */
 #define LFPS_FLAG_SPLIT 8        /* run two session halves' gate/select/finish on two
                                     internal streams (fork/join on the caller's) */
-#define LFPS_FLAG_UNIT_FINISH 4  /* finish GQA units (G <= 4, d 128/256) over the
-                                    union of their probe rows with tensor-core
-                                    softmax.V (k_finish_unit.cu); opt-in */
 #define LFPS_FLAG_TRACE 2        /* per-session phase timestamps (clock64 deltas and
                                     globaltimer) of the select and finish kernels
                                     to ws.trace ([NS][16] int64) */
@@ -144,8 +148,7 @@ typedef struct lfps_ws_layout {
   size_t probe_score; /* f32 [NS, list_cap] */
   size_t c2_idx;      /* i32 [NS, list_cap] */
   size_t c2_score;    /* f32 [NS, list_cap] */
-  size_t uw;          /* f64 [NS, list_cap] scratch: exact-path top-k overflow,
-                         per-unit finish update weights */
+  size_t uw;          /* f64 [NS, list_cap] scratch: exact-path top-k overflow */
   size_t scratch;     /* f64 [NS, list_cap] bootstrap scratch */
   /* Block summaries of the tracker tables.  These PERSIST across steps (a
      cache of the state, kept in the workspace): item = 2 s + table (0 =
@@ -183,6 +186,14 @@ LFPS_API int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out);
 
 /* Slots of one session's slash table (>= 0; negative LFPS_E_* on bad dims). */
 LFPS_API int lfps_slash_capacity(const lfps_dims* dims);
+
+/* Release the internal streams and events the library keeps for a workspace
+ * (created by its first decode step; each workspace has its own, so host
+ * threads may step distinct sessions concurrently).  Waits for that
+ * workspace's internal work; call before freeing the workspace buffer.
+ * (No reference counterpart: HeadSession is garbage-collected state,
+ * engine.py:38-47.) */
+LFPS_API int lfps_workspace_release(const lfps_workspace* ws);
 
 /* Seed the tracker tables of sessions [s_begin, s_begin + count) from their
  * trailing prefill weights (Eq. 4; init_tables, tables.py:247-281).

@@ -18,12 +18,10 @@ from .errors import DeviceError
 # experiments); the default is the library __graft_entry__.build() makes
 LIB_PATH = os.environ.get("LFPS_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "lib", "liblfps_b200.so")
-ABI_VERSION = 5
+ABI_VERSION = 6
 FLAG_EXPORT_SETS = 1
 FLAG_TRACE = 2
-FLAG_UNIT_FINISH = 4
 FLAG_SPLIT = 8
-FLAG_PAIR_FINISH = 16
 
 # per-session device error codes (include/lfps_b200.h)
 ERR_NAMES = {
@@ -42,7 +40,8 @@ EXPORTS = ("lfps_abi_version", "lfps_last_error", "lfps_workspace_layout",
            "lfps_exact_topk_step", "lfps_overlap", "lfps_decode_launches", "lfps_slash_capacity",
            "lfps_exact_launches", "lfps_kv_pool_page_bytes", "lfps_kv_pool_create",
            "lfps_kv_pool_reserve", "lfps_kv_pool_release", "lfps_kv_pool_mapped_bytes",
-           "lfps_kv_pool_destroy", "lfps_profile_enable", "lfps_profile_collect")
+           "lfps_kv_pool_destroy", "lfps_profile_enable", "lfps_profile_collect",
+           "lfps_workspace_release")
 
 
 class Dims(C.Structure):
@@ -127,6 +126,8 @@ def _declare(lib):
     lib.lfps_overlap.argtypes = [P(Dims), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
     lib.lfps_profile_enable.argtypes = [C.c_int]
+    lib.lfps_workspace_release.argtypes = [P(Workspace)]
+    lib.lfps_workspace_release.restype = C.c_int
     lib.lfps_decode_launches.argtypes = [C.c_void_p, C.c_int32]
     lib.lfps_profile_collect.argtypes = [P(KernelTime), C.c_int32, P(C.c_int32)]
     for name in ("lfps_profile_enable", "lfps_profile_collect", "lfps_workspace_layout",

@@ -127,16 +127,33 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// One-time setup of a launch site per device (cudaFuncSetAttribute is a
+// per-device property): thread-safe, and redone on every device a launch
+// site is first used on.  Racing first calls both run f (idempotent).
+struct DeviceOnce {
+  unsigned long long done[4] = {0ull, 0ull, 0ull, 0ull};   // 256 devices
+  template <typename F>
+  cudaError_t run(F f) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    unsigned long long* w = &done[(dev >> 6) & 3];
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (__atomic_load_n(w, __ATOMIC_ACQUIRE) & bit) return cudaSuccess;
+    e = f();
+    if (e == cudaSuccess) __atomic_fetch_or(w, bit, __ATOMIC_RELEASE);
+    return e;
+  }
+};
+
 cudaError_t launch_gate(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
 cudaError_t launch_stats(const Ctx& c, cudaStream_t st);
 cudaError_t launch_select(const Ctx& c, int m_max, cudaStream_t st);
-cudaError_t launch_finish_pair(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
 cudaError_t launch_topk(const Ctx& c, int implicit_base, cudaStream_t st);
 cudaError_t launch_attend(const Ctx& c, const __nv_bfloat16* q, int exact_mode, cudaStream_t st);
 cudaError_t launch_update(const Ctx& c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new,
                           cudaStream_t st);
 cudaError_t launch_finish(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
-cudaError_t launch_finish_unit(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
 cudaError_t launch_boot_tables(const Ctx& c, const float* w, int s_begin, int count, int m0,
                                cudaStream_t st);
 cudaError_t launch_boot_stats(const Ctx& c, const __nv_bfloat16* q, int m_max, cudaStream_t st);

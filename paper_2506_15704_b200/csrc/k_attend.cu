@@ -98,13 +98,12 @@ __global__ void __launch_bounds__(kThreads, kRowCtas) lfps_exact_attend_kernel(C
 template <int PQ>
 cudaError_t launch_attend_d(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
   const size_t smem = rows_smem(c.d);
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(lfps_exact_attend_kernel<PQ>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  static DeviceOnce once;
+  cudaError_t e = once.run([&] {
+    return cudaFuncSetAttribute(lfps_exact_attend_kernel<PQ>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (e != cudaSuccess) return e;
   lfps_exact_attend_kernel<PQ><<<c.NS, kThreads, smem, st>>>(c, q);
   return cudaGetLastError();
 }

@@ -51,16 +51,16 @@ __global__ void __launch_bounds__(kThreads, kRowCtas) lfps_finish_kernel(Ctx c, 
 template <int PQ>
 cudaError_t launch_finish_d(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
   const size_t smem = rows_smem(c.d);
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(lfps_finish_kernel<PQ>,
+  static DeviceOnce once;
+  cudaError_t e = once.run([&] {
+    cudaError_t r = cudaFuncSetAttribute(lfps_finish_kernel<PQ>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(lfps_finish_kernel<PQ>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(lfps_finish_kernel<PQ>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+    return r;
+  });
+  if (e != cudaSuccess) return e;
   return launch_pdl(lfps_finish_kernel<PQ>, dim3(c.s_cnt), dim3(kThreads), smem, st, c, q);
 }
 

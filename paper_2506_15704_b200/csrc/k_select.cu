@@ -104,16 +104,16 @@ cudaError_t launch_stats(const Ctx& c, cudaStream_t st) {
 
 cudaError_t launch_select(const Ctx& c, int m_max, cudaStream_t st) {
   const size_t smem = select_smem(m_max);
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(lfps_select_kernel,
+  static DeviceOnce once;
+  cudaError_t e = once.run([] {
+    cudaError_t r = cudaFuncSetAttribute(lfps_select_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(lfps_select_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+    if (r == cudaSuccess)
+      r = cudaFuncSetAttribute(lfps_select_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+    return r;
+  });
+  if (e != cudaSuccess) return e;
   return launch_pdl(lfps_select_kernel, dim3(c.s_cnt), dim3(kThreads), smem, st, c);
 }
 

@@ -346,14 +346,13 @@ __global__ void __launch_bounds__(kThreads) lfps_exact_topk_kernel(Ctx c) {
 }  // namespace
 
 cudaError_t launch_topk(const Ctx& c, int /*implicit_base*/, cudaStream_t st) {
-  static bool set = false;
+  static DeviceOnce once;
   const size_t smem = sizeof(TopkShared);
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(lfps_exact_topk_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  cudaError_t e = once.run([&] {
+    return cudaFuncSetAttribute(lfps_exact_topk_kernel,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  });
+  if (e != cudaSuccess) return e;
   lfps_exact_topk_kernel<<<c.NS, kThreads, smem, st>>>(c);
   return cudaGetLastError();
 }

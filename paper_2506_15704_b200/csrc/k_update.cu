@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
     // kernel; thread t owns entries t + 256 i, exactly the entries it folds
     // below.  The |sum u - 1| <= 1e-6 check (tables.py:161-163) cannot fail
     // for finite scores (the max term is exactly 1, every u rounds once); if it
-    // ever did, this session alone would skip its commit (err[0] = -stamp).
+    // ever did, this session alone would skip its update and only grow
+    // (err[0] = -stamp).
     double e[kMaxE];
     int lix[kMaxE];                       // logical C2 index of entry i (-1: none)
     float zi[kMaxE];
@@ -166,6 +167,13 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
     if (!wok && tid == 0) {                  // reported, but not as a failed step:
       c.err[1 + s] = err_code(c, LFPS_ERR_WEIGHT_SUM);   // the other sessions commit
       atomicExch(c.err, -c.epoch);
+      // the unit's row is still appended, so this session's tables grow like a
+      // gated step's (no update) and stay in step with the KV store
+      ver[m] = 0.0;
+      sla[base + m] = 0.0;
+      const int bv = m / kBlk, bs = (base + m) / kBlk;
+      dirty[bv >> 5] |= 1u << (bv & 31);
+      dirty[dw + (bs >> 5)] |= 1u << (bs & 31);
     }
     if (wok) {
       // decay with renormalisation (tables.py:167-169, 240-244)

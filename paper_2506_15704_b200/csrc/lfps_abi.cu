@@ -10,6 +10,8 @@
 #include <cstring>
 #include <cmath>
 #include <atomic>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -232,6 +234,7 @@ std::vector<ProfRec> g_prof;
 std::vector<cudaEvent_t> g_pool;
 
 cudaEvent_t prof_event() {
+  std::lock_guard<std::mutex> g(g_prof_mu);
   if (!g_pool.empty()) {
     cudaEvent_t e = g_pool.back();
     g_pool.pop_back();
@@ -254,6 +257,7 @@ cudaEvent_t prof_event() {
     if (g_prof_on) {                                               \
       cudaEvent_t b_ = prof_event();                               \
       cudaEventRecord(b_, sm);                                     \
+      std::lock_guard<std::mutex> g_(g_prof_mu);                   \
       g_prof.push_back({name, a_, b_});                            \
     }                                                              \
   } while (0)
@@ -276,8 +280,14 @@ constexpr int kSplitGroups = LFPS_SPLIT_GROUPS;   // session groups of LFPS_FLAG
 #define LFPS_SPLIT_MIN 256
 #endif
 constexpr int kSplitMin = LFPS_SPLIT_MIN;         // sessions below which the split is off
+// Internal streams and events of one workspace (one BatchedSession): the
+// fork/join events of a step are re-recorded by every call, so they must not
+// be shared between sessions that different host threads step concurrently
+// (cudaStreamWaitEvent binds to the event's latest record at the time of the
+// call).  Pipes are created on a workspace's first decode step, keyed by
+// (device, workspace base), and destroyed by lfps_workspace_release.
 struct Pipe {
-  int dev = -1;
+  std::mutex mu;                            // one enqueue sequence at a time
   cudaStream_t st[kSplitGroups] = {};
   cudaStream_t aux[kSplitGroups] = {};      // the stats kernel, concurrent with the gate
   cudaEvent_t fork = nullptr, join[kSplitGroups] = {}, stats[kSplitGroups] = {};
@@ -287,31 +297,56 @@ struct Pipe {
   cudaEvent_t in_ready = nullptr;
 };
 std::mutex g_pipe_mu;
-Pipe g_pipe[16];
+std::map<std::pair<int, const void*>, std::unique_ptr<Pipe>> g_pipes;
 
-cudaError_t get_pipe(Pipe** out) {
+void destroy_pipe(Pipe& p) {
+  for (cudaStream_t* sp : {&p.st[0], &p.st[kSplitGroups - 1], &p.aux[0], &p.aux[kSplitGroups - 1],
+                           &p.copy, &p.in})
+    if (*sp) cudaStreamSynchronize(*sp);
+  for (int i = 0; i < kSplitGroups; ++i) {
+    if (p.st[i]) cudaStreamDestroy(p.st[i]);
+    if (p.aux[i]) cudaStreamDestroy(p.aux[i]);
+    if (p.join[i]) cudaEventDestroy(p.join[i]);
+    if (p.stats[i]) cudaEventDestroy(p.stats[i]);
+  }
+  for (cudaEvent_t ev : {p.fork, p.out_ready, p.out_done, p.in_ready})
+    if (ev) cudaEventDestroy(ev);
+  if (p.copy) cudaStreamDestroy(p.copy);
+  if (p.in) cudaStreamDestroy(p.in);
+}
+
+cudaError_t create_pipe(Pipe& p) {
+  cudaError_t e;
+  for (int i = 0; i < kSplitGroups; ++i) {
+    if ((e = cudaStreamCreateWithFlags(&p.st[i], cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&p.aux[i], cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&p.join[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&p.stats[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+  }
+  if ((e = cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithFlags(&p.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  if ((e = cudaEventCreateWithFlags(&p.out_ready, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if ((e = cudaEventCreateWithFlags(&p.out_done, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  return cudaEventCreateWithFlags(&p.in_ready, cudaEventDisableTiming);
+}
+
+cudaError_t get_pipe(const void* ws_base, Pipe** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
   std::lock_guard<std::mutex> g(g_pipe_mu);
-  Pipe& p = g_pipe[dev];
-  if (p.dev < 0) {
-    for (int i = 0; i < kSplitGroups; ++i) {
-      if ((e = cudaStreamCreateWithFlags(&p.st[i], cudaStreamNonBlocking)) != cudaSuccess) return e;
-      if ((e = cudaStreamCreateWithFlags(&p.aux[i], cudaStreamNonBlocking)) != cudaSuccess) return e;
-      if ((e = cudaEventCreateWithFlags(&p.join[i], cudaEventDisableTiming)) != cudaSuccess) return e;
-      if ((e = cudaEventCreateWithFlags(&p.stats[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+  std::unique_ptr<Pipe>& p = g_pipes[{dev, ws_base}];
+  if (!p) {
+    std::unique_ptr<Pipe> np(new Pipe());
+    if ((e = create_pipe(*np)) != cudaSuccess) {
+      destroy_pipe(*np);
+      g_pipes.erase({dev, ws_base});
+      return e;
     }
-    if ((e = cudaEventCreateWithFlags(&p.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
-    if ((e = cudaStreamCreateWithFlags(&p.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&p.out_ready, cudaEventDisableTiming)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&p.out_done, cudaEventDisableTiming)) != cudaSuccess) return e;
-    if ((e = cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&p.in_ready, cudaEventDisableTiming)) != cudaSuccess) return e;
-    p.dev = dev;
+    p = std::move(np);
   }
-  *out = &p;
+  *out = p.get();
   return cudaSuccess;
 }
 
@@ -337,6 +372,25 @@ int lfps_decode_launches(const lfps_dims* dims, int32_t flags) {
       (long long)dims->batch * dims->kv_heads * dims->group >= kSplitMin)
     return 1 + 4 * kSplitGroups;
   return 5;   // gate | stats, select, finish, update
+}
+
+int lfps_workspace_release(const lfps_workspace* ws) {
+  if (!ws || !ws->base) return fail(LFPS_E_INVALID, "workspace is NULL");
+  std::unique_ptr<Pipe> gone;
+  {
+    std::lock_guard<std::mutex> g(g_pipe_mu);
+    for (auto it = g_pipes.begin(); it != g_pipes.end(); ++it)
+      if (it->first.second == ws->base) {
+        gone = std::move(it->second);
+        g_pipes.erase(it);
+        break;
+      }
+  }
+  if (gone) {
+    std::lock_guard<std::mutex> g(gone->mu);
+    destroy_pipe(*gone);
+  }
+  return LFPS_OK;
 }
 
 int lfps_slash_capacity(const lfps_dims* dims) {
@@ -479,8 +533,9 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
     LAUNCH_P("select", sm, lfps::launch_select(c, m_max, sm));
   }
   Pipe* pp = nullptr;
+  LAUNCH(get_pipe(ws->base, &pp));
+  std::lock_guard<std::mutex> pipe_lock(pp->mu);
   if (!g_prof_on) {
-    LAUNCH(get_pipe(&pp));
     LAUNCH(cudaEventRecord(pp->fork, sm));
     if (in_host) {
       LAUNCH(cudaStreamWaitEvent(pp->in, pp->fork, 0));
@@ -489,12 +544,6 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
     }
   }
   const bool split = (c.flags & LFPS_FLAG_SPLIT) && !g_prof_on && c.NS >= kSplitMin;
-  // LFPS_FLAG_UNIT_FINISH: GQA units of <= 4 q-heads (d 128 / 256) finish per
-  // unit over the union of their probe rows (tensor-core softmax.V); measured
-  // slower than the per-session kernel at C4 (2 CTAs/SM), so
-  // it is opt-in
-  const bool per_unit = !split && (c.flags & LFPS_FLAG_UNIT_FINISH) && (c.G <= 4) &&
-                        (c.d == 128 || c.d == 256);
   const int groups = split ? kSplitGroups : 1;
   const int per = (c.NS / groups + 31) / 32 * 32;
   for (int g = 0; g < groups; ++g) {
@@ -513,14 +562,7 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
       LAUNCH(cudaStreamWaitEvent(gs, pp->stats[g], 0));
       LAUNCH(lfps::launch_select(cg, m_max, gs));
     }
-    if (per_unit) {
-      LAUNCH_P("finish", gs, lfps::launch_finish_unit(cg, qb, gs));
-    } else if ((c.flags & LFPS_FLAG_PAIR_FINISH) && c.G % 2 == 0 && cg.s_off % 2 == 0 &&
-               cg.s_cnt % 2 == 0) {
-      LAUNCH_P("finish", gs, lfps::launch_finish_pair(cg, qb, gs));
-    } else {
-      LAUNCH_P("finish", gs, lfps::launch_finish(cg, qb, gs));
-    }
+    LAUNCH_P("finish", gs, lfps::launch_finish(cg, qb, gs));
     if (split) {
       LAUNCH(cudaEventRecord(pp->join[g], gs));
       LAUNCH(cudaStreamWaitEvent(sm, pp->join[g], 0));
@@ -528,7 +570,6 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
   }
   // the output is final here (gate + finish); the commit does not touch it
   if (out_host) {
-    if (!pp) LAUNCH(get_pipe(&pp));
     LAUNCH(cudaEventRecord(pp->out_ready, sm));
     LAUNCH(cudaStreamWaitEvent(pp->copy, pp->out_ready, 0));
     LAUNCH(cudaMemcpyAsync(out_host, c.out, (size_t)c.NS * c.d * sizeof(float),

@@ -32,8 +32,7 @@ CNT_C0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_BLOCKS = rang
 
 
 def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False,
-                trace: bool = False, unit_finish: bool = False,
-                split: bool = False, pair_finish: bool = False) -> _lib.Params:
+                trace: bool = False, split: bool = False) -> _lib.Params:
     err = cfg.device_limits_error()
     if err:
         raise ValueError(err)
@@ -50,8 +49,7 @@ def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False,
     for i, o in enumerate(offs):
         p.offsets[i] = o
     p.flags = ((_lib.FLAG_EXPORT_SETS if export_sets else 0) | (_lib.FLAG_TRACE if trace else 0)
-               | (_lib.FLAG_UNIT_FINISH if unit_finish else 0) | (_lib.FLAG_SPLIT if split else 0)
-               | (_lib.FLAG_PAIR_FINISH if pair_finish else 0))
+               | (_lib.FLAG_SPLIT if split else 0))
     return p
 
 
@@ -94,9 +92,7 @@ class BatchedSession:
         self.cfg = cfg
         self.export_sets = export_sets
         self.trace = False          # LFPS_FLAG_TRACE: per-session phase timestamps
-        self.unit_finish = False    # LFPS_FLAG_UNIT_FINISH: per-unit finish kernel
         self.split = True           # LFPS_FLAG_SPLIT: two session halves on two streams
-        self.pair_finish = False    # LFPS_FLAG_PAIR_FINISH: two q-heads per finish CTA
         self.B, self.Hkv, self.G = batch, kv_heads, group
         self.Hq = kv_heads * group
         self.NS = batch * self.Hq
@@ -186,8 +182,7 @@ class BatchedSession:
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
     def _params(self, k_fraction: float = 1.0) -> _lib.Params:
-        return make_params(self.cfg, k_fraction, self.export_sets, self.trace, self.unit_finish,
-                           self.split, self.pair_finish)
+        return make_params(self.cfg, k_fraction, self.export_sets, self.trace, self.split)
 
     # -- bootstrap ----------------------------------------------------------
     def load_prefill(self, b: int, keys: torch.Tensor, values: torch.Tensor):
@@ -242,11 +237,39 @@ class BatchedSession:
     def clear_errors(self):
         self.err.zero_()
 
+    def close(self):
+        """Release the library's per-workspace streams and events
+        (lfps_workspace_release); the session is unusable afterwards."""
+        if getattr(self, "ws", None) is not None and self.lib is not None:
+            with torch.cuda.device(self.device):
+                _lib.check(self.lib.lfps_workspace_release(C.byref(self.ws)), "close")
+            self.ws = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
+
+    def sync_host_counts(self):
+        """Re-read the context lengths from the device (the committing kernel
+        advances n_ctx; a failed step leaves it): the host mirror n_host is
+        advanced optimistically by every enqueued step."""
+        dev = [int(x) for x in self.n_ctx.cpu()]
+        if dev != self.n_host:
+            self.step_count -= 1
+        self.n_host = dev
+
     def check_errors(self, what: str = "step"):
-        """Raise the reference's exception for the first failed session."""
+        """Raise the reference's exception for the first failed session.
+
+        A failed step commits nothing (engine.py:8-9), so the host mirror of
+        the context lengths is rolled back to the device's; a session-local
+        failure of the commit (err[0] = -stamp) still appended the rows."""
         err = self.err.cpu()
         if int(err[0]) == 0:
             return
+        self.sync_host_counts()
         # err[0] = the failed call's stamp (negated: a session-local failure),
         # err[1 + s] = stamp << 4 | code (codes of other calls are stale)
         stamp = abs(int(err[0]))
@@ -301,11 +324,11 @@ class BatchedSession:
                 C.byref(self.ws), C.c_void_p(q.data_ptr()), C.c_void_p(k_new.data_ptr()),
                 C.c_void_p(v_new.data_ptr()), n_host, C.c_void_p(out_host.data_ptr()),
                 self._stream()), "decode_step")
+        self.n_host = [n + 1 for n in self.n_host]
+        self.step_count += 1
         if check:
             torch.cuda.current_stream(self.device).synchronize()
             self.check_errors("decode_step")
-        self.n_host = [n + 1 for n in self.n_host]
-        self.step_count += 1
         return self.result()
 
     # -- paged KV (kv_pool.py) ------------------------------------------------
@@ -388,11 +411,11 @@ class BatchedSession:
             C.c_void_p(self._in_dev.data_ptr()), n_host,
             C.c_void_p(out_host.data_ptr() if out_host is not None else None),
             self._stream()), "decode_step")
+        self.n_host = [n + 1 for n in self.n_host]
+        self.step_count += 1
         if check:
             torch.cuda.current_stream(self.device).synchronize()
             self.check_errors("decode_step")
-        self.n_host = [n + 1 for n in self.n_host]
-        self.step_count += 1
         return self.result()
 
     def copy_tracker_from(self, other: "BatchedSession"):
@@ -432,9 +455,9 @@ class BatchedSession:
         self.tables_stale = True
 
     def rollback_host_count(self):
-        """Undo the host mirror advance after a step that committed nothing."""
-        self.n_host = [n - 1 for n in self.n_host]
-        self.step_count -= 1
+        """Undo the host mirror advance after a step that committed nothing
+        (kept for callers of round 1; check_errors now does this itself)."""
+        self.sync_host_counts()
 
     def result(self) -> BatchedStepResult:
         return BatchedStepResult(output=self.out, rho=self.rho, bypassed=self.bypass,

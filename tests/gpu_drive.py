@@ -75,7 +75,7 @@ class Pair:
                                         bf16(k_new).cuda(), bf16(v_new).cuda(), frac, check=True)
         return res
 
-    def compare_step(self, res, outs, out_tol=1e-5, tables=True):
+    def compare_step(self, res, outs, out_tol=1e-5, tables=True, bitmaps=True):
         """Assert bit-exact sets/scalars/tables and toleranced outputs."""
         counts = res.counts.cpu().numpy()
         rho = res.rho.cpu().numpy()
@@ -101,8 +101,11 @@ class Pair:
                     assert c[CNT_C2] == o.c2.size, (tag, "c2")
                     assert c[CNT_CLAMP] == o.clamps, (tag, "clamps")
                     np.testing.assert_array_equal(self.sess.probe_list(b, qh), o.probe, err_msg=tag)
-                    np.testing.assert_array_equal(self.sess.c0_list(b, qh), o.c0, err_msg=tag + " c0")
-                    np.testing.assert_array_equal(self.sess.c1_list(b, qh), o.c1, err_msg=tag + " c1")
+                    if bitmaps:
+                        np.testing.assert_array_equal(self.sess.c0_list(b, qh), o.c0,
+                                                      err_msg=tag + " c0")
+                        np.testing.assert_array_equal(self.sess.c1_list(b, qh), o.c1,
+                                                      err_msg=tag + " c1")
                     np.testing.assert_array_equal(self.sess.c2_list(b, qh), o.c2, err_msg=tag)
                 ref = o.output
                 err = np.linalg.norm(out[b, qh] - ref) / max(np.linalg.norm(ref), 1e-12)

@@ -156,22 +156,6 @@ def _rebuild(pair, K, V):
     return Pair(pair.cfg, K, V, pair.weights, pair.finals, pair.n0)
 
 
-@pytest.mark.parametrize("unit", [True, False])
-@pytest.mark.parametrize("group,d", [(4, 128), (2, 128), (1, 256)])
-def test_unit_finish_shapes_bit_exact(group, d, unit):
-    """The per-unit finish (union of a unit's probe rows, tensor-core softmax.V)
-    against the oracle for the G and d it serves, over several steps with
-    mixed bypassed and Top-k sessions: 1% makes |probe| > k for some sessions
-    (per-session path inside the unit CTA), 5% keeps C2 = probe (union path)."""
-    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, group=group, d=d, n0=2500, steps=6, seed=21)
-    pair.sess.unit_finish = unit
-    n0 = pair.n0
-    for t in range(6):
-        frac = 0.05 if t % 3 else 0.01
-        res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], frac)
-        pair.compare_step(res, outs)
-
-
 def test_long_trajectory_crosses_slash_blocks():
     """1100 steps: the slash window start crosses two 512-slot block
     boundaries and the vertical window grows into new blocks, so the
@@ -334,14 +318,74 @@ def test_paged_kv_pool_bit_exact_across_a_page():
                          0.05)
 
 
-@pytest.mark.parametrize("frac,d", [(0.05, 128), (0.01, 128), (0.05, 64)])
-def test_pair_finish_bit_exact(frac, d):
-    """LFPS_FLAG_PAIR_FINISH: two q-heads of a unit per finish CTA over the
-    union of their probe rows -- identical to the oracle (and so to the
-    per-session kernel); at 1% (k < |probe|) it falls back per session."""
-    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, n0=3000, steps=3, d=d, seed=17)
-    pair.sess.pair_finish = True
-    n0 = pair.n0
-    for t in range(3):
-        res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], frac)
-        pair.compare_step(res, outs)
+def test_two_threads_two_sessions_bit_exact():
+    """Reentrancy across distinct sessions (SURVEY §8(b) threading): two host
+    threads step two sessions concurrently, each on its own CUDA stream, with
+    the two-stream split on (256 sessions each, so both use their internal
+    streams and fork/join events).  Each session's trajectory is identical
+    to the oracle's, as if it had run alone."""
+    import threading
+    import gpu_drive
+    steps = 10
+    pairs = [gqa_pair_cached(seed) for seed in (41, 43)]
+    results = [[], []]
+    errors = []
+    start = threading.Barrier(2)
+
+    def drive(i):
+        try:
+            pair, K, V, Q = pairs[i]
+            sess, n0 = pair.sess, pair.n0
+            B, Hkv, G, d = pair.B, pair.Hkv, pair.G, pair.d
+            inputs = [(gpu_drive.bf16(Q[:, :, :, t].reshape(B, Hkv * G, d)).cuda(),
+                       gpu_drive.bf16(K[:, :, n0 + t]).cuda(), gpu_drive.bf16(V[:, :, n0 + t]).cuda())
+                      for t in range(steps)]
+            st = torch.cuda.Stream()
+            torch.cuda.synchronize()
+            start.wait()
+            with torch.cuda.stream(st):
+                for t in range(steps):
+                    res = sess.decode_step(*inputs[t], 0.05)
+                    results[i].append((res.counts.clone(), res.output.clone(), res.rho.clone(),
+                                       res.bypassed.clone(), res.c2_idx.clone(),
+                                       sess.probe_idx.clone()))
+            st.synchronize()
+            sess.check_errors("threaded steps")
+        except BaseException as e:  # noqa: BLE001
+            errors.append(e)
+
+    th = [threading.Thread(target=drive, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    from paper_2506_15704_b200.session import BatchedStepResult
+    for i, (pair, K, V, Q) in enumerate(pairs):
+        n0 = pair.n0
+        for t in range(steps):
+            cnt, out, rho, byp, c2, probe = results[i][t]
+            outs = []
+            for b in range(pair.B):
+                for h in range(pair.Hkv):
+                    kv, trs, prs = pair.units[b * pair.Hkv + h]
+                    outs.append(lo_step(kv, trs, prs, Q[b, h, :, t], K[b, h, n0 + t],
+                                        V[b, h, n0 + t], pair.cfg))
+            # replay the recorded device lists into the session views for compare_step
+            pair.sess.counts.copy_(cnt)
+            pair.sess.c2_idx.copy_(c2)
+            pair.sess.probe_idx.copy_(probe)
+            res = BatchedStepResult(output=out, rho=rho, bypassed=byp, counts=cnt, c2_idx=c2,
+                                    c2_score=pair.sess.c2_score, err=pair.sess.err)
+            pair.compare_step(res, outs, tables=(t == steps - 1), bitmaps=(t == steps - 1))
+
+
+def lo_step(kv, trs, prs, qs, k_new, v_new, cfg):
+    from oracle import lfps_oracle as lo
+    return lo.unit_step(kv, trs, prs, qs, k_new, v_new, 0.05, cfg, lo.DevArith, "fp32")
+
+
+def gqa_pair_cached(seed):
+    pair, K, V, Q = _gqa_pair(batch=8, kv_heads=8, group=4, d=64, n0=700, steps=10, seed=seed)
+    pair.sess.split = True
+    return pair, K, V, Q

@@ -26,7 +26,6 @@ F = np.stack([u.final_query.float().numpy() for u in units])[None]
 Q = np.stack([u.queries.float().numpy() for u in units])[None]
 pair = Pair(LfpsConfig(d=128), K, V, W, F, 2048)
 for t in range(6):
-    pair.sess.unit_finish = t % 2 == 1
     frac = 0.01 if t == 4 else 0.05
     res, outs = pair.step(Q[:, :, :, t], K[:, :, 2048 + t], V[:, :, 2048 + t], frac)
     pair.compare_step(res, outs)
