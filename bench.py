@@ -65,8 +65,8 @@ def parse():
                     help="disable LFPS_FLAG_SPLIT (two session halves on two streams)")
     ap.add_argument("--paged", action="store_true",
                     help="K/V in a KvPool (2 MiB pages mapped as contexts grow; kv_pool.py)")
-    ap.add_argument("--gather", action="store_true",
-                    help="N > 1: all-gather each e2e step's outputs and C2 counts to rank 0 (NCCL)")
+    ap.add_argument("--no-gather", action="store_true",
+                    help="N > 1: skip the final all-gather of outputs and C2 counts in e2e")
     ap.add_argument("--verify", type=int, default=2,
                     help="after the run, replay this many (request, KV-head) units of rank 0 "
                          "through the CPU oracle and require bit-exact tables and sets")
@@ -562,23 +562,34 @@ def run_ours(args, world, rank, local):
     from paper_2506_15704_b200 import _lib
     from paper_2506_15704_b200.config import LfpsConfig
     from paper_2506_15704_b200.session import CNT_BLOCKS, CNT_C2, CNT_PROBE, BatchedSession
-    from paper_2506_15704_b200.workload import GqaSpec, populate
+    from paper_2506_15704_b200.sharded import ShardedSession, populate_sharded
+    from paper_2506_15704_b200.workload import GqaSpec, StepStream
 
     batch, ctx, hkv, group, d, frac, desc = CONFIGS[args.config]
-    b_local, b0 = shard_requests(batch, world, rank)
     e2e_steps = 0 if args.profile_only else args.steps
     recall_steps = 0 if args.profile_only else args.recall_steps
     prof_steps = min(args.steps, 8)
-    T = args.warmup + args.steps + prof_steps + 1 + e2e_steps + recall_steps
+    gather_steps = args.steps if world > 1 and not args.profile_only else 0
+    T = args.warmup + args.steps + gather_steps + prof_steps + 1 + e2e_steps + recall_steps
     T_in = min(T, 64)          # distinct synthetic step inputs, cycled
     cfg = LfpsConfig(d=d)
-    spec = GqaSpec(batch=b_local, kv_heads=hkv, group=group, d=d, n_prefill=ctx, steps=T_in,
-                   seed=42 + 7919 * b0)
+    # one spec for the whole batch: every unit is generated from its own seed,
+    # so the union of the ranks' units is exactly the single-GPU workload
+    spec = GqaSpec(batch=batch, kv_heads=hkv, group=group, d=d, n_prefill=ctx, steps=T_in,
+                   seed=42)
     dev = torch.device("cuda", torch.cuda.current_device())
     t_setup = time.time()
-    sess = BatchedSession(cfg, b_local, hkv, group, n_max=ctx + T + 8, device=dev,
-                          paged=args.paged)
-    stream = populate(sess, spec)
+    # (request, KV-head) units partitioned over the ranks (sharded.plan_shards:
+    # requests when B >= P, KV heads when B < P); no collective on the path
+    ss = ShardedSession(cfg, batch, hkv, group, n_max=ctx + T + 8, rank=rank, world=world,
+                        device=dev, paged=args.paged)
+    sess = ss.sess
+    b_local = ss.shard.nb
+    full = populate_sharded(ss, spec)
+    stream = StepStream(q=torch.stack([ss.local_q(x) for x in full.q]),
+                        k_new=torch.stack([ss.local_kv(x) for x in full.k_new]),
+                        v_new=torch.stack([ss.local_kv(x) for x in full.v_new]))
+    del full
     sess.split = not args.no_split
     setup_s = time.time() - t_setup
     cuda_stream = torch.cuda.current_stream(dev)
@@ -620,8 +631,25 @@ def run_ours(args, world, rank, local):
     sess.check_errors("timed steps")
     ms = allmax(world, ms_local)
 
+    # ---- N > 1: the same steps, each followed by the final all-gather of the
+    # batch's outputs and C2 counts (ShardedSession.gather), device-timed ----
+    gather_ms = None
+    if gather_steps:
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        barrier(world)
+        torch.cuda.synchronize(dev)
+        g0.record(cuda_stream)
+        for t in range(args.warmup + args.steps, args.warmup + args.steps + gather_steps):
+            step(t)
+            ss.gather(with_c2=False)
+        g1.record(cuda_stream)
+        torch.cuda.synchronize(dev)
+        barrier(world)
+        gather_ms = allmax(world, g0.elapsed_time(g1) / gather_steps)
+
     # ---- per-kernel CUDA events on the launch stream (separate pass) ----
-    prof_base = args.warmup + args.steps
+    prof_base = args.warmup + args.steps + gather_steps
     _lib.profile_enable(True)
     for t in range(prof_base, prof_base + prof_steps):
         step(t)
@@ -675,19 +703,14 @@ def run_ours(args, world, rank, local):
         torch.cuda.synchronize(dev)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        # --gather (N > 1): every step ends with an NCCL all-gather of the
-        # batch's outputs and C2 counts (equal shards), read back on rank 0 --
-        # the north star's final gather, after the decode path.  Opt-in: it
-        # has not been run on more than one GPU yet.
-        gather = args.gather and world > 1 and dist_backend() == "nccl"
+        # N > 1: every step ends with the north star's final gather, after
+        # the decode path: the batch's outputs and C2 counts all-gathered
+        # (ShardedSession.gather) and read back on rank 0
+        gather = not args.no_gather and world > 1
         if gather:
-            import torch.distributed as dist
-            cnt_d = torch.empty(sess.counts.shape, dtype=torch.int32, device=dev)
-            g_out = torch.empty((world,) + tuple(sess.out.shape), dtype=torch.float32, device=dev)
-            g_cnt = torch.empty((world,) + tuple(sess.counts.shape), dtype=torch.int32, device=dev)
-            out_h = torch.empty(g_out.shape, dtype=torch.float32).pin_memory()
-            cnt_h = torch.empty(g_cnt.shape, dtype=torch.int32).pin_memory()
-        base = args.warmup + args.steps + prof_steps
+            out_h = torch.empty(batch, hkv * group, d, dtype=torch.float32).pin_memory()
+            cnt_h = torch.empty(batch, hkv * group, dtype=torch.int32).pin_memory()
+        base = args.warmup + args.steps + gather_steps + prof_steps
         # Each step is what an autoregressive decode loop does: the step's
         # packed q | k_new | v_new goes in from pinned host memory and its
         # output must be back in host memory before the next step's query
@@ -705,11 +728,8 @@ def run_ours(args, world, rank, local):
                 # output back beside the commit kernel
                 sess.decode_step_host(inh[t % T_in], frac, out_host=out_h)
             else:
-                ind.copy_(inh[t % T_in], non_blocking=True)
-                sess.decode_step(qd, kd, vd, frac)
-                cnt_d.copy_(sess.counts)
-                dist.all_gather_into_tensor(g_out, sess.out)
-                dist.all_gather_into_tensor(g_cnt, cnt_d)
+                sess.decode_step_host(inh[t % T_in], frac)
+                g_out, g_cnt, _ = ss.gather(with_c2=False)
                 if rank == 0:
                     out_h.copy_(g_out, non_blocking=True)
                     cnt_h.copy_(g_cnt, non_blocking=True)
@@ -727,8 +747,9 @@ def run_ours(args, world, rank, local):
                "timing": "median host wall-clock per step (perf_counter), each step waiting for "
                          "its output in pinned host memory before the next starts; max over ranks",
                "device_span_us_per_step": dev_ms * 1e3,
-               "api": ("BatchedSession.decode_step (pinned host q/k/v copied in; outputs and C2 "
-                       "counts all-gathered over NCCL, read back on rank 0)" if gather else
+               "api": ("ShardedSession: BatchedSession.decode_step_host on each rank's shard "
+                       "(pinned host q|k_new|v_new in), then ShardedSession.gather: outputs and "
+                       "C2 counts all-gathered, read back on rank 0" if gather else
                        "BatchedSession.decode_step_host = lfps_decode_step_host_io (pinned "
                        "packed q|k_new|v_new in, copied by the call beside the stats kernels; "
                        "the output copied to pinned host memory beside the commit kernel)")}
@@ -740,7 +761,7 @@ def run_ours(args, world, rank, local):
         exact_kernel_ms = {}
         sess.exact_topk_step(stream.q[0], frac)        # warm-up (module load); read-only
         torch.cuda.synchronize(dev)
-        base = args.warmup + args.steps + prof_steps + e2e_steps
+        base = args.warmup + args.steps + gather_steps + prof_steps + e2e_steps
         for t in range(base, base + recall_steps):
             torch.cuda.synchronize(dev)
             a = torch.cuda.Event(enable_timing=True)
@@ -805,9 +826,14 @@ def run_ours(args, world, rank, local):
         "dtype": "f64", "dtypes": "fp64 tracker tables + gate, fp32 scores/softmax, bf16 K/V/q",
         "data": "synthetic (planted vertical bands + slash offsets; torch restatement of "
                 "the reference generator synth.py)",
-        "config": {"workload": desc, "batch": batch, "batch_per_gpu": b_local, "context": ctx,
+        "config": {"workload": desc, "batch": batch, "batch_per_gpu": b_local,
+                   "shard_rank0": {"requests": [ss.shard.b0, ss.shard.nb],
+                                   "kv_heads": [ss.shard.h0, ss.shard.nh]},
+                   "context": ctx,
                    "q_heads": hkv * group, "kv_heads": hkv, "d": d, "topk_fraction": frac,
-                   "sharding": "requests across ranks, no collective on the decode path",
+                   "sharding": ("(request, KV-head) units over ranks (sharded.plan_shards: requests "
+                                "when B >= P, KV heads when B < P), no collective on the decode "
+                                "path"),
                    "l2": "flushed before every timed step (512 MiB write); each step timed "
                          "by its own CUDA events",
                    "kv": ("paged (KvPool, %d MiB mapped)" % (sess.kv_mapped_bytes() >> 20)
@@ -838,6 +864,10 @@ def run_ours(args, world, rank, local):
     }
     if verified:
         line["verified_units"] = verified
+    if gather_ms is not None:
+        line["step_with_gather_us"] = gather_ms * 1e3
+        line["gather_note"] = ("device time per step incl. the all-gather of outputs [B, Hq, d] "
+                               "and C2 counts over %s (value excludes it)" % dist_backend())
     if e2e:
         line["e2e"] = e2e
     if recall:
