@@ -312,6 +312,75 @@ LFPS_API int lfps_kv_pool_release(lfps_kv_pool* pool, int32_t b);
 LFPS_API int64_t lfps_kv_pool_mapped_bytes(const lfps_kv_pool* pool);
 LFPS_API int lfps_kv_pool_destroy(lfps_kv_pool* pool);
 
+/* ---- Per-head stage API (k_stages.cu) ---------------------------------
+ * The reference also exposes each stage of the decode step on its own, on
+ * one head's float64 state (pkg/src/lfps/__init__.py:13-58).  These entry
+ * points are those stages on the device at the reference's precision: fp64
+ * K/V rows [n, d] (any d >= 1), fp64 tables, fp64 logits and softmax.  All
+ * arrays are device pointers; indices are int64 absolute positions unless
+ * stated; sets are sorted and unique.  One kernel launch each, on `stream`;
+ * argument checks on the host before the launch.  Data errors the reference
+ * raises are returned in a device int (*err) with the per-session codes
+ * above (LFPS_ERR_*). */
+
+/* row_logits (numerics.py:33-49): out[i] = keys[rows[i]] . q / sqrt(d);
+ * rows NULL = rows 0 .. nrows-1. */
+LFPS_API int lfps_stage_logits(const double* keys, int32_t d, const int64_t* rows, int32_t nrows,
+                               const double* q, double* out, void* stream);
+/* compute_thresholds (tables.py:295-317), or thresholds_oracle (:320-331)
+ * with materialize = 1, of ver[0, m) and sla[0, m) (phys values; sla points
+ * at logical slot 0) at lazy scale `scale`: out[7] = tau_v, mean_v, deg_v,
+ * tau_s, mean_s, deg_s, then 3 if kappa == 0 (ZeroDivisionError) else
+ * untouched.  scratch: 4096 doubles.  2 <= m <= 262144. */
+LFPS_API int lfps_stage_thresholds(const double* ver, const double* sla, int32_t m, double scale,
+                                   double a, int32_t materialize, double* out, double* scratch,
+                                   void* stream);
+/* Candidate stages (candidates.py:45-100) with thresholds thr[6] laid out
+ * as above: mode 0 select_initial (in_idx unused), 1 expand (in_idx = C0,
+ * offsets[n_off]), 2 finalize_probe_set (in_idx = C1; n, sink, window).
+ * out_idx: capacity m (modes 0, 1) or n (mode 2); *out_count on device. */
+LFPS_API int lfps_stage_candidates(int32_t mode, const double* ver, const double* sla, int32_t m,
+                                   double scale, const double* thr, const int64_t* in_idx,
+                                   int32_t n_in, const int32_t* offsets, int32_t n_off,
+                                   int64_t base_index, int32_t n, int32_t sink, int32_t window,
+                                   int64_t* out_idx, int32_t* out_count, void* stream);
+/* topk_from_scores (attention.py:34-47): Top-k of (idx ascending, scores)
+ * with lower-index ties; all of idx when k >= p. */
+LFPS_API int lfps_stage_topk(const int64_t* idx, const double* scores, int32_t p, int32_t k,
+                             int64_t* out_idx, int32_t* out_count, void* stream);
+/* attention_output (attention.py:66-85) over the rows idx[nidx] (sorted;
+ * NULL = all rows 0 .. nidx-1, full_attention_oracle :88-97): out[d] and
+ * the softmax weights[nidx]. */
+LFPS_API int lfps_stage_attend(const double* keys, const double* values, int32_t d,
+                               const int64_t* idx, int32_t nidx, const double* q, double* out,
+                               double* weights, int32_t* err, void* stream);
+/* ScoreTablePair.update (tables.py:144-200) after the host's checks (sum of
+ * weights, index range): rf != 0 renormalises by rf first; then the slash
+ * shift (slot base - 1 zeroed) and the residual fold at sel (logical) with
+ * the new lazy scale `scale`; *clamps = entries clamped.  tmp: k doubles. */
+LFPS_API int lfps_stage_update(double* ver, double* sla, int32_t base, int32_t m,
+                               const int64_t* sel, const double* weights, int32_t k, double rf,
+                               double scale, int64_t* clamps, double* tmp, void* stream);
+/* ScoreTablePair.grow (tables.py:202-220). */
+LFPS_API int lfps_stage_grow(double* ver, double* sla, int32_t base, int32_t m, int32_t carry,
+                             void* stream);
+/* init_tables (tables.py:247-281): w [s, m] -> ver[m], sla[m] (logical). */
+LFPS_API int lfps_stage_init_tables(const double* w, int32_t s, int32_t m, double r, double* ver,
+                                    double* sla, void* stream);
+/* compute_head_stats (gate.py:51-74): mean_key[d], mean_value[d], *sigma;
+ * tmp: n doubles. */
+LFPS_API int lfps_stage_head_stats(const double* keys, const double* values, int32_t n, int32_t d,
+                                   int32_t sink, const double* q, double* mean_key,
+                                   double* mean_value, double* sigma, double* tmp, int32_t* err,
+                                   void* stream);
+/* gate_logits + sparsity_from_logits + bypass_output (gate.py:77-147):
+ * out = [sink logits S | local logits L | gexp | w_sink | w_global |
+ * w_local | rho | bypass output d]. */
+LFPS_API int lfps_stage_gate(const double* keys, const double* values, int32_t n, int32_t d,
+                             int32_t sink, int32_t window, const double* q,
+                             const double* mean_key, const double* mean_value, double sigma,
+                             int32_t bypass_mode, double* out, int32_t* err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

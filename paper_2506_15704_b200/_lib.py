@@ -41,7 +41,10 @@ EXPORTS = ("lfps_abi_version", "lfps_last_error", "lfps_workspace_layout",
            "lfps_exact_launches", "lfps_kv_pool_page_bytes", "lfps_kv_pool_create",
            "lfps_kv_pool_reserve", "lfps_kv_pool_release", "lfps_kv_pool_mapped_bytes",
            "lfps_kv_pool_destroy", "lfps_profile_enable", "lfps_profile_collect",
-           "lfps_workspace_release")
+           "lfps_workspace_release", "lfps_stage_logits", "lfps_stage_thresholds",
+           "lfps_stage_candidates", "lfps_stage_topk", "lfps_stage_attend", "lfps_stage_update",
+           "lfps_stage_grow", "lfps_stage_init_tables", "lfps_stage_head_stats",
+           "lfps_stage_gate")
 
 
 class Dims(C.Structure):
@@ -128,6 +131,24 @@ def _declare(lib):
     lib.lfps_profile_enable.argtypes = [C.c_int]
     lib.lfps_workspace_release.argtypes = [P(Workspace)]
     lib.lfps_workspace_release.restype = C.c_int
+    # per-head stage API (k_stages.cu): device pointers as c_void_p
+    V, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    stage = {
+        "lfps_stage_logits": [V, I32, V, I32, V, V, V],
+        "lfps_stage_thresholds": [V, V, I32, D, D, I32, V, V, V],
+        "lfps_stage_candidates": [I32, V, V, I32, D, V, V, I32, V, I32, I64, I32, I32, I32, V, V,
+                                  V],
+        "lfps_stage_topk": [V, V, I32, I32, V, V, V],
+        "lfps_stage_attend": [V, V, I32, V, I32, V, V, V, V, V],
+        "lfps_stage_update": [V, V, I32, I32, V, V, I32, D, D, V, V, V],
+        "lfps_stage_grow": [V, V, I32, I32, I32, V],
+        "lfps_stage_init_tables": [V, I32, I32, D, V, V, V],
+        "lfps_stage_head_stats": [V, V, I32, I32, I32, V, V, V, V, V, V, V],
+        "lfps_stage_gate": [V, V, I32, I32, I32, I32, V, V, V, D, I32, V, V, V],
+    }
+    for name, args in stage.items():
+        getattr(lib, name).argtypes = args
+        getattr(lib, name).restype = C.c_int
     lib.lfps_decode_launches.argtypes = [C.c_void_p, C.c_int32]
     lib.lfps_profile_collect.argtypes = [P(KernelTime), C.c_int32, P(C.c_int32)]
     for name in ("lfps_profile_enable", "lfps_profile_collect", "lfps_workspace_layout",

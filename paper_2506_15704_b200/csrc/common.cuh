@@ -163,4 +163,31 @@ cudaError_t launch_overlap(const Ctx& c, const int* sel, const int* sel_cnt, con
                            cudaStream_t st);
 cudaError_t launch_clear_err(const Ctx& c, cudaStream_t st);
 
+// per-head stage API (k_stages.cu), fp64
+cudaError_t stage_logits(const double* keys, int d, const int64_t* rows, int nrows, const double* q,
+                         double* out, cudaStream_t st);
+cudaError_t stage_thresholds(const double* ver, const double* sla, int m, double scale, double a,
+                             int materialize, double* out, double* scratch, cudaStream_t st);
+cudaError_t stage_candidates(int mode, const double* ver, const double* sla, int m, double scale,
+                             const double* thr, const int64_t* in_idx, int n_in, const int* offsets,
+                             int n_off, long long base_index, int n, int sink, int window,
+                             int64_t* out_idx, int* out_count, cudaStream_t st);
+cudaError_t stage_topk(const int64_t* idx, const double* scores, int p, int k, int64_t* out_idx,
+                       int* out_count, cudaStream_t st);
+cudaError_t stage_attend(const double* keys, const double* values, int d, const int64_t* idx,
+                         int nidx, const double* q, double* out, double* weights, int* err,
+                         cudaStream_t st);
+cudaError_t stage_update(double* ver, double* sla, int base, int m, const int64_t* sel,
+                         const double* w, int k, double rf, double scale, long long* clamps,
+                         double* tmp, cudaStream_t st);
+cudaError_t stage_grow(double* ver, double* sla, int base, int m, int carry, cudaStream_t st);
+cudaError_t stage_init_tables(const double* w, int s, int m, double r, double* ver, double* sla,
+                              cudaStream_t st);
+cudaError_t stage_head_stats(const double* keys, const double* values, int n, int d, int sink,
+                             const double* q, double* mean_key, double* mean_value, double* sigma,
+                             double* logit_tmp, int* err, cudaStream_t st);
+cudaError_t stage_gate(const double* keys, const double* values, int n, int d, int sink, int window,
+                       const double* q, const double* mean_key, const double* mean_value,
+                       double sigma, int bypass_mode, double* out, int* err, cudaStream_t st);
+
 }  // namespace lfps

@@ -601,6 +601,106 @@ int lfps_exact_topk_step(const lfps_dims* dims, const lfps_params* p, const lfps
   return LFPS_OK;
 }
 
+// ---- per-head stage API (k_stages.cu) -------------------------------------
+#define STREAM(s) static_cast<cudaStream_t>(s)
+
+int lfps_stage_logits(const double* keys, int32_t d, const int64_t* rows, int32_t nrows,
+                      const double* q, double* out, void* stream) {
+  if (!keys || !q || !out || d < 1 || nrows < 0) return fail(LFPS_E_INVALID, "stage_logits: bad arguments");
+  if (nrows == 0) return LFPS_OK;
+  LAUNCH(lfps::stage_logits(keys, d, rows, nrows, q, out, STREAM(stream)));
+  return LFPS_OK;
+}
+
+int lfps_stage_thresholds(const double* ver, const double* sla, int32_t m, double scale, double a,
+                          int32_t materialize, double* out, double* scratch, void* stream) {
+  if (!ver || !sla || !out || !scratch) return fail(LFPS_E_INVALID, "stage_thresholds: NULL argument");
+  if (m < 2) return fail(LFPS_E_INVALID, "thresholds require at least 2 table slots");
+  if (m > 512 * lfps::kBlk)   // tables.cuh kLeaves segments
+    return fail(LFPS_E_UNSUPPORTED, "stage_thresholds: m <= %d", 512 * lfps::kBlk);
+  LAUNCH(lfps::stage_thresholds(ver, sla, m, scale, a, materialize, out, scratch, STREAM(stream)));
+  return LFPS_OK;
+}
+
+int lfps_stage_candidates(int32_t mode, const double* ver, const double* sla, int32_t m,
+                          double scale, const double* thr, const int64_t* in_idx, int32_t n_in,
+                          const int32_t* offsets, int32_t n_off, int64_t base_index, int32_t n,
+                          int32_t sink, int32_t window, int64_t* out_idx, int32_t* out_count,
+                          void* stream) {
+  if (mode < 0 || mode > 2 || !out_idx || !out_count) return fail(LFPS_E_INVALID, "stage_candidates: bad arguments");
+  if (mode != 2 && (!ver || !sla || !thr || m < 0)) return fail(LFPS_E_INVALID, "stage_candidates: tables");
+  if (mode != 0 && n_in > 0 && !in_idx) return fail(LFPS_E_INVALID, "stage_candidates: in_idx");
+  if (mode == 1 && (!offsets || n_off < 1)) return fail(LFPS_E_INVALID, "stage_candidates: offsets");
+  const long long U = mode == 2 ? n : m;
+  if (U < 0 || (U + 31) / 32 * 4 > 200 * 1024) return fail(LFPS_E_UNSUPPORTED, "stage_candidates: universe too large");
+  LAUNCH(lfps::stage_candidates(mode, ver, sla, m, scale, thr, in_idx, n_in, offsets, n_off, base_index,
+                                n, sink, window, out_idx, out_count, STREAM(stream)));
+  return LFPS_OK;
+}
+
+int lfps_stage_topk(const int64_t* idx, const double* scores, int32_t p, int32_t k, int64_t* out_idx,
+                    int32_t* out_count, void* stream) {
+  if (!idx || !scores || !out_idx || !out_count || p < 1 || k < 1) return fail(LFPS_E_INVALID, "stage_topk: bad arguments");
+  LAUNCH(lfps::stage_topk(idx, scores, p, k, out_idx, out_count, STREAM(stream)));
+  return LFPS_OK;
+}
+
+int lfps_stage_attend(const double* keys, const double* values, int32_t d, const int64_t* idx,
+                      int32_t nidx, const double* q, double* out, double* weights, int32_t* err,
+                      void* stream) {
+  if (!keys || !values || !q || !out || !weights || !err || d < 1 || nidx < 1)
+    return fail(LFPS_E_INVALID, "stage_attend: bad arguments");
+  LAUNCH(lfps::stage_attend(keys, values, d, idx, nidx, q, out, weights, err, STREAM(stream)));
+  return LFPS_OK;
+}
+
+int lfps_stage_update(double* ver, double* sla, int32_t base, int32_t m, const int64_t* sel,
+                      const double* weights, int32_t k, double rf, double scale, int64_t* clamps,
+                      double* tmp, void* stream) {
+  if (!ver || !sla || !sel || !weights || !clamps || !tmp || k < 1 || base < 1 || m < 0)
+    return fail(LFPS_E_INVALID, "stage_update: bad arguments");
+  LAUNCH(lfps::stage_update(ver, sla, base, m, sel, weights, k, rf, scale,
+                            reinterpret_cast<long long*>(clamps), tmp, STREAM(stream)));
+  return LFPS_OK;
+}
+
+int lfps_stage_grow(double* ver, double* sla, int32_t base, int32_t m, int32_t carry, void* stream) {
+  if (!ver || !sla || m < 0 || base < 0) return fail(LFPS_E_INVALID, "stage_grow: bad arguments");
+  LAUNCH(lfps::stage_grow(ver, sla, base, m, carry, STREAM(stream)));
+  return LFPS_OK;
+}
+
+int lfps_stage_init_tables(const double* w, int32_t s, int32_t m, double r, double* ver, double* sla,
+                           void* stream) {
+  if (!w || !ver || !sla || s < 1 || m < 1) return fail(LFPS_E_INVALID, "stage_init_tables: bad arguments");
+  LAUNCH(lfps::stage_init_tables(w, s, m, r, ver, sla, STREAM(stream)));
+  return LFPS_OK;
+}
+
+int lfps_stage_head_stats(const double* keys, const double* values, int32_t n, int32_t d, int32_t sink,
+                          const double* q, double* mean_key, double* mean_value, double* sigma,
+                          double* tmp, int32_t* err, void* stream) {
+  if (!keys || !values || !q || !mean_key || !mean_value || !sigma || !tmp || !err || d < 1)
+    return fail(LFPS_E_INVALID, "stage_head_stats: bad arguments");
+  if (n <= sink + 1) return fail(LFPS_E_INVALID, "need more than sink_count + 1 = %d rows, have %d", sink + 1, n);
+  LAUNCH(lfps::stage_head_stats(keys, values, n, d, sink, q, mean_key, mean_value, sigma, tmp, err,
+                                STREAM(stream)));
+  return LFPS_OK;
+}
+
+int lfps_stage_gate(const double* keys, const double* values, int32_t n, int32_t d, int32_t sink,
+                    int32_t window, const double* q, const double* mean_key, const double* mean_value,
+                    double sigma, int32_t bypass_mode, double* out, int32_t* err, void* stream) {
+  if (!keys || !values || !q || !mean_key || !mean_value || !out || !err || d < 1)
+    return fail(LFPS_E_INVALID, "stage_gate: bad arguments");
+  if (sink < 1 || sink > 31 || window < 1 || window > 64)
+    return fail(LFPS_E_UNSUPPORTED, "stage_gate: sink_count in [1, 31], local_window in [1, 64]");
+  if (n <= sink + window) return fail(LFPS_E_INVALID, "context shorter than sink_count + local_window");
+  LAUNCH(lfps::stage_gate(keys, values, n, d, sink, window, q, mean_key, mean_value, sigma, bypass_mode,
+                          out, err, STREAM(stream)));
+  return LFPS_OK;
+}
+
 int lfps_overlap(const lfps_dims* dims, const int32_t* sel, const int32_t* sel_cnt,
                  const int32_t* exact, const int32_t* exact_cnt, int32_t list_stride,
                  int32_t cnt_stride, double* eta, void* stream) {
