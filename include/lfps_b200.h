@@ -355,12 +355,13 @@ LFPS_API int lfps_stage_attend(const double* keys, const double* values, int32_t
                                const int64_t* idx, int32_t nidx, const double* q, double* out,
                                double* weights, int32_t* err, void* stream);
 /* ScoreTablePair.update (tables.py:144-200) after the host's checks (sum of
- * weights, index range): rf != 0 renormalises by rf first; then the slash
+ * weights, index range): renorm != 0 multiplies by rf first; then the slash
  * shift (slot base - 1 zeroed) and the residual fold at sel (logical) with
  * the new lazy scale `scale`; *clamps = entries clamped.  tmp: k doubles. */
 LFPS_API int lfps_stage_update(double* ver, double* sla, int32_t base, int32_t m,
-                               const int64_t* sel, const double* weights, int32_t k, double rf,
-                               double scale, int64_t* clamps, double* tmp, void* stream);
+                               const int64_t* sel, const double* weights, int32_t k,
+                               int32_t renorm, double rf, double scale, int64_t* clamps,
+                               double* tmp, void* stream);
 /* ScoreTablePair.grow (tables.py:202-220). */
 LFPS_API int lfps_stage_grow(double* ver, double* sla, int32_t base, int32_t m, int32_t carry,
                              void* stream);

@@ -140,7 +140,7 @@ def _declare(lib):
                                   V],
         "lfps_stage_topk": [V, V, I32, I32, V, V, V],
         "lfps_stage_attend": [V, V, I32, V, I32, V, V, V, V, V],
-        "lfps_stage_update": [V, V, I32, I32, V, V, I32, D, D, V, V, V],
+        "lfps_stage_update": [V, V, I32, I32, V, V, I32, I32, D, D, V, V, V],
         "lfps_stage_grow": [V, V, I32, I32, I32, V],
         "lfps_stage_init_tables": [V, I32, I32, D, V, V, V],
         "lfps_stage_head_stats": [V, V, I32, I32, I32, V, V, V, V, V, V, V],

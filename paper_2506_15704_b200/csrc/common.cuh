@@ -178,8 +178,8 @@ cudaError_t stage_attend(const double* keys, const double* values, int d, const 
                          int nidx, const double* q, double* out, double* weights, int* err,
                          cudaStream_t st);
 cudaError_t stage_update(double* ver, double* sla, int base, int m, const int64_t* sel,
-                         const double* w, int k, double rf, double scale, long long* clamps,
-                         double* tmp, cudaStream_t st);
+                         const double* w, int k, int renorm, double rf, double scale,
+                         long long* clamps, double* tmp, cudaStream_t st);
 cudaError_t stage_grow(double* ver, double* sla, int base, int m, int carry, cudaStream_t st);
 cudaError_t stage_init_tables(const double* w, int s, int m, double r, double* ver, double* sla,
                               cudaStream_t st);

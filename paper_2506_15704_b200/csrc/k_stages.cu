@@ -323,17 +323,17 @@ __global__ void stage_attend_kernel(const double* keys, const double* values, in
 
 // ---- ScoreTablePair.update (tables.py:144-200), after the host's checks ----
 // sla points at the slash buffer, base = the window start before this
-// update's shift.  rf != 0: renormalisation by rf first (vertical [0, m),
+// update's shift.  renorm: renormalisation by rf first (vertical [0, m),
 // slash [base, base + m], tables.py:240-244).  Then the shift (slot base - 1
 // zeroed), add = (w - 1 / (2k)) / scale folded into ver[sel] and
 // sla[base - 1 + sel] with numpy fancy-index semantics (reads, then writes in
 // order), negatives clamped to 0 and counted into *clamps.
 __global__ void stage_update_kernel(double* ver, double* sla, int base, int m, const int64_t* sel,
-                                    const double* w, int k, double rf, double scale,
+                                    const double* w, int k, int renorm, double rf, double scale,
                                     long long* clamps, double* tmp) {
   __shared__ double red[16];
   const int tid = threadIdx.x;
-  if (rf != 0.0) {
+  if (renorm) {
     for (int i = tid; i < m; i += kT) ver[i] = cmul(ver[i], rf);
     for (int i = tid; i <= m; i += kT) sla[base + i] = cmul(sla[base + i], rf);
     __syncthreads();
@@ -544,9 +544,10 @@ cudaError_t stage_attend(const double* keys, const double* values, int d, const 
 }
 
 cudaError_t stage_update(double* ver, double* sla, int base, int m, const int64_t* sel,
-                         const double* w, int k, double rf, double scale, long long* clamps,
-                         double* tmp, cudaStream_t st) {
-  stage_update_kernel<<<1, kT, 0, st>>>(ver, sla, base, m, sel, w, k, rf, scale, clamps, tmp);
+                         const double* w, int k, int renorm, double rf, double scale,
+                         long long* clamps, double* tmp, cudaStream_t st) {
+  stage_update_kernel<<<1, kT, 0, st>>>(ver, sla, base, m, sel, w, k, renorm, rf, scale, clamps,
+                                        tmp);
   return cudaGetLastError();
 }
 

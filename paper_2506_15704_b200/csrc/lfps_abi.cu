@@ -655,11 +655,11 @@ int lfps_stage_attend(const double* keys, const double* values, int32_t d, const
 }
 
 int lfps_stage_update(double* ver, double* sla, int32_t base, int32_t m, const int64_t* sel,
-                      const double* weights, int32_t k, double rf, double scale, int64_t* clamps,
-                      double* tmp, void* stream) {
+                      const double* weights, int32_t k, int32_t renorm, double rf, double scale,
+                      int64_t* clamps, double* tmp, void* stream) {
   if (!ver || !sla || !sel || !weights || !clamps || !tmp || k < 1 || base < 1 || m < 0)
     return fail(LFPS_E_INVALID, "stage_update: bad arguments");
-  LAUNCH(lfps::stage_update(ver, sla, base, m, sel, weights, k, rf, scale,
+  LAUNCH(lfps::stage_update(ver, sla, base, m, sel, weights, k, renorm, rf, scale,
                             reinterpret_cast<long long*>(clamps), tmp, STREAM(stream)));
   return LFPS_OK;
 }

@@ -18,7 +18,7 @@ from .store import KvStore
 
 def _snapshot(store: KvStore, n: int) -> KvStore:
     """A copy of the first n rows (the pre-append context of a step)."""
-    return KvStore._from_device(store._keys, store._values, n)
+    return KvStore._from_device(store._kt, store._vt, n)
 
 
 def exact_topk_step(q, store: KvStore, k: int, sink: int):

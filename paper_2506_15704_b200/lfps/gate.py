@@ -67,12 +67,12 @@ def compute_head_stats(store: KvStore, last_prefill_query, config: LfpsConfig) -
     sig = torch.empty(1, dtype=_dev.F64, device=dev)
     tmp = torch.empty(n, dtype=_dev.F64, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
-    _dev.call("lfps_stage_head_stats", _dev.ptr(store._keys), _dev.ptr(store._values), n, d, sink,
+    _dev.call("lfps_stage_head_stats", _dev.ptr(store._kt), _dev.ptr(store._vt), n, d, sink,
               _dev.ptr(_dev.f64(q)), _dev.ptr(mk), _dev.ptr(mv), _dev.ptr(sig), _dev.ptr(tmp),
               _dev.ptr(err), _dev.stream())
     _dev.raise_code(int(err.item()))
-    return HeadStats(sink_keys=_dev.host(store._keys[:sink]).copy(),
-                     sink_values=_dev.host(store._values[:sink]).copy(),
+    return HeadStats(sink_keys=_dev.host(store._kt[:sink]).copy(),
+                     sink_values=_dev.host(store._vt[:sink]).copy(),
                      mean_key=_dev.host(mk), mean_value=_dev.host(mv),
                      sigma_hat_sq=float(sig.item()), _dev_mean_key=mk, _dev_mean_value=mv)
 
@@ -97,7 +97,7 @@ def _gate_dev(q, store: KvStore, stats: HeadStats, config: LfpsConfig):
     out = torch.empty(S + L + 5 + d, dtype=_dev.F64, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     mk, mv = stats._device()
-    _dev.call("lfps_stage_gate", _dev.ptr(store._keys), _dev.ptr(store._values), n, d, S, L,
+    _dev.call("lfps_stage_gate", _dev.ptr(store._kt), _dev.ptr(store._vt), n, d, S, L,
               _dev.ptr(_dev.f64(q)), _dev.ptr(mk), _dev.ptr(mv), float(stats.sigma_hat_sq),
               1 if config.bypass_mode == "mean_only" else 0, _dev.ptr(out), _dev.ptr(err),
               _dev.stream())

@@ -143,14 +143,14 @@ class ScoreTablePair:
         if self._sla_base == 0:
             self._recenter()
         scale = self._scale * r
-        rf = 0.0
+        rf, renorm = 1.0, 0
         if scale < _RENORM_FLOOR:
-            rf, scale = scale, 1.0                 # _renormalize (tables.py:240-244)
+            rf, scale, renorm = scale, 1.0, 1      # _renormalize (tables.py:240-244)
         k = sel.shape[0]
         clamps = torch.zeros(1, dtype=_dev.I64, device=sel.device)
         tmp = torch.empty(k, dtype=_dev.F64, device=sel.device)
         _dev.call("lfps_stage_update", _dev.ptr(self._ver), _dev.ptr(self._sla), self._sla_base,
-                  self._m, _dev.ptr(sel), _dev.ptr(w), k, rf, scale, _dev.ptr(clamps),
+                  self._m, _dev.ptr(sel), _dev.ptr(w), k, renorm, rf, scale, _dev.ptr(clamps),
                   _dev.ptr(tmp), _dev.stream())
         self._scale = scale
         self._sla_base -= 1
