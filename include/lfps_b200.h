@@ -58,7 +58,7 @@ extern "C" {
 #define LFPS_API
 #endif
 
-#define LFPS_ABI_VERSION 6
+#define LFPS_ABI_VERSION 7
 
 #define LFPS_OK 0
 #define LFPS_E_INVALID -1   /* bad argument (shape, range, capacity) */
@@ -130,6 +130,17 @@ typedef struct lfps_state {
   double* mean_key;       /* [B * Hkv, d] prior K-bar (gate.py:71) */
   double* mean_value;     /* [B * Hkv, d] prior V-bar (gate.py:72) */
   double* sigma_hat_sq;   /* [NS] prior sigma^2 / |q|^2 (gate.py:67-73) */
+  /* Block-table KV (a serving caller's paged cache, vLLM-style): when
+     block_table is not NULL, k_cache / v_cache are pools [blocks,
+     block_rows, Hkv, d] and row r of (request b, KV head h) is pool row
+     (block_table[b * max_blocks + r / block_rows] * block_rows +
+     r % block_rows) * Hkv + h; block_rows is a power of two and n_max ==
+     max_blocks * block_rows.  The caller owns the table: the blocks of rows
+     [0, n_ctx[b] + 1) must be mapped before a decode step (the step appends
+     row n_ctx[b]).  NULL: the contiguous [B, Hkv, n_max, d] layout. */
+  const int32_t* block_table;
+  int32_t block_rows;
+  int32_t max_blocks;
 } lfps_state;
 
 /* Offsets (bytes) of every region inside one workspace buffer. */

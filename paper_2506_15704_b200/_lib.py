@@ -18,7 +18,7 @@ from .errors import DeviceError
 # experiments); the default is the library __graft_entry__.build() makes
 LIB_PATH = os.environ.get("LFPS_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "lib", "liblfps_b200.so")
-ABI_VERSION = 6
+ABI_VERSION = 7
 FLAG_EXPORT_SETS = 1
 FLAG_TRACE = 2
 FLAG_SPLIT = 8
@@ -65,7 +65,8 @@ class State(C.Structure):
                 ("ver", C.c_void_p), ("sla", C.c_void_p), ("scale", C.c_void_p),
                 ("sla_base", C.c_void_p), ("clamp_count", C.c_void_p),
                 ("mean_key", C.c_void_p), ("mean_value", C.c_void_p),
-                ("sigma_hat_sq", C.c_void_p)]
+                ("sigma_hat_sq", C.c_void_p), ("block_table", C.c_void_p),
+                ("block_rows", C.c_int32), ("max_blocks", C.c_int32)]
 
 
 class WsLayout(C.Structure):

@@ -71,16 +71,43 @@ struct Ctx {
   int2* hot;          // [2 NS][16 nblk + 1] per-step C0 words (k_select.cu)
   double* scratch;
   BlockWs bw;
+  // block-table KV (lfps_state.block_table): row r of unit (b, h) lives at
+  // pool row (bt[b][r >> bs_shift] << bs_shift | r & bs_mask) * Hkv + h of a
+  // [blocks, block_rows, Hkv, d] pool; bt == nullptr: contiguous [B, Hkv, n_max, d]
+  const int* bt;
+  int bs_shift, bs_mask, max_blocks;
 };
 
 // CNT_BLOCKS: table blocks the select kernel read (rebuilt + hot), a diagnostic
 enum { CNT_C0 = 0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_BLOCKS, CNT_N };
 
+// Row r of unit (b, h) -> its row number in the K / V buffers (row = d
+// elements): the unit's contiguous span, or the block table's block
+struct RowMap {
+  const int* bt;      // this request's block-table row (block table mode)
+  int base;           // first row of the unit (contiguous), or h (block table)
+  int shift, mask, hkv;
+  __device__ __forceinline__ RowMap(const Ctx& c, int b, int h) {
+    shift = c.bs_shift; mask = c.bs_mask; hkv = c.Hkv;
+    if (c.bt) {
+      bt = c.bt + (size_t)b * c.max_blocks;
+      base = h;
+    } else {
+      bt = nullptr;
+      base = (b * c.Hkv + h) * c.n_max;
+    }
+  }
+  __device__ __forceinline__ int operator()(int r) const {
+    if (!bt) return base + r;
+    return ((__ldg(bt + (r >> shift)) << shift) | (r & mask)) * hkv + base;
+  }
+};
+
 __device__ __forceinline__ const __nv_bfloat16* krow(const Ctx& c, int b, int h, int i) {
-  return c.K + (((size_t)b * c.Hkv + h) * c.n_max + i) * c.d;
+  return c.K + (size_t)RowMap(c, b, h)(i) * c.d;
 }
 __device__ __forceinline__ const __nv_bfloat16* vrow(const Ctx& c, int b, int h, int i) {
-  return c.V + (((size_t)b * c.Hkv + h) * c.n_max + i) * c.d;
+  return c.V + (size_t)RowMap(c, b, h)(i) * c.d;
 }
 
 // err[1 + s] = (call stamp << 4) | code: a code counts only for the call whose

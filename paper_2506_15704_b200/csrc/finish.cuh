@@ -113,8 +113,9 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
   if ((c.flags & LFPS_FLAG_TRACE) && tid == 0) c.trace[(size_t)s * 16 + 13] = now_ns();
   const int* pidx = c.probe_idx + (size_t)s * c.list_cap;
   float* pz = c.probe_score + (size_t)s * c.list_cap;
-  const __nv_bfloat16* kb = krow(c, b, h, 0);
-  const __nv_bfloat16* vb = vrow(c, b, h, 0);
+  const __nv_bfloat16* kb = c.K;                        // rows addressed through rm
+  const __nv_bfloat16* vb = c.V;
+  const RowMap rm(c, b, h);
   const Part<PQ> qp = ld_part<PQ>(q + (size_t)s * c.d, l8);   // packed bf16 partials of q
   int k = (int)rint(c.frac * (double)n);
   if (k < 1) k = 1;
@@ -143,7 +144,7 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
       }
     };
     stream_rows<kFused, PQ>(
-        stages, kb, vb, S + p, [&](int rid) { return rid < S ? rid : __ldg(pidxS + rid); },
+        stages, kb, vb, S + p, [&](int rid) { return rm(rid < S ? rid : __ldg(pidxS + rid)); },
         [&](const Rows2& r) {
           const float2 z = score_rows<PQ>(r, qp, c.sqrt_d_f32);
           if (r.ok[1]) {
@@ -159,7 +160,7 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
   } else {
     // ---- scores of the sinks and the probe rows -------------------------------------------
     stream_rows<kScore, PQ>(
-        stages, kb, vb, S + p, [&](int rid) { return rid < S ? rid : __ldg(pidxS + rid); },
+        stages, kb, vb, S + p, [&](int rid) { return rm(rid < S ? rid : __ldg(pidxS + rid)); },
         [&](const Rows2& r) {
           const float2 z = score_rows<PQ>(r, qp, c.sqrt_d_f32);
           if (l8 == 0) {
@@ -242,7 +243,7 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
       return z * kLog2e;
     };
     stream_rows<kAttend, PQ>(
-        stages, kb, vb, S + k2, [&](int rid) { return rid < S ? rid : c2i[rid - S]; },
+        stages, kb, vb, S + k2, [&](int rid) { return rm(rid < S ? rid : c2i[rid - S]); },
         [&](const Rows2& r) {
           if (r.ok[1]) {
             const float za = zof(r.rid[0]), zb = zof(r.rid[1]);

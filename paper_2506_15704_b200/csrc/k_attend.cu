@@ -33,11 +33,12 @@ __global__ void __launch_bounds__(kThreads, kRowCtas) lfps_exact_attend_kernel(C
   const int k2 = c.counts[(size_t)s * CNT_N + CNT_C2];
   const int* c2i = c.c2_idx + (size_t)s * c.list_cap;
   const float* c2z = c.c2_score + (size_t)s * c.list_cap;
-  const __nv_bfloat16* kb = krow(c, b, h, 0);
-  const __nv_bfloat16* vb = vrow(c, b, h, 0);
+  const __nv_bfloat16* kb = c.K;                        // rows addressed through rm
+  const __nv_bfloat16* vb = c.V;
+  const RowMap rm(c, b, h);
   const Part<PQ> qp = ld_part<PQ>(q + (size_t)s * c.d, l8);
   stream_rows<kScore, PQ>(
-      stages, kb, vb, S, [&](int rid) { return rid; },
+      stages, kb, vb, S, [&](int rid) { return rm(rid); },
       [&](const Rows2& r) {
         const float2 z = score_rows<PQ>(r, qp, c.sqrt_d_f32);
         if (l8 == 0 && r.ok[0]) sh.sink_z[r.rid[0]] = z.x;
@@ -47,7 +48,7 @@ __global__ void __launch_bounds__(kThreads, kRowCtas) lfps_exact_attend_kernel(C
   at.init();
   auto zof = [&](int rid) { return (rid < S ? sh.sink_z[rid] : __ldg(c2z + rid - S)) * kLog2e; };
   stream_rows<kAttend, PQ>(
-      stages, kb, vb, S + k2, [&](int rid) { return rid < S ? rid : __ldg(c2i + rid - S); },
+      stages, kb, vb, S + k2, [&](int rid) { return rm(rid < S ? rid : __ldg(c2i + rid - S)); },
       [&](const Rows2& r) {
         if (r.ok[1]) {
           at.absorb2(zof(r.rid[0]), ld_part_s<PQ>(r.v[0], l8), zof(r.rid[1]), ld_part_s<PQ>(r.v[1], l8));

@@ -76,21 +76,21 @@ __global__ void lfps_boot_mean_kernel(Ctx c) {
   const int t = threadIdx.x;
   if (t >= 2 * d) return;
   const int j = t % d;
-  const uint16_t* src = reinterpret_cast<const uint16_t*>(t < d ? c.K : c.V) +
-                        ((size_t)b * c.Hkv + h) * c.n_max * d;
+  const uint16_t* src = reinterpret_cast<const uint16_t*>(t < d ? c.K : c.V) + j;
+  const RowMap rm(c, b, h);
   double acc = 0.0;
   int i = S;
   for (; i + 4 <= n; i += 4) {
-    const float a0 = bf2f(src[(size_t)i * d + j]);
-    const float a1 = bf2f(src[(size_t)(i + 1) * d + j]);
-    const float a2 = bf2f(src[(size_t)(i + 2) * d + j]);
-    const float a3 = bf2f(src[(size_t)(i + 3) * d + j]);
+    const float a0 = bf2f(src[(size_t)rm(i) * d]);
+    const float a1 = bf2f(src[(size_t)rm(i + 1) * d]);
+    const float a2 = bf2f(src[(size_t)rm(i + 2) * d]);
+    const float a3 = bf2f(src[(size_t)rm(i + 3) * d]);
     acc = cadd(acc, (double)a0);
     acc = cadd(acc, (double)a1);
     acc = cadd(acc, (double)a2);
     acc = cadd(acc, (double)a3);
   }
-  for (; i < n; ++i) acc = cadd(acc, (double)bf2f(src[(size_t)i * d + j]));
+  for (; i < n; ++i) acc = cadd(acc, (double)bf2f(src[(size_t)rm(i) * d]));
   const double mean = cdiv(acc, (double)(n - S));
   (t < d ? c.mean_key : c.mean_value)[(size_t)u * d + j] = mean;
 }

@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_SCORE_CTAS) lfps_exact_score_ke
       q2[g][2 * t + 1] = make_float2(bf_hi(qp.a[t]), bf_hi(qp.b[t]));
     }
   }
-  const __nv_bfloat16* kb = krow(c, b, h, S);
+  const RowMap rm(c, b, h);
   const int gs = l8 % G;                              // the head this lane divides and writes
   float* out = c.probe_score + (size_t)(s0 + gs) * c.list_cap;
   // K rows stream through shared memory, kScoreStages tiles of kStep rows:
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_SCORE_CTAS) lfps_exact_score_ke
   constexpr int kChunks = kRowB / 16;
   constexpr int kStageB = kStep * kRowB;
   const uint32_t sb = smem_u32(kst) + grp * kRowB;
-  const uint8_t* kb8 = reinterpret_cast<const uint8_t*>(kb) + l8 * 16;
+  const uint8_t* kb8 = reinterpret_cast<const uint8_t*>(c.K) + l8 * 16;
   const int ntiles = (r1 - r0 + kStep - 1) / kStep;
   auto issue = [&](int tile) {
     if (tile < ntiles) {
@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(kThreads, LFPS_SCORE_CTAS) lfps_exact_score_ke
 #pragma unroll
           for (int ch = 0; ch < kChunks; ch += 8) {
             if (kChunks % 8 != 0 && ch + l8 >= kChunks) continue;
-            cp_async16_s(st + i * kGroups8 * kRowB + ch * 16, kb8 + (size_t)row * kRowB + ch * 16);
+            cp_async16_s(st + i * kGroups8 * kRowB + ch * 16,
+                         kb8 + (size_t)rm(S + row) * kRowB + ch * 16);
           }
         }
       }

@@ -101,8 +101,9 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
   // KV append of the unit's new row at position n (one session per unit)
   if (qh % c.G == 0) {
     const int u = b * c.Hkv + qh / c.G;
-    __nv_bfloat16* kd = c.Kw + ((size_t)u * c.n_max + n) * c.d;
-    __nv_bfloat16* vd = c.Vw + ((size_t)u * c.n_max + n) * c.d;
+    const size_t row = (size_t)RowMap(c, b, qh / c.G)(n) * c.d;
+    __nv_bfloat16* kd = c.Kw + row;
+    __nv_bfloat16* vd = c.Vw + row;
     for (int t = tid; t < c.d; t += kThreads) {
       kd[t] = k_new[(size_t)u * c.d + t];
       vd[t] = v_new[(size_t)u * c.d + t];

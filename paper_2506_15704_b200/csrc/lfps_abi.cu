@@ -169,6 +169,21 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
   if (!c->K || !c->V || !c->n_ctx || !c->ver || !c->sla || !c->scale || !c->sla_base ||
       !c->clamp_count || !c->mean_key || !c->mean_value || !c->sigma)
     return fail(LFPS_E_INVALID, "a state pointer is NULL");
+  c->bt = st->block_table;
+  c->bs_shift = 31;
+  c->bs_mask = 0x7fffffff;
+  c->max_blocks = 0;
+  if (st->block_table) {
+    const int br = st->block_rows;
+    if (br < 1 || br > (1 << 16) || (br & (br - 1)))
+      return fail(LFPS_E_INVALID, "block_rows must be a power of two in [1, 65536], got %d", br);
+    if (st->max_blocks < 1 || (long long)st->max_blocks * br != d->n_max)
+      return fail(LFPS_E_INVALID, "block table: n_max (%d) must equal max_blocks (%d) * block_rows (%d)",
+                  d->n_max, st->max_blocks, br);
+    c->bs_shift = __builtin_ctz((unsigned)br);
+    c->bs_mask = br - 1;
+    c->max_blocks = st->max_blocks;
+  }
   char* base = static_cast<char*>(ws->base);
   c->rho = reinterpret_cast<double*>(base + L.rho);
   c->bypass = reinterpret_cast<int*>(base + L.bypass);

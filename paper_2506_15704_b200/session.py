@@ -76,7 +76,7 @@ class BatchedSession:
     def __init__(self, cfg: LfpsConfig, batch: int, kv_heads: int, group: int, n_max: int,
                  m_cap: int | None = None, device: torch.device | str | None = None,
                  export_sets: bool = False, kv_cache: tuple | None = None,
-                 paged: bool = False):
+                 paged: bool = False, kv_blocks: tuple | None = None):
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device())
         device = torch.device(device)
@@ -98,6 +98,26 @@ class BatchedSession:
         self.NS = batch * self.Hq
         self.d = cfg.d
         self.n_max = int(n_max)
+        self.block_table = None
+        if kv_blocks is not None:
+            # a serving caller's block-table cache: (k_pool, v_pool, block_table,
+            # block_rows), pools bf16 [blocks, block_rows, Hkv, d], table int32
+            # [B, max_blocks] on the device; n_max = max_blocks * block_rows
+            if paged or kv_cache is not None:
+                raise ValueError("kv_blocks excludes paged=True and kv_cache")
+            k_pool, v_pool, table, block_rows = kv_blocks
+            block_rows = int(block_rows)
+            if tuple(table.shape[:1]) != (batch,) or table.dtype != torch.int32:
+                raise ValueError(f"block_table must be int32 [{batch}, max_blocks]")
+            for t in (k_pool, v_pool):
+                if (t.dim() != 4 or tuple(t.shape[1:]) != (block_rows, kv_heads, cfg.d)
+                        or t.dtype != torch.bfloat16):
+                    raise ValueError(f"kv pools must be bf16 [blocks, {block_rows}, {kv_heads}, "
+                                     f"{cfg.d}]")
+            self.block_table = table.contiguous()
+            self.block_rows = block_rows
+            self.n_max = int(table.shape[1]) * block_rows
+            n_max = self.n_max
         if paged:
             # whole pages per (request, KV head): round n_max up
             from .kv_pool import page_rows
@@ -119,6 +139,10 @@ class BatchedSession:
             from .kv_pool import KvPool
             self.kv_pool = KvPool(self.dims, dev)
             self.k_cache, self.v_cache = self.kv_pool.k, self.kv_pool.v
+        elif kv_blocks is not None:
+            self.k_cache, self.v_cache = kv_blocks[0], kv_blocks[1]
+            if self.k_cache.device != dev or self.v_cache.device != dev:
+                raise ValueError(f"kv pools must be on {dev}")
         elif kv_cache is not None:
             # an existing cache (e.g. one layer's rows reused by other layers'
             # trackers): bf16 [batch, kv_heads, n_max, d] pair on this device
@@ -146,7 +170,11 @@ class BatchedSession:
                                 _ptr(self.ver), _ptr(self.sla), _ptr(self.scale),
                                 _ptr(self.sla_base), _ptr(self.clamp_count),
                                 _ptr(self.mean_key), _ptr(self.mean_value),
-                                _ptr(self.sigma_hat_sq))
+                                _ptr(self.sigma_hat_sq),
+                                _ptr(self.block_table) if self.block_table is not None else None,
+                                self.block_rows if self.block_table is not None else 0,
+                                int(self.block_table.shape[1]) if self.block_table is not None
+                                else 0)
         self.ws = _lib.Workspace(_ptr(self.ws_buf), self.layout.total_bytes)
         self._views()
         self.step_count = 0
@@ -194,8 +222,8 @@ class BatchedSession:
             raise ValueError(
                 f"prefill needs more than sink_count + s = {self.cfg.sink_count + self.cfg.s} rows")
         self._back(b, n0 + 1, reload=True)
-        self.k_cache[b, :, :n0].copy_(keys)
-        self.v_cache[b, :, :n0].copy_(values)
+        for h in range(self.Hkv):
+            self._kv_write(b, h, 0, keys[h], values[h])
         self.n_host[b] = n0
         self.n_ctx[b] = n0
 
@@ -209,8 +237,7 @@ class BatchedSession:
             raise ValueError(
                 f"prefill needs more than sink_count + s = {self.cfg.sink_count + self.cfg.s} rows")
         self._back(b, n0 + 1, reload=True)
-        self.k_cache[b, h, :n0].copy_(keys)
-        self.v_cache[b, h, :n0].copy_(values)
+        self._kv_write(b, h, 0, keys, values)
         self.n_host[b] = n0
         self.n_ctx[b] = n0
 
@@ -331,6 +358,28 @@ class BatchedSession:
             self.check_errors("decode_step")
         return self.result()
 
+    def _kv_write(self, b: int, h: int, r0: int, keys: torch.Tensor, values: torch.Tensor):
+        """Rows [r0, r0 + len) of unit (b, h) into the cache (plumbing)."""
+        n = keys.shape[0]
+        if self.block_table is None:
+            self.k_cache[b, h, r0:r0 + n].copy_(keys)
+            self.v_cache[b, h, r0:r0 + n].copy_(values)
+            return
+        r = torch.arange(r0, r0 + n, device=self.device)
+        blk = self.block_table[b].long()[r // self.block_rows]
+        off = r % self.block_rows
+        self.k_cache[blk, off, h] = keys.to(self.device, torch.bfloat16)
+        self.v_cache[blk, off, h] = values.to(self.device, torch.bfloat16)
+
+    def kv_rows(self, b: int, h: int, n: int):
+        """(K, V) bf16 [n, d] copies of unit (b, h)'s first n rows."""
+        if self.block_table is None:
+            return self.k_cache[b, h, :n].clone(), self.v_cache[b, h, :n].clone()
+        r = torch.arange(n, device=self.device)
+        blk = self.block_table[b].long()[r // self.block_rows]
+        off = r % self.block_rows
+        return self.k_cache[blk, off, h], self.v_cache[blk, off, h]
+
     # -- paged KV (kv_pool.py) ------------------------------------------------
     def _back(self, b: int, rows: int, reload: bool = False):
         """Paged caches: back rows [0, rows) of request b before they are
@@ -448,8 +497,8 @@ class BatchedSession:
             n = self.n_host[b]
             if n >= self.n_max:
                 raise ValueError(f"request {b}: KV cache full")
-            self.k_cache[b, :, n].copy_(k_new[b])
-            self.v_cache[b, :, n].copy_(v_new[b])
+            for h in range(self.Hkv):
+                self._kv_write(b, h, n, k_new[b, h][None], v_new[b, h][None])
         self.n_ctx += 1
         self.n_host = [n + 1 for n in self.n_host]
         self.tables_stale = True

@@ -21,14 +21,26 @@ class Pair:
     [B, Hkv, G, s, n0 - S]; finals [B, Hkv, G, d]."""
 
     def __init__(self, cfg, keys, values, weights, finals, n0, n_max=None, m_cap=None,
-                 paged=False):
+                 paged=False, block_rows=None):
         B, Hkv, _, d = keys.shape
         G = weights.shape[2]
         self.cfg, self.B, self.Hkv, self.G, self.d, self.n0 = cfg, B, Hkv, G, d, n0
         self.host_io = False
         self.weights, self.finals = weights, finals
-        self.sess = BatchedSession(cfg, B, Hkv, G, n_max=n_max or keys.shape[2] + 8,
-                                   m_cap=m_cap, device="cuda", export_sets=True, paged=paged)
+        n_max = n_max or keys.shape[2] + 8
+        kv_blocks = None
+        if block_rows:
+            # a vLLM-style block-table cache: blocks of `block_rows` rows of all
+            # KV heads, handed out in a random order
+            max_blocks = -(-n_max // block_rows)
+            nblk = B * max_blocks + 3
+            perm = torch.randperm(nblk, generator=torch.Generator().manual_seed(7))[:B * max_blocks]
+            table = perm.reshape(B, max_blocks).to(torch.int32).cuda()
+            kp = torch.zeros(nblk, block_rows, Hkv, d, dtype=torch.bfloat16, device="cuda")
+            kv_blocks = (kp, torch.zeros_like(kp), table, block_rows)
+            m_cap = m_cap or n_max - cfg.sink_count + 2
+        self.sess = BatchedSession(cfg, B, Hkv, G, n_max=n_max, m_cap=m_cap, device="cuda",
+                                   export_sets=True, paged=paged, kv_blocks=kv_blocks)
         for b in range(B):
             self.sess.load_prefill(b, bf16(keys[b, :, :n0]).cuda(), bf16(values[b, :, :n0]).cuda())
         w = torch.as_tensor(np.ascontiguousarray(weights, dtype=np.float32))
@@ -122,7 +134,7 @@ class Pair:
 
 
 def gqa_pair(batch=2, kv_heads=2, group=4, n0=3000, steps=8, d=128, seed=3, spec_kw=None,
-              paged=False, n_max=None, **cfg_kw):
+              paged=False, n_max=None, block_rows=None, **cfg_kw):
     from paper_2506_15704_b200.config import LfpsConfig
     from paper_2506_15704_b200.workload import GqaSpec, gen_unit
     kw = dict(slash_offsets=(64, 65), band_width=6)
@@ -142,4 +154,4 @@ def gqa_pair(batch=2, kv_heads=2, group=4, n0=3000, steps=8, d=128, seed=3, spec
             qr.append(u.queries.float().numpy())
         K.append(kr); V.append(vr); W.append(wr); F.append(fr); Q.append(qr)
     K, V, W, F, Q = (np.asarray(x) for x in (K, V, W, F, Q))
-    return Pair(cfg, K, V, W, F, n0, paged=paged, n_max=n_max), K, V, Q
+    return Pair(cfg, K, V, W, F, n0, paged=paged, n_max=n_max, block_rows=block_rows), K, V, Q

@@ -389,3 +389,42 @@ def gqa_pair_cached(seed):
     pair, K, V, Q = _gqa_pair(batch=8, kv_heads=8, group=4, d=64, n0=700, steps=10, seed=seed)
     pair.sess.split = True
     return pair, K, V, Q
+
+
+@pytest.mark.parametrize("block_rows,d", [(16, 128), (64, 64)])
+def test_block_table_kv_bit_exact(block_rows, d):
+    """N4, the serving caller with a block table (vLLM-style 16-row blocks
+    in a random order, lfps_state.block_table): every kernel reads and the
+    commit appends rows through the table.  Multi-step parity with the
+    oracle (so identical to the contiguous cache), the exact path and full
+    attention over block-table rows."""
+    import math
+    import gpu_drive
+    from oracle import lfps_oracle as lo
+    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, n0=2500, steps=6, d=d, seed=59,
+                              block_rows=block_rows)
+    sess = pair.sess
+    assert sess.block_table is not None and sess.block_rows == block_rows
+    n0 = pair.n0
+    for t in range(6):
+        pair.host_io = t % 3 == 2
+        res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], 0.05 if t % 2 else 0.01)
+        pair.compare_step(res, outs)
+    kr, vr = sess.kv_rows(1, 1, n0 + 6)                 # appended rows went through the table
+    np.testing.assert_array_equal(kr.float().cpu().numpy(), K[1, 1, :n0 + 6])
+    q = Q[:, :, :, 5]
+    qd = gpu_drive.bf16(q.reshape(2, -1, d)).cuda()
+    sess.exact_topk_step(qd, 0.05)
+    torch.cuda.synchronize()
+    for h in range(2):
+        kv = pair.units[h][0]
+        for g in range(4):
+            k = max(1, round(0.05 * kv.n))
+            np.testing.assert_array_equal(sess.c2_list(0, h * 4 + g),
+                                          lo.topk_oracle(kv, q[0, h, g], k, 4, "fp32"))
+    full = sess.full_attention(qd).cpu().numpy()
+    kv = pair.units[0][0]
+    z = kv.keys[:kv.n] @ q[0, 0, 0] / math.sqrt(d)
+    w = np.exp(z - z.max())
+    ref = (w / w.sum()) @ kv.values[:kv.n]
+    assert np.linalg.norm(full[0, 0] - ref) / np.linalg.norm(ref) <= 1e-5
