@@ -220,6 +220,12 @@ LFPS_API int lfps_bootstrap_tables(const lfps_dims* dims, const lfps_params* p,
 LFPS_API int lfps_bootstrap_stats(const lfps_dims* dims, const lfps_params* p,
                          const lfps_state* st, const lfps_workspace* ws,
                          const void* last_query, void* stream);
+/* The same for requests [b_begin, b_begin + b_count) only (a request
+ * (re)loaded into a running batch); the other requests' priors stay. */
+LFPS_API int lfps_bootstrap_stats_requests(const lfps_dims* dims, const lfps_params* p,
+                                           const lfps_state* st, const lfps_workspace* ws,
+                                           const void* last_query, int32_t b_begin,
+                                           int32_t b_count, void* stream);
 
 /* One LFPS decode step for all B * Hq sessions (decode_step,
  * engine.py:97-201): gate, thresholds, candidates, fp32 probe scoring,

@@ -41,7 +41,7 @@ EXPORTS = ("lfps_abi_version", "lfps_last_error", "lfps_workspace_layout",
            "lfps_exact_launches", "lfps_kv_pool_page_bytes", "lfps_kv_pool_create",
            "lfps_kv_pool_reserve", "lfps_kv_pool_release", "lfps_kv_pool_mapped_bytes",
            "lfps_kv_pool_destroy", "lfps_profile_enable", "lfps_profile_collect",
-           "lfps_workspace_release", "lfps_stage_logits", "lfps_stage_thresholds",
+           "lfps_workspace_release", "lfps_bootstrap_stats_requests", "lfps_stage_logits", "lfps_stage_thresholds",
            "lfps_stage_candidates", "lfps_stage_topk", "lfps_stage_attend", "lfps_stage_update",
            "lfps_stage_grow", "lfps_stage_init_tables", "lfps_stage_head_stats",
            "lfps_stage_gate")
@@ -131,6 +131,9 @@ def _declare(lib):
                                  C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
     lib.lfps_profile_enable.argtypes = [C.c_int]
     lib.lfps_workspace_release.argtypes = [P(Workspace)]
+    lib.lfps_bootstrap_stats_requests.argtypes = [P(Dims), P(Params), P(State), P(Workspace),
+                                                  C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+    lib.lfps_bootstrap_stats_requests.restype = C.c_int
     lib.lfps_workspace_release.restype = C.c_int
     # per-head stage API (k_stages.cu): device pointers as c_void_p
     V, I32, I64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_double

@@ -183,7 +183,8 @@ cudaError_t launch_update(const Ctx& c, const __nv_bfloat16* k_new, const __nv_b
 cudaError_t launch_finish(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
 cudaError_t launch_boot_tables(const Ctx& c, const float* w, int s_begin, int count, int m0,
                                cudaStream_t st);
-cudaError_t launch_boot_stats(const Ctx& c, const __nv_bfloat16* q, int m_max, cudaStream_t st);
+cudaError_t launch_boot_stats(const Ctx& c, const __nv_bfloat16* q, int m_max, int b0, int nb,
+                              cudaStream_t st);
 cudaError_t launch_exact_score(const Ctx& c, const __nv_bfloat16* q, int m_max, cudaStream_t st);
 cudaError_t launch_overlap(const Ctx& c, const int* sel, const int* sel_cnt, const int* ex,
                            const int* ex_cnt, int list_stride, int cnt_stride, double* eta,

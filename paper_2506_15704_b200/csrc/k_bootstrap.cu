@@ -68,8 +68,8 @@ __global__ void lfps_boot_rowsum_kernel(Ctx c, const float* w, int s_begin, int 
 }
 
 // one CTA per unit, one thread per (matrix, column): sequential row sums
-__global__ void lfps_boot_mean_kernel(Ctx c) {
-  const int u = blockIdx.x;
+__global__ void lfps_boot_mean_kernel(Ctx c, int u0) {
+  const int u = u0 + blockIdx.x;
   const int b = u / c.Hkv, h = u % c.Hkv;
   const int n = c.n_ctx[b];
   const int S = c.S, d = c.d;
@@ -96,8 +96,8 @@ __global__ void lfps_boot_mean_kernel(Ctx c) {
 }
 
 // logits of every non-sink row for every session of a unit -> scratch
-__global__ void lfps_boot_logit_kernel(Ctx c, const __nv_bfloat16* q) {
-  const int u = blockIdx.y;
+__global__ void lfps_boot_logit_kernel(Ctx c, const __nv_bfloat16* q, int u0) {
+  const int u = u0 + blockIdx.y;
   const int b = u / c.Hkv, h = u % c.Hkv;
   const int n = c.n_ctx[b];
   const int S = c.S, d = c.d;
@@ -160,9 +160,9 @@ __device__ double block_table_sum(const double* x, int cnt, double mu, double* p
   return tot;
 }
 
-__global__ void lfps_boot_sigma_kernel(Ctx c, const __nv_bfloat16* q, int n2) {
+__global__ void lfps_boot_sigma_kernel(Ctx c, const __nv_bfloat16* q, int n2, int s0) {
   extern __shared__ double parts[];
-  const int s = blockIdx.x;
+  const int s = s0 + blockIdx.x;
   const int b = s / c.Hq;
   const int cnt = c.n_ctx[b] - c.S;
   const double* x = c.scratch + (size_t)s * c.list_cap;
@@ -201,21 +201,22 @@ cudaError_t launch_boot_tables(const Ctx& c, const float* w, int s_begin, int co
   return cudaGetLastError();
 }
 
-cudaError_t launch_boot_stats(const Ctx& c, const __nv_bfloat16* q, int m_max, cudaStream_t st) {
-  const int units = c.B * c.Hkv;
-  lfps_boot_mean_kernel<<<units, 2 * c.d, 0, st>>>(c);
+cudaError_t launch_boot_stats(const Ctx& c, const __nv_bfloat16* q, int m_max, int b0, int nb,
+                              cudaStream_t st) {
+  const int units = nb * c.Hkv, u0 = b0 * c.Hkv;
+  lfps_boot_mean_kernel<<<units, 2 * c.d, 0, st>>>(c, u0);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int per_unit = (148 * 8 + units - 1) / units;
   if (per_unit > 256) per_unit = 256;
-  lfps_boot_logit_kernel<<<dim3(per_unit, units), 256, 0, st>>>(c, q);
+  lfps_boot_logit_kernel<<<dim3(per_unit, units), 256, 0, st>>>(c, q, u0);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int nch = (m_max + 511) / 512;
   int n2 = 1;
   while (n2 < nch) n2 <<= 1;
   if (n2 < 32) n2 = 32;
-  lfps_boot_sigma_kernel<<<c.NS, 256, n2 * sizeof(double), st>>>(c, q, n2);
+  lfps_boot_sigma_kernel<<<nb * c.Hq, 256, n2 * sizeof(double), st>>>(c, q, n2, b0 * c.Hq);
   return cudaGetLastError();
 }
 

@@ -472,7 +472,24 @@ int lfps_bootstrap_stats(const lfps_dims* dims, const lfps_params* p, const lfps
   if (rc) return rc;
   if (!last_query) return fail(LFPS_E_INVALID, "last_query is NULL");
   cudaStream_t sm = static_cast<cudaStream_t>(stream);
-  LAUNCH(lfps::launch_boot_stats(c, static_cast<const __nv_bfloat16*>(last_query), c.m_cap, sm));
+  LAUNCH(lfps::launch_boot_stats(c, static_cast<const __nv_bfloat16*>(last_query), c.m_cap, 0, c.B,
+                                 sm));
+  return LFPS_OK;
+}
+
+int lfps_bootstrap_stats_requests(const lfps_dims* dims, const lfps_params* p,
+                                  const lfps_state* st, const lfps_workspace* ws,
+                                  const void* last_query, int32_t b_begin, int32_t b_count,
+                                  void* stream) {
+  lfps::Ctx c;
+  int rc = make_ctx(dims, p, st, ws, &c);
+  if (rc) return rc;
+  if (!last_query) return fail(LFPS_E_INVALID, "last_query is NULL");
+  if (b_begin < 0 || b_count < 1 || b_begin + b_count > c.B)
+    return fail(LFPS_E_INVALID, "request range [%d, %d) outside [0, %d)", b_begin, b_begin + b_count, c.B);
+  cudaStream_t sm = static_cast<cudaStream_t>(stream);
+  LAUNCH(lfps::launch_boot_stats(c, static_cast<const __nv_bfloat16*>(last_query), c.m_cap, b_begin,
+                                 b_count, sm));
   return LFPS_OK;
 }
 

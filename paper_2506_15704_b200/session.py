@@ -253,13 +253,20 @@ class BatchedSession:
             C.c_void_p(weights.data_ptr()), s_begin, count, m0, self._stream()),
             "bootstrap_tables")
 
-    def bootstrap_stats(self, last_query: torch.Tensor):
+    def bootstrap_stats(self, last_query: torch.Tensor, requests: tuple | None = None):
         """Freeze the gate priors (compute_head_stats, gate.py:51-74);
-        last_query bf16 [B, Hq, d]."""
+        last_query bf16 [B, Hq, d].  ``requests`` = (first, count) limits it
+        to those requests (one reloaded into a running batch)."""
         lq = last_query.to(self.device, torch.bfloat16).contiguous()
-        _lib.check(self.lib.lfps_bootstrap_stats(
+        if requests is None:
+            _lib.check(self.lib.lfps_bootstrap_stats(
+                C.byref(self.dims), C.byref(self._params()), C.byref(self.state),
+                C.byref(self.ws), C.c_void_p(lq.data_ptr()), self._stream()), "bootstrap_stats")
+            return
+        _lib.check(self.lib.lfps_bootstrap_stats_requests(
             C.byref(self.dims), C.byref(self._params()), C.byref(self.state), C.byref(self.ws),
-            C.c_void_p(lq.data_ptr()), self._stream()), "bootstrap_stats")
+            C.c_void_p(lq.data_ptr()), int(requests[0]), int(requests[1]), self._stream()),
+            "bootstrap_stats")
 
     def clear_errors(self):
         self.err.zero_()

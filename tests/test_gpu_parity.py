@@ -287,35 +287,65 @@ def test_decode_step_host_io_small_and_rejects():
 
 def test_paged_kv_pool_bit_exact_across_a_page():
     """N4 paged-KV caller: K/V in a KvPool (virtual [B, Hkv, n_max, d], 2 MiB
-    pages mapped as contexts grow).  The context crosses a page boundary
-    during the run (8192 rows per page at d=128, incl. the 64-row slack);
-    every step matches the oracle, through decode_step and the host-io entry
-    point; the exact path reads the paged rows; releasing a request returns
-    its pages and blocks further steps until it is reloaded."""
+    pages mapped as contexts grow).  The prefill ends 3 rows before the first
+    page boundary (8192 rows at d=128), so the appended rows of the 6 steps
+    land on BOTH pages and the probe / exact / full reads straddle it; every
+    step matches the oracle, through decode_step and the host-io entry point.
+    Releasing a request returns its pages and blocks further steps until it
+    is reloaded; after load_prefill + bootstrap the reloaded request decodes
+    again in the same batch (the other request continuing its trajectory)."""
+    from oracle import lfps_oracle as lo
     from paper_2506_15704_b200 import kv_pool
+    import gpu_drive
     rows = kv_pool.page_rows(128)
-    n0 = rows - kv_pool.SLACK_ROWS - 3
-    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, n0=n0, steps=6, seed=53, paged=True,
+    n0 = rows - 3
+    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, n0=n0, steps=12, seed=53, paged=True,
                               n_max=2 * rows)
     sess = pair.sess
     assert sess.kv_pool is not None and sess.n_max == 2 * rows
     page = kv_pool.page_bytes()
-    assert sess.kv_mapped_bytes() == 2 * 2 * 2 * page            # K+V x B x Hkv, one page
+    assert sess.kv_mapped_bytes() == 2 * 2 * 2 * 2 * page        # K+V x B x Hkv, 2 pages (slack)
     for t in range(6):
         pair.host_io = t % 2 == 1
         res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], 0.05)
         pair.compare_step(res, outs)
-    assert sess.kv_mapped_bytes() == 2 * 2 * 2 * 2 * page        # the second page
-    import gpu_drive
-    q = gpu_drive.bf16(Q[:, :, :, 6 - 1].reshape(2, -1, 128)).cuda()
+    for h in range(2):                                # rows rows-3 .. rows+2 were appended
+        kr, _ = sess.kv_rows(0, h, n0 + 6)
+        np.testing.assert_array_equal(kr.float().cpu().numpy()[rows - 3:], K[0, h, rows - 3:n0 + 6])
+    q = gpu_drive.bf16(Q[:, :, :, 5].reshape(2, -1, 128)).cuda()
     sess.exact_topk_step(q, 0.05)
     torch.cuda.synchronize()
     sess.check_errors("exact on paged rows")
+    for h in range(2):
+        kv = pair.units[h][0]
+        for g in range(4):
+            k = max(1, round(0.05 * kv.n))
+            np.testing.assert_array_equal(sess.c2_list(0, h * 4 + g),
+                                          lo.topk_oracle(kv, Q[0, h, g, 5], k, 4, "fp32"))
     sess.release_request(1)
     assert sess.kv_mapped_bytes() == 2 * 2 * 2 * page
     with pytest.raises(ValueError):
         sess.decode_step(q, gpu_drive.bf16(K[:, :, n0]).cuda(), gpu_drive.bf16(V[:, :, n0]).cuda(),
                          0.05)
+    # reload request 1 from its prefill, bootstrap its sessions, decode on
+    sess.load_prefill(1, gpu_drive.bf16(K[1, :, :n0]).cuda(), gpu_drive.bf16(V[1, :, :n0]).cuda())
+    w = torch.as_tensor(np.ascontiguousarray(pair.weights[1], dtype=np.float32))
+    sess.bootstrap_tables(8, w.reshape(8, pair.cfg.s, n0 - 4).cuda())
+    finals = np.concatenate([pair.finals[0].reshape(8, 128), pair.finals[1].reshape(8, 128)])
+    sess.bootstrap_stats(gpu_drive.bf16(finals.reshape(2, 8, 128)).cuda(), requests=(1, 1))
+    torch.cuda.synchronize()
+    sess.check_errors("reload")
+    for h in range(2):
+        pair.units[2 + h] = lo.bootstrap_unit(K[1, h, :n0], V[1, h, :n0], pair.weights[1, h],
+                                              pair.finals[1, h], pair.cfg, lo.DevArith)
+    # request 0 continues at step 6; request 1 restarts at step 0 (ragged contexts)
+    for t in range(6, 9):
+        qs = Q[:, :, :, t].copy()
+        qs[1] = Q[1, :, :, t - 6]
+        kn = np.stack([K[0, :, n0 + t], K[1, :, n0 + t - 6]])
+        vn = np.stack([V[0, :, n0 + t], V[1, :, n0 + t - 6]])
+        res, outs = pair.step(qs, kn, vn, 0.05)
+        pair.compare_step(res, outs)
 
 
 def test_two_threads_two_sessions_bit_exact():
