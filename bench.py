@@ -859,6 +859,7 @@ def run_ours(args, world, rank, local):
         "setup_s": setup_s,
         "step_ms_min_max": [min(step_ms), max(step_ms)],
         "bypassed_sessions_last_step": bypass,
+        "gate_near_epsilon_last_step": int(sess.gate_near_epsilon().sum()),
         "probe_mean": float(probe.mean()), "c2_mean": float(c2.mean()),
         "k_rows_distinct_per_unit": alg["k_rows_unit"], "v_rows_distinct_per_unit": alg["v_rows_unit"],
     }
@@ -886,14 +887,18 @@ def run_ours(args, world, rank, local):
 def run_c3(args, world, rank, local):
     """BASELINE.json config 3: batch 16 x 128k context, all 32 layers of a
     decode step.  The 32 layers' K/V (8.6 GB each) do not all fit one B200
-    next to their trackers, so one layer's KV cache is shared by 32 layer
-    sessions (each with its own tracker tables, bootstrapped from the same
-    prefill) -- the per-layer work and bytes are those of 32 distinct layers,
-    the cached rows are reused (SURVEY.md §7 "Memory feasibility")."""
+    next to their trackers, so one KV cache is shared by the 32 layer
+    sessions (SURVEY.md §7 "Memory feasibility").  Everything else is per
+    layer: each layer has its own query stream and last prefill queries
+    (workload.gen_unit(layer=...): a layer-specific query walk and jitter
+    over the shared planted keys), hence its own Eq. 4 tables, priors, probe
+    sets and trajectory -- 32 distinct layers' work, only the K/V rows are
+    shared (so the layers' row gathers can hit in L2 more than distinct
+    caches would)."""
     import torch
     from paper_2506_15704_b200.config import LfpsConfig
     from paper_2506_15704_b200.session import BatchedSession
-    from paper_2506_15704_b200.workload import GqaSpec, populate
+    from paper_2506_15704_b200.workload import GqaSpec, gen_unit, populate
     batch, ctx, layers, frac = 16, 131072, 32, 0.05
     b_local, b0 = shard_requests(batch, world, rank)
     T_in = 32
@@ -904,20 +909,34 @@ def run_c3(args, world, rank, local):
     n_max = ctx + args.warmup + args.steps + 8
     t_setup = time.time()
     sess = [BatchedSession(cfg, b_local, 8, 4, n_max=n_max, device=dev)]
-    stream = populate(sess[0], spec)
-    for _ in range(layers - 1):
+    streams = [populate(sess[0], spec)]
+    for layer in range(1, layers):
         s_l = BatchedSession(cfg, b_local, 8, 4, n_max=n_max, device=dev,
                              kv_cache=(sess[0].k_cache, sess[0].v_cache))
-        s_l.copy_tracker_from(sess[0])
+        s_l.n_ctx.copy_(sess[0].n_ctx)
+        s_l.n_host = list(sess[0].n_host)
+        q = torch.empty_like(streams[0].q)
+        finals = torch.empty(b_local, 32, 128, dtype=torch.bfloat16, device=dev)
+        for b in range(b_local):
+            for h in range(8):
+                u = gen_unit(spec, b, h, device=dev, layer=layer)
+                s_l.bootstrap_tables((b * 8 + h) * 4, u.weights)
+                q[:, b, h * 4:(h + 1) * 4] = u.queries.transpose(0, 1)
+                finals[b, h * 4:(h + 1) * 4] = u.final_query
+                del u
+        s_l.bootstrap_stats(finals)
+        torch.cuda.synchronize(dev)
+        s_l.check_errors(f"bootstrap layer {layer}")
         sess.append(s_l)
+        streams.append(type(streams[0])(q=q, k_new=streams[0].k_new, v_new=streams[0].v_new))
     for s_l in sess:
         s_l.split = not args.no_split
     setup_s = time.time() - t_setup
 
     def token_step(t):
         i = t % T_in
-        for s_l in sess:
-            s_l.decode_step(stream.q[i], stream.k_new[i], stream.v_new[i], frac)
+        for s_l, st in zip(sess, streams):
+            s_l.decode_step(st.q[i], st.k_new[i], st.v_new[i], frac)
 
     for t in range(args.warmup):
         token_step(t)
@@ -947,7 +966,8 @@ def run_c3(args, world, rank, local):
         "unit": "us/step", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
         "us_per_layer_step": ms * 1e3 / layers, "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic; one layer's KV cache shared by the 32 layer trackers",
+        "data": ("synthetic; one KV cache shared by the 32 layers, each layer with its own "
+                 "query stream, prefill weights, tables and priors"),
         "config": {"workload": "C3: batch 16 x 128k context, 32 layers, Llama-3.1-8B shapes, "
                                "Top-k 5%", "batch": batch, "batch_per_gpu": b_local,
                    "context": ctx, "layers": layers, "topk_fraction": frac,

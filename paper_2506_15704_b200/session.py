@@ -515,6 +515,14 @@ class BatchedSession:
         (kept for callers of round 1; check_errors now does this itself)."""
         self.sync_host_counts()
 
+    def gate_near_epsilon(self, tol: float = 1e-12) -> torch.Tensor:
+        """Sessions of the last step whose sink share rho lies within `tol`
+        of epsilon (bool [B, Hq]).  The gate's fp64 exp is the canonical
+        devmath.cexp, not libm's, so a rho this close to epsilon is where the
+        bypass decision could differ from the reference's (SURVEY §8(c)(4));
+        such decisions are reported, not hidden."""
+        return (self.rho - self.cfg.epsilon).abs() <= tol
+
     def result(self) -> BatchedStepResult:
         return BatchedStepResult(output=self.out, rho=self.rho, bypassed=self.bypass,
                                  counts=self.counts, c2_idx=self.c2_idx,

@@ -87,8 +87,14 @@ def _unit_generator(spec: GqaSpec, b: int, h: int, device) -> torch.Generator:
     return g
 
 
-def gen_unit(spec: GqaSpec, b: int, h: int, device="cpu", with_weights=True) -> GqaUnitData:
-    """Generate one (request b, KV-head h) unit."""
+def gen_unit(spec: GqaSpec, b: int, h: int, device="cpu", with_weights=True,
+             layer: int = 0) -> GqaUnitData:
+    """Generate one (request b, KV-head h) unit.
+
+    ``layer`` > 0 gives another attention layer over the SAME K/V rows (the
+    keys, values and planted band directions are layer 0's): its query walk
+    and jitter come from a layer-specific generator, so its queries, prefill
+    weights (hence tables) and trajectory differ (bench.py C3)."""
     d, G, S = spec.d, spec.group, spec.sink_count
     n0, steps = spec.n_prefill, spec.steps
     total = n0 + steps
@@ -111,6 +117,11 @@ def gen_unit(spec: GqaSpec, b: int, h: int, device="cpu", with_weights=True) -> 
     first_q = n0 - spec.s
     # AR(1) query walk per head
     base = torch.randn(G, nq, d, generator=gen, device=device, dtype=f32)
+    qgen = gen
+    if layer:
+        qgen = torch.Generator(device=device)
+        qgen.manual_seed(spec.seed * 1_000_003 + b * 1009 + h + 7_919_000 * layer)
+        base = torch.randn(G, nq, d, generator=qgen, device=device, dtype=f32)
     rho = spec.query_correlation
     blend = math.sqrt(1.0 - rho * rho)
     walk = torch.empty_like(base)
@@ -144,14 +155,14 @@ def gen_unit(spec: GqaSpec, b: int, h: int, device="cpu", with_weights=True) -> 
         for g in range(G):
             if jit:
                 for j in range(nb):
-                    side = torch.where(torch.rand(nq, generator=gen, device=device) < 0.5, 1, -1)
-                    mag = torch.randint(max(0, w - 1), w + jit + 1, (nq,), generator=gen,
+                    side = torch.where(torch.rand(nq, generator=qgen, device=device) < 0.5, 1, -1)
+                    mag = torch.randint(max(0, w - 1), w + jit + 1, (nq,), generator=qgen,
                                         device=device)
                     pos = (centres[g][j] + side * mag).clamp(min=S)
                     pos = torch.minimum(pos, t_idx)
                     boost(g, pos, spec.signal_gain)
             for o in spec.offsets:
-                dj = torch.randint(-jit, jit + 1, (nq,), generator=gen, device=device) if jit \
+                dj = torch.randint(-jit, jit + 1, (nq,), generator=qgen, device=device) if jit \
                     else torch.zeros(nq, dtype=torch.long, device=device)
                 pos = (t_idx - o + dj).clamp(min=S)
                 pos = torch.minimum(pos, t_idx)
