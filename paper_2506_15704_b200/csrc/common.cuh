@@ -82,14 +82,17 @@ struct Ctx {
 enum { CNT_C0 = 0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_BLOCKS, CNT_N };
 
 // Row r of unit (b, h) -> its row number in the K / V buffers (row = d
-// elements): the unit's contiguous span, or the block table's block
-struct RowMap {
+// elements): the unit's contiguous span, or the block table's block.
+// MODE 0: contiguous only; 1: block table only; 2: decided per call
+// (c.bt), for the kernels off the hot path.
+template <int MODE>
+struct RowMapT {
   const int* bt;      // this request's block-table row (block table mode)
   int base;           // first row of the unit (contiguous), or h (block table)
   int shift, mask, hkv;
-  __device__ __forceinline__ RowMap(const Ctx& c, int b, int h) {
+  __device__ __forceinline__ RowMapT(const Ctx& c, int b, int h) {
     shift = c.bs_shift; mask = c.bs_mask; hkv = c.Hkv;
-    if (c.bt) {
+    if (MODE == 1 || (MODE == 2 && c.bt)) {
       bt = c.bt + (size_t)b * c.max_blocks;
       base = h;
     } else {
@@ -98,10 +101,11 @@ struct RowMap {
     }
   }
   __device__ __forceinline__ int operator()(int r) const {
-    if (!bt) return base + r;
+    if (MODE == 0 || (MODE == 2 && !bt)) return base + r;
     return ((__ldg(bt + (r >> shift)) << shift) | (r & mask)) * hkv + base;
   }
 };
+using RowMap = RowMapT<2>;
 
 __device__ __forceinline__ const __nv_bfloat16* krow(const Ctx& c, int b, int h, int i) {
   return c.K + (size_t)RowMap(c, b, h)(i) * c.d;

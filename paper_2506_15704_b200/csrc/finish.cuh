@@ -94,7 +94,7 @@ __device__ __forceinline__ void finish_tail(const Ctx& c, int s, uint8_t* stages
 
 // The whole back half of one session's step, run by a 256-thread CTA.
 // `stages` is kStages x [K tile | V tile] of dynamic shared memory.
-template <int PQ>
+template <int PQ, int RM>
 __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16* q, int s,
                                                uint8_t* stages, FinishShared& sh) {
   const int tid = threadIdx.x;
@@ -113,9 +113,13 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
   if ((c.flags & LFPS_FLAG_TRACE) && tid == 0) c.trace[(size_t)s * 16 + 13] = now_ns();
   const int* pidx = c.probe_idx + (size_t)s * c.list_cap;
   float* pz = c.probe_score + (size_t)s * c.list_cap;
-  const __nv_bfloat16* kb = c.K;                        // rows addressed through rm
-  const __nv_bfloat16* vb = c.V;
-  const RowMap rm(c, b, h);
+  // contiguous cache: the unit's base in registers and unit-local rows
+  // (parameter-bank bases get rematerialised inside the row loop);
+  // block table: the pool base and pool rows
+  const __nv_bfloat16* kb = RM == 0 ? krow(c, b, h, 0) : c.K;
+  const __nv_bfloat16* vb = RM == 0 ? vrow(c, b, h, 0) : c.V;
+  const RowMapT<RM> rmap(c, b, h);
+  auto rm = [&](int r) { return RM == 0 ? r : rmap(r); };
   const Part<PQ> qp = ld_part<PQ>(q + (size_t)s * c.d, l8);   // packed bf16 partials of q
   int k = (int)rint(c.frac * (double)n);
   if (k < 1) k = 1;

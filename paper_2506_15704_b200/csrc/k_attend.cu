@@ -33,9 +33,11 @@ __global__ void __launch_bounds__(kThreads, kRowCtas) lfps_exact_attend_kernel(C
   const int k2 = c.counts[(size_t)s * CNT_N + CNT_C2];
   const int* c2i = c.c2_idx + (size_t)s * c.list_cap;
   const float* c2z = c.c2_score + (size_t)s * c.list_cap;
-  const __nv_bfloat16* kb = c.K;                        // rows addressed through rm
-  const __nv_bfloat16* vb = c.V;
-  const RowMap rm(c, b, h);
+  // contiguous: the unit's base, unit-local rows; block table: pool rows
+  const RowMap rmap(c, b, h);
+  const __nv_bfloat16* kb = c.bt ? c.K : krow(c, b, h, 0);
+  const __nv_bfloat16* vb = c.bt ? c.V : vrow(c, b, h, 0);
+  auto rm = [&](int r) { return c.bt ? rmap(r) : r; };
   const Part<PQ> qp = ld_part<PQ>(q + (size_t)s * c.d, l8);
   stream_rows<kScore, PQ>(
       stages, kb, vb, S, [&](int rid) { return rm(rid); },

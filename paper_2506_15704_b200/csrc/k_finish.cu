@@ -39,29 +39,36 @@ namespace {
 
 using namespace fin;
 
-template <int PQ>
+// RM: the row mapping (RowMapT) -- 0 contiguous cache, 1 block table
+template <int PQ, int RM>
 __global__ void __launch_bounds__(kThreads, kRowCtas) lfps_finish_kernel(Ctx c, const __nv_bfloat16* q) {
   extern __shared__ __align__(128) uint8_t stages[];      // kStages x [K tile | V tile]
   __shared__ FinishShared sh;
   pdl_wait();                                             // the select kernel's lists
-  finish_session<PQ>(c, q, c.s_off + blockIdx.x, stages, sh);
+  finish_session<PQ, RM>(c, q, c.s_off + blockIdx.x, stages, sh);
   pdl_trigger();
 }
 
-template <int PQ>
-cudaError_t launch_finish_d(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
+template <int PQ, int RM>
+cudaError_t launch_finish_rm(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
   const size_t smem = rows_smem(c.d);
   static DeviceOnce once;
   cudaError_t e = once.run([&] {
-    cudaError_t r = cudaFuncSetAttribute(lfps_finish_kernel<PQ>,
+    cudaError_t r = cudaFuncSetAttribute(lfps_finish_kernel<PQ, RM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (r == cudaSuccess)
-      r = cudaFuncSetAttribute(lfps_finish_kernel<PQ>, cudaFuncAttributePreferredSharedMemoryCarveout,
+      r = cudaFuncSetAttribute(lfps_finish_kernel<PQ, RM>,
+                               cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
     return r;
   });
   if (e != cudaSuccess) return e;
-  return launch_pdl(lfps_finish_kernel<PQ>, dim3(c.s_cnt), dim3(kThreads), smem, st, c, q);
+  return launch_pdl(lfps_finish_kernel<PQ, RM>, dim3(c.s_cnt), dim3(kThreads), smem, st, c, q);
+}
+
+template <int PQ>
+cudaError_t launch_finish_d(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
+  return c.bt ? launch_finish_rm<PQ, 1>(c, q, st) : launch_finish_rm<PQ, 0>(c, q, st);
 }
 
 }  // namespace

@@ -48,7 +48,8 @@ __device__ __forceinline__ Part<PQ> ldg_part(const __nv_bfloat16* row, int l8) {
   return r;
 }
 
-template <int PQ, int G>
+// RM: RowMapT mode -- 0 contiguous cache (unit base, local rows), 1 block table
+template <int PQ, int G, int RM>
 __global__ void __launch_bounds__(kThreads, LFPS_SCORE_CTAS) lfps_exact_score_kernel(Ctx c, const __nv_bfloat16* q) {
   const int u = blockIdx.y;
   const int b = u / c.Hkv, h = u % c.Hkv;
@@ -74,7 +75,11 @@ __global__ void __launch_bounds__(kThreads, LFPS_SCORE_CTAS) lfps_exact_score_ke
       q2[g][2 * t + 1] = make_float2(bf_hi(qp.a[t]), bf_hi(qp.b[t]));
     }
   }
-  const RowMap rm(c, b, h);
+  // contiguous: the unit's base in registers, unit-local rows; block table:
+  // the pool base, pool rows (RowMap)
+  const RowMapT<RM> rmap(c, b, h);
+  const __nv_bfloat16* kbase = RM ? c.K : krow(c, b, h, 0);
+  auto rm = [&](int r) { return RM ? rmap(r) : r; };
   const int gs = l8 % G;                              // the head this lane divides and writes
   float* out = c.probe_score + (size_t)(s0 + gs) * c.list_cap;
   // K rows stream through shared memory, kScoreStages tiles of kStep rows:
@@ -86,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_SCORE_CTAS) lfps_exact_score_ke
   constexpr int kChunks = kRowB / 16;
   constexpr int kStageB = kStep * kRowB;
   const uint32_t sb = smem_u32(kst) + grp * kRowB;
-  const uint8_t* kb8 = reinterpret_cast<const uint8_t*>(c.K) + l8 * 16;
+  const uint8_t* kb8 = reinterpret_cast<const uint8_t*>(kbase) + l8 * 16;
   const int ntiles = (r1 - r0 + kStep - 1) / kStep;
   auto issue = [&](int tile) {
     if (tile < ntiles) {
@@ -142,8 +147,8 @@ __global__ void __launch_bounds__(kThreads, LFPS_SCORE_CTAS) lfps_exact_score_ke
   cp_async_wait<0>();
 }
 
-template <int PQ>
-cudaError_t launch_exact_d(const Ctx& c, const __nv_bfloat16* q, int m_max, cudaStream_t st) {
+template <int PQ, int RM>
+cudaError_t launch_exact_rm(const Ctx& c, const __nv_bfloat16* q, int m_max, cudaStream_t st) {
   const int units = c.B * c.Hkv;
   // ~4 waves of 148 SMs x 2 CTAs over all units, >= 1 step of rows per CTA
   int per_unit = (148 * 2 * 4 + units - 1) / units;
@@ -160,14 +165,19 @@ cudaError_t launch_exact_d(const Ctx& c, const __nv_bfloat16* q, int m_max, cuda
   };
   cudaError_t e;
   switch (c.G) {
-    case 1: e = go(lfps_exact_score_kernel<PQ, 1>); break;
-    case 2: e = go(lfps_exact_score_kernel<PQ, 2>); break;
-    case 4: e = go(lfps_exact_score_kernel<PQ, 4>); break;
-    case 8: e = go(lfps_exact_score_kernel<PQ, 8>); break;
+    case 1: e = go(lfps_exact_score_kernel<PQ, 1, RM>); break;
+    case 2: e = go(lfps_exact_score_kernel<PQ, 2, RM>); break;
+    case 4: e = go(lfps_exact_score_kernel<PQ, 4, RM>); break;
+    case 8: e = go(lfps_exact_score_kernel<PQ, 8, RM>); break;
     default: return cudaErrorInvalidValue;
   }
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+template <int PQ>
+cudaError_t launch_exact_d(const Ctx& c, const __nv_bfloat16* q, int m_max, cudaStream_t st) {
+  return c.bt ? launch_exact_rm<PQ, 1>(c, q, m_max, st) : launch_exact_rm<PQ, 0>(c, q, m_max, st);
 }
 
 }  // namespace
