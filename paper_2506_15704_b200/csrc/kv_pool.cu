@@ -99,9 +99,24 @@ struct lfps_kv_pool {
   std::vector<std::vector<CUmemGenericAllocationHandle>> pages[2];   // per (b, h)
   int64_t mapped = 0;
   std::mutex mu;
+  cudaStream_t zero = nullptr;     // zeroes fresh pages (created on first growth)
 };
 
 namespace {
+
+// the pool's device current for the scope of a call (callers may sit on
+// another device); restores the caller's device
+struct DeviceScope {
+  int prev = -1;
+  explicit DeviceScope(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceScope() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
 
 int unmap_span(const Driver* drv, lfps_kv_pool* p, size_t u) {
   int rc = LFPS_OK;
@@ -178,6 +193,7 @@ int lfps_kv_pool_reserve(lfps_kv_pool* p, int32_t b, int32_t h, int64_t rows) {
   const Driver* drv = driver();
   if (!drv) return no_driver();
   std::lock_guard<std::mutex> g(p->mu);
+  DeviceScope scope(p->dev);
   const size_t u = (size_t)b * p->Hkv + h;
   const int64_t want_rows = rows + kSlackRows < p->n_max ? rows + kSlackRows : p->n_max;
   const size_t want = ((size_t)want_rows * p->d * 2 + p->page - 1) / p->page;
@@ -207,13 +223,16 @@ int lfps_kv_pool_reserve(lfps_kv_pool* p, int32_t b, int32_t h, int64_t rows) {
       p->mapped += (int64_t)p->page;
       // fresh pages hold whatever the memory held: zero them, as the
       // contiguous cache is, so that padding rows a kernel touches past the
-      // context (weight 0) are finite
-      if (cudaMemsetAsync(reinterpret_cast<void*>(at), 0, p->page, 0) != cudaSuccess)
+      // context (weight 0) are finite -- on the pool's own stream, so the
+      // wait below does not drain the device
+      if (!p->zero && cudaStreamCreateWithFlags(&p->zero, cudaStreamNonBlocking) != cudaSuccess)
+        return lfps_abi_fail(LFPS_E_CUDA, "cudaStreamCreate failed");
+      if (cudaMemsetAsync(reinterpret_cast<void*>(at), 0, p->page, p->zero) != cudaSuccess)
         return lfps_abi_fail(LFPS_E_CUDA, "cudaMemsetAsync failed");
       grew = true;
     }
   }
-  if (grew && cudaStreamSynchronize(0) != cudaSuccess)
+  if (grew && cudaStreamSynchronize(p->zero) != cudaSuccess)
     return lfps_abi_fail(LFPS_E_CUDA, "cudaStreamSynchronize failed");
   return LFPS_OK;
 }
@@ -223,7 +242,8 @@ int lfps_kv_pool_release(lfps_kv_pool* p, int32_t b) {
   if (b < 0 || b >= p->B) return lfps_abi_fail(LFPS_E_INVALID, "release: request out of range");
   const Driver* drv = driver();
   if (!drv) return no_driver();
-  // the caller's queued work may still read these rows
+  DeviceScope scope(p->dev);
+  // the caller's queued work on the pool's device may still read these rows
   if (cudaDeviceSynchronize() != cudaSuccess)
     return lfps_abi_fail(LFPS_E_CUDA, "cudaDeviceSynchronize failed");
   std::lock_guard<std::mutex> g(p->mu);
@@ -244,8 +264,10 @@ int lfps_kv_pool_destroy(lfps_kv_pool* p) {
   if (!p) return LFPS_OK;
   const Driver* drv = driver();
   if (!drv) return no_driver();
+  DeviceScope scope(p->dev);
   if (cudaDeviceSynchronize() != cudaSuccess)
     return lfps_abi_fail(LFPS_E_CUDA, "cudaDeviceSynchronize failed");
+  if (p->zero) cudaStreamDestroy(p->zero);
   int rc = LFPS_OK;
   {
     std::lock_guard<std::mutex> g(p->mu);

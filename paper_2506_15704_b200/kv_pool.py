@@ -69,8 +69,9 @@ class KvPool:
         """Back rows [0, rows) (+ the kernels' slack) of request b, all heads."""
         if rows <= self.backed[b]:
             return
-        for h in range(self.dims.kv_heads):
-            _lib.check(self.lib.lfps_kv_pool_reserve(self._h, b, h, rows), "kv pool reserve")
+        with torch.cuda.device(self.device):
+            for h in range(self.dims.kv_heads):
+                _lib.check(self.lib.lfps_kv_pool_reserve(self._h, b, h, rows), "kv pool reserve")
         want = min(rows + SLACK_ROWS, self.dims.n_max)
         pages = -(-want // self.rows_per_page)
         self.backed[b] = (self.dims.n_max if want >= self.dims.n_max
@@ -78,7 +79,8 @@ class KvPool:
 
     def release(self, b: int) -> None:
         """Unmap request b's pages (its rows become inaccessible)."""
-        _lib.check(self.lib.lfps_kv_pool_release(self._h, b), "kv pool release")
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.lfps_kv_pool_release(self._h, b), "kv pool release")
         self.backed[b] = 0
 
     def mapped_bytes(self) -> int:
