@@ -65,11 +65,17 @@ class KvPool:
         self.rows_per_page = page_bytes() // (2 * dims.d)
         self.backed = [0] * dims.batch          # rows usable per request (all heads)
 
+    def _on_device(self):
+        """The pool's device current for a C call (the caller may be on another)."""
+        import contextlib
+        dev = getattr(self, "device", None)
+        return torch.cuda.device(dev) if dev is not None else contextlib.nullcontext()
+
     def reserve(self, b: int, rows: int) -> None:
         """Back rows [0, rows) (+ the kernels' slack) of request b, all heads."""
         if rows <= self.backed[b]:
             return
-        with torch.cuda.device(self.device):
+        with self._on_device():
             for h in range(self.dims.kv_heads):
                 _lib.check(self.lib.lfps_kv_pool_reserve(self._h, b, h, rows), "kv pool reserve")
         want = min(rows + SLACK_ROWS, self.dims.n_max)
@@ -79,7 +85,7 @@ class KvPool:
 
     def release(self, b: int) -> None:
         """Unmap request b's pages (its rows become inaccessible)."""
-        with torch.cuda.device(self.device):
+        with self._on_device():
             _lib.check(self.lib.lfps_kv_pool_release(self._h, b), "kv pool release")
         self.backed[b] = 0
 
