@@ -1,9 +1,10 @@
 """Small end-to-end run for compute-sanitizer (memcheck / racecheck / synccheck):
-decode steps through the per-session and the per-unit finish, a Top-k (1%)
-step, and the exact path, on a B=1, 2 KV-head, G=4, n=2048 batch; then two
-steps of a 256-session batch (8 x 8 KV heads x 4, d=64) through the
-two-group stream split, the second with host inputs and output
-(lfps_decode_step_host_io)."""
+decode steps, a Top-k (1%) step, and the exact path, on a B=1, 2 KV-head,
+G=4, n=2048 batch; two steps of a 256-session batch (8 x 8 KV heads x 4,
+d=64) through the two-group stream split, the second with host inputs and
+output (lfps_decode_step_host_io); two steps and the exact path over a
+block-table KV cache; and the per-head fp64 stage API (k_stages.cu):
+prefill_bootstrap, decode steps, topk_oracle, full attention."""
 import os
 import sys
 
@@ -51,5 +52,31 @@ for t in range(2):
     pair.host_io = t == 1           # lfps_decode_step_host_io: input copy beside stats
     res, outs = pair.step(Q[:, :, :, t], K[:, :, 700 + t], V[:, :, 700 + t], 0.05)
     pair.compare_step(res, outs, tables=(t == 1))
+torch.cuda.synchronize()
+
+# block-table KV (16-row blocks in a random order)
+from gpu_drive import gqa_pair  # noqa: E402
+pair, K, V, Q = gqa_pair(batch=2, kv_heads=2, n0=1500, steps=2, seed=59, block_rows=16)
+for t in range(2):
+    res, outs = pair.step(Q[:, :, :, t], K[:, :, 1500 + t], V[:, :, 1500 + t], 0.05)
+    pair.compare_step(res, outs)
+pair.sess.exact_topk_step(gpu_drive.bf16(Q[:, :, :, 1].reshape(2, -1, 128)).cuda(), 0.05)
+torch.cuda.synchronize()
+
+# the per-head stage API (fp64)
+import paper_2506_15704_b200.lfps as lfps  # noqa: E402
+rng = np.random.default_rng(3)
+n, d, s_ = 300, 32, 4
+cfg = lfps.LfpsConfig(d=d, s=s_, sink_count=2, local_window=3)
+w = rng.random((s_, n - 2))
+w /= w.sum(axis=1, keepdims=True)
+ses = lfps.prefill_bootstrap(rng.standard_normal((n, d)), rng.standard_normal((n, d)), w,
+                             rng.standard_normal(d), cfg)
+for _ in range(4):
+    lfps.decode_step(ses, rng.standard_normal(d), rng.standard_normal(d), rng.standard_normal(d),
+                     0.05)
+q = rng.standard_normal(d)
+lfps.topk_oracle(q, ses.store, 15, 2)
+lfps.full_attention_oracle(q, ses.store)
 torch.cuda.synchronize()
 print("sanitize run ok")
