@@ -104,6 +104,11 @@ typedef struct lfps_params {
 } lfps_params;
 
 /* lfps_params.flags */
+#define LFPS_FLAG_GRAPH 16       /* enqueue a decode step as one CUDA-graph launch: the
+                                    step is captured once per (shapes, params,
+                                    state, workspace, device buffers, context
+                                    bucket) and replayed; the call stamp is then
+                                    drawn on the device (ws.done[1]) */
 #define LFPS_FLAG_SPLIT 8        /* run two session halves' gate/select/finish on two
                                     internal streams (fork/join on the caller's) */
 #define LFPS_FLAG_TRACE 2        /* per-session phase timestamps (clock64 deltas and
@@ -172,7 +177,8 @@ typedef struct lfps_ws_layout {
   size_t valid;       /* i32 [NS] summaries of session s are current */
   size_t wstat;       /* f64 [NS, 2] max and normaliser of the update softmax */
   size_t trace;       /* i64 [NS, 16] phase timestamps (LFPS_FLAG_TRACE) */
-  size_t done;        /* u32 commit-kernel completion counter (kept at 0) */
+  size_t done;        /* u32 [16]: [0] commit-kernel completion counter (kept at
+                         0), [1] the call stamp of a CUDA-graph step */
   size_t hot;         /* i32x2 [2 NS, 16 nblk + 1] per-step C0 words of each
                          table: (count, table blocks read), then (logical
                          index of the word's first slot, slot bits) */

@@ -22,6 +22,7 @@ ABI_VERSION = 7
 FLAG_EXPORT_SETS = 1
 FLAG_TRACE = 2
 FLAG_SPLIT = 8
+FLAG_GRAPH = 16
 
 # per-session device error codes (include/lfps_b200.h)
 ERR_NAMES = {

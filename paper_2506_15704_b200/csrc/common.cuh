@@ -37,6 +37,8 @@ struct Ctx {
   int s, S, L, bypass_mode, exhaustive, n_off, flags;
   int s_off, s_cnt;   // session range [s_off, s_off + s_cnt) of a per-session launch
   int epoch;          // call stamp in [1, 2^27): err[0] == epoch <=> this call failed
+  const int* stamp;   // CUDA-graph steps: the stamp in device memory (set by the
+                      // step's first kernel), used instead of epoch
   int off[16];
   // state
   const __nv_bfloat16* K;
@@ -117,10 +119,14 @@ __device__ __forceinline__ const __nv_bfloat16* vrow(const Ctx& c, int b, int h,
 // err[1 + s] = (call stamp << 4) | code: a code counts only for the call whose
 // stamp err[0] holds, so no kernel has to clear the codes before the gate and
 // the stats kernel (which run concurrently) may raise them
-__device__ __forceinline__ int err_code(const Ctx& c, int code) { return (c.epoch << 4) | code; }
+__device__ __forceinline__ int call_stamp(const Ctx& c) {
+  return c.stamp ? *reinterpret_cast<const volatile int*>(c.stamp) : c.epoch;
+}
+__device__ __forceinline__ int err_code(const Ctx& c, int code) { return (call_stamp(c) << 4) | code; }
 __device__ __forceinline__ void set_err(const Ctx& c, int s, int code) {
-  c.err[1 + s] = err_code(c, code);
-  atomicExch(c.err, c.epoch);
+  const int ep = call_stamp(c);
+  c.err[1 + s] = (ep << 4) | code;
+  atomicExch(c.err, ep);
 }
 
 // phase timestamps (LFPS_FLAG_TRACE): slot k of session s = clock64() - t0;
@@ -194,6 +200,7 @@ cudaError_t launch_overlap(const Ctx& c, const int* sel, const int* sel_cnt, con
                            const int* ex_cnt, int list_stride, int cnt_stride, double* eta,
                            cudaStream_t st);
 cudaError_t launch_clear_err(const Ctx& c, cudaStream_t st);
+cudaError_t launch_step_begin(const Ctx& c, cudaStream_t st);
 
 // per-head stage API (k_stages.cu), fp64
 cudaError_t stage_logits(const double* keys, int d, const int64_t* rows, int nrows, const double* q,

@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
   const int b = s / c.Hq, qh = s % c.Hq;
   pdl_wait();                                 // the finish kernel's lists and scores
   // independent prologue loads, issued together
-  const int failed = c.err[0] == c.epoch;
+  const int ep = call_stamp(c);
+  const int failed = c.err[0] == ep;
   const int n = c.n_ctx[b];
   int base = c.sla_base[s];
   const int byp = c.bypass[s];
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
     const bool wok = fabs(wsum - 1.0) <= 1e-6;        // block-uniform
     if (!wok && tid == 0) {                  // reported, but not as a failed step:
       c.err[1 + s] = err_code(c, LFPS_ERR_WEIGHT_SUM);   // the other sessions commit
-      atomicExch(c.err, -c.epoch);
+      atomicExch(c.err, -ep);
       // the unit's row is still appended, so this session's tables grow like a
       // gated step's (no update) and stay in step with the KV store
       ver[m] = 0.0;
@@ -278,10 +279,18 @@ __global__ void __launch_bounds__(kThreads, LFPS_UPDATE_CTAS) lfps_update_kernel
       // err[0] after a step: 0 = committed (a stale stamp of an earlier failed
       // call is dropped here), this call's stamp = failed
       const int e0 = atomicAdd(c.err, 0);
-      if (e0 != c.epoch && e0 != -c.epoch) c.err[0] = 0;
+      if (e0 != ep && e0 != -ep) c.err[0] = 0;
     }
   }
   pdl_trigger();
+}
+
+// first node of a CUDA-graph decode step: the step's call stamp, drawn in
+// device memory from [2^26, 2^27 - 2) (host-drawn stamps are below 2^26)
+__global__ void lfps_step_begin_kernel(int* stamp) {
+  int e = *stamp + 1;
+  if (e < (1 << 26) || e >= (1 << 27) - 2) e = 1 << 26;
+  *stamp = e;
 }
 
 __global__ void lfps_clear_err_kernel(Ctx c) {
@@ -294,6 +303,11 @@ __global__ void lfps_clear_err_kernel(Ctx c) {
 cudaError_t launch_update(const Ctx& c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new,
                           cudaStream_t st) {
   return launch_pdl(lfps_update_kernel, dim3(c.NS), dim3(kThreads), 0, st, c, k_new, v_new);
+}
+
+cudaError_t launch_step_begin(const Ctx& c, cudaStream_t st) {
+  lfps_step_begin_kernel<<<1, 1, 0, st>>>(const_cast<int*>(c.stamp));
+  return cudaGetLastError();
 }
 
 cudaError_t launch_clear_err(const Ctx& c, cudaStream_t st) {

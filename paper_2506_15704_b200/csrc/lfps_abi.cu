@@ -283,7 +283,7 @@ cudaEvent_t prof_event() {
 // so no clearing kernel is needed (per-session codes are cleared by the gate)
 std::atomic<int> g_epoch{1};
 int next_epoch() {
-  int e = g_epoch.fetch_add(1) & 0x7ffffff;          // stamp << 4 fits an int32
+  int e = g_epoch.fetch_add(1) & 0x3ffffff;          // < 2^26; graph steps draw [2^26, 2^27)
   return (e && e != kOtherStamp) ? e : next_epoch();
 }
 
@@ -310,11 +310,43 @@ struct Pipe {
   cudaEvent_t out_ready = nullptr, out_done = nullptr;
   cudaStream_t in = nullptr;                // host input copy beside the stats kernel
   cudaEvent_t in_ready = nullptr;
+  cudaStream_t cap = nullptr;               // CUDA-graph capture of a decode step
+  std::vector<struct StepGraph*> graphs;    // captured steps, most recent last
 };
 std::mutex g_pipe_mu;
+
+// A decode step captured as a CUDA graph (see decode_impl): everything a
+// replay cannot change is in the key; the host buffers of the input and
+// output copies are set per replay on their memcpy nodes.
+struct GraphKey {
+  lfps_dims dims;
+  lfps_params params;
+  lfps_state state;
+  const void* ws;
+  const void *q, *k_new, *v_new;
+  int m_bucket, has_in, has_out;
+  bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(*this)) == 0; }
+};
+struct StepGraph {
+  GraphKey key;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t in_node = nullptr, out_node = nullptr;
+  const void* in_host = nullptr;
+  void* out_host = nullptr;
+  size_t in_bytes = 0, out_bytes = 0;
+  ~StepGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  }
+};
+constexpr int kMaxGraphs = 4;
 std::map<std::pair<int, const void*>, std::unique_ptr<Pipe>> g_pipes;
 
 void destroy_pipe(Pipe& p) {
+  for (StepGraph* g : p.graphs) delete g;
+  p.graphs.clear();
+  if (p.cap) cudaStreamDestroy(p.cap);
   for (cudaStream_t* sp : {&p.st[0], &p.st[kSplitGroups - 1], &p.aux[0], &p.aux[kSplitGroups - 1],
                            &p.copy, &p.in})
     if (*sp) cudaStreamSynchronize(*sp);
@@ -343,6 +375,7 @@ cudaError_t create_pipe(Pipe& p) {
   if ((e = cudaEventCreateWithFlags(&p.out_ready, cudaEventDisableTiming)) != cudaSuccess) return e;
   if ((e = cudaEventCreateWithFlags(&p.out_done, cudaEventDisableTiming)) != cudaSuccess) return e;
   if ((e = cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking)) != cudaSuccess) return e;
+  if ((e = cudaStreamCreateWithFlags(&p.cap, cudaStreamNonBlocking)) != cudaSuccess) return e;
   return cudaEventCreateWithFlags(&p.in_ready, cudaEventDisableTiming);
 }
 
@@ -531,43 +564,31 @@ int lfps_decode_step_host_io(const lfps_dims* dims, const lfps_params* p, const 
   return decode_impl(dims, p, st, ws, q, k_new, v_new, n_host, out_host, in_host, stream);
 }
 
-static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
-                       const lfps_workspace* ws, const void* q, const void* k_new,
-                       const void* v_new, const int32_t* n_host, void* out_host,
-                       const void* in_host, void* stream) {
-  lfps::Ctx c;
-  int rc = make_ctx(dims, p, st, ws, &c);
-  if (rc) return rc;
-  if (!q || !k_new || !v_new) return fail(LFPS_E_INVALID, "q/k_new/v_new is NULL");
-  int m_max = 0;
-  rc = check_context(c, n_host, true, &m_max);
-  if (rc) return rc;
-  cudaStream_t sm = static_cast<cudaStream_t>(stream);
+// Enqueue one decode step on stream sm (the caller's, or the capture stream).
+// The stats kernel does not depend on the gate (it serves every session), so
+// the two run concurrently: stats on an internal stream forked from sm,
+// joined before select.  LFPS_FLAG_SPLIT additionally runs kSplitGroups
+// session groups, each [gate | stats] -> select -> finish, on their own
+// streams; the update (commit) joins them on sm.  Under lfps_profile_enable
+// everything runs serially on sm so each kernel is timed alone.  Host
+// inputs (lfps_decode_step_host_io): q | k_new | v_new are contiguous from q
+// on; the copy starts with the step on its own stream (after the caller's
+// previous work, which may still read the buffer) and only the gate waits
+// for it -- the stats kernel does not read the inputs.  A graph step
+// (c.stamp set) starts with the kernel that draws its call stamp.
+static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const void* q,
+                        const void* k_new, const void* v_new, void* out_host,
+                        const void* in_host, int m_max) {
   const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
-  c.epoch = next_epoch();
-  // The stats kernel does not depend on the gate (it serves every session),
-  // so the two run concurrently: stats on an internal stream forked from
-  // the caller's, joined before select.  LFPS_FLAG_SPLIT additionally runs
-  // kSplitGroups session groups, each [gate | stats] -> select -> finish, on
-  // their own streams; the update (commit) joins them on the caller's
-  // stream.  Under lfps_profile_enable everything runs serially on the
-  // caller's stream so each kernel is timed alone.
-  // host inputs (lfps_decode_step_host_io): q | k_new | v_new are contiguous
-  // from q on; the copy starts with the call on its own stream (after the
-  // caller's previous work, which may still read the buffer) and only the
-  // gate waits for it -- the stats kernel does not read the inputs
   const size_t in_bytes = ((size_t)c.NS + 2 * (size_t)c.B * c.Hkv) * c.d * sizeof(__nv_bfloat16);
+  if (c.stamp) LAUNCH(lfps::launch_step_begin(c, sm));
   if (in_host && g_prof_on)
     LAUNCH(cudaMemcpyAsync(const_cast<void*>(q), in_host, in_bytes, cudaMemcpyHostToDevice, sm));
   if (g_prof_on) {
     LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
     LAUNCH_P("stats", sm, lfps::launch_stats(c, sm));
     LAUNCH_P("select", sm, lfps::launch_select(c, m_max, sm));
-  }
-  Pipe* pp = nullptr;
-  LAUNCH(get_pipe(ws->base, &pp));
-  std::lock_guard<std::mutex> pipe_lock(pp->mu);
-  if (!g_prof_on) {
+  } else {
     LAUNCH(cudaEventRecord(pp->fork, sm));
     if (in_host) {
       LAUNCH(cudaStreamWaitEvent(pp->in, pp->fork, 0));
@@ -611,6 +632,110 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
   LAUNCH_P("update", sm, lfps::launch_update(c, static_cast<const __nv_bfloat16*>(k_new),
                                               static_cast<const __nv_bfloat16*>(v_new), sm));
   if (out_host) LAUNCH(cudaStreamWaitEvent(sm, pp->out_done, 0));
+  return LFPS_OK;
+}
+
+// Capture a step as a CUDA graph (on the pipe's capture stream) and find its
+// host-copy nodes.
+static int capture_step(lfps::Ctx c, Pipe* pp, const GraphKey& key, const void* q,
+                        const void* k_new, const void* v_new, void* out_host,
+                        const void* in_host, int m_bucket, StepGraph** out) {
+  StepGraph* g = new StepGraph();
+  g->key = key;
+  cudaError_t e = cudaStreamBeginCapture(pp->cap, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) { delete g; return cuda_fail(e, "cudaStreamBeginCapture"); }
+  const int rc = enqueue_step(c, pp, pp->cap, q, k_new, v_new, out_host, in_host, m_bucket);
+  e = cudaStreamEndCapture(pp->cap, &g->graph);
+  if (rc) { delete g; return rc; }
+  if (e != cudaSuccess) { delete g; return cuda_fail(e, "cudaStreamEndCapture"); }
+  size_t nn = 0;
+  if ((e = cudaGraphGetNodes(g->graph, nullptr, &nn)) != cudaSuccess) { delete g; return cuda_fail(e, "cudaGraphGetNodes"); }
+  std::vector<cudaGraphNode_t> nodes(nn);
+  if ((e = cudaGraphGetNodes(g->graph, nodes.data(), &nn)) != cudaSuccess) { delete g; return cuda_fail(e, "cudaGraphGetNodes"); }
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nd, &t) != cudaSuccess || t != cudaGraphNodeTypeMemcpy) continue;
+    cudaMemcpy3DParms mp = {};
+    if (cudaGraphMemcpyNodeGetParams(nd, &mp) != cudaSuccess) continue;
+    if (mp.kind == cudaMemcpyHostToDevice) g->in_node = nd;
+    else if (mp.kind == cudaMemcpyDeviceToHost) g->out_node = nd;
+  }
+  if ((e = cudaGraphInstantiate(&g->exec, g->graph, 0)) != cudaSuccess) {
+    delete g;
+    return cuda_fail(e, "cudaGraphInstantiate");
+  }
+  g->in_host = in_host;
+  g->out_host = out_host;
+  g->in_bytes = ((size_t)c.NS + 2 * (size_t)c.B * c.Hkv) * c.d * sizeof(__nv_bfloat16);
+  g->out_bytes = (size_t)c.NS * c.d * sizeof(float);
+  *out = g;
+  return LFPS_OK;
+}
+
+static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
+                       const lfps_workspace* ws, const void* q, const void* k_new,
+                       const void* v_new, const int32_t* n_host, void* out_host,
+                       const void* in_host, void* stream) {
+  lfps::Ctx c;
+  int rc = make_ctx(dims, p, st, ws, &c);
+  if (rc) return rc;
+  if (!q || !k_new || !v_new) return fail(LFPS_E_INVALID, "q/k_new/v_new is NULL");
+  int m_max = 0;
+  rc = check_context(c, n_host, true, &m_max);
+  if (rc) return rc;
+  cudaStream_t sm = static_cast<cudaStream_t>(stream);
+  Pipe* pp = nullptr;
+  LAUNCH(get_pipe(ws->base, &pp));
+  std::lock_guard<std::mutex> pipe_lock(pp->mu);
+  if (g_prof_on || !(c.flags & LFPS_FLAG_GRAPH)) {
+    c.epoch = next_epoch();
+    return enqueue_step(c, pp, sm, q, k_new, v_new, out_host, in_host, m_max);
+  }
+  // CUDA-graph step: replays a captured step when nothing baked into it has
+  // changed (shapes, parameters, state and workspace, device buffers, the
+  // select kernel's context bucket); the call stamp then comes from device
+  // memory (ws.done[1], drawn by the step's first kernel)
+  const int m_bucket = (m_max + 8191) / 8192 * 8192;
+  GraphKey key;
+  memset(&key, 0, sizeof(key));
+  key.dims = *dims;
+  key.params = *p;
+  key.state = *st;
+  key.ws = ws->base;
+  key.q = q; key.k_new = k_new; key.v_new = v_new;
+  key.m_bucket = m_bucket;
+  key.has_in = in_host != nullptr;
+  key.has_out = out_host != nullptr;
+  c.epoch = 0;
+  c.stamp = reinterpret_cast<const int*>(c.done + 1);
+  StepGraph* g = nullptr;
+  for (size_t i = 0; i < pp->graphs.size(); ++i)
+    if (pp->graphs[i]->key == key) {
+      g = pp->graphs[i];
+      pp->graphs.erase(pp->graphs.begin() + i);
+      pp->graphs.push_back(g);
+      break;
+    }
+  if (!g) {
+    rc = capture_step(c, pp, key, q, k_new, v_new, out_host, in_host, m_bucket, &g);
+    if (rc) return rc;
+    if ((int)pp->graphs.size() == kMaxGraphs) {
+      delete pp->graphs.front();
+      pp->graphs.erase(pp->graphs.begin());
+    }
+    pp->graphs.push_back(g);
+  }
+  if (in_host && in_host != g->in_host) {
+    LAUNCH(cudaGraphExecMemcpyNodeSetParams1D(g->exec, g->in_node, const_cast<void*>(q), in_host,
+                                              g->in_bytes, cudaMemcpyHostToDevice));
+    g->in_host = in_host;
+  }
+  if (out_host && out_host != g->out_host) {
+    LAUNCH(cudaGraphExecMemcpyNodeSetParams1D(g->exec, g->out_node, out_host, c.out, g->out_bytes,
+                                              cudaMemcpyDeviceToHost));
+    g->out_host = out_host;
+  }
+  LAUNCH(cudaGraphLaunch(g->exec, sm));
   return LFPS_OK;
 }
 

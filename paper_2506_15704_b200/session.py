@@ -32,7 +32,7 @@ CNT_C0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_BLOCKS = rang
 
 
 def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False,
-                trace: bool = False, split: bool = False) -> _lib.Params:
+                trace: bool = False, split: bool = False, graph: bool = False) -> _lib.Params:
     err = cfg.device_limits_error()
     if err:
         raise ValueError(err)
@@ -49,7 +49,7 @@ def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False,
     for i, o in enumerate(offs):
         p.offsets[i] = o
     p.flags = ((_lib.FLAG_EXPORT_SETS if export_sets else 0) | (_lib.FLAG_TRACE if trace else 0)
-               | (_lib.FLAG_SPLIT if split else 0))
+               | (_lib.FLAG_SPLIT if split else 0) | (_lib.FLAG_GRAPH if graph else 0))
     return p
 
 
@@ -93,6 +93,7 @@ class BatchedSession:
         self.export_sets = export_sets
         self.trace = False          # LFPS_FLAG_TRACE: per-session phase timestamps
         self.split = True           # LFPS_FLAG_SPLIT: two session halves on two streams
+        self.graph = True           # LFPS_FLAG_GRAPH: a step is one CUDA-graph launch
         self.B, self.Hkv, self.G = batch, kv_heads, group
         self.Hq = kv_heads * group
         self.NS = batch * self.Hq
@@ -209,8 +210,8 @@ class BatchedSession:
     def _stream(self):
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
-    def _params(self, k_fraction: float = 1.0) -> _lib.Params:
-        return make_params(self.cfg, k_fraction, self.export_sets, self.trace, self.split)
+    def _params(self, k_fraction: float = 1.0, graph: bool = False) -> _lib.Params:
+        return make_params(self.cfg, k_fraction, self.export_sets, self.trace, self.split, graph)
 
     # -- bootstrap ----------------------------------------------------------
     def load_prefill(self, b: int, keys: torch.Tensor, values: torch.Tensor):
@@ -343,9 +344,10 @@ class BatchedSession:
                 raise ValueError(f"{name} must be a contiguous bf16 tensor on {self.device}")
         self._back_step()
         n_host = (C.c_int32 * self.B)(*self.n_host)
+        graph = self.graph and (out_host is None or out_host.is_pinned())
         if out_host is None:
             _lib.check(self.lib.lfps_decode_step(
-                C.byref(self.dims), C.byref(self._params(k_fraction)), C.byref(self.state),
+                C.byref(self.dims), C.byref(self._params(k_fraction, graph)), C.byref(self.state),
                 C.byref(self.ws), C.c_void_p(q.data_ptr()), C.c_void_p(k_new.data_ptr()),
                 C.c_void_p(v_new.data_ptr()), n_host, self._stream()), "decode_step")
         else:
@@ -354,7 +356,7 @@ class BatchedSession:
                 raise ValueError(f"out_host must be a contiguous f32 CPU tensor of shape "
                                  f"{tuple(self.out.shape)}")
             _lib.check(self.lib.lfps_decode_step_host_out(
-                C.byref(self.dims), C.byref(self._params(k_fraction)), C.byref(self.state),
+                C.byref(self.dims), C.byref(self._params(k_fraction, graph)), C.byref(self.state),
                 C.byref(self.ws), C.c_void_p(q.data_ptr()), C.c_void_p(k_new.data_ptr()),
                 C.c_void_p(v_new.data_ptr()), n_host, C.c_void_p(out_host.data_ptr()),
                 self._stream()), "decode_step")
@@ -461,8 +463,10 @@ class BatchedSession:
         if self._in_dev is None:
             self._in_dev = torch.empty(nbytes // 2, dtype=torch.bfloat16, device=self.device)
         n_host = (C.c_int32 * self.B)(*self.n_host)
+        graph = (self.graph and inputs_host.is_pinned()
+                 and (out_host is None or out_host.is_pinned()))
         _lib.check(self.lib.lfps_decode_step_host_io(
-            C.byref(self.dims), C.byref(self._params(k_fraction)), C.byref(self.state),
+            C.byref(self.dims), C.byref(self._params(k_fraction, graph)), C.byref(self.state),
             C.byref(self.ws), C.c_void_p(inputs_host.data_ptr()),
             C.c_void_p(self._in_dev.data_ptr()), n_host,
             C.c_void_p(out_host.data_ptr() if out_host is not None else None),

@@ -458,3 +458,58 @@ def test_block_table_kv_bit_exact(block_rows, d):
     w = np.exp(z - z.max())
     ref = (w / w.sum()) @ kv.values[:kv.n]
     assert np.linalg.norm(full[0, 0] - ref) / np.linalg.norm(ref) <= 1e-5
+
+
+@pytest.mark.parametrize("host_io,split", [(False, False), (True, False), (False, True)])
+def test_graph_replay_bit_exact(host_io, split):
+    """LFPS_FLAG_GRAPH: the step is captured once and replayed (device inputs
+    copied into the same buffers every step, or packed host inputs through
+    the captured copy node, whose host pointer is updated per replay); the
+    call stamp comes from the device.  Parity with the oracle every step,
+    then a failing step (non-finite query) raises and commits nothing, and
+    the following replays commit again."""
+    import gpu_drive
+    B, Hkv, G, d = (8, 8, 4, 64) if split else (2, 2, 4, 128)
+    pair, K, V, Q = _gqa_pair(batch=B, kv_heads=Hkv, group=G, d=d, n0=900, steps=8, seed=83)
+    sess = pair.sess
+    sess.graph = True
+    sess.split = split
+    qd = torch.empty(B, Hkv * G, d, dtype=torch.bfloat16, device="cuda")
+    kd = torch.empty(B, Hkv, d, dtype=torch.bfloat16, device="cuda")
+    vd = torch.empty_like(kd)
+    n0 = pair.n0
+
+    def device_step(q, k, v, frac, check=True):
+        qd.copy_(gpu_drive.bf16(q.reshape(B, Hkv * G, d)))
+        kd.copy_(gpu_drive.bf16(k))
+        vd.copy_(gpu_drive.bf16(v))
+        return sess.decode_step(qd, kd, vd, frac, check=check)
+
+    for t in range(8):
+        if t == 5:                                     # a failing step in the middle
+            qbad = Q[:, :, :, t].copy()
+            qbad[0, 0, 1, 3] = np.inf
+            before = [x.clone() for x in (sess.ver, sess.sla, sess.scale, sess.n_ctx)]
+            with pytest.raises(ValueError):
+                if host_io:
+                    sess.decode_step_host(sess.pack_step_inputs(
+                        gpu_drive.bf16(qbad.reshape(B, Hkv * G, d)), gpu_drive.bf16(K[:, :, n0 + t]),
+                        gpu_drive.bf16(V[:, :, n0 + t])), 0.05, check=True)
+                else:
+                    device_step(qbad, K[:, :, n0 + t], V[:, :, n0 + t], 0.05)
+            after = (sess.ver, sess.sla, sess.scale, sess.n_ctx)
+            assert all(torch.equal(x, y) for x, y in zip(before, after))
+        if host_io:
+            pair.host_io = True
+            res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], 0.05)
+        else:
+            res = device_step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], 0.05)
+            outs = []
+            from oracle import lfps_oracle as lo
+            for b in range(B):
+                for h in range(Hkv):
+                    kv, trs, prs = pair.units[b * Hkv + h]
+                    outs.append(lo.unit_step(kv, trs, prs, Q[b, h, :, t], K[b, h, n0 + t],
+                                             V[b, h, n0 + t], 0.05, pair.cfg, lo.DevArith,
+                                             "fp32"))
+        pair.compare_step(res, outs, tables=(t % 3 == 2 or t == 7))
