@@ -62,7 +62,7 @@ def parse():
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = all host cores")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-graph", action="store_true",
-                    help="enqueue each step kernel by kernel (no CUDA-graph replay)")
+                    help="e2e: enqueue each host-input step kernel by kernel (no CUDA graph)")
     ap.add_argument("--no-split", action="store_true",
                     help="disable LFPS_FLAG_SPLIT (two session halves on two streams)")
     ap.add_argument("--paged", action="store_true",

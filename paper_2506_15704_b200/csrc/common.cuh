@@ -120,7 +120,9 @@ __device__ __forceinline__ const __nv_bfloat16* vrow(const Ctx& c, int b, int h,
 // stamp err[0] holds, so no kernel has to clear the codes before the gate and
 // the stats kernel (which run concurrently) may raise them
 __device__ __forceinline__ int call_stamp(const Ctx& c) {
-  return c.stamp ? *reinterpret_cast<const volatile int*>(c.stamp) : c.epoch;
+  const int* p = c.stamp;
+  const int e = c.epoch;
+  return p ? __ldcg(p) : e;
 }
 __device__ __forceinline__ int err_code(const Ctx& c, int code) { return (call_stamp(c) << 4) | code; }
 __device__ __forceinline__ void set_err(const Ctx& c, int s, int code) {

@@ -312,6 +312,8 @@ struct Pipe {
   cudaEvent_t in_ready = nullptr;
   cudaStream_t cap = nullptr;               // CUDA-graph capture of a decode step
   std::vector<struct StepGraph*> graphs;    // captured steps, most recent last
+  void* stage = nullptr;                    // graph steps with device inputs: the
+  size_t stage_bytes = 0;                   // inputs are copied here first
 };
 std::mutex g_pipe_mu;
 
@@ -346,6 +348,7 @@ std::map<std::pair<int, const void*>, std::unique_ptr<Pipe>> g_pipes;
 void destroy_pipe(Pipe& p) {
   for (StepGraph* g : p.graphs) delete g;
   p.graphs.clear();
+  if (p.stage) cudaFree(p.stage);
   if (p.cap) cudaStreamDestroy(p.cap);
   for (cudaStream_t* sp : {&p.st[0], &p.st[kSplitGroups - 1], &p.aux[0], &p.aux[kSplitGroups - 1],
                            &p.copy, &p.in})
@@ -708,6 +711,30 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
   key.has_out = out_host != nullptr;
   c.epoch = 0;
   c.stamp = reinterpret_cast<const int*>(c.done + 1);
+  if (!in_host) {
+    // device inputs: copied into the pipe's staging buffer, so that one
+    // graph serves callers whose input tensors change from step to step
+    const size_t qb = (size_t)c.NS * c.d * 2, kb = (size_t)c.B * c.Hkv * c.d * 2;
+    if (pp->stage_bytes < qb + 2 * kb) {
+      if (pp->stage) {
+        cudaStreamSynchronize(sm);
+        cudaFree(pp->stage);
+      }
+      pp->stage = nullptr;
+      pp->stage_bytes = 0;
+      LAUNCH(cudaMalloc(&pp->stage, qb + 2 * kb));
+      pp->stage_bytes = qb + 2 * kb;
+    }
+    char* st = static_cast<char*>(pp->stage);
+    if (q != st) LAUNCH(cudaMemcpyAsync(st, q, qb, cudaMemcpyDeviceToDevice, sm));
+    if (k_new != st + qb) LAUNCH(cudaMemcpyAsync(st + qb, k_new, kb, cudaMemcpyDeviceToDevice, sm));
+    if (v_new != st + qb + kb)
+      LAUNCH(cudaMemcpyAsync(st + qb + kb, v_new, kb, cudaMemcpyDeviceToDevice, sm));
+    q = st;
+    k_new = st + qb;
+    v_new = st + qb + kb;
+    key.q = q; key.k_new = k_new; key.v_new = v_new;
+  }
   StepGraph* g = nullptr;
   for (size_t i = 0; i < pp->graphs.size(); ++i)
     if (pp->graphs[i]->key == key) {

@@ -93,7 +93,13 @@ class BatchedSession:
         self.export_sets = export_sets
         self.trace = False          # LFPS_FLAG_TRACE: per-session phase timestamps
         self.split = True           # LFPS_FLAG_SPLIT: two session halves on two streams
-        self.graph = True           # LFPS_FLAG_GRAPH: a step is one CUDA-graph launch
+        # LFPS_FLAG_GRAPH: a step is one CUDA-graph launch.  It cuts the host's
+        # enqueue time (C4 ~100 -> ~60 us) but the replayed step runs slower on
+        # the device than the stream-launched kernels (PDL overlap, the input
+        # staging copies); so by default only the host-input path, where the
+        # host is on the critical path of every step, uses it
+        self.graph = True           # decode_step_host
+        self.graph_device = False   # decode_step
         self.B, self.Hkv, self.G = batch, kv_heads, group
         self.Hq = kv_heads * group
         self.NS = batch * self.Hq
@@ -344,7 +350,7 @@ class BatchedSession:
                 raise ValueError(f"{name} must be a contiguous bf16 tensor on {self.device}")
         self._back_step()
         n_host = (C.c_int32 * self.B)(*self.n_host)
-        graph = self.graph and (out_host is None or out_host.is_pinned())
+        graph = self.graph_device and (out_host is None or out_host.is_pinned())
         if out_host is None:
             _lib.check(self.lib.lfps_decode_step(
                 C.byref(self.dims), C.byref(self._params(k_fraction, graph)), C.byref(self.state),

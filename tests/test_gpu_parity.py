@@ -472,7 +472,7 @@ def test_graph_replay_bit_exact(host_io, split):
     B, Hkv, G, d = (8, 8, 4, 64) if split else (2, 2, 4, 128)
     pair, K, V, Q = _gqa_pair(batch=B, kv_heads=Hkv, group=G, d=d, n0=900, steps=8, seed=83)
     sess = pair.sess
-    sess.graph = True
+    sess.graph = sess.graph_device = True
     sess.split = split
     qd = torch.empty(B, Hkv * G, d, dtype=torch.bfloat16, device="cuda")
     kd = torch.empty(B, Hkv, d, dtype=torch.bfloat16, device="cuda")
