@@ -58,7 +58,7 @@ extern "C" {
 #define LFPS_API
 #endif
 
-#define LFPS_ABI_VERSION 7
+#define LFPS_ABI_VERSION 8
 
 #define LFPS_OK 0
 #define LFPS_E_INVALID -1   /* bad argument (shape, range, capacity) */
@@ -104,6 +104,10 @@ typedef struct lfps_params {
 } lfps_params;
 
 /* lfps_params.flags */
+#define LFPS_FLAG_UNIT_FINISH 32 /* per-unit finish (k_unit.cu: the G q-heads of a
+                                    KV head over the union of their probe sets,
+                                    row slices merged) instead of the per-session
+                                    finish; G = 2 / 4 and d = 64 / 128 only */
 #define LFPS_FLAG_GRAPH 16       /* enqueue a decode step as one CUDA-graph launch: the
                                     step is captured once per (shapes, params,
                                     state, workspace, device buffers, context
@@ -184,6 +188,11 @@ typedef struct lfps_ws_layout {
                          index of the word's first slot, slot bits) */
   size_t thr_next;    /* f64 [NS, 2, 4] thresholds computed for the select
                          kernel (copied to thr for the non-gated sessions) */
+  /* Per-unit finish (one (request, KV-head) unit's G q-heads over the union
+     of their probe sets, in row slices; written and read within a step). */
+  size_t unit_dir;    /* i32 [NS, 17] probe rows below each row-slice boundary */
+  size_t unit_part;   /* f32 [B * Hkv, 16, G, d + 4] per-slice softmax partials */
+  size_t unit_ticket; /* u32 [B * Hkv] slices finished (kept at 0 between steps) */
   int32_t nblk;       /* blocks per item (slash_cap / 512) */
   int32_t dirty_words;
   int32_t words;      /* bitmap words per (session, table, kind) */

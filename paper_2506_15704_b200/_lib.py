@@ -18,11 +18,12 @@ from .errors import DeviceError
 # experiments); the default is the library __graft_entry__.build() makes
 LIB_PATH = os.environ.get("LFPS_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "lib", "liblfps_b200.so")
-ABI_VERSION = 7
+ABI_VERSION = 8
 FLAG_EXPORT_SETS = 1
 FLAG_TRACE = 2
 FLAG_SPLIT = 8
 FLAG_GRAPH = 16
+FLAG_UNIT_FINISH = 32
 
 # per-session device error codes (include/lfps_b200.h)
 ERR_NAMES = {
@@ -78,7 +79,8 @@ class WsLayout(C.Structure):
                 ("scratch", C.c_size_t), ("bsum", C.c_size_t), ("bmax", C.c_size_t),
                 ("dirty", C.c_size_t), ("valid", C.c_size_t), ("wstat", C.c_size_t), ("trace", C.c_size_t),
                 ("done", C.c_size_t), ("hot", C.c_size_t),
-                ("thr_next", C.c_size_t),
+                ("thr_next", C.c_size_t), ("unit_dir", C.c_size_t), ("unit_part", C.c_size_t),
+                ("unit_ticket", C.c_size_t),
                 ("nblk", C.c_int32), ("dirty_words", C.c_int32), ("words", C.c_int32),
                 ("list_cap", C.c_int32)]
 

@@ -78,7 +78,13 @@ struct Ctx {
   // [blocks, block_rows, Hkv, d] pool; bt == nullptr: contiguous [B, Hkv, n_max, d]
   const int* bt;
   int bs_shift, bs_mask, max_blocks;
+  // per-unit finish (k_unit.cu)
+  int unit_nsl;        // row slices (finish CTAs) per unit of this launch
+  int* unit_dir;       // [NS, kUnitMaxSlices + 1] probe rows below each slice boundary (select)
+  float* unit_part;    // [units, kUnitMaxSlices, G, d + 4] slice partials (m, s, C2 max, check, acc)
+  unsigned* unit_ticket;   // [units] slices finished (the last one merges and resets it)
 };
+constexpr int kUnitMaxSlices = 16;
 
 // CNT_BLOCKS: table blocks the select kernel read (rebuilt + hot), a diagnostic
 enum { CNT_C0 = 0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_BLOCKS, CNT_N };
@@ -188,6 +194,9 @@ struct DeviceOnce {
 cudaError_t launch_gate(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
 cudaError_t launch_stats(const Ctx& c, cudaStream_t st);
 cudaError_t launch_select(const Ctx& c, int m_max, cudaStream_t st);
+cudaError_t launch_select_unit(const Ctx& c, int m_max, cudaStream_t st);
+cudaError_t launch_finish_unit(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
+bool unit_finish_supported(int G, int d);
 cudaError_t launch_topk(const Ctx& c, int implicit_base, cudaStream_t st);
 cudaError_t launch_attend(const Ctx& c, const __nv_bfloat16* q, int exact_mode, cudaStream_t st);
 cudaError_t launch_update(const Ctx& c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new,
