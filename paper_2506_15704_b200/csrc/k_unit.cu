@@ -15,21 +15,23 @@
 //            a table of rows with their member heads and list ranks, in
 //            shared memory (per-head bitmaps of the range, one block scan),
 //            in chunks of kChunk rows
-//   rows     16 lanes per row (lane l holds canonical partial l: d/16
-//            contiguous elements), two rows per warp per step; each warp
-//            streams its rows through its own ring of kUSt stages with
-//            cp.async (16 B per lane, L2 only), warp barriers only
-//   scores   z_g = (K . q_g) / fp32(sqrt d) for the G heads in the canonical
-//            order of devmath.sdot32 (engine.py:168-170): one fma.rn.f32.bf16
-//            chain per lane and head, then folds 8, 4, 2, 1 as a
-//            reduce-scatter over the heads (each lane ends with one head's
+//   rows     two rows per warp per step, both half-warps on both rows: half
+//            h owns G/2 of the heads (their q, softmax states and
+//            accumulators), lane l of a half canonical partial l (d/16
+//            contiguous elements) of every row; each warp streams its rows
+//            through its own ring of kUSt stages with cp.async (16 B per
+//            lane, L2 only), warp barriers only
+//   scores   z_g = (K . q_g) / fp32(sqrt d) in the canonical order of
+//            devmath.sdot32 (engine.py:168-170): one fma.rn.f32.bf16 chain
+//            per lane, row and head, then folds 8, 4, 2, 1 as a
+//            reduce-scatter over (row, head) (each lane ends with one
 //            score, one IEEE division per lane) -- bit-identical to the
 //            per-session kernel; a member row's score goes to its head's C2
 //            score list at its rank
 //   attend   per head an online (max, sum, acc) in the base-2 domain
 //            (MUFU.EX2, packed fp32x2 FMAs) over sinks u C2 (engine.py:173-181,
-//            attention.py:66-85); half-warp states merged per CTA, slices
-//            merged by the last CTA, fp32
+//            attention.py:66-85); warp states merged per CTA, slices merged
+//            by the last CTA, fp32
 //   checks   sinks and C2 scores finite (numerics.py:61-62); the C2 max of
 //            each head to wstat for k_update.cu's canonical fp64 weights
 #include "finish.cuh"
@@ -41,10 +43,10 @@ namespace {
 using namespace fin;
 
 #ifndef LFPS_UNIT_MINB
-#define LFPS_UNIT_MINB 2         // resident CTAs per SM (registers: ~100 per thread at G = 4)
+#define LFPS_UNIT_MINB 3         // resident CTAs per SM
 #endif
 #ifndef LFPS_UNIT_STAGES
-#define LFPS_UNIT_STAGES 12
+#define LFPS_UNIT_STAGES 8
 #endif
 constexpr int kUSt = LFPS_UNIT_STAGES;   // ring stages per warp (one row per half-warp each)
 constexpr int kChunk = 512;      // union rows per chunk (the row table in shared memory)
@@ -63,7 +65,7 @@ struct UnitShared {
   int next_l0, next_a[G];               // where the next chunk starts (more rows than kChunk)
   int p[G], byp[G];
   int scan[kWarps][G + 1];
-  float m[16][G], s[16][G], mx[16][G], ck[16][G];
+  float m[kWarps][G], s[kWarps][G], mx[kWarps][G], ck[kWarps][G];
   int last;
 };
 
@@ -78,23 +80,24 @@ __device__ __forceinline__ void lds_part(uint32_t addr, uint32_t (&w)[PQ / 2]) {
   }
 }
 
-// Canonical folds 8, 4, 2, 1 of the G heads' partials as a reduce-scatter:
-// the result is head (l16 >> kHeadShift)'s full sum.  Every add is
-// x_l + x_(l^h) of devmath.sdot32's tree (IEEE addition commutes).
-template <int G>
-__device__ __forceinline__ float fold_heads(const float (&x)[G], int l16) {
+// Canonical folds 8, 4, 2, 1 of a half-warp's partials of two rows x HPL
+// heads as a reduce-scatter: lane l16 ends with row (l16 >> 3) of head
+// ((l16 >> 2) & 1 when HPL = 2).  Every add is x_l + x_(l^h) of
+// devmath.sdot32's tree (IEEE addition commutes).
+template <int HPL>
+__device__ __forceinline__ float fold_rows(const float (&x)[2][HPL], int l16) {
+  const bool b3 = (l16 & 8) != 0;
   float v;
-  if constexpr (G == 4) {
-    const bool b3 = (l16 & 8) != 0, b2 = (l16 & 4) != 0;
-    const float r0 = __shfl_xor_sync(LFPS_FULL, b3 ? x[0] : x[2], 8);
-    const float r1 = __shfl_xor_sync(LFPS_FULL, b3 ? x[1] : x[3], 8);
-    const float a0 = __fadd_rn(b3 ? x[2] : x[0], r0);
-    const float a1 = __fadd_rn(b3 ? x[3] : x[1], r1);
+  if constexpr (HPL == 2) {
+    const bool b2 = (l16 & 4) != 0;
+    const float r0 = __shfl_xor_sync(LFPS_FULL, b3 ? x[0][0] : x[1][0], 8);
+    const float r1 = __shfl_xor_sync(LFPS_FULL, b3 ? x[0][1] : x[1][1], 8);
+    const float a0 = __fadd_rn(b3 ? x[1][0] : x[0][0], r0);
+    const float a1 = __fadd_rn(b3 ? x[1][1] : x[0][1], r1);
     v = __fadd_rn(b2 ? a1 : a0, __shfl_xor_sync(LFPS_FULL, b2 ? a0 : a1, 4));
   } else {
-    static_assert(G == 2, "G = 2 or 4");
-    const bool b3 = (l16 & 8) != 0;
-    v = __fadd_rn(b3 ? x[1] : x[0], __shfl_xor_sync(LFPS_FULL, b3 ? x[0] : x[1], 8));
+    static_assert(HPL == 1, "G = 2 or 4");
+    v = __fadd_rn(b3 ? x[1][0] : x[0][0], __shfl_xor_sync(LFPS_FULL, b3 ? x[0][0] : x[1][0], 8));
     v = __fadd_rn(v, __shfl_xor_sync(LFPS_FULL, v, 4));
   }
   v = __fadd_rn(v, __shfl_xor_sync(LFPS_FULL, v, 2));
@@ -111,7 +114,6 @@ __global__ void __launch_bounds__(kThreads, LFPS_UNIT_MINB)
   constexpr int D = PQ * 16;
   constexpr int kRowB = D * 2;                  // bytes of one K (or V) row
   constexpr int kStB = 4 * kRowB;               // one stage of a warp: 2 rows x (K | V)
-  constexpr int kLpH = 16 / G;                  // lanes per head after the fold
   const int nsl = c.unit_nsl;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   pdl_wait();                                   // the select kernel's lists and directory
@@ -147,12 +149,17 @@ __global__ void __launch_bounds__(kThreads, LFPS_UNIT_MINB)
     pdl_trigger();
     return;
   }
-  const int hw = lane >> 4, l16 = lane & 15, slot = warp * 2 + hw;
-  const int hh = l16 / kLpH;                    // the head this lane's folded score belongs to
-  const bool writer = (l16 % kLpH) == 0;
+  // Both half-warps work on the warp's two rows of a step; half hw owns
+  // heads hw HPL .. hw HPL + HPL - 1 (their q partials, softmax states and
+  // accumulators), lane l16 canonical partial l16 of every row.
+  constexpr int HPL = G / 2;
+  const int hw = lane >> 4, l16 = lane & 15;
+  const int rr = l16 >> 3;                      // the row of this lane's folded score
+  const int hh = hw * HPL + (HPL == 2 ? (l16 >> 2) & 1 : 0);   // ... and its head
+  const bool writer = (l16 & (8 / HPL - 1)) == 0;
   float* c2z = c.c2_score + (size_t)(u * G + hh) * c.list_cap;
   const RowMapT<RM> rmap(c, b, h);
-  // this lane's 16-byte chunks of a K and a V row, and of a stage
+  // copies: half hw stages row hw of a step; this lane's 16-byte chunks
   const uint8_t* ksrc = reinterpret_cast<const uint8_t*>(RM == 0 ? krow(c, b, h, 0) : c.K);
   const uint8_t* vsrc = reinterpret_cast<const uint8_t*>(RM == 0 ? vrow(c, b, h, 0) : c.V);
   uint32_t dst0 = smem_u32(stages) + warp * (kUSt * kStB) + hw * (2 * kRowB);
@@ -165,32 +172,33 @@ __global__ void __launch_bounds__(kThreads, LFPS_UNIT_MINB)
     ksrc = (l16 < 8 ? ksrc : vsrc) + ch * 16;
     dst0 += (l16 < 8 ? 0 : kRowB) + ch * 16;
   }
-  const uint32_t rd0 = smem_u32(stages) + warp * (kUSt * kStB) + hw * (2 * kRowB) + l16 * (PQ * 2);
+  const uint32_t rd0 = smem_u32(stages) + warp * (kUSt * kStB) + l16 * (PQ * 2);
 
-  // q: lane l16 holds canonical partial l16 (PQ elements, packed bf16) of every head
-  uint32_t qw[G][PQ / 2];
+  // q: lane l16 holds canonical partial l16 (PQ elements, packed bf16) of its heads
+  uint32_t qw[HPL][PQ / 2];
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const uint32_t* qp = reinterpret_cast<const uint32_t*>(q + (size_t)(u * G + g) * D) + l16 * (PQ / 2);
+  for (int j = 0; j < HPL; ++j) {
+    const uint32_t* qp =
+        reinterpret_cast<const uint32_t*>(q + (size_t)(u * G + hw * HPL + j) * D) + l16 * (PQ / 2);
     if constexpr (PQ == 8) {
       const uint4 x = *reinterpret_cast<const uint4*>(qp);
-      qw[g][0] = x.x; qw[g][1] = x.y; qw[g][2] = x.z; qw[g][3] = x.w;
+      qw[j][0] = x.x; qw[j][1] = x.y; qw[j][2] = x.z; qw[j][3] = x.w;
     } else {
       const uint2 x = *reinterpret_cast<const uint2*>(qp);
-      qw[g][0] = x.x; qw[g][1] = x.y;
+      qw[j][0] = x.x; qw[j][1] = x.y;
     }
   }
 
-  float m[G], ssum[G];
-  float2 acc[G][PQ / 2];
+  float m[HPL], ssum[HPL];
+  float2 acc[HPL][PQ / 2];
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
-    m[g] = -INFINITY;
-    ssum[g] = 0.0f;
+  for (int j = 0; j < HPL; ++j) {
+    m[j] = -INFINITY;
+    ssum[j] = 0.0f;
 #pragma unroll
-    for (int t = 0; t < PQ / 2; ++t) acc[g][t] = make_float2(0.0f, 0.0f);
+    for (int t = 0; t < PQ / 2; ++t) acc[j][t] = make_float2(0.0f, 0.0f);
   }
-  float chk = 0.0f, mxc = -INFINITY;            // of head hh
+  float chk = 0.0f, mxc = -INFINITY;            // of head hh over the rows of parity rr
 
   // the slice's logical rows [l0, l1); chunks of <= kChunk union rows
   const int R = (m_ + nsl - 1) / nsl;
@@ -343,6 +351,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_UNIT_MINB)
     };
     const int niter = (nv + 15) / 16;
 #pragma unroll 1
+    const int slot = warp * 2 + hw;             // the row this half-warp stages
     for (int t = 0; t < kUSt - 1; ++t) issue(t, t * 16 + slot);
     int rs = 0, ws = kUSt - 1;
 #pragma unroll 1
@@ -351,67 +360,88 @@ __global__ void __launch_bounds__(kThreads, LFPS_UNIT_MINB)
       __syncwarp();                             // ... and the rest of the warp's
       issue(ws, (it + kUSt - 1) * 16 + slot);
       ws = ws + 1 == kUSt ? 0 : ws + 1;
-      const uint32_t ka = rd0 + rs * kStB;
+      const uint32_t ka = rd0 + rs * kStB;       // row 0 of the step; row 1 at + 2 kRowB
       rs = rs + 1 == kUSt ? 0 : rs + 1;
-      const int vv = it * 16 + slot;
-      const int e = vv < nv ? us.ent[vv] : 0;   // no row: no member heads
-      const int emask = e >> 24;
-      uint32_t kw[PQ / 2];
-      lds_part<PQ>(ka, kw);
-      float dots[G];
+      const int v0 = it * 16 + warp * 2;
+      int e[2];                                 // row | member heads << 24 (no row: none)
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        float pa = 0.0f;
+      for (int r = 0; r < 2; ++r) e[r] = v0 + r < nv ? us.ent[v0 + r] : 0;
+      float dots[2][HPL];
 #pragma unroll
-        for (int t = 0; t < PQ / 2; ++t) {
-          pa = fma_lo(kw[t], qw[g][t], pa);
-          pa = fma_hi(kw[t], qw[g][t], pa);
+      for (int r = 0; r < 2; ++r) {
+        uint32_t kw[PQ / 2];
+        lds_part<PQ>(ka + r * 2 * kRowB, kw);
+#pragma unroll
+        for (int j2 = 0; j2 < HPL; ++j2) {
+          float pa = 0.0f;
+#pragma unroll
+          for (int t = 0; t < PQ / 2; ++t) {
+            pa = fma_lo(kw[t], qw[j2][t], pa);
+            pa = fma_hi(kw[t], qw[j2][t], pa);
+          }
+          dots[r][j2] = pa;
         }
-        dots[g] = pa;
       }
-      const float z = __fdiv_rn(fold_heads<G>(dots, l16), c.sqrt_d_f32);
-      if ((emask >> hh) & 1) {
+      const float z = __fdiv_rn(fold_rows<HPL>(dots, l16), c.sqrt_d_f32);
+      const int er = rr ? e[1] : e[0];
+      if ((er >> (24 + hh)) & 1) {
         chk = __fmaf_rn(z, 0.0f, chk);
-        if (vv >= ns) {
+        const int vr = v0 + rr;
+        if (vr >= ns) {
           mxc = fmaxf(mxc, z);
-          if (writer) c2z[us.a[hh] + us.off[vv * G + hh]] = z;
+          if (writer) c2z[us.a[hh] + us.off[vr * G + hh]] = z;
         }
       }
       const float zl = z * kLog2e;
-      float zg[G];
+      float zg[2][HPL];
 #pragma unroll
-      for (int g = 0; g < G; ++g) zg[g] = __shfl_sync(LFPS_FULL, zl, (hw << 4) + g * kLpH);
-      if (!emask) continue;                     // no row (stale stage bits) or no member
-      uint32_t vw[PQ / 2];
-      lds_part<PQ>(ka + kRowB, vw);
-      float2 vf[PQ / 2];
+      for (int r = 0; r < 2; ++r)
 #pragma unroll
-      for (int t = 0; t < PQ / 2; ++t) vf[t] = make_float2(bf_lo(vw[t]), bf_hi(vw[t]));
+        for (int j2 = 0; j2 < HPL; ++j2)
+          zg[r][j2] = __shfl_sync(LFPS_FULL, zl, (hw << 4) + r * 8 + j2 * 4);
+      const int mk0 = (e[0] >> (24 + hw * HPL)) & ((1 << HPL) - 1);   // this half's member heads
+      const int mk1 = (e[1] >> (24 + hw * HPL)) & ((1 << HPL) - 1);
+      if (!(mk0 | mk1)) continue;               // no row (stale stage bits) or no member
       // rescale a head only when its max grows by more than 2^kRescale (the
       // weights stay <= 2^kRescale; the state is consistent either way): one
-      // rarely taken branch for all heads
+      // rarely taken branch
       bool grow = false;
 #pragma unroll
-      for (int g = 0; g < G; ++g) grow |= ((emask >> g) & 1) && zg[g] > m[g] + kRescale;
+      for (int j2 = 0; j2 < HPL; ++j2)
+        grow |= (((mk0 >> j2) & 1) && zg[0][j2] > m[j2] + kRescale) ||
+                (((mk1 >> j2) & 1) && zg[1][j2] > m[j2] + kRescale);
       if (grow) {
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          if (((emask >> g) & 1) && zg[g] > m[g] + kRescale) {
-            const float r = ex2(m[g] - zg[g]);
-            ssum[g] *= r;
+        for (int j2 = 0; j2 < HPL; ++j2) {
+          float mn = m[j2];
+          if ((mk0 >> j2) & 1) mn = fmaxf(mn, zg[0][j2]);
+          if ((mk1 >> j2) & 1) mn = fmaxf(mn, zg[1][j2]);
+          if (mn > m[j2] + kRescale) {
+            const float r = ex2(m[j2] - mn);
+            ssum[j2] *= r;
 #pragma unroll
-            for (int t = 0; t < PQ / 2; ++t) acc[g][t] = fmul2(acc[g][t], make_float2(r, r));
-            m[g] = zg[g];
+            for (int t = 0; t < PQ / 2; ++t) acc[j2][t] = fmul2(acc[j2][t], make_float2(r, r));
+            m[j2] = mn;
           }
         }
       }
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float w = ((emask >> g) & 1) ? ex2(zg[g] - m[g]) : 0.0f;
-        ssum[g] += w;
-        const float2 w2 = make_float2(w, w);
+      for (int r = 0; r < 2; ++r) {
+        const int mk = r ? mk1 : mk0;
+        if (!mk) continue;                      // (a missing row's stage bits are stale)
+        uint32_t vw[PQ / 2];
+        lds_part<PQ>(ka + r * 2 * kRowB + kRowB, vw);
+        float2 vf[PQ / 2];
 #pragma unroll
-        for (int t = 0; t < PQ / 2; ++t) acc[g][t] = ffma2(vf[t], w2, acc[g][t]);
+        for (int t = 0; t < PQ / 2; ++t) vf[t] = make_float2(bf_lo(vw[t]), bf_hi(vw[t]));
+#pragma unroll
+        for (int j2 = 0; j2 < HPL; ++j2) {
+          const float w = ((mk >> j2) & 1) ? ex2(zg[r][j2] - m[j2]) : 0.0f;
+          ssum[j2] += w;
+          const float2 w2 = make_float2(w, w);
+#pragma unroll
+          for (int t = 0; t < PQ / 2; ++t) acc[j2][t] = ffma2(vf[t], w2, acc[j2][t]);
+        }
       }
     }
     cp_async_wait<0>();
@@ -431,29 +461,32 @@ __global__ void __launch_bounds__(kThreads, LFPS_UNIT_MINB)
   __syncthreads();                              // the stages become merge scratch
 
   // ---- this CTA's 16 half-warp states -> the slice partial of each head ----------------
-  float* part = reinterpret_cast<float*>(stages);   // [16 slots][G][D]
+  float* part = reinterpret_cast<float*>(stages);   // [kWarps][G][D]
 #pragma unroll
-  for (int g = 0; g < G; ++g) {
+  for (int j = 0; j < HPL; ++j) {
 #pragma unroll
     for (int t = 0; t < PQ / 2; ++t)
-      *reinterpret_cast<float2*>(part + (slot * G + g) * D + l16 * PQ + 2 * t) = acc[g][t];
+      *reinterpret_cast<float2*>(part + (warp * G + hw * HPL + j) * D + l16 * PQ + 2 * t) = acc[j][t];
   }
   if (l16 == 0) {
 #pragma unroll
-    for (int g = 0; g < G; ++g) { us.m[slot][g] = m[g]; us.s[slot][g] = ssum[g]; }
+    for (int j = 0; j < HPL; ++j) { us.m[warp][hw * HPL + j] = m[j]; us.s[warp][hw * HPL + j] = ssum[j]; }
   }
-  if (writer) { us.mx[slot][hh] = mxc; us.ck[slot][hh] = chk; }
+  // the checks of head hh: rows of both parities
+  mxc = fmaxf(mxc, __shfl_xor_sync(LFPS_FULL, mxc, 8));
+  chk += __shfl_xor_sync(LFPS_FULL, chk, 8);
+  if (writer && rr == 0) { us.mx[warp][hh] = mxc; us.ck[warp][hh] = chk; }
   __syncthreads();
   float* up = c.unit_part + ((size_t)u * kUnitMaxSlices + sl) * G * (D + 4);
   for (int x = tid; x < G * D; x += kThreads) {
     const int g = x / D, el = x - g * D;
     float M = -INFINITY;
 #pragma unroll
-    for (int k2 = 0; k2 < 16; ++k2) M = fmaxf(M, us.m[k2][g]);
+    for (int k2 = 0; k2 < kWarps; ++k2) M = fmaxf(M, us.m[k2][g]);
     float num = 0.0f, den = 0.0f;
     if (M != -INFINITY) {
 #pragma unroll 4
-      for (int k2 = 0; k2 < 16; ++k2) {
+      for (int k2 = 0; k2 < kWarps; ++k2) {
         if (us.m[k2][g] == -INFINITY) continue;
         const float f = ex2(us.m[k2][g] - M);
         num = fmaf(f, part[(k2 * G + g) * D + el], num);
@@ -465,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_UNIT_MINB)
     if (el == 0) {
       float mx = -INFINITY, ck = 0.0f;
 #pragma unroll
-      for (int k2 = 0; k2 < 16; ++k2) { mx = fmaxf(mx, us.mx[k2][g]); ck += us.ck[k2][g]; }
+      for (int k2 = 0; k2 < kWarps; ++k2) { mx = fmaxf(mx, us.mx[k2][g]); ck += us.ck[k2][g]; }
       pg[0] = M;
       pg[1] = den;
       pg[2] = mx;
