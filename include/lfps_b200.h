@@ -196,7 +196,7 @@ typedef struct lfps_ws_layout {
   int32_t nblk;       /* blocks per item (slash_cap / 512) */
   int32_t dirty_words;
   int32_t words;      /* bitmap words per (session, table, kind) */
-  int32_t list_cap;   /* capacity of each per-session list */
+  int32_t list_cap;   /* capacity of each per-session list (m_cap rounded up to 32) */
 } lfps_ws_layout;
 
 typedef struct lfps_workspace {

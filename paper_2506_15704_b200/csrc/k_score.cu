@@ -48,6 +48,33 @@ __device__ __forceinline__ Part<PQ> ldg_part(const __nv_bfloat16* row, int l8) {
   return r;
 }
 
+// The canonical folds at lane distances LVL .. 1 of N values per lane (one
+// per head) as a reduce-scatter: at each level the lanes whose LVL bit is
+// set keep the upper half of the values, the others the lower half, so that
+// the lane ends with the full sum of value (l8 / (8 / N)) and each level
+// costs N / 2 shuffles.  Every add is x_l + x_(l^LVL) of devmath.sdot32's
+// tree (IEEE addition commutes), bit-identical to N butterflies.
+template <int N, int LVL>
+struct FoldScatter {
+  static __device__ __forceinline__ float run(const float (&v)[N], int l8) {
+    if constexpr (N == 1) {
+      float x = v[0];
+#pragma unroll
+      for (int o = LVL; o >= 1; o >>= 1) x = __fadd_rn(x, __shfl_xor_sync(LFPS_FULL, x, o));
+      return x;
+    } else {
+      const bool hi = (l8 & LVL) != 0;
+      float keep[N / 2];
+#pragma unroll
+      for (int i = 0; i < N / 2; ++i) {
+        const float send = hi ? v[i] : v[i + N / 2];
+        keep[i] = __fadd_rn(hi ? v[i + N / 2] : v[i], __shfl_xor_sync(LFPS_FULL, send, LVL));
+      }
+      return FoldScatter<N / 2, LVL / 2>::run(keep, l8);
+    }
+  }
+};
+
 // RM: RowMapT mode -- 0 contiguous cache (unit base, local rows), 1 block table
 template <int PQ, int G, int RM>
 __global__ void __launch_bounds__(kThreads, LFPS_SCORE_CTAS) lfps_exact_score_kernel(Ctx c, const __nv_bfloat16* q) {
@@ -80,7 +107,8 @@ __global__ void __launch_bounds__(kThreads, LFPS_SCORE_CTAS) lfps_exact_score_ke
   const RowMapT<RM> rmap(c, b, h);
   const __nv_bfloat16* kbase = RM ? c.K : krow(c, b, h, 0);
   auto rm = [&](int r) { return RM ? rmap(r) : r; };
-  const int gs = l8 % G;                              // the head this lane divides and writes
+  const int gs = l8 / (8 / G);                        // the head this lane divides and writes
+  const bool writer = l8 % (8 / G) == 0;
   float* out = c.probe_score + (size_t)(s0 + gs) * c.list_cap;
   // K rows stream through shared memory, kScoreStages tiles of kStep rows:
   // each 8-lane group copies (cp.async) and reads only its own rows, so the
@@ -129,19 +157,18 @@ __global__ void __launch_bounds__(kThreads, LFPS_SCORE_CTAS) lfps_exact_score_ke
         kp[2 * t] = make_float2(bf_lo(kr.a[t]), bf_lo(kr.b[t]));
         kp[2 * t + 1] = make_float2(bf_hi(kr.a[t]), bf_hi(kr.b[t]));
       }
-      float mine = 0.0f;
+      float v[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         float2 p = make_float2(0.0f, 0.0f);
 #pragma unroll
         for (int e = 0; e < PQ; ++e) p = ffma2(kp[e], q2[g][e], p);
-        float v = __fadd_rn(p.x, p.y);              // canonical fold 8 (in-lane), 4, 2, 1
-#pragma unroll
-        for (int hh = 4; hh >= 1; hh >>= 1) v = __fadd_rn(v, __shfl_xor_sync(LFPS_FULL, v, hh));
-        if (g == gs) mine = v;
+        v[g] = __fadd_rn(p.x, p.y);                 // canonical fold 8 (in-lane)
       }
-      const float z = __fdiv_rn(mine, c.sqrt_d_f32);
-      if (rr < r1 && l8 < G) out[rr] = z;
+      // folds 4, 2, 1 as a reduce-scatter over the heads: lane l8 ends with
+      // head gs's score
+      const float z = __fdiv_rn(FoldScatter<G, 4>::run(v, l8), c.sqrt_d_f32);
+      if (rr < r1 && writer) out[rr] = z;
     }
   }
   cp_async_wait<0>();

@@ -7,22 +7,26 @@
 // {z > kth} plus the lowest-index entries with z == kth, emitted in index
 // order.  Keys are order-preserving uint32 maps of the fp32 scores with -0.0
 // canonicalised to +0.0 (canon.cuh score_key).  One 512-thread CTA per
-// session; the m scores (512 KiB at 128k) are streamed twice:
+// session; the m scores (512 KiB at 128k) are streamed ONCE:
 //
 //   0  a strided sample of 4096 keys; its order statistics at ranks around
 //      k m / 4096 (+- 4 sqrt(rank) + 16), found by two radix selects in
 //      shared memory (not a full sort), bound a key window
 //      [lo, hi] that holds the k-th largest key with overwhelming probability;
-//   1  one pass counts the keys above hi per warp chunk and collects the
-//      window's (key, index) pairs in shared memory;
+//   1  one pass appends the (score, index) pairs above hi to a global
+//      buffer (the session's uw scratch) and the window's to shared memory,
+//      warp-aggregated;
 //   2  if the window provably holds the k-th key (keys above hi < k <=
 //      keys above hi + window size, and the window fit), an MSB-first radix
-//      select over the window finds it exactly; otherwise the kernel falls
-//      back to a 2048-bin histogram pass over all keys plus the same select
-//      on the k-th bin;
-//   3  every warp re-walks its index chunk and writes its selections at
-//      warp-scan offsets, so the output is sorted.
-// Loads are float4 (4 keys per lane) with two in flight.
+//      select over the window finds it exactly (ties: a second radix select
+//      over the tied entries' indices finds the lowest need_eq of them);
+//   3  the selected indices are set in a bitmap of the session's rows, the
+//      bitmap's word prefixes give every selection its output position in
+//      index order, and each selected pair is written there.
+// If the window misses, the kernel falls back to a 2048-bin histogram pass
+// over all keys, the same select on the k-th bin, and an ordered emission
+// pass in which every warp re-walks its index chunk.  Loads are float4 (4
+// keys per lane) with four in flight.
 #include "common.cuh"
 #include "canon.cuh"
 
@@ -38,12 +42,12 @@ constexpr int kShift = 21;
 constexpr int kCand = 6144;                 // window candidates kept in shared memory
 
 struct TopkShared {
-  unsigned samp[kSample];                   // fallback histogram (kBins <= kSample)
-  uint2 cand[kCand];                        // (key, index)
+  unsigned samp[kSample];                   // fallback histogram (kBins <= kSample); tie scratch
+  uint2 cand[kCand];                        // window: (score bits, index); fallback: (key, index)
   int wsum[kWarps];
   int above[kWarps];                        // keys above the window, per warp chunk
   int gtc[kWarps], eqc[kWarps];             // window keys > kth / == kth, per warp chunk
-  int ncand, over;
+  int ncand, over, nabove, neq;
   unsigned hist[256];
   unsigned sel_digit;
   int sel_want;
@@ -55,14 +59,15 @@ __device__ __forceinline__ uint32_t key_at(const float* z, int j) { return score
 // prefix: the key value whose descending rank contains `want` (1-based),
 // i.e. the want-th largest; returns it and sets *need_eq to how many keys
 // equal to it are still to be taken.
+template <typename KeyOf>
 __device__ uint32_t radix_select(TopkShared& sh, const uint2* keys, int nk, uint32_t prefix,
-                                 uint32_t mask, int first_shift, int want, int* need_eq) {
+                                 uint32_t mask, int first_shift, int want, int* need_eq, KeyOf key_of) {
   const int tid = threadIdx.x;
   for (int shift = first_shift; shift >= 0; shift -= 8) {
     if (tid < 256) sh.hist[tid] = 0;
     __syncthreads();
     for (int i = tid; i < nk; i += kThreads) {
-      const uint32_t key = keys[i].x;
+      const uint32_t key = key_of(keys[i]);
       if ((key & mask) == prefix) atomicAdd(&sh.hist[(key >> shift) & 255u], 1u);
     }
     __syncthreads();
@@ -100,6 +105,9 @@ __device__ uint32_t radix_select(TopkShared& sh, const uint2* keys, int nk, uint
   *need_eq = want;
   return prefix;
 }
+__device__ __forceinline__ uint32_t key_x(uint2 e) { return e.x; }
+__device__ __forceinline__ uint32_t key_bits(uint2 e) { return score_key(__uint_as_float(e.x)); }
+
 
 __global__ void __launch_bounds__(kThreads) lfps_exact_topk_kernel(Ctx c) {
   extern __shared__ uint8_t dyn[];
@@ -144,65 +152,184 @@ __global__ void __launch_bounds__(kThreads) lfps_exact_topk_kernel(Ctx c) {
     const int rh = r - delta, rl = r + delta;
     int dummy;
     // (sorted descending, sample entry q would be the (q + 1)-th largest key)
-    hi = rh <= 0 ? 0xffffffffu : radix_select(sh, sh.cand, kSample, 0u, 0u, 24, rh + 1, &dummy);
-    lo = rl >= kSample ? 0u : radix_select(sh, sh.cand, kSample, 0u, 0u, 24, rl + 1, &dummy);
-    if (tid == 0) { sh.ncand = 0; sh.over = 0; }
+    hi = rh <= 0 ? 0xffffffffu : radix_select(sh, sh.cand, kSample, 0u, 0u, 24, rh + 1, &dummy, key_x);
+    lo = rl >= kSample ? 0u : radix_select(sh, sh.cand, kSample, 0u, 0u, 24, rl + 1, &dummy, key_x);
+    if (tid == 0) { sh.ncand = 0; sh.over = 0; sh.nabove = 0; sh.neq = 0; }
     __syncthreads();
   }
 
-  // ---- 1: keys above the window per chunk; window candidates ------------------------
-  int above = 0;
+  // ---- 1: the pairs above the window (global buffer) and in it (shared) -----------------
+  uint2* abuf = reinterpret_cast<uint2*>(c.uw + (size_t)s * c.list_cap);   // list_cap pairs
   if (use_window) {
-    auto visit = [&](uint32_t key, int j) {
-      if (key > hi) {
-        ++above;
-      } else if (key >= lo) {
-        const int at = atomicAdd(&sh.ncand, 1);
-        if (at < kCand) sh.cand[at] = make_uint2(key, (uint32_t)j);
+    // per lane 16 keys a round: the flags as bit masks, one warp scan of both
+    // counts and one atomic per buffer and warp
+    auto round = [&](const float (&zv)[16], const int (&jv)[16], int nok) {
+      uint32_t ma = 0u, mw = 0u;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint32_t key = score_key(zv[i]);
+        const bool ok = i < nok;
+        ma |= (uint32_t)(ok && key > hi) << i;
+        mw |= (uint32_t)(ok && key <= hi && key >= lo) << i;
+      }
+      const int cnt = __popc(ma) | (__popc(mw) << 16);
+      int x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(LFPS_FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      const int tot = __shfl_sync(LFPS_FULL, x, 31);
+      if (!tot) return;
+      int base = 0;
+      if (lane == 0 && (tot & 0xffff)) base = atomicAdd(&sh.nabove, tot & 0xffff);
+      if (lane == 1 && (tot >> 16)) base = atomicAdd(&sh.ncand, tot >> 16);
+      const int ba = __shfl_sync(LFPS_FULL, base, 0) + ((x - cnt) & 0xffff);
+      const int bw = __shfl_sync(LFPS_FULL, base, 1) + ((x - cnt) >> 16);
+      // (static indices keep zv / jv in registers)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint2 e = make_uint2(__float_as_uint(zv[i]), (uint32_t)jv[i]);
+        if ((ma >> i) & 1) abuf[ba + __popc(ma & ((1u << i) - 1u))] = e;
+        const int at = bw + __popc(mw & ((1u << i) - 1u));
+        if (((mw >> i) & 1) && at < kCand) sh.cand[at] = e;
       }
     };
     if (vec_ok) {
       // four float4 loads (16 keys) in flight per lane
-      for (int base0 = j0 + 4 * lane; base0 < j1; base0 += 512) {
-        float4 v[4];
+      for (int base0 = j0; base0 < j1; base0 += 512) {
+        float zv[16];
+        int jv[16];
+        int nok = 16;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int base = base0 + 128 * u;
-          v[u] = base + 3 < j1 ? __ldg(reinterpret_cast<const float4*>(z + base))
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int base = base0 + 128 * u;
+          const int base = base0 + 128 * u + 4 * lane;
+          float4 v;
           if (base + 3 < j1) {
-            visit(score_key(v[u].x), base); visit(score_key(v[u].y), base + 1);
-            visit(score_key(v[u].z), base + 2); visit(score_key(v[u].w), base + 3);
+            v = __ldg(reinterpret_cast<const float4*>(z + base));
           } else {
-            for (int j = base; j < j1; ++j) visit(key_at(z, j), j);
+            v = make_float4(base < j1 ? z[base] : 0.f, base + 1 < j1 ? z[base + 1] : 0.f,
+                            base + 2 < j1 ? z[base + 2] : 0.f, 0.f);
+            if (nok == 16) nok = 4 * u + max(0, min(4, j1 - base));
           }
+          zv[4 * u] = v.x; zv[4 * u + 1] = v.y; zv[4 * u + 2] = v.z; zv[4 * u + 3] = v.w;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) jv[4 * u + e] = base + e;
         }
+        round(zv, jv, nok);
       }
     } else {
-      for (int j = j0 + lane; j < j1; j += 32) visit(key_at(z, j), j);
+      for (int b0 = j0; b0 < j1; b0 += 32 * 16) {
+        float zv[16];
+        int jv[16];
+        int nok = 16;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int j = b0 + 32 * i + lane;
+          zv[i] = j < j1 ? z[j] : 0.f;
+          jv[i] = j;
+          if (j >= j1 && nok == 16) nok = i;
+        }
+        round(zv, jv, nok);
+      }
     }
   }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) above += __shfl_xor_sync(LFPS_FULL, above, o);
-  if (lane == 0) { sh.above[warp] = above; sh.gtc[warp] = 0; sh.eqc[warp] = 0; }
+  if (lane == 0) { sh.gtc[warp] = 0; sh.eqc[warp] = 0; }
   __syncthreads();
-  int tot_above = 0;
-  for (int w = 0; w < kWarps; ++w) tot_above += sh.above[w];
+  const int tot_above = use_window ? sh.nabove : 0;
   const int nc = use_window ? sh.ncand : 0;
   // the window provably holds the k-th key?
   use_window = use_window && nc <= kCand && tot_above < k && tot_above + nc >= k;
 
+  if (use_window) {
+    // ---- 2: the k-th key in the window; ties by lowest index ---------------------------
+    int need_eq;
+    const uint32_t kth = radix_select(sh, sh.cand, nc, 0u, 0u, 24, k - tot_above, &need_eq, key_bits);
+    uint2* eqs = reinterpret_cast<uint2*>(sh.samp);            // kSample / 2 tied entries
+    for (int i = tid; i < nc; i += kThreads) {
+      const uint2 e = sh.cand[i];
+      if (key_bits(e) == kth) {
+        const int at = atomicAdd(&sh.neq, 1);
+        if (at < kSample / 2) eqs[at] = make_uint2(~e.y, e.y);   // largest ~j = smallest j
+      }
+    }
+    __syncthreads();
+    const int neq = sh.neq;
+    uint32_t jmax = 0xffffffffu;                                 // ties taken: index <= jmax
+    if (need_eq < neq) {
+      if (neq > kSample / 2) {                                   // (more ties than the scratch)
+        use_window = false;
+      } else {
+        int dummy;
+        jmax = ~radix_select(sh, eqs, neq, 0u, 0u, 24, need_eq, &dummy, key_x);
+      }
+    }
+    if (use_window) {
+      // ---- 3: selected rows -> bitmap -> positions in index order -------------------------
+      const int W = (p + 31) / 32;
+      uint32_t* bm = reinterpret_cast<uint32_t*>(&sh + 1);
+      int* pre = reinterpret_cast<int*>(bm + W);
+      for (int w = tid; w < W; w += kThreads) bm[w] = 0u;
+      __syncthreads();
+      auto taken = [&](uint2 e) {
+        const uint32_t key = key_bits(e);
+        return key > kth || (key == kth && e.y <= jmax);
+      };
+      for (int i = tid; i < tot_above; i += kThreads) {
+        const uint32_t j = __ldcg(&abuf[i].y);
+        atomicOr(bm + (j >> 5), 1u << (j & 31));
+      }
+      for (int i = tid; i < nc; i += kThreads) {
+        const uint2 e = sh.cand[i];
+        if (taken(e)) atomicOr(bm + (e.y >> 5), 1u << (e.y & 31));
+      }
+      __syncthreads();
+      const int per = (W + kThreads - 1) / kThreads;
+      const int w0 = min(W, tid * per), w1 = min(W, w0 + per);
+      int cntw = 0;
+      for (int w = w0; w < w1; ++w) cntw += __popc(bm[w]);
+      int x = cntw;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(LFPS_FULL, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) sh.wsum[warp] = x;
+      __syncthreads();
+      int run = x - cntw, total = 0;
+      for (int w = 0; w < kWarps; ++w) {
+        run += w < warp ? sh.wsum[w] : 0;
+        total += sh.wsum[w];
+      }
+      for (int w = w0; w < w1; ++w) {
+        pre[w] = run;
+        run += __popc(bm[w]);
+      }
+      __syncthreads();
+      auto emit = [&](uint2 e) {
+        const uint32_t j = e.y;
+        const int pos = pre[j >> 5] + __popc(bm[j >> 5] & ((1u << (j & 31)) - 1u));
+        out_i[pos] = S + (int)j;
+        out_z[pos] = __uint_as_float(e.x);
+      };
+      for (int i = tid; i < tot_above; i += kThreads) emit(__ldcg(&abuf[i]));
+      for (int i = tid; i < nc; i += kThreads) {
+        const uint2 e = sh.cand[i];
+        if (taken(e)) emit(e);
+      }
+      if (tid == 0) cnt[CNT_C2] = total;
+      return;
+    }
+    __syncthreads();
+  }
+  // ---- fallback: per-chunk counts, histogram select, ordered emission pass --------------
+  int above = 0;
   uint32_t kth;
   int need_eq;
   const uint2* cand = sh.cand;
-  int ncand = nc;
-  if (use_window) {
-    kth = radix_select(sh, cand, ncand, 0u, 0u, 24, k - tot_above, &need_eq);
-  } else {
+  int ncand;
+  (void)above;
+  {
     // ---- fallback: 2048-bin histogram over all keys, then the k-th bin ----------------
     unsigned* hist = sh.samp;                      // 2048 bins
     for (int i = tid; i < kBins; i += kThreads) hist[i] = 0;
@@ -259,7 +386,7 @@ __global__ void __launch_bounds__(kThreads) lfps_exact_topk_kernel(Ctx c) {
     if (lane == 0) sh.above[warp] = ab;
     __syncthreads();
     cand = store;
-    kth = radix_select(sh, cand, ncand, bstar << kShift, ~0u << kShift, 16, want, &need_eq);
+    kth = radix_select(sh, cand, ncand, bstar << kShift, ~0u << kShift, 16, want, &need_eq, key_x);
     // radix_select's top pass (bits 16..23) covers the remaining 21 bits in 3
     // passes of 8 (bits above 21 already fixed by the prefix)
   }
@@ -347,12 +474,14 @@ __global__ void __launch_bounds__(kThreads) lfps_exact_topk_kernel(Ctx c) {
 
 cudaError_t launch_topk(const Ctx& c, int /*implicit_base*/, cudaStream_t st) {
   static DeviceOnce once;
-  const size_t smem = sizeof(TopkShared);
+  // TopkShared, then the selection bitmap and its word prefixes (list_cap rows)
+  const size_t smem = sizeof(TopkShared) + (size_t)(c.list_cap + 31) / 32 * 8;
   cudaError_t e = once.run([&] {
     return cudaFuncSetAttribute(lfps_exact_topk_kernel,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (e != cudaSuccess) return e;
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
   lfps_exact_topk_kernel<<<c.NS, kThreads, smem, st>>>(c);
   return cudaGetLastError();
 }

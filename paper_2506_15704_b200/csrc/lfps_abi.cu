@@ -99,9 +99,11 @@ int slash_cap(int m_cap) { return 2 * slash_home(m_cap); }
 int layout(const lfps_dims* d, lfps_ws_layout* L) {
   const size_t NS = (size_t)d->batch * d->kv_heads * d->group;
   const size_t NI = 2 * NS;
-  const size_t cap = (size_t)d->m_cap;
+  // per-session lists: m_cap entries rounded up to 32 (128-byte aligned rows,
+  // so every session's score list takes the vector loads of k_topk.cu)
+  const size_t cap = align_up((size_t)d->m_cap, 32);
   memset(L, 0, sizeof(*L));
-  L->list_cap = d->m_cap;
+  L->list_cap = (int)cap;
   L->words = (int)((cap + 511) / 512 * 16);   // whole 512-slot chunks
   L->nblk = slash_cap(d->m_cap) / lfps::kBlk;
   L->dirty_words = (L->nblk + 31) / 32;

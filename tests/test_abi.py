@@ -72,7 +72,7 @@ def test_workspace_layout_regions_are_disjoint_and_aligned():
         assert b > a
     assert all(o % 256 == 0 for o, _ in offs)
     assert lay.total_bytes > offs[-1][0]
-    assert lay.list_cap == 33000 and lay.words * 32 >= 33000
+    assert lay.list_cap >= 33000 and lay.list_cap % 32 == 0 and lay.words * 32 >= 33000
     assert lay.nblk * 512 == _lib.slash_capacity(dims) >= 2 * 33000
     assert lay.dirty_words * 32 >= lay.nblk and lay.dirty_words <= 32
 

@@ -5,7 +5,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --clock-control none -k regex:"lfps_(gate|stats|select|finish|unit|update)" -s 12 -c 12 --csv --log-file gpurun_out/pu/launches.csv \
   python bench.py --profile-only --steps 3 --warmup 3 > gpurun_out/pu/ncu_list.log 2>&1; echo list rc $?
 timeout 1500 ncu --set full --clock-control none --import-source on \
-  -k regex:"lfps_(select|unit)" -s 6 -c 2 -o gpurun_out/pu/prof_c4 -f \
+  -k regex:"lfps_(select|unit|finish)" -s 6 -c 2 -o gpurun_out/pu/prof_c4 -f \
   python bench.py --profile-only --steps 2 --warmup 2 > gpurun_out/pu/ncu_full.log 2>&1; echo full rc $?
 python tools/ncu_summary.py gpurun_out/pu/prof_c4.ncu-rep > gpurun_out/pu/summary.txt 2>&1
 cat gpurun_out/pu/summary.txt
