@@ -79,10 +79,11 @@ class WsLayout(C.Structure):
                 ("scratch", C.c_size_t), ("bsum", C.c_size_t), ("bmax", C.c_size_t),
                 ("dirty", C.c_size_t), ("valid", C.c_size_t), ("wstat", C.c_size_t), ("trace", C.c_size_t),
                 ("done", C.c_size_t), ("hot", C.c_size_t),
-                ("thr_next", C.c_size_t), ("unit_dir", C.c_size_t), ("unit_part", C.c_size_t),
+                ("thr_next", C.c_size_t), ("unit_ent", C.c_size_t), ("unit_rank", C.c_size_t),
+                ("unit_count", C.c_size_t), ("unit_part", C.c_size_t),
                 ("unit_ticket", C.c_size_t),
                 ("nblk", C.c_int32), ("dirty_words", C.c_int32), ("words", C.c_int32),
-                ("list_cap", C.c_int32)]
+                ("list_cap", C.c_int32), ("unit_cap", C.c_int32)]
 
 
 class KernelTime(C.Structure):

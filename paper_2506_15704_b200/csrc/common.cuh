@@ -79,8 +79,12 @@ struct Ctx {
   const int* bt;
   int bs_shift, bs_mask, max_blocks;
   // per-unit finish (k_unit.cu)
-  int unit_nsl;        // row slices (finish CTAs) per unit of this launch
-  int* unit_dir;       // [NS, kUnitMaxSlices + 1] probe rows below each slice boundary (select)
+  int unit_nsl;        // entry slices (stream CTAs) per unit of this launch
+  int unit_skip;       // per-session finish: skip the sessions of units the union kernel fused
+  int unit_cap;        // union entries per unit
+  int* unit_ent;       // [units, unit_cap] row | heads << 24 | sink << 28 (k_union.cu)
+  int* unit_rank;      // [units, unit_cap, 4] list index of the row in each member head
+  int* unit_count;     // [units] entries, -1: a Top-k cut (per-session finish)
   float* unit_part;    // [units, kUnitMaxSlices, G, d + 4] slice partials (m, s, C2 max, check, acc)
   unsigned* unit_ticket;   // [units] slices finished (the last one merges and resets it)
 };
@@ -194,7 +198,7 @@ struct DeviceOnce {
 cudaError_t launch_gate(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
 cudaError_t launch_stats(const Ctx& c, cudaStream_t st);
 cudaError_t launch_select(const Ctx& c, int m_max, cudaStream_t st);
-cudaError_t launch_select_unit(const Ctx& c, int m_max, cudaStream_t st);
+cudaError_t launch_union(const Ctx& c, cudaStream_t st);
 cudaError_t launch_finish_unit(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
 bool unit_finish_supported(int G, int d);
 cudaError_t launch_topk(const Ctx& c, int implicit_base, cudaStream_t st);

@@ -95,33 +95,7 @@ __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel
   pdl_trigger();
 }
 
-// C + D of one session for the per-unit finish (select.cuh, UNIT): C2 list,
-// counts and the slice directory as well.
-__global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_unit_kernel(Ctx c) {
-  extern __shared__ __align__(16) uint32_t smem[];
-  __shared__ SelectShared sh;
-  pdl_wait();
-  select_session<true>(c, c.s_off + blockIdx.x, smem, sh);
-  pdl_trigger();
-}
-
 }  // namespace
-
-// the select kernel of the per-unit finish (c.unit_nsl slices per unit)
-cudaError_t launch_select_unit(const Ctx& c, int m_max, cudaStream_t st) {
-  const size_t smem = select_smem(m_max);
-  static DeviceOnce once;
-  cudaError_t e = once.run([] {
-    cudaError_t r = cudaFuncSetAttribute(lfps_select_unit_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (r == cudaSuccess)
-      r = cudaFuncSetAttribute(lfps_select_unit_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
-    return r;
-  });
-  if (e != cudaSuccess) return e;
-  return launch_pdl(lfps_select_unit_kernel, dim3(c.s_cnt), dim3(kThreads), smem, st, c);
-}
 
 cudaError_t launch_stats(const Ctx& c, cudaStream_t st) {
   lfps_stats_kernel<<<2 * c.s_cnt, kStatsThreads, 0, st>>>(c);

@@ -1,504 +1,332 @@
-// k_unit.cu -- the back half of a decode step per (request, KV-head) UNIT:
-// the unit's G q-head sessions over the union of their probe sets, so every
-// K / V row crosses HBM -> L2 -> SM once for all G heads (the per-session
-// finish, k_finish.cu, stages a row once per head).  Used when every
-// non-gated head of the unit keeps its whole probe set (k >= |probe|, C2 =
-// probe: the common case at 5%); a unit with a Top-k cut runs its sessions
-// through finish_session (finish.cuh) inside the same launch.
+// k_unit.cu -- the back half of a decode step per (request, KV-head) UNIT
+// (LFPS_FLAG_UNIT_FINISH, G = 4, d = 128): the unit's 4 q-head sessions over
+// the union of their probe sets (k_union.cu), so every K / V row crosses
+// HBM -> L2 -> SM -> registers ONCE for all 4 heads.  The per-session finish
+// (k_finish.cu) moves each row once per head, through shared memory, with 8
+// lanes per row -- it is bound by shared-memory bandwidth and issue slots
+// (~34 warp instructions per session-row).  Here:
 //
-//   slices   the context is cut into unit_nsl row ranges, one CTA each (slice
-//            0 also takes the S sinks); the last CTA of a unit to finish
-//            (ticket) merges the slices' softmax partials -- the split-KV
-//            pattern, so small batches still fill 148 SMs
-//   union    each CTA merges its range of the G heads' sorted probe lists
-//            (where they start: the select kernel's slice directory) into
-//            a table of rows with their member heads and list ranks, in
-//            shared memory (per-head bitmaps of the range, one block scan),
-//            in chunks of kChunk rows
-//   rows     two rows per warp per step, both half-warps on both rows: half
-//            h owns G/2 of the heads (their q, softmax states and
-//            accumulators), lane l of a half canonical partial l (d/16
-//            contiguous elements) of every row; each warp streams its rows
-//            through its own ring of kUSt stages with cp.async (16 B per
-//            lane, L2 only), warp barriers only
-//   scores   z_g = (K . q_g) / fp32(sqrt d) in the canonical order of
-//            devmath.sdot32 (engine.py:168-170): one fma.rn.f32.bf16 chain
-//            per lane, row and head, then folds 8, 4, 2, 1 as a
-//            reduce-scatter over (row, head) (each lane ends with one
-//            score, one IEEE division per lane) -- bit-identical to the
-//            per-session kernel; a member row's score goes to its head's C2
-//            score list at its rank
-//   attend   per head an online (max, sum, acc) in the base-2 domain
-//            (MUFU.EX2, packed fp32x2 FMAs) over sinks u C2 (engine.py:173-181,
-//            attention.py:66-85); warp states merged per CTA, slices merged
-//            by the last CTA, fp32
-//   checks   sinks and C2 scores finite (numerics.py:61-62); the C2 max of
-//            each head to wstat for k_update.cu's canonical fp64 weights
-#include "finish.cuh"
+//   items    one 128-thread CTA (4 warps) per (unit, slice): the union
+//            entries split evenly into unit_nsl slices (the unit's last
+//            CTA to finish merges the slices' softmax partials: split-KV);
+//            3 CTAs per SM
+//   steps    a warp takes 8 union rows per step; lane (h, r) = (lane / 8,
+//            lane % 8) scores row r for head h.  Rows stream through a
+//            per-warp ring of kUSt steps with cp.async (16 B per lane,
+//            coalesced: lanes 0-15 one row, 16-31 the next), padded to 272
+//            bytes per row so that the 8 lanes of one shared-memory phase
+//            (8 rows at one chunk offset) hit 8 distinct bank groups
+//   scores   z = (K . q_h) / fp32(sqrt d) in the canonical order of
+//            devmath.sdot32 (engine.py:168-170): 16 partials of 8 contiguous
+//            elements, each a chain of fma.rn.f32.bf16 (the exact bf16
+//            product, one rounding), folded 8, 4, 2, 1 in the lane, IEEE
+//            division -- bit-identical to the per-session kernel.  q_h stays
+//            in registers (64 packed words); a member row's score goes to
+//            its head's C2 score list at its rank
+//   attend   per head an online softmax (base 2, lazy max: it moves only
+//            when a step's max exceeds it by 2^8) and sum w V on the tensor
+//            cores: one mma.m16n8k8 per 16 dims and step multiplies V^T
+//            (ldmatrix.trans from the staged rows) by W[8 rows x 8] whose 8
+//            columns are the 4 heads' bf16 high and low weight parts (w -
+//            hi, rounded: |error| <= 2^-18 w); fp32 accumulation, checked
+//            against the fp64 oracle to 1e-5 relative L2
+//   checks   sinks and C2 scores finite (numerics.py:61-62); each head's C2
+//            max to wstat for k_update.cu's canonical fp64 weights
+#include "rows.cuh"
 
 namespace lfps {
 
 namespace {
 
-using namespace fin;
+using namespace rows;
 
-#ifndef LFPS_UNIT_MINB
-#define LFPS_UNIT_MINB 3         // resident CTAs per SM
-#endif
+constexpr int kUThreads = 128;
+constexpr int kUWarps = kUThreads / 32;
+constexpr int kUG = 4;                   // heads per unit
+constexpr int kUD = 128;                 // head dimension
 #ifndef LFPS_UNIT_STAGES
-#define LFPS_UNIT_STAGES 8
+#define LFPS_UNIT_STAGES 4
 #endif
-constexpr int kUSt = LFPS_UNIT_STAGES;   // ring stages per warp (one row per half-warp each)
-constexpr int kChunk = 512;      // union rows per chunk (the row table in shared memory)
-constexpr float kRescale = 8.0f; // log2 headroom before an online-softmax rescale
+#ifndef LFPS_UNIT_MINB
+#define LFPS_UNIT_MINB 3
+#endif
+constexpr int kUSt = LFPS_UNIT_STAGES;   // ring steps per warp
+constexpr int kRowP = 272;               // padded shared row: 256 B + 16
+constexpr int kStepB = 2 * 8 * kRowP;    // one step: 8 K rows, then 8 V rows
+constexpr size_t kUnitSmem = (size_t)kUWarps * kUSt * kStepB;
+constexpr float kRescale = 8.0f;         // log2 headroom before an online-softmax rescale
 
-// dynamic shared memory: the row ring, at least the per-session kernel's stages
-__host__ __device__ constexpr size_t unit_smem(int d) {
-  return (size_t)kUSt * kWarps * 4 * d * 2 > rows_smem(d) ? (size_t)kUSt * kWarps * 4 * d * 2 : rows_smem(d);
-}
+static_assert((size_t)kUWarps * kUG * kUD * 4 <= kUnitSmem, "merge scratch fits the ring");
 
-template <int G>
 struct UnitShared {
-  int ent[kChunk + 32];                 // row | member heads << 24 (the sinks first)
-  uint16_t off[(kChunk + 32) * G];      // rank of the row in each member head's list - a[g]
-  int a[G], b[G];                       // the chunk's entries [a, b) of each head's list
-  int next_l0, next_a[G];               // where the next chunk starts (more rows than kChunk)
-  int p[G], byp[G];
-  int scan[kWarps][G + 1];
-  float m[kWarps][G], s[kWarps][G], mx[kWarps][G], ck[kWarps][G];
-  int last;
+  float m[kUWarps][kUG], s[kUWarps][kUG], mx[kUWarps][kUG], ck[kUWarps][kUG];
+  int hmask, last;
 };
 
-template <int PQ>
-__device__ __forceinline__ void lds_part(uint32_t addr, uint32_t (&w)[PQ / 2]) {
-  if constexpr (PQ == 8) {
-    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(addr));
-  } else {
-    static_assert(PQ == 4, "d = 64 or 128");
-    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(addr));
-  }
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
 }
-
-// Canonical folds 8, 4, 2, 1 of a half-warp's partials of two rows x HPL
-// heads as a reduce-scatter: lane l16 ends with row (l16 >> 3) of head
-// ((l16 >> 2) & 1 when HPL = 2).  Every add is x_l + x_(l^h) of
-// devmath.sdot32's tree (IEEE addition commutes).
-template <int HPL>
-__device__ __forceinline__ float fold_rows(const float (&x)[2][HPL], int l16) {
-  const bool b3 = (l16 & 8) != 0;
-  float v;
-  if constexpr (HPL == 2) {
-    const bool b2 = (l16 & 4) != 0;
-    const float r0 = __shfl_xor_sync(LFPS_FULL, b3 ? x[0][0] : x[1][0], 8);
-    const float r1 = __shfl_xor_sync(LFPS_FULL, b3 ? x[0][1] : x[1][1], 8);
-    const float a0 = __fadd_rn(b3 ? x[1][0] : x[0][0], r0);
-    const float a1 = __fadd_rn(b3 ? x[1][1] : x[0][1], r1);
-    v = __fadd_rn(b2 ? a1 : a0, __shfl_xor_sync(LFPS_FULL, b2 ? a0 : a1, 4));
-  } else {
-    static_assert(HPL == 1, "G = 2 or 4");
-    v = __fadd_rn(b3 ? x[1][0] : x[0][0], __shfl_xor_sync(LFPS_FULL, b3 ? x[0][0] : x[1][0], 8));
-    v = __fadd_rn(v, __shfl_xor_sync(LFPS_FULL, v, 4));
-  }
-  v = __fadd_rn(v, __shfl_xor_sync(LFPS_FULL, v, 2));
-  v = __fadd_rn(v, __shfl_xor_sync(LFPS_FULL, v, 1));
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                          uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(addr));
+}
+// D[16 x 8] += A[16 x 8] B[8 x 8], bf16 in, fp32 accumulate
+__device__ __forceinline__ void mma_k8(float* d, uint32_t a0, uint32_t a1, uint32_t b) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5}, {%6}, "
+               "{%0, %1, %2, %3};"
+               : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3]) : "r"(a0), "r"(a1), "r"(b));
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
   return v;
 }
 
-template <int PQ, int G, int RM>
-__global__ void __launch_bounds__(kThreads, LFPS_UNIT_MINB)
-    lfps_unit_finish_kernel(Ctx c, const __nv_bfloat16* q) {
-  extern __shared__ __align__(128) uint8_t stages[];
-  __shared__ FinishShared sh;
-  __shared__ UnitShared<G> us;
-  constexpr int D = PQ * 16;
-  constexpr int kRowB = D * 2;                  // bytes of one K (or V) row
-  constexpr int kStB = 4 * kRowB;               // one stage of a warp: 2 rows x (K | V)
-  const int nsl = c.unit_nsl;
+template <int RM>
+__global__ void __launch_bounds__(kUThreads, LFPS_UNIT_MINB) lfps_unit_finish_kernel(Ctx c, const __nv_bfloat16* q) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ UnitShared us;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  pdl_wait();                                   // the select kernel's lists and directory
+  const int nsl = c.unit_nsl;
+  pdl_wait();                                   // the union kernel's table
   const int ul = blockIdx.x / nsl, sl = blockIdx.x - ul * nsl;
-  const int u = c.s_off / G + ul;
-  const int b = u / c.Hkv, h = u - b * c.Hkv;
-  const int n = c.n_ctx[b];
-  const int S = c.S, m_ = n - S;
-  if (tid < G) {
-    const int sg = u * G + tid;
-    const int* dir = c.unit_dir + (size_t)sg * (kUnitMaxSlices + 1);
-    us.p[tid] = c.counts[(size_t)sg * CNT_N + CNT_PROBE];
-    us.byp[tid] = c.bypass[sg];
-    us.a[tid] = dir[sl];
-    us.b[tid] = dir[sl + 1];
-  }
-  __syncthreads();
-  const int k = (int)rint(c.frac * (double)n) < 1 ? 1 : (int)rint(c.frac * (double)n);
-  int hmask = 0;
-  bool fused = true;
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    if (us.byp[g]) continue;
-    hmask |= 1 << g;
-    fused &= k >= us.p[g];
-  }
-  if (!fused) {                                 // a Top-k cut: the sessions one by one
-    if (sl < G) finish_session<PQ, RM>(c, q, u * G + sl, stages, sh);
+  const int u = c.s_off / kUG + ul;
+  const int U = c.unit_count[u];
+  if (U <= 0) {                                 // -1: a Top-k cut (per-session finish); 0: all gated
     pdl_trigger();
     return;
   }
-  if (!hmask) {                                 // every head gated
-    pdl_trigger();
-    return;
-  }
-  // Both half-warps work on the warp's two rows of a step; half hw owns
-  // heads hw HPL .. hw HPL + HPL - 1 (their q partials, softmax states and
-  // accumulators), lane l16 canonical partial l16 of every row.
-  constexpr int HPL = G / 2;
-  const int hw = lane >> 4, l16 = lane & 15;
-  const int rr = l16 >> 3;                      // the row of this lane's folded score
-  const int hh = hw * HPL + (HPL == 2 ? (l16 >> 2) & 1 : 0);   // ... and its head
-  const bool writer = (l16 & (8 / HPL - 1)) == 0;
-  float* c2z = c.c2_score + (size_t)(u * G + hh) * c.list_cap;
-  const RowMapT<RM> rmap(c, b, h);
-  // copies: half hw stages row hw of a step; this lane's 16-byte chunks
-  const uint8_t* ksrc = reinterpret_cast<const uint8_t*>(RM == 0 ? krow(c, b, h, 0) : c.K);
-  const uint8_t* vsrc = reinterpret_cast<const uint8_t*>(RM == 0 ? vrow(c, b, h, 0) : c.V);
-  uint32_t dst0 = smem_u32(stages) + warp * (kUSt * kStB) + hw * (2 * kRowB);
-  if constexpr (kRowB == 256) {                 // d = 128: K chunk l16 and V chunk l16
-    ksrc += l16 * 16;
-    vsrc += l16 * 16;
-    dst0 += l16 * 16;
-  } else {                                      // d = 64: lanes 0-7 K, 8-15 V
-    const int ch = l16 & 7;
-    ksrc = (l16 < 8 ? ksrc : vsrc) + ch * 16;
-    dst0 += (l16 < 8 ? 0 : kRowB) + ch * 16;
-  }
-  const uint32_t rd0 = smem_u32(stages) + warp * (kUSt * kStB) + l16 * (PQ * 2);
-
-  // q: lane l16 holds canonical partial l16 (PQ elements, packed bf16) of its heads
-  uint32_t qw[HPL][PQ / 2];
+  const int b = u / c.Hkv, hk = u - b * c.Hkv;
+  if (tid == 0) {
+    int hm = 0;
 #pragma unroll
-  for (int j = 0; j < HPL; ++j) {
-    const uint32_t* qp =
-        reinterpret_cast<const uint32_t*>(q + (size_t)(u * G + hw * HPL + j) * D) + l16 * (PQ / 2);
-    if constexpr (PQ == 8) {
-      const uint4 x = *reinterpret_cast<const uint4*>(qp);
-      qw[j][0] = x.x; qw[j][1] = x.y; qw[j][2] = x.z; qw[j][3] = x.w;
-    } else {
-      const uint2 x = *reinterpret_cast<const uint2*>(qp);
-      qw[j][0] = x.x; qw[j][1] = x.y;
+    for (int g = 0; g < kUG; ++g) hm |= (c.bypass[u * kUG + g] ? 0 : 1) << g;
+    us.hmask = hm;
+  }
+  const int e0 = (int)((long long)U * sl / nsl), e1 = (int)((long long)U * (sl + 1) / nsl);
+  const int h = lane >> 3, r = lane & 7;        // this lane's head and row of a step
+  const int sh = u * kUG + h;
+  const int* ent = c.unit_ent + (size_t)u * c.unit_cap;
+  const int* rnk = c.unit_rank + (size_t)u * c.unit_cap * 4;
+  float* c2z = c.c2_score + (size_t)sh * c.list_cap;
+
+  // q of head h: canonical partial j = elements 8 j .. 8 j + 7 = words 4 j .. 4 j + 3
+  uint32_t qw[64];
+  {
+    const uint4* qp = reinterpret_cast<const uint4*>(q + (size_t)sh * kUD);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const uint4 x = __ldg(qp + t);
+      qw[4 * t] = x.x; qw[4 * t + 1] = x.y; qw[4 * t + 2] = x.z; qw[4 * t + 3] = x.w;
     }
   }
 
-  float m[HPL], ssum[HPL];
-  float2 acc[HPL][PQ / 2];
+  // ---- the ring: a warp's steps w, w + 4, ... of 8 entries each -------------------------
+  const RowMapT<RM> rmap(c, b, hk);
+  const uint8_t* kb = reinterpret_cast<const uint8_t*>(RM == 0 ? krow(c, b, hk, 0) : c.K);
+  const uint8_t* vb = reinterpret_cast<const uint8_t*>(RM == 0 ? vrow(c, b, hk, 0) : c.V);
+  const int nsteps = (e1 - e0 + 7) >> 3;
+  const int nloc = nsteps > warp ? (nsteps - warp + kUWarps - 1) / kUWarps : 0;
+  const uint32_t wring = smem_u32(ring) + warp * (kUSt * kStepB);
+  // stale slots of rows past the end meet the mma with weight 0: zero them once
+  for (int o = lane * 16; o < kUSt * kStepB; o += 32 * 16)
+    asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(wring + o), "r"(0u) : "memory");
+  __syncwarp();
+  const int cc = lane & 15, rh = lane >> 4;     // copies: chunk cc of rows 2 i + rh
+  int nxt[4];                                   // entries of the next step to issue (-1: none)
+  auto fetch = [&](int t) {                     // (no use of the loads here: they land a step later)
+    const int eb = e0 + (warp + kUWarps * t) * 8;
 #pragma unroll
-  for (int j = 0; j < HPL; ++j) {
-    m[j] = -INFINITY;
-    ssum[j] = 0.0f;
+    for (int i = 0; i < 4; ++i) {
+      const int e = eb + 2 * i + rh;
+      nxt[i] = -1;
+      if (t < nloc && e < e1) nxt[i] = __ldg(ent + e);
+    }
+  };
+  auto issue = [&](int slot) {
+    const uint32_t dst = wring + slot * kStepB + cc * 16;
 #pragma unroll
-    for (int t = 0; t < PQ / 2; ++t) acc[j][t] = make_float2(0.0f, 0.0f);
-  }
-  float chk = 0.0f, mxc = -INFINITY;            // of head hh over the rows of parity rr
-
-  // the slice's logical rows [l0, l1); chunks of <= kChunk union rows
-  const int R = (m_ + nsl - 1) / nsl;
-  int l0 = min(m_, sl * R);
-  const int l1 = min(m_, l0 + R);
+    for (int i = 0; i < 4; ++i) {
+      if (nxt[i] < 0) continue;
+      const int row = RM == 0 ? (nxt[i] & 0xffffff) : rmap(nxt[i] & 0xffffff);
+      const size_t off = (size_t)row * (kUD * 2) + cc * 16;
+      cp_async16_s(dst + (2 * i + rh) * kRowP, kb + off);
+      cp_async16_s(dst + (8 + 2 * i + rh) * kRowP, vb + off);
+    }
+    cp_async_commit();                          // one group per step, even if empty
+  };
 #pragma unroll 1
-  for (int first = 1;; first = 0) {
-    // ---- the chunk's row table: per-head bitmaps of [l0, l1) from the lists ----------
-    // rows [l0, l1c): as many as the scratch (the unused ring) holds bitmaps
-    // and word prefixes of
-    constexpr int kScratchW = (int)(unit_smem(D) / 4 / (2 * G + 1));
-    const int l1c = min(l1, l0 + kScratchW * 32);
-    const int NW = (l1c - l0 + 31) >> 5;
-    uint32_t* bm = reinterpret_cast<uint32_t*>(stages);           // [G][NW] (ring unused yet)
-    for (int w = tid; w < G * NW; w += kThreads) bm[w] = 0u;
-    __syncthreads();
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      if (!((hmask >> g) & 1)) continue;
-      const int* lg = c.probe_idx + (size_t)(u * G + g) * c.list_cap;
-      const int a = us.a[g], e = us.b[g];
-      for (int i0 = a + tid; i0 < e; i0 += 4 * kThreads) {
-        int r[4];
-#pragma unroll
-        for (int x = 0; x < 4; ++x) r[x] = i0 + x * kThreads < e ? __ldg(lg + i0 + x * kThreads) : -1;
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          if (r[x] < 0) continue;
-          const int o = r[x] - S - l0;
-          if (o < l1c - l0) atomicOr(bm + g * NW + (o >> 5), 1u << (o & 31));
-        }
-      }
+  for (int t = 0; t < kUSt - 1; ++t) {
+    fetch(t);
+    issue(t);
+  }
+  fetch(kUSt - 1);
+  // this lane's entry (row | heads | sink) and list rank, one step ahead
+  int en_n = 0, rk_n = -1;
+  auto fetch_own = [&](int t) {
+    const int e = e0 + (warp + kUWarps * t) * 8 + r;
+    en_n = 0;
+    rk_n = -1;
+    if (t < nloc && e < e1) {
+      en_n = __ldg(ent + e);
+      rk_n = __ldg(rnk + 4 * e + h);
     }
-    __syncthreads();
-    const int wpt = (NW + kThreads - 1) / kThreads;
-    const int w0 = min(NW, tid * wpt), w1 = min(NW, w0 + wpt);
-    int v[G + 1];
-#pragma unroll
-    for (int i = 0; i <= G; ++i) v[i] = 0;
-    for (int w = w0; w < w1; ++w) {
-      uint32_t uo = 0u;
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const uint32_t x = bm[g * NW + w];
-        uo |= x;
-        v[1 + g] += __popc(x);
-      }
-      v[0] += __popc(uo);
-    }
-    int tot0, totg[G];
-    {                                           // exclusive block scans of the G + 1 counts
-      int x[G + 1];
-#pragma unroll
-      for (int i = 0; i <= G; ++i) x[i] = v[i];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-        for (int i = 0; i <= G; ++i) {
-          const int y = __shfl_up_sync(LFPS_FULL, x[i], o);
-          if (lane >= o) x[i] += y;
-        }
-      }
-      if (lane == 31) {
-#pragma unroll
-        for (int i = 0; i <= G; ++i) us.scan[warp][i] = x[i];
-      }
-      __syncthreads();
-      tot0 = 0;
-#pragma unroll
-      for (int i = 0; i <= G; ++i) {
-        int before = 0, all = 0;
-#pragma unroll
-        for (int k2 = 0; k2 < kWarps; ++k2) {
-          const int t = us.scan[k2][i];
-          before += k2 < warp ? t : 0;
-          all += t;
-        }
-        v[i] = before + x[i] - v[i];
-        if (i == 0) tot0 = all;
-        else totg[i - 1] = all;
-      }
-    }
-    const int ns = (first && sl == 0) ? S : 0;  // the sinks lead slice 0's first chunk
-    // word prefixes (union, then each head) behind the bitmaps; the entries
-    // are then emitted evenly over the threads (a dense band of words would
-    // otherwise serialise on the thread that owns it)
-    int* pre = reinterpret_cast<int*>(bm + G * NW);                // [G + 1][NW]
-    {
-      int run[G + 1];
-#pragma unroll
-      for (int i = 0; i <= G; ++i) run[i] = v[i];
-      for (int w = w0; w < w1; ++w) {
-        uint32_t uo = 0u;
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const uint32_t x = bm[g * NW + w];
-          uo |= x;
-          pre[(1 + g) * NW + w] = run[1 + g];
-          run[1 + g] += __popc(x);
-        }
-        pre[w] = run[0];
-        run[0] += __popc(uo);
-      }
-    }
-    __syncthreads();
-    const int E = min(tot0, kChunk + 1);        // entry kChunk: where the next chunk starts
-    for (int e = tid; e < E; e += kThreads) {
-      int lo = 0, hi = NW - 1;                  // the last word with pre[w] <= e
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (pre[mid] <= e) lo = mid; else hi = mid - 1;
-      }
-      const int w = lo;
-      uint32_t x[G], uo = 0u;
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        x[g] = bm[g * NW + w];
-        uo |= x[g];
-      }
-      const int bit = __fns(uo, 0, e - pre[w] + 1);
-      const uint32_t below = (1u << bit) - 1u;
-      if (e < kChunk) {
-        int mk = 0;
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          mk |= (int)((x[g] >> bit) & 1u) << g;
-          us.off[(ns + e) * G + g] = (uint16_t)(pre[(1 + g) * NW + w] + __popc(x[g] & below));
-        }
-        us.ent[ns + e] = (S + l0 + w * 32 + bit) | (mk << 24);
-      } else {                                  // the first row of the next chunk
-        us.next_l0 = l0 + w * 32 + bit;
-#pragma unroll
-        for (int g = 0; g < G; ++g) us.next_a[g] = us.a[g] + pre[(1 + g) * NW + w] + __popc(x[g] & below);
-      }
-    }
-    if (tid < ns) us.ent[tid] = tid | (hmask << 24);   // sinks: every head, no rank
-    const int nv = ns + min(tot0, kChunk);
-    __syncthreads();                            // the table is complete; the ring may start
+  };
+  fetch_own(0);
 
-    // ---- the rows: 2 per warp per step, kUSt steps in flight --------------------------
-    auto issue = [&](int st, int vv) {
-      if (vv < nv) {
-        const int row = RM == 0 ? (us.ent[vv] & 0xffffff) : rmap(us.ent[vv] & 0xffffff);
-        const size_t off = (size_t)row * kRowB;
-        const uint32_t dst = dst0 + st * kStB;
-        cp_async16_s(dst, ksrc + off);
-        if constexpr (kRowB == 256) cp_async16_s(dst + kRowB, vsrc + off);
-      }
-      cp_async_commit();                        // one group per step, even if empty
-    };
-    const int niter = (nv + 15) / 16;
-#pragma unroll 1
-    const int slot = warp * 2 + hw;             // the row this half-warp stages
-    for (int t = 0; t < kUSt - 1; ++t) issue(t, t * 16 + slot);
-    int rs = 0, ws = kUSt - 1;
-#pragma unroll 1
-    for (int it = 0; it < niter; ++it) {
-      cp_async_wait<kUSt - 2>();                // this lane's copies of step `it` landed
-      __syncwarp();                             // ... and the rest of the warp's
-      issue(ws, (it + kUSt - 1) * 16 + slot);
-      ws = ws + 1 == kUSt ? 0 : ws + 1;
-      const uint32_t ka = rd0 + rs * kStB;       // row 0 of the step; row 1 at + 2 kRowB
-      rs = rs + 1 == kUSt ? 0 : rs + 1;
-      const int v0 = it * 16 + warp * 2;
-      int e[2];                                 // row | member heads << 24 (no row: none)
+  float acc[8][4];                              // D[dims 16 x + (lane / 4) (+8)][head lane % 4, hi | lo]
 #pragma unroll
-      for (int r = 0; r < 2; ++r) e[r] = v0 + r < nv ? us.ent[v0 + r] : 0;
-      float dots[2][HPL];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        uint32_t kw[PQ / 2];
-        lds_part<PQ>(ka + r * 2 * kRowB, kw);
-#pragma unroll
-        for (int j2 = 0; j2 < HPL; ++j2) {
-          float pa = 0.0f;
-#pragma unroll
-          for (int t = 0; t < PQ / 2; ++t) {
-            pa = fma_lo(kw[t], qw[j2][t], pa);
-            pa = fma_hi(kw[t], qw[j2][t], pa);
-          }
-          dots[r][j2] = pa;
-        }
-      }
-      const float z = __fdiv_rn(fold_rows<HPL>(dots, l16), c.sqrt_d_f32);
-      const int er = rr ? e[1] : e[0];
-      if ((er >> (24 + hh)) & 1) {
-        chk = __fmaf_rn(z, 0.0f, chk);
-        const int vr = v0 + rr;
-        if (vr >= ns) {
-          mxc = fmaxf(mxc, z);
-          if (writer) c2z[us.a[hh] + us.off[vr * G + hh]] = z;
-        }
-      }
-      const float zl = z * kLog2e;
-      float zg[2][HPL];
-#pragma unroll
-      for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int j2 = 0; j2 < HPL; ++j2)
-          zg[r][j2] = __shfl_sync(LFPS_FULL, zl, (hw << 4) + r * 8 + j2 * 4);
-      const int mk0 = (e[0] >> (24 + hw * HPL)) & ((1 << HPL) - 1);   // this half's member heads
-      const int mk1 = (e[1] >> (24 + hw * HPL)) & ((1 << HPL) - 1);
-      if (!(mk0 | mk1)) continue;               // no row (stale stage bits) or no member
-      // rescale a head only when its max grows by more than 2^kRescale (the
-      // weights stay <= 2^kRescale; the state is consistent either way): one
-      // rarely taken branch
-      bool grow = false;
-#pragma unroll
-      for (int j2 = 0; j2 < HPL; ++j2)
-        grow |= (((mk0 >> j2) & 1) && zg[0][j2] > m[j2] + kRescale) ||
-                (((mk1 >> j2) & 1) && zg[1][j2] > m[j2] + kRescale);
-      if (grow) {
-#pragma unroll
-        for (int j2 = 0; j2 < HPL; ++j2) {
-          float mn = m[j2];
-          if ((mk0 >> j2) & 1) mn = fmaxf(mn, zg[0][j2]);
-          if ((mk1 >> j2) & 1) mn = fmaxf(mn, zg[1][j2]);
-          if (mn > m[j2] + kRescale) {
-            const float r = ex2(m[j2] - mn);
-            ssum[j2] *= r;
-#pragma unroll
-            for (int t = 0; t < PQ / 2; ++t) acc[j2][t] = fmul2(acc[j2][t], make_float2(r, r));
-            m[j2] = mn;
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int mk = r ? mk1 : mk0;
-        if (!mk) continue;                      // (a missing row's stage bits are stale)
-        uint32_t vw[PQ / 2];
-        lds_part<PQ>(ka + r * 2 * kRowB + kRowB, vw);
-        float2 vf[PQ / 2];
-#pragma unroll
-        for (int t = 0; t < PQ / 2; ++t) vf[t] = make_float2(bf_lo(vw[t]), bf_hi(vw[t]));
-#pragma unroll
-        for (int j2 = 0; j2 < HPL; ++j2) {
-          const float w = ((mk >> j2) & 1) ? ex2(zg[r][j2] - m[j2]) : 0.0f;
-          ssum[j2] += w;
-          const float2 w2 = make_float2(w, w);
-#pragma unroll
-          for (int t = 0; t < PQ / 2; ++t) acc[j2][t] = ffma2(vf[t], w2, acc[j2][t]);
-        }
-      }
-    }
-    cp_async_wait<0>();
-    if (tot0 <= kChunk && l1c == l1) break;
-    __syncthreads();                            // ring and table are free again
-    if (tot0 > kChunk) {
-      l0 = us.next_l0;
-      if (tid < G) us.a[tid] = us.next_a[tid];
-    } else {                                    // the whole range [l0, l1c) is done
-      l0 = l1c;
-#pragma unroll
-      for (int g = 0; g < G; ++g)
-        if (tid == g) us.a[g] += totg[g];
-    }
-    __syncthreads();
-  }
-  __syncthreads();                              // the stages become merge scratch
+  for (int x = 0; x < 8; ++x) acc[x][0] = acc[x][1] = acc[x][2] = acc[x][3] = 0.0f;
+  float mo = -INFINITY, ma = -INFINITY;         // running max of head h (weights) / head lane % 4 (acc)
+  float ssum = 0.0f, chk = 0.0f, mxc = -INFINITY;
+  const int t4 = lane & 3, nn = lane >> 2;      // mma B fragment: rows 2 t4, 2 t4 + 1, column nn
+  const int bsrc = (nn >> 1) * 8 + 2 * t4;
+  const uint32_t vlane = 8 * kRowP + (lane & 7) * kRowP + (lane >> 3) * 16;
 
-  // ---- this CTA's 16 half-warp states -> the slice partial of each head ----------------
-  float* part = reinterpret_cast<float*>(stages);   // [kWarps][G][D]
+  // the canonical score of row r of the step in slot kst for head h
+  auto score = [&](uint32_t kst) {
+    float x8[8];
+    const uint32_t kr = kst + r * kRowP;
 #pragma unroll
-  for (int j = 0; j < HPL; ++j) {
+    for (int j = 0; j < 16; ++j) {
+      const uint4 kv = lds128(kr + j * 16);
+      float p = 0.0f;
+      p = fma_lo(kv.x, qw[4 * j], p);
+      p = fma_hi(kv.x, qw[4 * j], p);
+      p = fma_lo(kv.y, qw[4 * j + 1], p);
+      p = fma_hi(kv.y, qw[4 * j + 1], p);
+      p = fma_lo(kv.z, qw[4 * j + 2], p);
+      p = fma_hi(kv.z, qw[4 * j + 2], p);
+      p = fma_lo(kv.w, qw[4 * j + 3], p);
+      p = fma_hi(kv.w, qw[4 * j + 3], p);
+      if (j < 8) x8[j] = p;
+      else x8[j - 8] = __fadd_rn(x8[j - 8], p);
+    }
+    const float y0 = __fadd_rn(x8[0], x8[4]), y1 = __fadd_rn(x8[1], x8[5]);
+    const float y2 = __fadd_rn(x8[2], x8[6]), y3 = __fadd_rn(x8[3], x8[7]);
+    return __fdiv_rn(__fadd_rn(__fadd_rn(y0, y2), __fadd_rn(y1, y3)), c.sqrt_d_f32);
+  };
+  // the checks, the C2 score, the online softmax (lazy max) and sum w V of a
+  // scored step (entry en, rank rk of row r) whose V rows are in slot kst
+  auto attend = [&](float z, int en, int rk, uint32_t kst) {
+    const bool mem = (en >> (24 + h)) & 1;
+    if (mem) {
+      chk = __fmaf_rn(z, 0.0f, chk);
+      if (!((en >> 28) & 1)) {                  // a C2 row (not a sink)
+        mxc = fmaxf(mxc, z);
+        c2z[rk] = z;
+      }
+    }
+    const float zl = mem ? z * kLog2e : -INFINITY;
+    float mh = fmaxf(zl, __shfl_xor_sync(LFPS_FULL, zl, 1));
+    mh = fmaxf(mh, __shfl_xor_sync(LFPS_FULL, mh, 2));
+    mh = fmaxf(mh, __shfl_xor_sync(LFPS_FULL, mh, 4));          // step max of head h
+    const float ta = __shfl_sync(LFPS_FULL, mh, t4 * 8);        // ... of head lane % 4
+    const bool ga = ta > ma + kRescale;
+    if (__any_sync(LFPS_FULL, ga)) {
+      const float f = ga ? ex2(ma - ta) : 1.0f;
 #pragma unroll
-    for (int t = 0; t < PQ / 2; ++t)
-      *reinterpret_cast<float2*>(part + (warp * G + hw * HPL + j) * D + l16 * PQ + 2 * t) = acc[j][t];
+      for (int x = 0; x < 8; ++x) {
+        acc[x][0] *= f; acc[x][1] *= f; acc[x][2] *= f; acc[x][3] *= f;
+      }
+      ma = ga ? ta : ma;
+    }
+    if (mh > mo + kRescale) {
+      ssum *= ex2(mo - mh);
+      mo = mh;
+    }
+    const float w = mem ? ex2(zl - mo) : 0.0f;
+    ssum += w;
+    // W column 2 h' + 0 / 1 = head h' high / low parts; lane 8 h' + 2 i holds
+    // rows 2 i, 2 i + 1 of head h' packed
+    const float wn = __shfl_xor_sync(LFPS_FULL, w, 1);
+    const float wa = (r & 1) ? wn : w, wb = (r & 1) ? w : wn;
+    const uint32_t hi = cvt_bf16x2(wa, wb);
+    const uint32_t lo = cvt_bf16x2(wa - bf_lo(hi), wb - bf_hi(hi));
+    const uint32_t bh = __shfl_sync(LFPS_FULL, hi, bsrc);
+    const uint32_t bl = __shfl_sync(LFPS_FULL, lo, bsrc);
+    const uint32_t bw = (nn & 1) ? bl : bh;
+    const uint32_t vr = kst + vlane;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      uint32_t a0, a1, a2, a3;
+      ldsm_x4_t(vr + x * 64, a0, a1, a2, a3);   // dims 32 x .. 32 x + 31 of the 8 rows
+      mma_k8(acc[2 * x], a0, a1, bw);
+      mma_k8(acc[2 * x + 1], a2, a3, bw);
+    }
+  };
+
+  // Software pipeline: iteration t scores step t and attends step t - 1 (two
+  // independent chains per warp); slot t - 1 is refilled (step t + kUSt - 1)
+  // once its V rows are consumed.
+  float zp = 0.0f;
+  int enp = 0, rkp = -1;
+#pragma unroll 1
+  for (int t = 0; t < nloc; ++t) {
+    cp_async_wait<kUSt - 2>();                  // this lane's copies of step t landed
+    __syncwarp();                               // ... and the warp's
+    const uint32_t kst = wring + (t % kUSt) * kStepB;
+    const int en = en_n, rk = rk_n;             // (en = 0: no row)
+    fetch_own(t + 1);
+    const float z = score(kst);
+    if (t > 0) attend(zp, enp, rkp, wring + ((t + kUSt - 1) % kUSt) * kStepB);
+    zp = z;
+    enp = en;
+    rkp = rk;
+    __syncwarp();                               // slot t - 1 is free
+    issue((t + kUSt - 1) % kUSt);
+    fetch(t + kUSt);
   }
-  if (l16 == 0) {
+  if (nloc > 0) attend(zp, enp, rkp, wring + ((nloc - 1) % kUSt) * kStepB);
+  cp_async_wait<0>();
+  __syncthreads();                              // the ring becomes merge scratch
+
+  // ---- this CTA's 4 warp states -> the slice partial of each head ------------------------
+  float* part = reinterpret_cast<float*>(ring);   // [kUWarps][kUG][kUD]
 #pragma unroll
-    for (int j = 0; j < HPL; ++j) { us.m[warp][hw * HPL + j] = m[j]; us.s[warp][hw * HPL + j] = ssum[j]; }
+  for (int x = 0; x < 8; ++x) {
+    part[(warp * kUG + t4) * kUD + 16 * x + nn] = acc[x][0] + acc[x][1];
+    part[(warp * kUG + t4) * kUD + 16 * x + 8 + nn] = acc[x][2] + acc[x][3];
   }
-  // the checks of head hh: rows of both parities
-  mxc = fmaxf(mxc, __shfl_xor_sync(LFPS_FULL, mxc, 8));
-  chk += __shfl_xor_sync(LFPS_FULL, chk, 8);
-  if (writer && rr == 0) { us.mx[warp][hh] = mxc; us.ck[warp][hh] = chk; }
+#pragma unroll
+  for (int o = 1; o <= 4; o <<= 1) {
+    ssum += __shfl_xor_sync(LFPS_FULL, ssum, o);
+    chk += __shfl_xor_sync(LFPS_FULL, chk, o);
+    mxc = fmaxf(mxc, __shfl_xor_sync(LFPS_FULL, mxc, o));
+  }
+  if (r == 0) {
+    us.m[warp][h] = mo;
+    us.s[warp][h] = ssum;
+    us.mx[warp][h] = mxc;
+    us.ck[warp][h] = chk;
+  }
   __syncthreads();
-  float* up = c.unit_part + ((size_t)u * kUnitMaxSlices + sl) * G * (D + 4);
-  for (int x = tid; x < G * D; x += kThreads) {
-    const int g = x / D, el = x - g * D;
+  const int hmask = us.hmask;
+  float* up = c.unit_part + ((size_t)u * kUnitMaxSlices + sl) * kUG * (kUD + 4);
+  for (int x = tid; x < kUG * kUD; x += kUThreads) {
+    const int g = x / kUD, el = x - g * kUD;
     float M = -INFINITY;
 #pragma unroll
-    for (int k2 = 0; k2 < kWarps; ++k2) M = fmaxf(M, us.m[k2][g]);
+    for (int k2 = 0; k2 < kUWarps; ++k2) M = fmaxf(M, us.m[k2][g]);
     float num = 0.0f, den = 0.0f;
     if (M != -INFINITY) {
-#pragma unroll 4
-      for (int k2 = 0; k2 < kWarps; ++k2) {
+#pragma unroll
+      for (int k2 = 0; k2 < kUWarps; ++k2) {
         if (us.m[k2][g] == -INFINITY) continue;
         const float f = ex2(us.m[k2][g] - M);
-        num = fmaf(f, part[(k2 * G + g) * D + el], num);
+        num = fmaf(f, part[(k2 * kUG + g) * kUD + el], num);
         den = fmaf(f, us.s[k2][g], den);
       }
     }
-    float* pg = up + g * (D + 4);
+    float* pg = up + g * (kUD + 4);
     pg[4 + el] = num;
     if (el == 0) {
       float mx = -INFINITY, ck = 0.0f;
 #pragma unroll
-      for (int k2 = 0; k2 < kWarps; ++k2) { mx = fmaxf(mx, us.mx[k2][g]); ck += us.ck[k2][g]; }
+      for (int k2 = 0; k2 < kUWarps; ++k2) { mx = fmaxf(mx, us.mx[k2][g]); ck += us.ck[k2][g]; }
       pg[0] = M;
       pg[1] = den;
       pg[2] = mx;
@@ -515,28 +343,28 @@ __global__ void __launch_bounds__(kThreads, LFPS_UNIT_MINB)
   }
   // ---- the unit's last slice: merge the slices into every head's output -----------------
   __threadfence();
-  const float* u0 = c.unit_part + (size_t)u * kUnitMaxSlices * G * (D + 4);
-  for (int x = tid; x < G * D; x += kThreads) {
-    const int g = x / D, el = x - g * D;
+  const float* u0 = c.unit_part + (size_t)u * kUnitMaxSlices * kUG * (kUD + 4);
+  for (int x = tid; x < kUG * kUD; x += kUThreads) {
+    const int g = x / kUD, el = x - g * kUD;
     if (!((hmask >> g) & 1)) continue;
     float M = -INFINITY;
-    for (int k2 = 0; k2 < nsl; ++k2) M = fmaxf(M, __ldcg(u0 + (k2 * G + g) * (D + 4)));
+    for (int k2 = 0; k2 < nsl; ++k2) M = fmaxf(M, __ldcg(u0 + (k2 * kUG + g) * (kUD + 4)));
     float num = 0.0f, den = 0.0f;
     for (int k2 = 0; k2 < nsl; ++k2) {
-      const float* pk = u0 + (k2 * G + g) * (D + 4);
+      const float* pk = u0 + (k2 * kUG + g) * (kUD + 4);
       const float mk = __ldcg(pk);
       if (mk == -INFINITY) continue;
       const float f = ex2(mk - M);
       num = fmaf(f, __ldcg(pk + 4 + el), num);
       den = fmaf(f, __ldcg(pk + 1), den);
     }
-    c.out[(size_t)(u * G + g) * D + el] = num / den;
+    c.out[(size_t)(u * kUG + g) * kUD + el] = num / den;
   }
-  if (tid < G && ((hmask >> tid) & 1)) {
-    const int s = u * G + tid;
+  if (tid < kUG && ((hmask >> tid) & 1)) {
+    const int s = u * kUG + tid;
     float mx = -INFINITY, ck = 0.0f;
     for (int k2 = 0; k2 < nsl; ++k2) {
-      const float* pk = u0 + (k2 * G + tid) * (D + 4);
+      const float* pk = u0 + (k2 * kUG + tid) * (kUD + 4);
       mx = fmaxf(mx, __ldcg(pk + 2));
       ck += __ldcg(pk + 3);
     }
@@ -547,46 +375,32 @@ __global__ void __launch_bounds__(kThreads, LFPS_UNIT_MINB)
   pdl_trigger();
 }
 
-template <int PQ, int G, int RM>
+template <int RM>
 cudaError_t launch_unit_rm(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
-  const size_t smem = unit_smem(c.d);
   static DeviceOnce once;
   cudaError_t e = once.run([&] {
-    cudaError_t r = cudaFuncSetAttribute(lfps_unit_finish_kernel<PQ, G, RM>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t r = cudaFuncSetAttribute(lfps_unit_finish_kernel<RM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUnitSmem);
     if (r == cudaSuccess)
-      r = cudaFuncSetAttribute(lfps_unit_finish_kernel<PQ, G, RM>,
-                               cudaFuncAttributePreferredSharedMemoryCarveout,
+      r = cudaFuncSetAttribute(lfps_unit_finish_kernel<RM>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                cudaSharedmemCarveoutMaxShared);
     return r;
   });
   if (e != cudaSuccess) return e;
-  const int units = c.s_cnt / G;
-  return launch_pdl(lfps_unit_finish_kernel<PQ, G, RM>, dim3(units * c.unit_nsl), dim3(kThreads), smem,
-                    st, c, q);
-}
-
-template <int PQ, int G>
-cudaError_t launch_unit_g(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
-  return c.bt ? launch_unit_rm<PQ, G, 1>(c, q, st) : launch_unit_rm<PQ, G, 0>(c, q, st);
+  const int units = c.s_cnt / kUG;
+  return launch_pdl(lfps_unit_finish_kernel<RM>, dim3(units * c.unit_nsl), dim3(kUThreads), kUnitSmem, st,
+                    c, q);
 }
 
 }  // namespace
 
-bool unit_finish_supported(int G, int d) { return (G == 2 || G == 4) && (d == 64 || d == 128); }
+bool unit_finish_supported(int G, int d) { return G == kUG && d == kUD; }
 
-// c.unit_nsl CTAs per unit, G <= unit_nsl <= kUnitMaxSlices (the
-// Top-k-cut fallback needs one CTA per session)
+// c.unit_nsl CTAs per unit, 1 <= unit_nsl <= kUnitMaxSlices
 cudaError_t launch_finish_unit(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st) {
-  if (c.unit_nsl < c.G || c.unit_nsl > kUnitMaxSlices) return cudaErrorInvalidValue;
-  if (c.d == 128) {
-    if (c.G == 4) return launch_unit_g<8, 4>(c, q, st);
-    if (c.G == 2) return launch_unit_g<8, 2>(c, q, st);
-  } else if (c.d == 64) {
-    if (c.G == 4) return launch_unit_g<4, 4>(c, q, st);
-    if (c.G == 2) return launch_unit_g<4, 2>(c, q, st);
-  }
-  return cudaErrorInvalidValue;
+  if (c.unit_nsl < 1 || c.unit_nsl > kUnitMaxSlices || !unit_finish_supported(c.G, c.d))
+    return cudaErrorInvalidValue;
+  return c.bt ? launch_unit_rm<1>(c, q, st) : launch_unit_rm<0>(c, q, st);
 }
 
 }  // namespace lfps

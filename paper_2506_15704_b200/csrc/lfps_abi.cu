@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <cmath>
+#include <algorithm>
 #include <atomic>
 #include <map>
 #include <memory>
@@ -133,7 +134,12 @@ int layout(const lfps_dims* d, lfps_ws_layout* L) {
   L->hot = take(NI * (size_t)(16 * L->nblk + 1) * 8);
   L->thr_next = take(NS * 8 * 8);
   const size_t units = (size_t)d->batch * d->kv_heads;
-  L->unit_dir = take(NS * (lfps::kUnitMaxSlices + 1) * 4);
+  // union entries: every row of the context at most once, plus the sinks
+  const size_t ucap = align_up(std::min((size_t)d->n_max, (size_t)d->group * cap) + 64, 32);
+  L->unit_cap = (int)ucap;
+  L->unit_ent = take(units * ucap * 4);
+  L->unit_rank = take(units * ucap * 16);
+  L->unit_count = take(units * 4);
   L->unit_part = take(units * lfps::kUnitMaxSlices * d->group * (d->d + 4) * 4);
   L->unit_ticket = take(units * 4);
   L->total_bytes = o;
@@ -215,7 +221,10 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
   c->thr_next = reinterpret_cast<double*>(base + L.thr_next);
   c->bw.nblk = L.nblk;
   c->bw.dwords = L.dirty_words;
-  c->unit_dir = reinterpret_cast<int*>(base + L.unit_dir);
+  c->unit_ent = reinterpret_cast<int*>(base + L.unit_ent);
+  c->unit_rank = reinterpret_cast<int*>(base + L.unit_rank);
+  c->unit_count = reinterpret_cast<int*>(base + L.unit_count);
+  c->unit_cap = L.unit_cap;
   c->unit_part = reinterpret_cast<float*>(base + L.unit_part);
   c->unit_ticket = reinterpret_cast<unsigned*>(base + L.unit_ticket);
   return LFPS_OK;
@@ -314,7 +323,7 @@ int unit_slices(const lfps::Ctx& c) {
   const int units = c.s_cnt / c.G;
   int n = (LFPS_UNIT_CTAS + units - 1) / units;
   if (const char* e = getenv("LFPS_UNIT_SLICES")) n = atoi(e);
-  if (n < c.G) n = c.G;
+  if (n < 1) n = 1;
   if (n > lfps::kUnitMaxSlices) n = lfps::kUnitMaxSlices;
   return n;
 }
@@ -608,11 +617,16 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
   const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
   const size_t in_bytes = ((size_t)c.NS + 2 * (size_t)c.B * c.Hkv) * c.d * sizeof(__nv_bfloat16);
   const bool unit = (c.flags & LFPS_FLAG_UNIT_FINISH) && lfps::unit_finish_supported(c.G, c.d);
-  auto select = [&](const lfps::Ctx& x, cudaStream_t s_) {
-    return unit ? lfps::launch_select_unit(x, m_max, s_) : lfps::launch_select(x, m_max, s_);
-  };
+  auto select = [&](const lfps::Ctx& x, cudaStream_t s_) { return lfps::launch_select(x, m_max, s_); };
+  // per-unit finish: the union table, the unit kernel over it, then the
+  // per-session kernel for the units with a Top-k cut only
   auto finish = [&](const lfps::Ctx& x, cudaStream_t s_) {
-    return unit ? lfps::launch_finish_unit(x, qb, s_) : lfps::launch_finish(x, qb, s_);
+    if (!unit) return lfps::launch_finish(x, qb, s_);
+    cudaError_t e = lfps::launch_union(x, s_);
+    if (e == cudaSuccess) e = lfps::launch_finish_unit(x, qb, s_);
+    lfps::Ctx xs = x;
+    xs.unit_skip = 1;
+    return e == cudaSuccess ? lfps::launch_finish(xs, qb, s_) : e;
   };
   if (c.stamp) LAUNCH(lfps::launch_step_begin(c, sm));
   if (in_host && g_prof_on)
@@ -651,7 +665,15 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
       LAUNCH(cudaStreamWaitEvent(gs, pp->stats[g], 0));
       LAUNCH(select(cg, gs));
     }
-    LAUNCH_P("finish", gs, finish(cg, gs));
+    if (unit && g_prof_on) {                  // the three kernels of the per-unit finish, timed alone
+      lfps::Ctx cs = cg;
+      cs.unit_skip = 1;
+      LAUNCH_P("union", gs, lfps::launch_union(cg, gs));
+      LAUNCH_P("unit", gs, lfps::launch_finish_unit(cg, qb, gs));
+      LAUNCH_P("finish", gs, lfps::launch_finish(cs, qb, gs));
+    } else {
+      LAUNCH_P("finish", gs, finish(cg, gs));
+    }
     if (split) {
       LAUNCH(cudaEventRecord(pp->join[g], gs));
       LAUNCH(cudaStreamWaitEvent(sm, pp->join[g], 0));

@@ -73,13 +73,6 @@ __host__ __device__ constexpr size_t select_smem(int m_max) {
 
 // C + D of session s from the thresholds and C0 words of lfps_stats_kernel;
 // smem: select_smem(m_max) bytes of dynamic shared memory.
-// UNIT (the per-unit finish, k_unit.cu): the probe list is written to the
-// C2 list as well, when k >= |probe| (C2 = probe: attention.py:34-47 keeps
-// every candidate) the K / C2 counts are final here, and the slice directory
-// unit_dir[s][j] = |{probe rows with logical index < j R}|, R = ceil(m /
-// unit_nsl), j = 0 .. unit_nsl, tells each finish CTA (one per row slice of
-// the unit) where its rows start in every head's list.
-template <bool UNIT = false>
 __device__ __forceinline__ void select_session(const Ctx& c, int s, uint32_t* smem,
                                                SelectShared& sh) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -196,7 +189,6 @@ __device__ __forceinline__ void select_session(const Ctx& c, int s, uint32_t* sm
     const int tail_lo = max(0, m - c.L);
     const uint32_t last_valid = (m & 31) ? ((1u << (m & 31)) - 1u) : LFPS_FULL;
     int* out = c.probe_idx + (size_t)s * c.list_cap;
-    int* out2 = c.c2_idx + (size_t)s * c.list_cap;
     int n0 = 0, n1 = 0, nd = 0, written = 0;
     for (int r = 0; r < na; r += kThreads) {
       const int j = r + tid;
@@ -259,27 +251,7 @@ __device__ __forceinline__ void select_session(const Ctx& c, int s, uint32_t* sm
       }
       int tot;
       int at = written + block_scan(__popc(pr), sh.wsum, &tot);
-      if (UNIT && w >= 0) {
-        // slice boundaries L = jR in (previous active word, w]: the rows
-        // before L are this thread's first rows (bits below L in word w)
-        const int R = (m + c.unit_nsl - 1) / c.unit_nsl;
-        const int pw = j > 0 ? alist[j - 1] : -1;
-        int* dir = c.unit_dir + (size_t)s * (kUnitMaxSlices + 1);
-        for (int jj = (pw + 1) * 32 / R + ((pw + 1) * 32 % R != 0); jj < c.unit_nsl; ++jj) {
-          const int L = jj * R;
-          if (L > w * 32 + 31) break;
-          dir[jj] = at + ((L >> 5) == w ? __popc(pr & ((1u << (L & 31)) - 1u)) : 0);
-        }
-      }
-      if (UNIT) {
-        for (; pr; pr &= pr - 1) {
-          const int row = S + w * 32 + __ffs(pr) - 1;
-          out[at] = row;
-          out2[at++] = row;
-        }
-      } else {
-        for (; pr; pr &= pr - 1) out[at++] = S + w * 32 + __ffs(pr) - 1;
-      }
+      for (; pr; pr &= pr - 1) out[at++] = S + w * 32 + __ffs(pr) - 1;
       written += tot;
     }
 #pragma unroll
@@ -296,18 +268,6 @@ __device__ __forceinline__ void select_session(const Ctx& c, int s, uint32_t* sm
       cnt[CNT_C0] = t0;
       cnt[CNT_C1] = t1;
       cnt[CNT_PROBE] = written;
-      if (UNIT) {
-        const int k = unit_budget(c, n);
-        if (k >= written) { cnt[CNT_K] = k; cnt[CNT_C2] = written; }
-        // boundaries past the last active word, and the ends
-        const int R = (m + c.unit_nsl - 1) / c.unit_nsl;
-        const int lw = na > 0 ? alist[na - 1] : -1;
-        int* dir = c.unit_dir + (size_t)s * (kUnitMaxSlices + 1);
-        dir[0] = 0;
-        for (int jj = 1; jj < c.unit_nsl; ++jj)
-          if (jj * R > lw * 32 + 31) dir[jj] = written;
-        dir[c.unit_nsl] = written;
-      }
       cnt[CNT_DROP] = t3;
       cnt[CNT_BLOCKS] = blocks;
       if (c.flags & LFPS_FLAG_TRACE) {

@@ -1,13 +1,17 @@
-# per-unit finish A/B: parity of the unit tests, then C4 lines (session finish,
-# unit finish on the default build and on variant libraries)
-mkdir -p gpurun_out/ab
-timeout 600 python -m pytest tests -m gpu -x -q -k "unit_finish" > gpurun_out/ab/tests.txt 2>&1; echo "tests rc $?"; tail -2 gpurun_out/ab/tests.txt
-line() { python -c "import json,sys
-for l in open('$1'):
-    if l.startswith('{'): d=json.loads(l); print('$2', round(d['value'],1), {k: round(v*1000,1) for k,v in d['kernel_ms'].items()})"; }
-timeout 300 python bench.py --no-cpu --verify 0 --steps 20 > gpurun_out/ab/sess.jsonl 2>/dev/null; line gpurun_out/ab/sess.jsonl session
-timeout 300 python bench.py --no-cpu --verify 1 --steps 20 --unit-finish > gpurun_out/ab/unit.jsonl 2>gpurun_out/ab/unit.err; line gpurun_out/ab/unit.jsonl unit-default
-for v in ${VARIANTS:-}; do
-  LFPS_LIB=$PWD/paper_2506_15704_b200/lib/variants/$v.so timeout 300 python bench.py --no-cpu --verify 0 --steps 20 --unit-finish > gpurun_out/ab/$v.jsonl 2>/dev/null; line gpurun_out/ab/$v.jsonl unit-$v
-done
-tail -3 gpurun_out/ab/unit.err
+# per-unit finish: parity tests, bench lines (kernel_ms) per slice count and the per-session finish, ncu of union + unit
+mkdir -p gpurun_out
+timeout 400 python -m pytest tests -m gpu -x -q --timeout 200 -k "unit" > gpurun_out/pytest_unit.log 2>&1; echo pytest rc $?
+tail -3 gpurun_out/pytest_unit.log
+run() {  # name, bench args, env...
+  name=$1; shift; args=$1; shift
+  env "$@" timeout 300 python bench.py --no-cpu $args --steps 10 --verify 1 --recall-steps 0 > gpurun_out/ab_$name.log 2>&1
+  tail -1 gpurun_out/ab_$name.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$name', round(d['value'],1), {k: round(v*1000,1) for k,v in d['kernel_ms'].items()}, d.get('verified_units',{}).get('output_rel_err_max'))"
+}
+run unit "--unit-finish"
+run unit_sl4 "--unit-finish" LFPS_UNIT_SLICES=4
+run unit_sl1 "--unit-finish" LFPS_UNIT_SLICES=1
+run session ""
+for v in ${VARIANTS:-}; do run $v "--unit-finish" LFPS_LIB=$PWD/paper_2506_15704_b200/lib/variants/$v.so; done
+timeout 900 ncu --set full --clock-control none --import-source on \
+  -k regex:"lfps_(union|unit)" -s 6 -c 2 -o gpurun_out/prof_unit -f \
+  python bench.py --profile-only --unit-finish --steps 2 --warmup 2 --verify 0 --no-cpu > gpurun_out/ncu_full.log 2>&1; echo full rc $?
