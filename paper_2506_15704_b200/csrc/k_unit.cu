@@ -45,7 +45,7 @@ constexpr int kUWarps = kUThreads / 32;
 constexpr int kUG = 4;                   // heads per unit
 constexpr int kUD = 128;                 // head dimension
 #ifndef LFPS_UNIT_STAGES
-#define LFPS_UNIT_STAGES 4
+#define LFPS_UNIT_STAGES 3
 #endif
 #ifndef LFPS_UNIT_MINB
 #define LFPS_UNIT_MINB 3
@@ -53,7 +53,9 @@ constexpr int kUD = 128;                 // head dimension
 constexpr int kUSt = LFPS_UNIT_STAGES;   // ring steps per warp
 constexpr int kRowP = 272;               // padded shared row: 256 B + 16
 constexpr int kStepB = 2 * 8 * kRowP;    // one step: 8 K rows, then 8 V rows
-constexpr size_t kUnitSmem = (size_t)kUWarps * kUSt * kStepB;
+constexpr int kRingB = kUWarps * kUSt * kStepB;
+constexpr int kEC = 1024;                // union entries per shared-memory chunk
+constexpr size_t kUnitSmem = (size_t)kRingB + kEC * 20;
 constexpr float kRescale = 8.0f;         // log2 headroom before an online-softmax rescale
 
 static_assert((size_t)kUWarps * kUG * kUD * 4 <= kUnitSmem, "merge scratch fits the ring");
@@ -124,58 +126,17 @@ __global__ void __launch_bounds__(kUThreads, LFPS_UNIT_MINB) lfps_unit_finish_ke
     }
   }
 
-  // ---- the ring: a warp's steps w, w + 4, ... of 8 entries each -------------------------
+  // ---- the entries, kEC at a time in shared memory; a warp's steps w, w + 4, ... -------
   const RowMapT<RM> rmap(c, b, hk);
   const uint8_t* kb = reinterpret_cast<const uint8_t*>(RM == 0 ? krow(c, b, hk, 0) : c.K);
   const uint8_t* vb = reinterpret_cast<const uint8_t*>(RM == 0 ? vrow(c, b, hk, 0) : c.V);
-  const int nsteps = (e1 - e0 + 7) >> 3;
-  const int nloc = nsteps > warp ? (nsteps - warp + kUWarps - 1) / kUWarps : 0;
   const uint32_t wring = smem_u32(ring) + warp * (kUSt * kStepB);
+  int* sent = reinterpret_cast<int*>(ring + kRingB);             // [kEC] entries
+  int4* srk = reinterpret_cast<int4*>(ring + kRingB + kEC * 4);  // [kEC] list ranks
   // stale slots of rows past the end meet the mma with weight 0: zero them once
   for (int o = lane * 16; o < kUSt * kStepB; o += 32 * 16)
     asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(wring + o), "r"(0u) : "memory");
-  __syncwarp();
   const int cc = lane & 15, rh = lane >> 4;     // copies: chunk cc of rows 2 i + rh
-  int nxt[4];                                   // entries of the next step to issue (-1: none)
-  auto fetch = [&](int t) {                     // (no use of the loads here: they land a step later)
-    const int eb = e0 + (warp + kUWarps * t) * 8;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int e = eb + 2 * i + rh;
-      nxt[i] = -1;
-      if (t < nloc && e < e1) nxt[i] = __ldg(ent + e);
-    }
-  };
-  auto issue = [&](int slot) {
-    const uint32_t dst = wring + slot * kStepB + cc * 16;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (nxt[i] < 0) continue;
-      const int row = RM == 0 ? (nxt[i] & 0xffffff) : rmap(nxt[i] & 0xffffff);
-      const size_t off = (size_t)row * (kUD * 2) + cc * 16;
-      cp_async16_s(dst + (2 * i + rh) * kRowP, kb + off);
-      cp_async16_s(dst + (8 + 2 * i + rh) * kRowP, vb + off);
-    }
-    cp_async_commit();                          // one group per step, even if empty
-  };
-#pragma unroll 1
-  for (int t = 0; t < kUSt - 1; ++t) {
-    fetch(t);
-    issue(t);
-  }
-  fetch(kUSt - 1);
-  // this lane's entry (row | heads | sink) and list rank, one step ahead
-  int en_n = 0, rk_n = -1;
-  auto fetch_own = [&](int t) {
-    const int e = e0 + (warp + kUWarps * t) * 8 + r;
-    en_n = 0;
-    rk_n = -1;
-    if (t < nloc && e < e1) {
-      en_n = __ldg(ent + e);
-      rk_n = __ldg(rnk + 4 * e + h);
-    }
-  };
-  fetch_own(0);
 
   float acc[8][4];                              // D[dims 16 x + (lane / 4) (+8)][head lane % 4, hi | lo]
 #pragma unroll
@@ -186,101 +147,118 @@ __global__ void __launch_bounds__(kUThreads, LFPS_UNIT_MINB) lfps_unit_finish_ke
   const int bsrc = (nn >> 1) * 8 + 2 * t4;
   const uint32_t vlane = 8 * kRowP + (lane & 7) * kRowP + (lane >> 3) * 16;
 
-  // the canonical score of row r of the step in slot kst for head h
-  auto score = [&](uint32_t kst) {
-    float x8[8];
-    const uint32_t kr = kst + r * kRowP;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const uint4 kv = lds128(kr + j * 16);
-      float p = 0.0f;
-      p = fma_lo(kv.x, qw[4 * j], p);
-      p = fma_hi(kv.x, qw[4 * j], p);
-      p = fma_lo(kv.y, qw[4 * j + 1], p);
-      p = fma_hi(kv.y, qw[4 * j + 1], p);
-      p = fma_lo(kv.z, qw[4 * j + 2], p);
-      p = fma_hi(kv.z, qw[4 * j + 2], p);
-      p = fma_lo(kv.w, qw[4 * j + 3], p);
-      p = fma_hi(kv.w, qw[4 * j + 3], p);
-      if (j < 8) x8[j] = p;
-      else x8[j - 8] = __fadd_rn(x8[j - 8], p);
-    }
-    const float y0 = __fadd_rn(x8[0], x8[4]), y1 = __fadd_rn(x8[1], x8[5]);
-    const float y2 = __fadd_rn(x8[2], x8[6]), y3 = __fadd_rn(x8[3], x8[7]);
-    return __fdiv_rn(__fadd_rn(__fadd_rn(y0, y2), __fadd_rn(y1, y3)), c.sqrt_d_f32);
-  };
-  // the checks, the C2 score, the online softmax (lazy max) and sum w V of a
-  // scored step (entry en, rank rk of row r) whose V rows are in slot kst
-  auto attend = [&](float z, int en, int rk, uint32_t kst) {
-    const bool mem = (en >> (24 + h)) & 1;
-    if (mem) {
-      chk = __fmaf_rn(z, 0.0f, chk);
-      if (!((en >> 28) & 1)) {                  // a C2 row (not a sink)
-        mxc = fmaxf(mxc, z);
-        c2z[rk] = z;
-      }
-    }
-    const float zl = mem ? z * kLog2e : -INFINITY;
-    float mh = fmaxf(zl, __shfl_xor_sync(LFPS_FULL, zl, 1));
-    mh = fmaxf(mh, __shfl_xor_sync(LFPS_FULL, mh, 2));
-    mh = fmaxf(mh, __shfl_xor_sync(LFPS_FULL, mh, 4));          // step max of head h
-    const float ta = __shfl_sync(LFPS_FULL, mh, t4 * 8);        // ... of head lane % 4
-    const bool ga = ta > ma + kRescale;
-    if (__any_sync(LFPS_FULL, ga)) {
-      const float f = ga ? ex2(ma - ta) : 1.0f;
-#pragma unroll
-      for (int x = 0; x < 8; ++x) {
-        acc[x][0] *= f; acc[x][1] *= f; acc[x][2] *= f; acc[x][3] *= f;
-      }
-      ma = ga ? ta : ma;
-    }
-    if (mh > mo + kRescale) {
-      ssum *= ex2(mo - mh);
-      mo = mh;
-    }
-    const float w = mem ? ex2(zl - mo) : 0.0f;
-    ssum += w;
-    // W column 2 h' + 0 / 1 = head h' high / low parts; lane 8 h' + 2 i holds
-    // rows 2 i, 2 i + 1 of head h' packed
-    const float wn = __shfl_xor_sync(LFPS_FULL, w, 1);
-    const float wa = (r & 1) ? wn : w, wb = (r & 1) ? w : wn;
-    const uint32_t hi = cvt_bf16x2(wa, wb);
-    const uint32_t lo = cvt_bf16x2(wa - bf_lo(hi), wb - bf_hi(hi));
-    const uint32_t bh = __shfl_sync(LFPS_FULL, hi, bsrc);
-    const uint32_t bl = __shfl_sync(LFPS_FULL, lo, bsrc);
-    const uint32_t bw = (nn & 1) ? bl : bh;
-    const uint32_t vr = kst + vlane;
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      uint32_t a0, a1, a2, a3;
-      ldsm_x4_t(vr + x * 64, a0, a1, a2, a3);   // dims 32 x .. 32 x + 31 of the 8 rows
-      mma_k8(acc[2 * x], a0, a1, bw);
-      mma_k8(acc[2 * x + 1], a2, a3, bw);
-    }
-  };
-
-  // Software pipeline: iteration t scores step t and attends step t - 1 (two
-  // independent chains per warp); slot t - 1 is refilled (step t + kUSt - 1)
-  // once its V rows are consumed.
-  float zp = 0.0f;
-  int enp = 0, rkp = -1;
 #pragma unroll 1
-  for (int t = 0; t < nloc; ++t) {
-    cp_async_wait<kUSt - 2>();                  // this lane's copies of step t landed
-    __syncwarp();                               // ... and the warp's
-    const uint32_t kst = wring + (t % kUSt) * kStepB;
-    const int en = en_n, rk = rk_n;             // (en = 0: no row)
-    fetch_own(t + 1);
-    const float z = score(kst);
-    if (t > 0) attend(zp, enp, rkp, wring + ((t + kUSt - 1) % kUSt) * kStepB);
-    zp = z;
-    enp = en;
-    rkp = rk;
-    __syncwarp();                               // slot t - 1 is free
-    issue((t + kUSt - 1) % kUSt);
-    fetch(t + kUSt);
+  for (int c0 = e0; c0 < e1; c0 += kEC) {
+    const int ne = min(kEC, e1 - c0);
+    __syncthreads();                            // the previous chunk's table is consumed
+    for (int i = tid; i < ne; i += kUThreads) {
+      sent[i] = __ldg(ent + c0 + i);
+      srk[i] = __ldg(reinterpret_cast<const int4*>(rnk) + c0 + i);
+    }
+    __syncthreads();
+    const int nsteps = (ne + 7) >> 3;
+    const int nloc = nsteps > warp ? (nsteps - warp + kUWarps - 1) / kUWarps : 0;
+    // copy the K and V rows of local step t into ring slot `slot`
+    auto issue = [&](int slot, int t) {
+      if (t < nloc) {
+        const uint32_t dst = wring + slot * kStepB + cc * 16;
+        const int eb = (warp + kUWarps * t) * 8;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int e = eb + 2 * i + rh;
+          if (e >= ne) continue;
+          const int r0 = sent[e] & 0xffffff;
+          const int row = RM == 0 ? r0 : rmap(r0);
+          const size_t off = (size_t)row * (kUD * 2) + cc * 16;
+          cp_async16_s(dst + (2 * i + rh) * kRowP, kb + off);
+          cp_async16_s(dst + (8 + 2 * i + rh) * kRowP, vb + off);
+        }
+      }
+      cp_async_commit();                        // one group per step, even if empty
+    };
+#pragma unroll 1
+    for (int t = 0; t < kUSt - 1; ++t) issue(t, t);
+#pragma unroll 1
+    for (int t = 0; t < nloc; ++t) {
+      cp_async_wait<kUSt - 2>();                // this lane's copies of step t landed
+      __syncwarp();                             // ... and the warp's; slot t - 1 is free
+      issue((t + kUSt - 1) % kUSt, t + kUSt - 1);
+      const uint32_t kst = wring + (t % kUSt) * kStepB;
+      const int e = (warp + kUWarps * t) * 8 + r;
+      const int en = e < ne ? sent[e] : 0;      // (0: no row)
+      const int rk = (&srk[e < ne ? e : 0].x)[h];
+
+      // ---- the canonical score of row r for head h -----------------------------------
+      float x8[8];
+      const uint32_t kr = kst + r * kRowP;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const uint4 kv = lds128(kr + j * 16);
+        float p = 0.0f;
+        p = fma_lo(kv.x, qw[4 * j], p);
+        p = fma_hi(kv.x, qw[4 * j], p);
+        p = fma_lo(kv.y, qw[4 * j + 1], p);
+        p = fma_hi(kv.y, qw[4 * j + 1], p);
+        p = fma_lo(kv.z, qw[4 * j + 2], p);
+        p = fma_hi(kv.z, qw[4 * j + 2], p);
+        p = fma_lo(kv.w, qw[4 * j + 3], p);
+        p = fma_hi(kv.w, qw[4 * j + 3], p);
+        if (j < 8) x8[j] = p;
+        else x8[j - 8] = __fadd_rn(x8[j - 8], p);
+      }
+      const float y0 = __fadd_rn(x8[0], x8[4]), y1 = __fadd_rn(x8[1], x8[5]);
+      const float y2 = __fadd_rn(x8[2], x8[6]), y3 = __fadd_rn(x8[3], x8[7]);
+      const float z = __fdiv_rn(__fadd_rn(__fadd_rn(y0, y2), __fadd_rn(y1, y3)), c.sqrt_d_f32);
+
+      const bool mem = (en >> (24 + h)) & 1;
+      if (mem) {
+        chk = __fmaf_rn(z, 0.0f, chk);
+        if (!((en >> 28) & 1)) {                // a C2 row (not a sink)
+          mxc = fmaxf(mxc, z);
+          c2z[rk] = z;
+        }
+      }
+      // ---- online softmax (lazy max) and sum w V ---------------------------------------
+      const float zl = mem ? z * kLog2e : -INFINITY;
+      float mh = fmaxf(zl, __shfl_xor_sync(LFPS_FULL, zl, 1));
+      mh = fmaxf(mh, __shfl_xor_sync(LFPS_FULL, mh, 2));
+      mh = fmaxf(mh, __shfl_xor_sync(LFPS_FULL, mh, 4));        // step max of head h
+      const float ta = __shfl_sync(LFPS_FULL, mh, t4 * 8);      // ... of head lane % 4
+      const bool ga = ta > ma + kRescale;
+      if (__any_sync(LFPS_FULL, ga)) {
+        const float f = ga ? ex2(ma - ta) : 1.0f;
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          acc[x][0] *= f; acc[x][1] *= f; acc[x][2] *= f; acc[x][3] *= f;
+        }
+        ma = ga ? ta : ma;
+      }
+      if (mh > mo + kRescale) {
+        ssum *= ex2(mo - mh);
+        mo = mh;
+      }
+      const float w = mem ? ex2(zl - mo) : 0.0f;
+      ssum += w;
+      // W column 2 h' + 0 / 1 = head h' high / low parts; lane 8 h' + 2 i holds
+      // rows 2 i, 2 i + 1 of head h' packed
+      const float wn = __shfl_xor_sync(LFPS_FULL, w, 1);
+      const float wa = (r & 1) ? wn : w, wb = (r & 1) ? w : wn;
+      const uint32_t hi = cvt_bf16x2(wa, wb);
+      const uint32_t lo = cvt_bf16x2(wa - bf_lo(hi), wb - bf_hi(hi));
+      const uint32_t bh = __shfl_sync(LFPS_FULL, hi, bsrc);
+      const uint32_t bl = __shfl_sync(LFPS_FULL, lo, bsrc);
+      const uint32_t bw = (nn & 1) ? bl : bh;
+      const uint32_t vr = kst + vlane;
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4_t(vr + x * 64, a0, a1, a2, a3); // dims 32 x .. 32 x + 31 of the 8 rows
+        mma_k8(acc[2 * x], a0, a1, bw);
+        mma_k8(acc[2 * x + 1], a2, a3, bw);
+      }
+    }
+    cp_async_wait<0>();
   }
-  if (nloc > 0) attend(zp, enp, rkp, wring + ((nloc - 1) % kUSt) * kStepB);
   cp_async_wait<0>();
   __syncthreads();                              // the ring becomes merge scratch
 
