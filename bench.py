@@ -61,8 +61,6 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=6, help="steps per CPU worker sample")
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = all host cores")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--unit-finish", action="store_true",
-                    help="per-unit finish kernel (csrc/k_unit.cu) instead of the per-session one")
     ap.add_argument("--no-graph", action="store_true",
                     help="e2e: enqueue each host-input step kernel by kernel (no CUDA graph)")
     ap.add_argument("--no-split", action="store_true",
@@ -595,7 +593,6 @@ def run_ours(args, world, rank, local):
                         v_new=torch.stack([ss.local_kv(x) for x in full.v_new]))
     del full
     sess.split = not args.no_split
-    sess.unit_finish = args.unit_finish
     sess.graph = not args.no_graph
     setup_s = time.time() - t_setup
     cuda_stream = torch.cuda.current_stream(dev)

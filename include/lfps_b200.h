@@ -104,10 +104,6 @@ typedef struct lfps_params {
 } lfps_params;
 
 /* lfps_params.flags */
-#define LFPS_FLAG_UNIT_FINISH 32 /* per-unit finish (k_unit.cu: the G q-heads of a
-                                    KV head over the union of their probe sets,
-                                    row slices merged) instead of the per-session
-                                    finish; G = 2 / 4 and d = 64 / 128 only */
 #define LFPS_FLAG_GRAPH 16       /* enqueue a decode step as one CUDA-graph launch: the
                                     step is captured once per (shapes, params,
                                     state, workspace, device buffers, context
@@ -188,22 +184,10 @@ typedef struct lfps_ws_layout {
                          index of the word's first slot, slot bits) */
   size_t thr_next;    /* f64 [NS, 2, 4] thresholds computed for the select
                          kernel (copied to thr for the non-gated sessions) */
-  /* Per-unit finish (LFPS_FLAG_UNIT_FINISH: one (request, KV-head) unit's G
-     q-heads over the union of their probe sets, in entry slices; written and
-     read within a step). */
-  size_t unit_ent;    /* i32 [B * Hkv, unit_cap] union rows: row | heads << 24
-                         | sink << 28 (sinks first, then each head's new rows) */
-  size_t unit_rank;   /* i32 [B * Hkv, unit_cap, 4] the row's index in each member
-                         head's probe list (-1: not a member) */
-  size_t unit_count;  /* i32 [B * Hkv] union entries; -1: a Top-k cut (the unit's
-                         sessions run the per-session finish) */
-  size_t unit_part;   /* f32 [B * Hkv, 16, G, d + 4] per-slice softmax partials */
-  size_t unit_ticket; /* u32 [B * Hkv] slices finished (kept at 0 between steps) */
   int32_t nblk;       /* blocks per item (slash_cap / 512) */
   int32_t dirty_words;
   int32_t words;      /* bitmap words per (session, table, kind) */
   int32_t list_cap;   /* capacity of each per-session list (m_cap rounded up to 32) */
-  int32_t unit_cap;   /* union entries per unit */
 } lfps_ws_layout;
 
 typedef struct lfps_workspace {

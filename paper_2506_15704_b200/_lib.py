@@ -23,7 +23,6 @@ FLAG_EXPORT_SETS = 1
 FLAG_TRACE = 2
 FLAG_SPLIT = 8
 FLAG_GRAPH = 16
-FLAG_UNIT_FINISH = 32
 
 # per-session device error codes (include/lfps_b200.h)
 ERR_NAMES = {
@@ -79,11 +78,9 @@ class WsLayout(C.Structure):
                 ("scratch", C.c_size_t), ("bsum", C.c_size_t), ("bmax", C.c_size_t),
                 ("dirty", C.c_size_t), ("valid", C.c_size_t), ("wstat", C.c_size_t), ("trace", C.c_size_t),
                 ("done", C.c_size_t), ("hot", C.c_size_t),
-                ("thr_next", C.c_size_t), ("unit_ent", C.c_size_t), ("unit_rank", C.c_size_t),
-                ("unit_count", C.c_size_t), ("unit_part", C.c_size_t),
-                ("unit_ticket", C.c_size_t),
+                ("thr_next", C.c_size_t),
                 ("nblk", C.c_int32), ("dirty_words", C.c_int32), ("words", C.c_int32),
-                ("list_cap", C.c_int32), ("unit_cap", C.c_int32)]
+                ("list_cap", C.c_int32)]
 
 
 class KernelTime(C.Structure):

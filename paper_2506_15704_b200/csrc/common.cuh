@@ -67,7 +67,7 @@ struct Ctx {
   float* probe_score;
   int* c2_idx;
   float* c2_score;
-  double* uw;       // [NS, list_cap] scratch (exact top-k overflow, per-unit finish weights)
+  double* uw;       // [NS, list_cap] scratch (exact top-k overflow)
   long long* trace; // [NS, 16] phase timestamps (LFPS_FLAG_TRACE)
   unsigned* done;     // [1] CTAs finished in the commit kernel (last one bumps n_ctx)
   int2* hot;          // [2 NS][16 nblk + 1] per-step C0 words (k_select.cu)
@@ -78,17 +78,7 @@ struct Ctx {
   // [blocks, block_rows, Hkv, d] pool; bt == nullptr: contiguous [B, Hkv, n_max, d]
   const int* bt;
   int bs_shift, bs_mask, max_blocks;
-  // per-unit finish (k_unit.cu)
-  int unit_nsl;        // entry slices (stream CTAs) per unit of this launch
-  int unit_skip;       // per-session finish: skip the sessions of units the union kernel fused
-  int unit_cap;        // union entries per unit
-  int* unit_ent;       // [units, unit_cap] row | heads << 24 | sink << 28 (k_union.cu)
-  int* unit_rank;      // [units, unit_cap, 4] list index of the row in each member head
-  int* unit_count;     // [units] entries, -1: a Top-k cut (per-session finish)
-  float* unit_part;    // [units, kUnitMaxSlices, G, d + 4] slice partials (m, s, C2 max, check, acc)
-  unsigned* unit_ticket;   // [units] slices finished (the last one merges and resets it)
 };
-constexpr int kUnitMaxSlices = 16;
 
 // CNT_BLOCKS: table blocks the select kernel read (rebuilt + hot), a diagnostic
 enum { CNT_C0 = 0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_BLOCKS, CNT_N };
@@ -198,9 +188,6 @@ struct DeviceOnce {
 cudaError_t launch_gate(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
 cudaError_t launch_stats(const Ctx& c, cudaStream_t st);
 cudaError_t launch_select(const Ctx& c, int m_max, cudaStream_t st);
-cudaError_t launch_union(const Ctx& c, cudaStream_t st);
-cudaError_t launch_finish_unit(const Ctx& c, const __nv_bfloat16* q, cudaStream_t st);
-bool unit_finish_supported(int G, int d);
 cudaError_t launch_topk(const Ctx& c, int implicit_base, cudaStream_t st);
 cudaError_t launch_attend(const Ctx& c, const __nv_bfloat16* q, int exact_mode, cudaStream_t st);
 cudaError_t launch_update(const Ctx& c, const __nv_bfloat16* k_new, const __nv_bfloat16* v_new,

@@ -45,14 +45,7 @@ __global__ void __launch_bounds__(kThreads, kRowCtas) lfps_finish_kernel(Ctx c, 
   extern __shared__ __align__(128) uint8_t stages[];      // kStages x [K tile | V tile]
   __shared__ FinishShared sh;
   pdl_wait();                                             // the select kernel's lists
-  const int s = c.s_off + blockIdx.x;
-  // LFPS_FLAG_UNIT_FINISH: only the sessions of units with a Top-k cut (the
-  // union kernel's count -1) are left to this kernel
-  if (c.unit_skip && c.unit_count[s / c.G] >= 0) {
-    pdl_trigger();
-    return;
-  }
-  finish_session<PQ, RM>(c, q, s, stages, sh);
+  finish_session<PQ, RM>(c, q, c.s_off + blockIdx.x, stages, sh);
   pdl_trigger();
 }
 

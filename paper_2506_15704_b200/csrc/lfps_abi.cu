@@ -133,15 +133,6 @@ int layout(const lfps_dims* d, lfps_ws_layout* L) {
   L->done = take(64);
   L->hot = take(NI * (size_t)(16 * L->nblk + 1) * 8);
   L->thr_next = take(NS * 8 * 8);
-  const size_t units = (size_t)d->batch * d->kv_heads;
-  // union entries: every row of the context at most once, plus the sinks
-  const size_t ucap = align_up(std::min((size_t)d->n_max, (size_t)d->group * cap) + 64, 32);
-  L->unit_cap = (int)ucap;
-  L->unit_ent = take(units * ucap * 4);
-  L->unit_rank = take(units * ucap * 16);
-  L->unit_count = take(units * 4);
-  L->unit_part = take(units * lfps::kUnitMaxSlices * d->group * (d->d + 4) * 4);
-  L->unit_ticket = take(units * 4);
   L->total_bytes = o;
   return LFPS_OK;
 }
@@ -221,12 +212,6 @@ int make_ctx(const lfps_dims* d, const lfps_params* p, const lfps_state* st,
   c->thr_next = reinterpret_cast<double*>(base + L.thr_next);
   c->bw.nblk = L.nblk;
   c->bw.dwords = L.dirty_words;
-  c->unit_ent = reinterpret_cast<int*>(base + L.unit_ent);
-  c->unit_rank = reinterpret_cast<int*>(base + L.unit_rank);
-  c->unit_count = reinterpret_cast<int*>(base + L.unit_count);
-  c->unit_cap = L.unit_cap;
-  c->unit_part = reinterpret_cast<float*>(base + L.unit_part);
-  c->unit_ticket = reinterpret_cast<unsigned*>(base + L.unit_ticket);
   return LFPS_OK;
 }
 
@@ -313,20 +298,6 @@ constexpr int kSplitGroups = LFPS_SPLIT_GROUPS;   // session groups of LFPS_FLAG
 #define LFPS_SPLIT_MIN 256
 #endif
 constexpr int kSplitMin = LFPS_SPLIT_MIN;         // sessions below which the split is off
-#ifndef LFPS_UNIT_CTAS
-#define LFPS_UNIT_CTAS 888
-#endif
-// per-unit finish: row slices (CTAs) per unit so that a launch has about
-// LFPS_UNIT_CTAS CTAs (3 resident per SM, two waves), in [G, kUnitMaxSlices]
-// (LFPS_UNIT_SLICES in the environment fixes the count: tests and A/B runs)
-int unit_slices(const lfps::Ctx& c) {
-  const int units = c.s_cnt / c.G;
-  int n = (LFPS_UNIT_CTAS + units - 1) / units;
-  if (const char* e = getenv("LFPS_UNIT_SLICES")) n = atoi(e);
-  if (n < 1) n = 1;
-  if (n > lfps::kUnitMaxSlices) n = lfps::kUnitMaxSlices;
-  return n;
-}
 // Internal streams and events of one workspace (one BatchedSession): the
 // fork/join events of a step are re-recorded by every call, so they must not
 // be shared between sessions that different host threads step concurrently
@@ -616,27 +587,13 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
                         const void* in_host, int m_max) {
   const __nv_bfloat16* qb = static_cast<const __nv_bfloat16*>(q);
   const size_t in_bytes = ((size_t)c.NS + 2 * (size_t)c.B * c.Hkv) * c.d * sizeof(__nv_bfloat16);
-  const bool unit = (c.flags & LFPS_FLAG_UNIT_FINISH) && lfps::unit_finish_supported(c.G, c.d);
-  auto select = [&](const lfps::Ctx& x, cudaStream_t s_) { return lfps::launch_select(x, m_max, s_); };
-  // per-unit finish: the union table, the unit kernel over it, then the
-  // per-session kernel for the units with a Top-k cut only
-  auto finish = [&](const lfps::Ctx& x, cudaStream_t s_) {
-    if (!unit) return lfps::launch_finish(x, qb, s_);
-    cudaError_t e = lfps::launch_union(x, s_);
-    if (e == cudaSuccess) e = lfps::launch_finish_unit(x, qb, s_);
-    lfps::Ctx xs = x;
-    xs.unit_skip = 1;
-    return e == cudaSuccess ? lfps::launch_finish(xs, qb, s_) : e;
-  };
   if (c.stamp) LAUNCH(lfps::launch_step_begin(c, sm));
   if (in_host && g_prof_on)
     LAUNCH(cudaMemcpyAsync(const_cast<void*>(q), in_host, in_bytes, cudaMemcpyHostToDevice, sm));
   if (g_prof_on) {
     LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
     LAUNCH_P("stats", sm, lfps::launch_stats(c, sm));
-    lfps::Ctx c1 = c;
-    c1.unit_nsl = unit_slices(c1);
-    LAUNCH_P("select", sm, select(c1, sm));
+    LAUNCH_P("select", sm, lfps::launch_select(c, m_max, sm));
   } else {
     LAUNCH(cudaEventRecord(pp->fork, sm));
     if (in_host) {
@@ -652,7 +609,6 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
     lfps::Ctx cg = c;
     cg.s_off = g * per;
     cg.s_cnt = g == groups - 1 ? c.NS - g * per : per;
-    cg.unit_nsl = unit_slices(cg);
     cudaStream_t gs = split ? pp->st[g] : sm;
     if (!g_prof_on) {
       cudaStream_t as = pp->aux[g];
@@ -663,17 +619,9 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
       if (in_host) LAUNCH(cudaStreamWaitEvent(gs, pp->in_ready, 0));
       LAUNCH(lfps::launch_gate(cg, qb, gs));
       LAUNCH(cudaStreamWaitEvent(gs, pp->stats[g], 0));
-      LAUNCH(select(cg, gs));
+      LAUNCH(lfps::launch_select(cg, m_max, gs));
     }
-    if (unit && g_prof_on) {                  // the three kernels of the per-unit finish, timed alone
-      lfps::Ctx cs = cg;
-      cs.unit_skip = 1;
-      LAUNCH_P("union", gs, lfps::launch_union(cg, gs));
-      LAUNCH_P("unit", gs, lfps::launch_finish_unit(cg, qb, gs));
-      LAUNCH_P("finish", gs, lfps::launch_finish(cs, qb, gs));
-    } else {
-      LAUNCH_P("finish", gs, finish(cg, gs));
-    }
+    LAUNCH_P("finish", gs, lfps::launch_finish(cg, qb, gs));
     if (split) {
       LAUNCH(cudaEventRecord(pp->join[g], gs));
       LAUNCH(cudaStreamWaitEvent(sm, pp->join[g], 0));

@@ -32,8 +32,7 @@ CNT_C0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_BLOCKS = rang
 
 
 def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False,
-                trace: bool = False, split: bool = False, graph: bool = False,
-                unit_finish: bool = False) -> _lib.Params:
+                trace: bool = False, split: bool = False, graph: bool = False) -> _lib.Params:
     err = cfg.device_limits_error()
     if err:
         raise ValueError(err)
@@ -50,8 +49,7 @@ def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False,
     for i, o in enumerate(offs):
         p.offsets[i] = o
     p.flags = ((_lib.FLAG_EXPORT_SETS if export_sets else 0) | (_lib.FLAG_TRACE if trace else 0)
-               | (_lib.FLAG_SPLIT if split else 0) | (_lib.FLAG_GRAPH if graph else 0)
-               | (_lib.FLAG_UNIT_FINISH if unit_finish else 0))
+               | (_lib.FLAG_SPLIT if split else 0) | (_lib.FLAG_GRAPH if graph else 0))
     return p
 
 
@@ -95,9 +93,6 @@ class BatchedSession:
         self.export_sets = export_sets
         self.trace = False          # LFPS_FLAG_TRACE: per-session phase timestamps
         self.split = True           # LFPS_FLAG_SPLIT: two session halves on two streams
-        # LFPS_FLAG_UNIT_FINISH: the per-unit finish kernel (csrc/k_unit.cu;
-        # G = 2 / 4, d = 64 / 128) instead of the per-session one
-        self.unit_finish = False
         # LFPS_FLAG_GRAPH: a step is one CUDA-graph launch.  It cuts the host's
         # enqueue time (C4 ~100 -> ~60 us) but the replayed step runs slower on
         # the device than the stream-launched kernels (PDL overlap, the input
@@ -224,15 +219,14 @@ class BatchedSession:
     def _params(self, k_fraction: float = 1.0, graph: bool = False) -> _lib.Params:
         # the C side only reads the struct: one per distinct argument set
         # (building it costs ~14 us of Python, a third of a C1 step)
-        key = (self.cfg, float(k_fraction), self.export_sets, self.trace, self.split, graph,
-               self.unit_finish)
+        key = (self.cfg, float(k_fraction), self.export_sets, self.trace, self.split, graph)
         cache = self.__dict__.setdefault("_params_cache", {})
         p = cache.get(key)
         if p is None:
             if len(cache) > 64:
                 cache.clear()
             p = cache[key] = make_params(self.cfg, k_fraction, self.export_sets, self.trace,
-                                         self.split, graph, self.unit_finish)
+                                         self.split, graph)
         return p
 
     # -- bootstrap ----------------------------------------------------------

@@ -66,7 +66,7 @@ def test_workspace_layout_regions_are_disjoint_and_aligned():
     dims = _lib.Dims(4, 8, 4, 128, 33000, 33000)
     lay = _lib.workspace_layout(dims)
     offs = sorted((getattr(lay, f), f) for f, _ in _lib.WsLayout._fields_
-                  if f not in ("total_bytes", "words", "list_cap", "nblk", "dirty_words", "unit_cap",
+                  if f not in ("total_bytes", "words", "list_cap", "nblk", "dirty_words",
                                "scratch"))
     for (a, _), (b, _) in zip(offs, offs[1:]):
         assert b > a

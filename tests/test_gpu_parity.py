@@ -516,43 +516,3 @@ def test_graph_replay_bit_exact(host_io, split):
         pair.compare_step(res, outs, tables=(t % 3 == 2 or t == 7))
 
 
-@pytest.mark.parametrize("slices,unit_finish,group,d", [
-    (None, True, 4, 128), (4, True, 4, 128), (16, True, 2, 128), (5, True, 4, 64),
-    (None, False, 4, 128)])
-def test_unit_finish_slices_bit_exact(monkeypatch, slices, unit_finish, group, d):
-    """The per-unit finish (csrc/k_unit.cu) against the oracle: row slices
-    merged by the unit's last CTA (LFPS_UNIT_SLICES fixes their count), the
-    Top-k-cut units falling back to the per-session code inside the same
-    launch (budgets alternate so that units mix both cases), and the
-    per-session kernel on the same inputs."""
-    if slices:
-        monkeypatch.setenv("LFPS_UNIT_SLICES", str(slices))
-    steps = 6
-    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, group=group, d=d, n0=5000, steps=steps)
-    pair.sess.unit_finish = unit_finish
-    n0 = pair.n0
-    fused = 0
-    for t in range(steps):
-        frac = (0.05, 0.02, 0.2)[t % 3]
-        res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], frac)
-        pair.compare_step(res, outs)
-        cnt = res.counts.cpu().numpy()
-        fused += int((cnt[..., CNT_K] >= cnt[..., CNT_PROBE]).sum())
-    assert 0 < fused < steps * pair.sess.NS       # both kinds of unit occurred
-
-
-@pytest.mark.parametrize("slices", [4, 7])
-def test_unit_finish_dense_chunks(monkeypatch, slices):
-    """Exhaustive fallback at k = n (C2 = every row): each per-unit finish
-    slice holds more union rows than one shared-memory chunk (512), so the
-    chunk loop (continuation rows and list ranks) runs."""
-    monkeypatch.setenv("LFPS_UNIT_SLICES", str(slices))
-    pair, K, V, Q = _gqa_pair(batch=1, kv_heads=2, n0=4500, steps=3, exhaustive_fallback=True)
-    pair.sess.unit_finish = True
-    n0 = pair.n0
-    for t in range(3):
-        res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], 1.0)
-        pair.compare_step(res, outs, bitmaps=False)
-        cnt = res.counts.cpu().numpy()
-        assert (cnt[..., CNT_K] >= cnt[..., CNT_PROBE]).all()
-        assert cnt[..., CNT_PROBE].min() > 512 * slices
