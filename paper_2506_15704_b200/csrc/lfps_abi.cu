@@ -666,6 +666,8 @@ static int capture_step(lfps::Ctx c, Pipe* pp, const GraphKey& key, const void* 
     if (mp.kind == cudaMemcpyHostToDevice) g->in_node = nd;
     else if (mp.kind == cudaMemcpyDeviceToHost) g->out_node = nd;
   }
+  if (const char* dot = getenv("LFPS_GRAPH_DOT"))     // diagnostics: the captured step
+    cudaGraphDebugDotPrint(g->graph, dot, cudaGraphDebugDotFlagsVerbose);
   if ((e = cudaGraphInstantiate(&g->exec, g->graph, 0)) != cudaSuccess) {
     delete g;
     return cuda_fail(e, "cudaGraphInstantiate");
