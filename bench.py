@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--cpu-steps", type=int, default=6, help="steps per CPU worker sample")
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = all host cores")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--prefetch", action="store_true",
+                    help="C3: each layer's candidate sets built ahead on a second stream "
+                         "(lfps_decode_prefetch), the layers' gate/finish/commit in order")
     ap.add_argument("--no-graph", action="store_true",
                     help="e2e: enqueue each host-input step kernel by kernel (no CUDA graph)")
     ap.add_argument("--no-split", action="store_true",
@@ -936,10 +939,30 @@ def run_c3(args, world, rank, local):
         s_l.split = not args.no_split
     setup_s = time.time() - t_setup
 
+    side = torch.cuda.Stream(dev)
+    pre_ev = [torch.cuda.Event() for _ in range(layers)]
+
     def token_step(t):
         i = t % T_in
-        for s_l, st in zip(sess, streams):
-            s_l.decode_step(st.q[i], st.k_new[i], st.v_new[i], frac)
+        if not args.prefetch:
+            for s_l, st in zip(sess, streams):
+                s_l.decode_step(st.q[i], st.k_new[i], st.v_new[i], frac)
+            return
+        # The q-independent half of every layer's step (thresholds, C0, C1,
+        # probe sets: lfps_decode_prefetch) runs ahead on a second stream,
+        # in layer order, once the previous token's commits are done; the
+        # layers' gate / finish / commit run in order on the main stream,
+        # each after its own layer's prefetch (a real model's layer l + 1
+        # queries exist only after layer l).
+        main = torch.cuda.current_stream(dev)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            for s_l, ev in zip(sess, pre_ev):
+                s_l.prefetch()
+                ev.record(side)
+        for s_l, st, ev in zip(sess, streams, pre_ev):
+            main.wait_event(ev)
+            s_l.decode_step(st.q[i], st.k_new[i], st.v_new[i], frac, prefetched=True)
 
     for t in range(args.warmup):
         token_step(t)
@@ -974,7 +997,11 @@ def run_c3(args, world, rank, local):
         "config": {"workload": "C3: batch 16 x 128k context, 32 layers, Llama-3.1-8B shapes, "
                                "Top-k 5%", "batch": batch, "batch_per_gpu": b_local,
                    "context": ctx, "layers": layers, "topk_fraction": frac,
-                   "l2": "flushed before every timed step"},
+                   "l2": "flushed before every timed step",
+                   "schedule": ("index ahead: every layer's candidate construction "
+                                "(lfps_decode_prefetch) on a second stream, the layers' "
+                                "gate/finish/commit in order on the main stream"
+                                if args.prefetch else "layers in order, whole steps")},
         "clocks": clock_info, "setup_s": setup_s}), flush=True)
 
 

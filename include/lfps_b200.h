@@ -104,6 +104,11 @@ typedef struct lfps_params {
 } lfps_params;
 
 /* lfps_params.flags */
+#define LFPS_FLAG_PREFETCHED 64  /* the step's candidate construction (thresholds,
+                                    C0, C1, probe sets: stats + select) was run
+                                    ahead by lfps_decode_prefetch on this
+                                    workspace; the step runs the gate, the
+                                    finish and the commit only */
 #define LFPS_FLAG_GRAPH 16       /* enqueue a decode step as one CUDA-graph launch: the
                                     step is captured once per (shapes, params,
                                     state, workspace, device buffers, context
@@ -274,6 +279,23 @@ LFPS_API int lfps_decode_step_host_io(const lfps_dims* dims, const lfps_params* 
                      const lfps_state* st, const lfps_workspace* ws,
                      const void* in_host, void* in_dev, const int32_t* n_host,
                      void* out_host, void* stream);
+
+/* The q-independent half of the next decode step, run ahead: the tracker
+ * thresholds, C0, C1 and the probe sets of every session depend on the
+ * tables and the context only (engine.py:146-160: compute_thresholds,
+ * select_initial, expand, finalize_probe_set do not read q), so they can be
+ * built while the caller still computes the step's queries (e.g. during the
+ * previous layers of the model).  The next lfps_decode_step* call on this
+ * workspace with LFPS_FLAG_PREFETCHED in its params then runs the gate, the
+ * finish and the commit only; it must follow on the same stream (or after
+ * an event) with the same dims, params (except k_fraction) and state, and
+ * no other decode step may run on the workspace in between.  A session the
+ * gate bypasses reports no candidates, as in the normal step; a kappa = 0
+ * threshold (tables.py:314-315) fails the step only for a non-bypassed
+ * session, as in the normal step.  Not captured as a CUDA graph. */
+LFPS_API int lfps_decode_prefetch(const lfps_dims* dims, const lfps_params* p,
+                                  const lfps_state* st, const lfps_workspace* ws,
+                                  const int32_t* n_host, void* stream);
 
 /* Bytes of the packed step input of lfps_decode_step_host_io (< 0: invalid
  * dims). */

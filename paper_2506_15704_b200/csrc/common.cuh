@@ -36,6 +36,8 @@ struct Ctx {
   float sqrt_d_f32;
   int s, S, L, bypass_mode, exhaustive, n_off, flags;
   int s_off, s_cnt;   // session range [s_off, s_off + s_cnt) of a per-session launch
+  int prefetch;       // lfps_decode_prefetch: the select kernel runs ahead of the gate
+                      // (every session; kappa = 0 is raised by the finish kernel)
   int epoch;          // call stamp in [1, 2^27): err[0] == epoch <=> this call failed
   const int* stamp;   // CUDA-graph steps: the stamp in device memory (set by the
                       // step's first kernel), used instead of epoch

@@ -105,8 +105,18 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
   int* cnt = c.counts + (size_t)s * CNT_N;
 
   if (c.bypass[s]) {
-    if (tid == 0) { cnt[CNT_K] = 0; cnt[CNT_C2] = 0; cnt[CNT_CLAMP] = 0; }
+    if (tid == 0) {
+      cnt[CNT_K] = 0; cnt[CNT_C2] = 0; cnt[CNT_CLAMP] = 0;
+      // a prefetched select built this session's sets before the gate ran
+      if (c.flags & LFPS_FLAG_PREFETCHED) { cnt[CNT_C0] = 0; cnt[CNT_C1] = 0; cnt[CNT_PROBE] = 0; cnt[CNT_DROP] = 0; }
+    }
     return;
+  }
+  if ((c.flags & LFPS_FLAG_PREFETCHED) && tid < 2 && !c.exhaustive) {
+    // kappa = 0 (tables.py:314-315) fails a non-bypassed step only; the
+    // prefetched select exported the thresholds instead of raising it
+    const double* th = c.thr + (size_t)(2 * s + tid) * 4;
+    if (th[2] == 0.0 && th[3] == 0.0) set_err(c, s, LFPS_ERR_KAPPA_ZERO);
   }
   const int p = cnt[CNT_PROBE];
   const long long t0 = now_clk();

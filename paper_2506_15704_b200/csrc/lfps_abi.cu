@@ -317,6 +317,8 @@ struct Pipe {
   std::vector<struct StepGraph*> graphs;    // captured steps, most recent last
   void* stage = nullptr;                    // graph steps with device inputs: the
   size_t stage_bytes = 0;                   // inputs are copied here first
+  int pre_epoch = 0;                        // lfps_decode_prefetch's call stamp, until the
+                                            // LFPS_FLAG_PREFETCHED step that consumes it
 };
 std::mutex g_pipe_mu;
 
@@ -422,10 +424,13 @@ int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out) {
 // clear, gate, select, finish, update (with append and commit); with
 // LFPS_FLAG_SPLIT (and >= 256 sessions) gate/select/finish run per half
 int lfps_decode_launches(const lfps_dims* dims, int32_t flags) {
+  // per group: gate | stats, select, finish (LFPS_FLAG_PREFETCHED: gate,
+  // finish -- stats and select ran in lfps_decode_prefetch), then the update
+  const int per = (flags & LFPS_FLAG_PREFETCHED) ? 2 : 4;
   if (dims && (flags & LFPS_FLAG_SPLIT) &&
       (long long)dims->batch * dims->kv_heads * dims->group >= kSplitMin)
-    return 1 + 4 * kSplitGroups;
-  return 5;   // gate | stats, select, finish, update
+    return 1 + per * kSplitGroups;
+  return 1 + per;
 }
 
 int lfps_workspace_release(const lfps_workspace* ws) {
@@ -537,6 +542,28 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
                        const void* v_new, const int32_t* n_host, void* out_host,
                        const void* in_host, void* stream);
 
+int lfps_decode_prefetch(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
+                         const lfps_workspace* ws, const int32_t* n_host, void* stream) {
+  lfps::Ctx c;
+  int rc = make_ctx(dims, p, st, ws, &c);
+  if (rc) return rc;
+  int m_max = 0;
+  rc = check_context(c, n_host, true, &m_max);
+  if (rc) return rc;
+  cudaStream_t sm = static_cast<cudaStream_t>(stream);
+  Pipe* pp = nullptr;
+  LAUNCH(get_pipe(ws->base, &pp));
+  std::lock_guard<std::mutex> pipe_lock(pp->mu);
+  c.epoch = next_epoch();
+  c.prefetch = 1;
+  // thresholds + C0 words of every (session, table), then C + D of every
+  // session, on the caller's stream (no gate: nothing here reads q)
+  LAUNCH_P("stats", sm, lfps::launch_stats(c, sm));
+  LAUNCH_P("select", sm, lfps::launch_select(c, m_max, sm));
+  pp->pre_epoch = c.epoch;
+  return LFPS_OK;
+}
+
 int lfps_decode_step(const lfps_dims* dims, const lfps_params* p, const lfps_state* st,
                      const lfps_workspace* ws, const void* q, const void* k_new,
                      const void* v_new, const int32_t* n_host, void* stream) {
@@ -590,10 +617,13 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
   if (c.stamp) LAUNCH(lfps::launch_step_begin(c, sm));
   if (in_host && g_prof_on)
     LAUNCH(cudaMemcpyAsync(const_cast<void*>(q), in_host, in_bytes, cudaMemcpyHostToDevice, sm));
+  const bool pre = (c.flags & LFPS_FLAG_PREFETCHED) != 0;   // stats + select already ran
   if (g_prof_on) {
     LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
-    LAUNCH_P("stats", sm, lfps::launch_stats(c, sm));
-    LAUNCH_P("select", sm, lfps::launch_select(c, m_max, sm));
+    if (!pre) {
+      LAUNCH_P("stats", sm, lfps::launch_stats(c, sm));
+      LAUNCH_P("select", sm, lfps::launch_select(c, m_max, sm));
+    }
   } else {
     LAUNCH(cudaEventRecord(pp->fork, sm));
     if (in_host) {
@@ -613,13 +643,17 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
     if (!g_prof_on) {
       cudaStream_t as = pp->aux[g];
       if (split) LAUNCH(cudaStreamWaitEvent(gs, pp->fork, 0));
-      LAUNCH(cudaStreamWaitEvent(as, pp->fork, 0));
-      LAUNCH(lfps::launch_stats(cg, as));
-      LAUNCH(cudaEventRecord(pp->stats[g], as));
+      if (!pre) {
+        LAUNCH(cudaStreamWaitEvent(as, pp->fork, 0));
+        LAUNCH(lfps::launch_stats(cg, as));
+        LAUNCH(cudaEventRecord(pp->stats[g], as));
+      }
       if (in_host) LAUNCH(cudaStreamWaitEvent(gs, pp->in_ready, 0));
       LAUNCH(lfps::launch_gate(cg, qb, gs));
-      LAUNCH(cudaStreamWaitEvent(gs, pp->stats[g], 0));
-      LAUNCH(lfps::launch_select(cg, m_max, gs));
+      if (!pre) {
+        LAUNCH(cudaStreamWaitEvent(gs, pp->stats[g], 0));
+        LAUNCH(lfps::launch_select(cg, m_max, gs));
+      }
     }
     LAUNCH_P("finish", gs, lfps::launch_finish(cg, qb, gs));
     if (split) {
@@ -695,6 +729,15 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
   Pipe* pp = nullptr;
   LAUNCH(get_pipe(ws->base, &pp));
   std::lock_guard<std::mutex> pipe_lock(pp->mu);
+  if (c.flags & LFPS_FLAG_PREFETCHED) {
+    // the candidate sets come from lfps_decode_prefetch; the step shares its
+    // call stamp, so an error raised ahead still fails this step
+    if (!pp->pre_epoch)
+      return fail(LFPS_E_INVALID, "LFPS_FLAG_PREFETCHED without a preceding lfps_decode_prefetch");
+    c.epoch = pp->pre_epoch;
+    pp->pre_epoch = 0;
+    return enqueue_step(c, pp, sm, q, k_new, v_new, out_host, in_host, m_max);
+  }
   if (g_prof_on || !(c.flags & LFPS_FLAG_GRAPH)) {
     c.epoch = next_epoch();
     return enqueue_step(c, pp, sm, q, k_new, v_new, out_host, in_host, m_max);

@@ -79,7 +79,7 @@ __device__ __forceinline__ void select_session(const Ctx& c, int s, uint32_t* sm
   int* cnt = c.counts + (size_t)s * CNT_N;
   const int b = s / c.Hq;
   // independent prologue loads, issued together (one round trip, not four)
-  const int byp = c.bypass[s];
+  const int byp = c.prefetch ? 0 : c.bypass[s];   // run ahead of the gate: every session
   const int n = c.n_ctx[b];
   const int base = c.sla_base[s];
   double tau = 0.0, mean = 0.0, degv = 0.0, kap = 0.0, sc = 1.0;
@@ -140,7 +140,7 @@ __device__ __forceinline__ void select_session(const Ctx& c, int s, uint32_t* sm
       sh.thr0[t] = sh.deg[t] ? NAN : cdiv(tau, sc);
       sh.thrf[t] = cdiv(mean, sc);
       thr[0] = tau; thr[1] = mean; thr[2] = degv; thr[3] = kap;   // export
-      if (!sh.deg[t] && kap == 0.0) set_err(c, s, LFPS_ERR_KAPPA_ZERO);
+      if (!sh.deg[t] && kap == 0.0 && !c.prefetch) set_err(c, s, LFPS_ERR_KAPPA_ZERO);
     }
   }
   __syncthreads();

@@ -32,7 +32,8 @@ CNT_C0, CNT_C1, CNT_PROBE, CNT_DROP, CNT_K, CNT_C2, CNT_CLAMP, CNT_BLOCKS = rang
 
 
 def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False,
-                trace: bool = False, split: bool = False, graph: bool = False) -> _lib.Params:
+                trace: bool = False, split: bool = False, graph: bool = False,
+                prefetched: bool = False) -> _lib.Params:
     err = cfg.device_limits_error()
     if err:
         raise ValueError(err)
@@ -49,7 +50,8 @@ def make_params(cfg: LfpsConfig, k_fraction: float, export_sets: bool = False,
     for i, o in enumerate(offs):
         p.offsets[i] = o
     p.flags = ((_lib.FLAG_EXPORT_SETS if export_sets else 0) | (_lib.FLAG_TRACE if trace else 0)
-               | (_lib.FLAG_SPLIT if split else 0) | (_lib.FLAG_GRAPH if graph else 0))
+               | (_lib.FLAG_SPLIT if split else 0) | (_lib.FLAG_GRAPH if graph else 0)
+               | (_lib.FLAG_PREFETCHED if prefetched else 0))
     return p
 
 
@@ -216,17 +218,19 @@ class BatchedSession:
     def _stream(self):
         return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
-    def _params(self, k_fraction: float = 1.0, graph: bool = False) -> _lib.Params:
+    def _params(self, k_fraction: float = 1.0, graph: bool = False,
+                prefetched: bool = False) -> _lib.Params:
         # the C side only reads the struct: one per distinct argument set
         # (building it costs ~14 us of Python, a third of a C1 step)
-        key = (self.cfg, float(k_fraction), self.export_sets, self.trace, self.split, graph)
+        key = (self.cfg, float(k_fraction), self.export_sets, self.trace, self.split, graph,
+               prefetched)
         cache = self.__dict__.setdefault("_params_cache", {})
         p = cache.get(key)
         if p is None:
             if len(cache) > 64:
                 cache.clear()
             p = cache[key] = make_params(self.cfg, k_fraction, self.export_sets, self.trace,
-                                         self.split, graph)
+                                         self.split, graph, prefetched)
         return p
 
     # -- bootstrap ----------------------------------------------------------
@@ -336,9 +340,26 @@ class BatchedSession:
         raise ValueError(f"{what}: session {s}: {msg}")
 
     # -- decode ---------------------------------------------------------------
+    def prefetch(self):
+        """Run the q-independent half of the next decode step ahead
+        (lfps_decode_prefetch): thresholds, C0, C1 and the probe sets of every
+        session depend on the tables and the context only (engine.py:146-160),
+        so they can be built on the current stream while the caller still
+        computes the step's queries -- e.g. beside earlier layers of the
+        model.  The next decode_step / decode_step_host must pass
+        ``prefetched=True`` (same stream, or ordered after it)."""
+        if self.tables_stale:
+            raise ValueError("tables out of sync with the KV store (append_rows was used)")
+        self._back_step()
+        n_host = (C.c_int32 * self.B)(*self.n_host)
+        _lib.check(self.lib.lfps_decode_prefetch(
+            C.byref(self.dims), C.byref(self._params(1.0)), C.byref(self.state), C.byref(self.ws),
+            n_host, self._stream()), "decode_prefetch")
+
     def decode_step(self, q: torch.Tensor, k_new: torch.Tensor, v_new: torch.Tensor,
                     k_fraction: float, check: bool = False,
-                    out_host: torch.Tensor | None = None) -> BatchedStepResult:
+                    out_host: torch.Tensor | None = None,
+                    prefetched: bool = False) -> BatchedStepResult:
         """One LFPS decode step for all sessions (engine.py:97-201).
 
         q bf16 [B, Hq, d]; k_new, v_new bf16 [B, Hkv, d] (device).  On a
@@ -346,7 +367,8 @@ class BatchedSession:
         raises it.  ``out_host`` (f32 [B, Hq, d], pinned host memory) receives
         the step's output as soon as it is final, copied beside the commit
         kernel (lfps_decode_step_host_out); it is filled once the current
-        stream passes this call."""
+        stream passes this call.  ``prefetched``: the candidate sets were built
+        by ``prefetch()`` (the step runs the gate, the finish and the commit)."""
         if not 0.0 < k_fraction <= 1.0:
             raise ValueError(f"k_fraction must be in (0, 1], got {k_fraction}")
         if self.tables_stale:
@@ -361,9 +383,10 @@ class BatchedSession:
         self._back_step()
         n_host = (C.c_int32 * self.B)(*self.n_host)
         graph = self.graph_device and (out_host is None or out_host.is_pinned())
+        params = self._params(k_fraction, graph and not prefetched, prefetched)
         if out_host is None:
             _lib.check(self.lib.lfps_decode_step(
-                C.byref(self.dims), C.byref(self._params(k_fraction, graph)), C.byref(self.state),
+                C.byref(self.dims), C.byref(params), C.byref(self.state),
                 C.byref(self.ws), C.c_void_p(q.data_ptr()), C.c_void_p(k_new.data_ptr()),
                 C.c_void_p(v_new.data_ptr()), n_host, self._stream()), "decode_step")
         else:
@@ -372,7 +395,7 @@ class BatchedSession:
                 raise ValueError(f"out_host must be a contiguous f32 CPU tensor of shape "
                                  f"{tuple(self.out.shape)}")
             _lib.check(self.lib.lfps_decode_step_host_out(
-                C.byref(self.dims), C.byref(self._params(k_fraction, graph)), C.byref(self.state),
+                C.byref(self.dims), C.byref(params), C.byref(self.state),
                 C.byref(self.ws), C.c_void_p(q.data_ptr()), C.c_void_p(k_new.data_ptr()),
                 C.c_void_p(v_new.data_ptr()), n_host, C.c_void_p(out_host.data_ptr()),
                 self._stream()), "decode_step")
@@ -454,7 +477,7 @@ class BatchedSession:
 
     def decode_step_host(self, inputs_host: torch.Tensor, k_fraction: float,
                          out_host: torch.Tensor | None = None,
-                         check: bool = False) -> BatchedStepResult:
+                         check: bool = False, prefetched: bool = False) -> BatchedStepResult:
         """decode_step with host inputs (lfps_decode_step_host_io):
         ``inputs_host`` is a contiguous CPU bf16 tensor packed as
         [q | k_new | v_new] (``pack_step_inputs``; pinned for an asynchronous
@@ -483,7 +506,8 @@ class BatchedSession:
         graph = (self.graph and inputs_host.is_pinned()
                  and (out_host is None or out_host.is_pinned()))
         _lib.check(self.lib.lfps_decode_step_host_io(
-            C.byref(self.dims), C.byref(self._params(k_fraction, graph)), C.byref(self.state),
+            C.byref(self.dims), C.byref(self._params(k_fraction, graph and not prefetched, prefetched)),
+            C.byref(self.state),
             C.byref(self.ws), C.c_void_p(inputs_host.data_ptr()),
             C.c_void_p(self._in_dev.data_ptr()), n_host,
             C.c_void_p(out_host.data_ptr() if out_host is not None else None),

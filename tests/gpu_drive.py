@@ -76,15 +76,20 @@ class Pair:
 
     def _device_step(self, q, k_new, v_new, frac):
         B, Hkv, G, d = self.B, self.Hkv, self.G, self.d
+        pre = getattr(self, "prefetch", False)
+        if pre:                   # lfps_decode_prefetch, then the step with LFPS_FLAG_PREFETCHED
+            self.sess.prefetch()
         if self.host_io:          # lfps_decode_step_host_io: packed pinned inputs, host output
             packed = self.sess.pack_step_inputs(bf16(q.reshape(B, Hkv * G, d)), bf16(k_new),
                                                 bf16(v_new))
             host = torch.full(tuple(self.sess.out.shape), float("nan")).pin_memory()
-            res = self.sess.decode_step_host(packed, frac, out_host=host, check=True)
+            res = self.sess.decode_step_host(packed, frac, out_host=host, check=True,
+                                             prefetched=pre)
             assert torch.equal(host, self.sess.out.cpu())
         else:
             res = self.sess.decode_step(bf16(q.reshape(B, Hkv * G, d)).cuda(),
-                                        bf16(k_new).cuda(), bf16(v_new).cuda(), frac, check=True)
+                                        bf16(k_new).cuda(), bf16(v_new).cuda(), frac, check=True,
+                                        prefetched=pre)
         return res
 
     def compare_step(self, res, outs, out_tol=1e-5, tables=True, bitmaps=True):

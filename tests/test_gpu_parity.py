@@ -516,3 +516,44 @@ def test_graph_replay_bit_exact(host_io, split):
         pair.compare_step(res, outs, tables=(t % 3 == 2 or t == 7))
 
 
+
+
+@pytest.mark.parametrize("epsilon,host_io,split,frac", [
+    (1.0, False, True, 0.05), (1e-6, True, True, 0.05), (0.3, False, False, 0.01),
+    (0.6, True, False, 0.05)])
+def test_prefetched_steps_bit_exact(epsilon, host_io, split, frac):
+    """lfps_decode_prefetch + a LFPS_FLAG_PREFETCHED step: the thresholds, C0,
+    C1 and probe sets built ahead of the gate (they do not depend on q,
+    engine.py:146-160) give the same step as the normal path -- sets,
+    counts (bypassed sessions report none), tables and outputs against the
+    oracle -- with gated sessions (epsilon), the stream split, host I/O and
+    Top-k cuts (1%)."""
+    pair, K, V, Q = _gqa_pair(batch=8, kv_heads=8, group=4, d=64, n0=900, steps=6, seed=7,
+                              epsilon=epsilon)
+    pair.sess.split = split
+    pair.host_io = host_io
+    pair.prefetch = True
+    n0 = pair.n0
+    for t in range(6):
+        res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], frac)
+        pair.compare_step(res, outs, tables=(t % 2 == 1))
+        cnt = res.counts.cpu().numpy()
+        byp = res.bypassed.cpu().numpy().astype(bool)
+        assert (cnt[byp][:, :6] == 0).all()          # no candidates on a bypassed session
+
+
+def test_prefetched_step_requires_a_prefetch():
+    """A LFPS_FLAG_PREFETCHED step without a preceding lfps_decode_prefetch on
+    the workspace is rejected before any launch (and a prefetch serves one
+    step only)."""
+    pair, K, V, Q = _gqa_pair(batch=1, kv_heads=2, n0=700, steps=2)
+    B, Hkv, G, d = pair.B, pair.Hkv, pair.G, pair.d
+    q = torch.zeros(B, Hkv * G, d, dtype=torch.bfloat16, device="cuda")
+    kv = torch.zeros(B, Hkv, d, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError, match="lfps_decode_prefetch"):
+        pair.sess.decode_step(q, kv, kv, 0.05, prefetched=True)
+    pair.prefetch = True
+    res, outs = pair.step(Q[:, :, :, 0], K[:, :, pair.n0], V[:, :, pair.n0], 0.05)
+    pair.compare_step(res, outs)
+    with pytest.raises(ValueError, match="lfps_decode_prefetch"):
+        pair.sess.decode_step(q, kv, kv, 0.05, prefetched=True)
