@@ -45,6 +45,10 @@ CONFIGS = {
            "C3: batch 16 x 128k context, all 32 layers, Llama-3.1-8B shapes, Top-k 5%"),
     "c1": (1, 16384, 8, 4, 128, 0.05,
            "C1: batch 1 x 16k context, Llama-3.1-8B shapes, 1 layer, Top-k 5%"),
+    # one rank's share of C4 on 2 / 4 / 8 GPUs (request split), on one GPU
+    "c4s2": (32, 131072, 8, 4, 128, 0.05, "C4 per-rank share at 2 GPUs: batch 32 x 128k, 1 layer, Top-k 5%"),
+    "c4s4": (16, 131072, 8, 4, 128, 0.05, "C4 per-rank share at 4 GPUs: batch 16 x 128k, 1 layer, Top-k 5%"),
+    "c4s8": (8, 131072, 8, 4, 128, 0.05, "C4 per-rank share at 8 GPUs: batch 8 x 128k, 1 layer, Top-k 5%"),
 }
 METRIC = "LFPS index+sparse-attn us/decode-step/layer"
 UNIT = "us/step"
