@@ -3,7 +3,8 @@ decode steps, a Top-k (1%) step, and the exact path, on a B=1, 2 KV-head,
 G=4, n=2048 batch; two steps of a 256-session batch (8 x 8 KV heads x 4,
 d=64) through the two-group stream split, the second with host inputs and
 output (lfps_decode_step_host_io); two steps and the exact path over a
-block-table KV cache; and the per-head fp64 stage API (k_stages.cu):
+block-table KV cache; prefetched steps (lfps_decode_prefetch); and the
+per-head fp64 stage API (k_stages.cu):
 prefill_bootstrap, decode steps, topk_oracle, full attention."""
 import os
 import sys
@@ -52,6 +53,16 @@ for t in range(2):
     pair.host_io = t == 1           # lfps_decode_step_host_io: input copy beside stats
     res, outs = pair.step(Q[:, :, :, t], K[:, :, 700 + t], V[:, :, 700 + t], 0.05)
     pair.compare_step(res, outs, tables=(t == 1))
+torch.cuda.synchronize()
+
+# index ahead: lfps_decode_prefetch + LFPS_FLAG_PREFETCHED steps (split off, host I/O)
+from gpu_drive import gqa_pair  # noqa: E402
+pair, K, V, Q = gqa_pair(batch=2, kv_heads=2, n0=1500, steps=3, seed=61)
+pair.prefetch = True
+for t in range(3):
+    pair.host_io = t == 2
+    res, outs = pair.step(Q[:, :, :, t], K[:, :, 1500 + t], V[:, :, 1500 + t], 0.05)
+    pair.compare_step(res, outs)
 torch.cuda.synchronize()
 
 # block-table KV (16-row blocks in a random order)
