@@ -735,15 +735,19 @@ def run_ours(args, world, rank, local):
             if not gather:
                 # lfps_decode_step_host_io: the library copies the packed
                 # inputs on its own stream beside the stats kernels and the
-                # output back beside the commit kernel
+                # output back beside the commit kernel; the host waits for
+                # the output only (lfps_wait_output) -- the commit may still
+                # run while it builds the next step, which is stream-ordered
+                # after it
                 sess.decode_step_host(inh[t % T_in], frac, out_host=out_h)
+                sess.wait_output()
             else:
                 sess.decode_step_host(inh[t % T_in], frac)
                 g_out, g_cnt, _ = ss.gather(with_c2=False)
                 if rank == 0:
                     out_h.copy_(g_out, non_blocking=True)
                     cnt_h.copy_(g_cnt, non_blocking=True)
-            cuda_stream.synchronize()            # the output is in host memory
+                cuda_stream.synchronize()        # the gathered output is in host memory
             lat.append(time.perf_counter() - h0)
         e1.record(cuda_stream)
         torch.cuda.synchronize(dev)
@@ -755,7 +759,8 @@ def run_ours(args, world, rank, local):
                "h2d_bytes_per_step": int(ind.numel() * ind.element_size()),
                "d2h_bytes_per_step": int(d2h if rank == 0 or not gather else 0),
                "timing": "median host wall-clock per step (perf_counter), each step waiting for "
-                         "its output in pinned host memory before the next starts; max over ranks",
+                         "its output in pinned host memory before the next starts (lfps_wait_output; "
+                         "the step's commit may still run); max over ranks",
                "device_span_us_per_step": dev_ms * 1e3,
                "api": ("ShardedSession: BatchedSession.decode_step_host on each rank's shard "
                        "(pinned host q|k_new|v_new in), then ShardedSession.gather: outputs and "

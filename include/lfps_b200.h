@@ -58,7 +58,7 @@ extern "C" {
 #define LFPS_API
 #endif
 
-#define LFPS_ABI_VERSION 8
+#define LFPS_ABI_VERSION 9
 
 #define LFPS_OK 0
 #define LFPS_E_INVALID -1   /* bad argument (shape, range, capacity) */
@@ -296,6 +296,14 @@ LFPS_API int lfps_decode_step_host_io(const lfps_dims* dims, const lfps_params* 
 LFPS_API int lfps_decode_prefetch(const lfps_dims* dims, const lfps_params* p,
                                   const lfps_state* st, const lfps_workspace* ws,
                                   const int32_t* n_host, void* stream);
+
+/* Block the calling host thread until the output of the last decode step
+ * with a host output (lfps_decode_step_host_out / _host_io) on this workspace
+ * is in host memory.  The step's commit (tracker update, KV append) may
+ * still be running: an autoregressive loop needs only the output to build
+ * the next step's queries, and the next step is ordered after the commit on
+ * the stream anyway. */
+LFPS_API int lfps_wait_output(const lfps_workspace* ws);
 
 /* Bytes of the packed step input of lfps_decode_step_host_io (< 0: invalid
  * dims). */

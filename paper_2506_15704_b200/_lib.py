@@ -18,7 +18,7 @@ from .errors import DeviceError
 # experiments); the default is the library __graft_entry__.build() makes
 LIB_PATH = os.environ.get("LFPS_LIB") or os.path.join(
     os.path.dirname(os.path.abspath(__file__)), "lib", "liblfps_b200.so")
-ABI_VERSION = 8
+ABI_VERSION = 9
 FLAG_EXPORT_SETS = 1
 FLAG_TRACE = 2
 FLAG_SPLIT = 8
@@ -39,7 +39,7 @@ ERR_NAMES = {
 EXPORTS = ("lfps_abi_version", "lfps_last_error", "lfps_workspace_layout",
            "lfps_bootstrap_tables", "lfps_bootstrap_stats", "lfps_decode_step",
            "lfps_decode_step_host_out", "lfps_decode_step_host_io", "lfps_step_input_bytes",
-           "lfps_decode_prefetch",
+           "lfps_decode_prefetch", "lfps_wait_output",
            "lfps_exact_topk_step", "lfps_overlap", "lfps_decode_launches", "lfps_slash_capacity",
            "lfps_exact_launches", "lfps_kv_pool_page_bytes", "lfps_kv_pool_create",
            "lfps_kv_pool_reserve", "lfps_kv_pool_release", "lfps_kv_pool_mapped_bytes",
@@ -117,6 +117,7 @@ def _declare(lib):
                                              C.c_void_p]
     lib.lfps_decode_prefetch.argtypes = [P(Dims), P(Params), P(State), P(Workspace), C.c_void_p,
                                          C.c_void_p]
+    lib.lfps_wait_output.argtypes = [P(Workspace)]
     lib.lfps_step_input_bytes.argtypes = [P(Dims)]
     lib.lfps_step_input_bytes.restype = C.c_int64
     lib.lfps_kv_pool_page_bytes.argtypes = []

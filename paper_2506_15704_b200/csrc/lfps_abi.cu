@@ -311,6 +311,8 @@ struct Pipe {
   cudaEvent_t fork = nullptr, join[kSplitGroups] = {}, stats[kSplitGroups] = {};
   cudaStream_t copy = nullptr;              // host output copy beside the commit
   cudaEvent_t out_ready = nullptr, out_done = nullptr;
+  cudaEvent_t out_ext = nullptr;            // the output copy's completion for the host
+                                            // (recorded as an external event node in graphs)
   cudaStream_t in = nullptr;                // host input copy beside the stats kernel
   cudaEvent_t in_ready = nullptr;
   cudaStream_t cap = nullptr;               // CUDA-graph capture of a decode step
@@ -364,7 +366,7 @@ void destroy_pipe(Pipe& p) {
     if (p.join[i]) cudaEventDestroy(p.join[i]);
     if (p.stats[i]) cudaEventDestroy(p.stats[i]);
   }
-  for (cudaEvent_t ev : {p.fork, p.out_ready, p.out_done, p.in_ready})
+  for (cudaEvent_t ev : {p.fork, p.out_ready, p.out_done, p.out_ext, p.in_ready})
     if (ev) cudaEventDestroy(ev);
   if (p.copy) cudaStreamDestroy(p.copy);
   if (p.in) cudaStreamDestroy(p.in);
@@ -382,6 +384,7 @@ cudaError_t create_pipe(Pipe& p) {
   if ((e = cudaStreamCreateWithFlags(&p.copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
   if ((e = cudaEventCreateWithFlags(&p.out_ready, cudaEventDisableTiming)) != cudaSuccess) return e;
   if ((e = cudaEventCreateWithFlags(&p.out_done, cudaEventDisableTiming)) != cudaSuccess) return e;
+  if ((e = cudaEventCreateWithFlags(&p.out_ext, cudaEventDisableTiming)) != cudaSuccess) return e;
   if ((e = cudaStreamCreateWithFlags(&p.in, cudaStreamNonBlocking)) != cudaSuccess) return e;
   if ((e = cudaStreamCreateWithFlags(&p.cap, cudaStreamNonBlocking)) != cudaSuccess) return e;
   return cudaEventCreateWithFlags(&p.in_ready, cudaEventDisableTiming);
@@ -411,6 +414,24 @@ cudaError_t get_pipe(const void* ws_base, Pipe** out) {
 extern "C" {
 
 int lfps_abi_version(void) { return LFPS_ABI_VERSION; }
+
+int lfps_wait_output(const lfps_workspace* ws) {
+  if (!ws || !ws->base) return fail(LFPS_E_INVALID, "workspace is NULL");
+  Pipe* pp = nullptr;
+  {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    std::lock_guard<std::mutex> g(g_pipe_mu);
+    auto it = g_pipes.find({dev, ws->base});
+    if (it == g_pipes.end()) return fail(LFPS_E_INVALID, "no decode step on this workspace yet");
+    pp = it->second.get();
+  }
+  // the last host-output step's copy (its event is re-recorded by every such
+  // step, in CUDA-graph replays too)
+  cudaError_t e = cudaEventSynchronize(pp->out_ext);
+  return e == cudaSuccess ? LFPS_OK : cuda_fail(e, "cudaEventSynchronize");
+}
 
 const char* lfps_last_error(void) { return g_err; }
 
@@ -667,6 +688,11 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
     LAUNCH(cudaStreamWaitEvent(pp->copy, pp->out_ready, 0));
     LAUNCH(cudaMemcpyAsync(out_host, c.out, (size_t)c.NS * c.d * sizeof(float),
                            cudaMemcpyDeviceToHost, pp->copy));
+    // (the host's event first: the join on out_done then covers its graph
+    // node; under capture it is recorded as an external event node so that
+    // replays record it)
+    if (c.stamp) LAUNCH(cudaEventRecordWithFlags(pp->out_ext, pp->copy, cudaEventRecordExternal));
+    else LAUNCH(cudaEventRecord(pp->out_ext, pp->copy));
     LAUNCH(cudaEventRecord(pp->out_done, pp->copy));
   }
   LAUNCH_P("update", sm, lfps::launch_update(c, static_cast<const __nv_bfloat16*>(k_new),

@@ -519,6 +519,14 @@ class BatchedSession:
             self.check_errors("decode_step")
         return self.result()
 
+    def wait_output(self):
+        """Block until the last host-output step's output (``out_host`` of
+        decode_step_host / decode_step) is in host memory
+        (lfps_wait_output).  Its commit may still be running on the device:
+        an autoregressive loop needs only the output before it builds the next
+        step's queries, and the next step is stream-ordered after the commit."""
+        _lib.check(self.lib.lfps_wait_output(C.byref(self.ws)), "wait_output")
+
     def copy_tracker_from(self, other: "BatchedSession"):
         """Take over another session's tracker state, priors and context
         counts (same dims): e.g. one layer's bootstrap reused by other layers.

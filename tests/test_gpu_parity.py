@@ -557,3 +557,27 @@ def test_prefetched_step_requires_a_prefetch():
     pair.compare_step(res, outs)
     with pytest.raises(ValueError, match="lfps_decode_prefetch"):
         pair.sess.decode_step(q, kv, kv, 0.05, prefetched=True)
+
+
+def test_wait_output_returns_the_step_output():
+    """lfps_wait_output: after decode_step_host with a pinned host output, the
+    host waits for the output copy only (the commit may still run); the host
+    buffer then holds the step's output, bit-identical to the device's once
+    the stream is done -- through the stream-launched and the CUDA-graph
+    step."""
+    pair, K, V, Q = _gqa_pair(batch=1, kv_heads=2, n0=900, steps=4, seed=71)
+    sess = pair.sess
+    B, Hkv, G, d = pair.B, pair.Hkv, pair.G, pair.d
+    import gpu_drive
+    for t, graph in enumerate((False, True, True, False)):
+        sess.graph = graph
+        packed = sess.pack_step_inputs(gpu_drive.bf16(Q[:, :, :, t].reshape(B, Hkv * G, d)),
+                                       gpu_drive.bf16(K[:, :, pair.n0 + t]),
+                                       gpu_drive.bf16(V[:, :, pair.n0 + t]))
+        host = torch.full(tuple(sess.out.shape), float("nan")).pin_memory()
+        sess.decode_step_host(packed, 0.05, out_host=host)
+        sess.wait_output()
+        got = host.clone()
+        torch.cuda.synchronize()
+        assert torch.equal(got, sess.out.cpu())
+        sess.check_errors("wait_output steps")
