@@ -764,6 +764,7 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
     pp->pre_epoch = 0;
     return enqueue_step(c, pp, sm, q, k_new, v_new, out_host, in_host, m_max);
   }
+  pp->pre_epoch = 0;        // a full step changes the tables: an earlier prefetch is stale
   if (g_prof_on || !(c.flags & LFPS_FLAG_GRAPH)) {
     c.epoch = next_epoch();
     return enqueue_step(c, pp, sm, q, k_new, v_new, out_host, in_host, m_max);

@@ -544,8 +544,8 @@ def test_prefetched_steps_bit_exact(epsilon, host_io, split, frac):
 
 def test_prefetched_step_requires_a_prefetch():
     """A LFPS_FLAG_PREFETCHED step without a preceding lfps_decode_prefetch on
-    the workspace is rejected before any launch (and a prefetch serves one
-    step only)."""
+    the workspace is rejected before any launch; a prefetch serves one step
+    only, and a full step in between makes it stale."""
     pair, K, V, Q = _gqa_pair(batch=1, kv_heads=2, n0=700, steps=2)
     B, Hkv, G, d = pair.B, pair.Hkv, pair.G, pair.d
     q = torch.zeros(B, Hkv * G, d, dtype=torch.bfloat16, device="cuda")
@@ -554,6 +554,13 @@ def test_prefetched_step_requires_a_prefetch():
         pair.sess.decode_step(q, kv, kv, 0.05, prefetched=True)
     pair.prefetch = True
     res, outs = pair.step(Q[:, :, :, 0], K[:, :, pair.n0], V[:, :, pair.n0], 0.05)
+    pair.compare_step(res, outs)
+    with pytest.raises(ValueError, match="lfps_decode_prefetch"):
+        pair.sess.decode_step(q, kv, kv, 0.05, prefetched=True)
+    # a full step after a prefetch makes the prefetched sets stale
+    pair.sess.prefetch()
+    pair.prefetch = False
+    res, outs = pair.step(Q[:, :, :, 1], K[:, :, pair.n0 + 1], V[:, :, pair.n0 + 1], 0.05)
     pair.compare_step(res, outs)
     with pytest.raises(ValueError, match="lfps_decode_prefetch"):
         pair.sess.decode_step(q, kv, kv, 0.05, prefetched=True)
