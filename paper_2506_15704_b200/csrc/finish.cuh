@@ -148,12 +148,14 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
 
   if (k >= p) {
     // ---- C2 = probe (the common case): score and attend in ONE pass ---------------------
-    auto keep = [&](int rid, float z) {                 // a C2 / sink score of this group
+    // a C2 / sink score: each lane keeps the row it folded in the
+    // reduce-scatter (lanes 0-3 row a, 4-7 row b), lanes 0 and 4 store it
+    auto keep = [&](int rid, float z) {
       chk = __fmaf_rn(z, 0.0f, chk);
       if (rid >= S) {
         mxc = fmaxf(mxc, z);
-        if (l8 == 0) c2zS[rid] = z;
-      } else if (l8 == 0) {
+        if ((l8 & 3) == 0) c2zS[rid] = z;
+      } else if ((l8 & 3) == 0) {
         sh.sink_z[rid] = z;
       }
     };
@@ -161,12 +163,13 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
         stages, kb, vb, S + p, [&](int rid) { return rm(rid < S ? rid : __ldg(pidxS + rid)); },
         [&](const Rows2& r) {
           const float2 z = score_rows<PQ>(r, qp, c.sqrt_d_f32);
+          {
+            const bool b4 = (l8 & 4) != 0;
+            if (b4 ? r.ok[1] : r.ok[0]) keep(b4 ? r.rid[1] : r.rid[0], b4 ? z.y : z.x);
+          }
           if (r.ok[1]) {
-            keep(r.rid[0], z.x);
-            keep(r.rid[1], z.y);
             at.absorb2(z.x * kLog2e, ld_part_s<PQ>(r.v[0], l8), z.y * kLog2e, ld_part_s<PQ>(r.v[1], l8));
           } else if (r.ok[0]) {
-            keep(r.rid[0], z.x);
             at.absorb(z.x * kLog2e, ld_part_s<PQ>(r.v[0], l8));
           }
         });

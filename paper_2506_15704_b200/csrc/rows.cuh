@@ -335,7 +335,9 @@ __device__ __forceinline__ void stream_rows(uint8_t* stages, const __nv_bfloat16
   constexpr int kRowStep = kGroups8 * kRowB;          // group row 0 -> group row 1
   const int grp = threadIdx.x >> 3, l8 = threadIdx.x & 7;
   const int ntiles = (nrows + kTileR - 1) / kTileR;
-  const uint32_t sb = smem_u32(stages) + grp * kRowB;
+  uint32_t sb0 = smem_u32(stages);
+  asm volatile("" : "+r"(sb0));                       // kept in a register, not rematerialised per tile
+  const uint32_t sb = sb0 + grp * kRowB;
   const uint32_t my_cp = sb + l8 * 16;                // this thread's first chunk, stage 0
   const uint8_t* kb8 = reinterpret_cast<const uint8_t*>(kb) + l8 * 16;
   const uint8_t* vb8 = reinterpret_cast<const uint8_t*>(vb) + l8 * 16;
