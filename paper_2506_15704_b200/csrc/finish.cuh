@@ -93,12 +93,12 @@ __device__ __forceinline__ void finish_tail(const Ctx& c, int s, uint8_t* stages
 }
 
 // The whole back half of one session's step, run by a 256-thread CTA.
-// `stages` is kStages x [K tile | V tile] of dynamic shared memory.
+// `stages` is kStagesR x [K tile | V tile] of dynamic shared memory.
 template <int PQ, int RM>
 __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16* q, int s,
                                                uint8_t* stages, FinishShared& sh) {
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5, l8 = tid & 7, grp = tid >> 3;
+  const int l8 = tid & 7;
   const int b = s / c.Hq, h = (s % c.Hq) / c.G;
   const int n = c.n_ctx[b];
   const int S = c.S;

@@ -42,7 +42,7 @@ using namespace fin;
 // RM: the row mapping (RowMapT) -- 0 contiguous cache, 1 block table
 template <int PQ, int RM>
 __global__ void __launch_bounds__(kThreads, kRowCtas) lfps_finish_kernel(Ctx c, const __nv_bfloat16* q) {
-  extern __shared__ __align__(128) uint8_t stages[];      // kStages x [K tile | V tile]
+  extern __shared__ __align__(128) uint8_t stages[];      // kStagesR x [K tile | V tile]
   __shared__ FinishShared sh;
   pdl_wait();                                             // the select kernel's lists
   finish_session<PQ, RM>(c, q, c.s_off + blockIdx.x, stages, sh);

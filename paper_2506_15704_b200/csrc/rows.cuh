@@ -14,8 +14,6 @@ namespace rows {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kGroups8 = kThreads / 8;   // 8-lane row groups
-constexpr int kTile = 32;                // k_finish_unit.cu: rows per stage (one per row group)
-constexpr int kStages = 3;               // k_finish_unit.cu: stages
 constexpr int kR = 2;                    // stream_rows: max rows per 8-lane group per tile
 // rows per group per tile for d = 16 PQ: two (one tile = 64 rows), one for
 // d = 256 so that a stage stays at 32 KB
@@ -27,7 +25,10 @@ __host__ __device__ constexpr int rows_per_group(int pq) { return pq >= 16 ? 1 :
 #define LFPS_ROW_STAGES 2
 #endif
 constexpr int kStagesR = LFPS_ROW_STAGES;   // stream_rows: stages
-constexpr int kRowCtas = kStagesR == 2 ? 3 : 2;   // resident stream_rows CTAs per SM (smem)
+#ifndef LFPS_ROW_CTAS
+#define LFPS_ROW_CTAS (kStagesR == 2 ? 3 : 2)
+#endif
+constexpr int kRowCtas = LFPS_ROW_CTAS;   // resident stream_rows CTAs per SM (smem)
 // dynamic shared memory of a stream_rows kernel (K block + V block per stage)
 __host__ __device__ constexpr size_t rows_smem(int d) {
   return (size_t)kStagesR * kGroups8 * rows_per_group(d / 16) * d * 2 * 2;

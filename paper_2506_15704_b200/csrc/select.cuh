@@ -16,6 +16,10 @@ using namespace tbl;
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
+#ifndef LFPS_SEL_DEPTH
+#define LFPS_SEL_DEPTH 4
+#endif
+constexpr int kSelDepth = LFPS_SEL_DEPTH;   // F reads in flight per thread
 
 // exclusive scan over the 256 threads of the block; total in *total
 __device__ __forceinline__ int block_scan(int v, int* warp_sums, int* total) {
@@ -215,13 +219,13 @@ __device__ __forceinline__ void select_session(const Ctx& c, int s, uint32_t* sm
         fword[tid] = w;
         fc1[tid] = 0u;
         __syncthreads();
-        for (int g0 = tid; g0 < K; g0 += 4 * kThreads) {
-          int e[4];
-          long long xv[4], xs[4];
+        for (int g0 = tid; g0 < K; g0 += kSelDepth * kThreads) {
+          int e[kSelDepth];
+          long long xv[kSelDepth], xs[kSelDepth];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) e[q] = g0 + kThreads * q < K ? fbuf[g0 + kThreads * q] : -1;
+          for (int q = 0; q < kSelDepth; ++q) e[q] = g0 + kThreads * q < K ? fbuf[g0 + kThreads * q] : -1;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < kSelDepth; ++q) {
             xv[q] = xs[q] = -1ll;
             if (e[q] >= 0) {
               const int i = fword[e[q] >> 5] * 32 + (e[q] & 31);
@@ -230,7 +234,7 @@ __device__ __forceinline__ void select_session(const Ctx& c, int s, uint32_t* sm
             }
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < kSelDepth; ++q)
             if (e[q] >= 0 && (xv[q] > tfv || xs[q] > tfs))
               atomicOr(&fc1[e[q] >> 5], 1u << (e[q] & 31));
         }
