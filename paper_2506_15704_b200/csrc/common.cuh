@@ -36,7 +36,8 @@ struct Ctx {
   float sqrt_d_f32;
   int s, S, L, bypass_mode, exhaustive, n_off, flags;
   int s_off, s_cnt;   // session range [s_off, s_off + s_cnt) of a per-session launch
-  int prefetch;       // lfps_decode_prefetch: the select kernel runs ahead of the gate
+  int prefetch;       // the sets were built ahead of the gate (lfps_decode_prefetch, or
+                      // beside it): the finish handles gated sessions and kappa = 0
                       // (every session; kappa = 0 is raised by the finish kernel)
   int epoch;          // call stamp in [1, 2^27): err[0] == epoch <=> this call failed
   const int* stamp;   // CUDA-graph steps: the stamp in device memory (set by the

@@ -108,11 +108,11 @@ __device__ __forceinline__ void finish_session(const Ctx& c, const __nv_bfloat16
     if (tid == 0) {
       cnt[CNT_K] = 0; cnt[CNT_C2] = 0; cnt[CNT_CLAMP] = 0;
       // a prefetched select built this session's sets before the gate ran
-      if (c.flags & LFPS_FLAG_PREFETCHED) { cnt[CNT_C0] = 0; cnt[CNT_C1] = 0; cnt[CNT_PROBE] = 0; cnt[CNT_DROP] = 0; }
+      if (c.prefetch) { cnt[CNT_C0] = 0; cnt[CNT_C1] = 0; cnt[CNT_PROBE] = 0; cnt[CNT_DROP] = 0; }
     }
     return;
   }
-  if ((c.flags & LFPS_FLAG_PREFETCHED) && tid < 2 && !c.exhaustive) {
+  if (c.prefetch && tid < 2 && !c.exhaustive) {
     // kappa = 0 (tables.py:314-315) fails a non-bypassed step only; the
     // prefetched select exported the thresholds instead of raising it
     const double* th = c.thr + (size_t)(2 * s + tid) * 4;

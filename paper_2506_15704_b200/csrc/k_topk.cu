@@ -323,12 +323,10 @@ __global__ void __launch_bounds__(kThreads) lfps_exact_topk_kernel(Ctx c) {
     __syncthreads();
   }
   // ---- fallback: per-chunk counts, histogram select, ordered emission pass --------------
-  int above = 0;
   uint32_t kth;
   int need_eq;
   const uint2* cand = sh.cand;
   int ncand;
-  (void)above;
   {
     // ---- fallback: 2048-bin histogram over all keys, then the k-th bin ----------------
     unsigned* hist = sh.samp;                      // 2048 bins

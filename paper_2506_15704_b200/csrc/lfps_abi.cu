@@ -298,6 +298,10 @@ constexpr int kSplitGroups = LFPS_SPLIT_GROUPS;   // session groups of LFPS_FLAG
 #define LFPS_SPLIT_MIN 256
 #endif
 constexpr int kSplitMin = LFPS_SPLIT_MIN;         // sessions below which the split is off
+#ifndef LFPS_SELECT_AHEAD
+#define LFPS_SELECT_AHEAD 1
+#endif
+constexpr bool kSelectAhead = LFPS_SELECT_AHEAD != 0;   // select beside the gate, not after it
 // Internal streams and events of one workspace (one BatchedSession): the
 // fork/join events of a step are re-recorded by every call, so they must not
 // be shared between sessions that different host threads step concurrently
@@ -447,10 +451,9 @@ int lfps_workspace_layout(const lfps_dims* dims, lfps_ws_layout* out) {
 int lfps_decode_launches(const lfps_dims* dims, int32_t flags) {
   // per group: gate | stats, select, finish (LFPS_FLAG_PREFETCHED: gate,
   // finish -- stats and select ran in lfps_decode_prefetch), then the update
+  const long long ns = dims ? (long long)dims->batch * dims->kv_heads * dims->group : 0;
   const int per = (flags & LFPS_FLAG_PREFETCHED) ? 2 : 4;
-  if (dims && (flags & LFPS_FLAG_SPLIT) &&
-      (long long)dims->batch * dims->kv_heads * dims->group >= kSplitMin)
-    return 1 + per * kSplitGroups;
+  if (dims && (flags & LFPS_FLAG_SPLIT) && ns >= kSplitMin) return 1 + per * kSplitGroups;
   return 1 + per;
 }
 
@@ -619,10 +622,13 @@ int lfps_decode_step_host_io(const lfps_dims* dims, const lfps_params* p, const 
 }
 
 // Enqueue one decode step on stream sm (the caller's, or the capture stream).
-// The stats kernel does not depend on the gate (it serves every session), so
-// the two run concurrently: stats on an internal stream forked from sm,
-// joined before select.  LFPS_FLAG_SPLIT additionally runs kSplitGroups
-// session groups, each [gate | stats] -> select -> finish, on their own
+// Stats and select do not depend on the gate (they serve every session, and
+// the finish treats gated sessions and kappa = 0 as after a prefetch), so
+// they run beside it: stats -> select on an internal stream forked from sm,
+// joined before the finish.  (Select after the gate, LFPS_SELECT_AHEAD=0,
+// measured the same on the device and 10 us slower end to end at C1/C2:
+// the gate waits for the input copy.)  LFPS_FLAG_SPLIT additionally runs
+// kSplitGroups session groups, each [gate | stats -> select] -> finish, on their own
 // streams; the update (commit) joins them on sm.  Under lfps_profile_enable
 // everything runs serially on sm so each kernel is timed alone.  Host
 // inputs (lfps_decode_step_host_io): q | k_new | v_new are contiguous from q
@@ -639,11 +645,14 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
   if (in_host && g_prof_on)
     LAUNCH(cudaMemcpyAsync(const_cast<void*>(q), in_host, in_bytes, cudaMemcpyHostToDevice, sm));
   const bool pre = (c.flags & LFPS_FLAG_PREFETCHED) != 0;   // stats + select already ran
+  const bool ahead = !pre && kSelectAhead;   // select beside the gate
   if (g_prof_on) {
+    lfps::Ctx cf = c;
+    cf.prefetch = ahead;
     LAUNCH_P("gate", sm, lfps::launch_gate(c, qb, sm));
     if (!pre) {
-      LAUNCH_P("stats", sm, lfps::launch_stats(c, sm));
-      LAUNCH_P("select", sm, lfps::launch_select(c, m_max, sm));
+      LAUNCH_P("stats", sm, lfps::launch_stats(cf, sm));
+      LAUNCH_P("select", sm, lfps::launch_select(cf, m_max, sm));
     }
   } else {
     LAUNCH(cudaEventRecord(pp->fork, sm));
@@ -660,18 +669,28 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
     lfps::Ctx cg = c;
     cg.s_off = g * per;
     cg.s_cnt = g == groups - 1 ? c.NS - g * per : per;
+    if (ahead) cg.prefetch = 1;
     cudaStream_t gs = split ? pp->st[g] : sm;
     if (!g_prof_on) {
       cudaStream_t as = pp->aux[g];
       if (split) LAUNCH(cudaStreamWaitEvent(gs, pp->fork, 0));
-      if (!pre) {
+      if (ahead) {
+        // the sets are built beside the gate (and the input copy): select
+        // follows stats on the side stream, the finish joins both
+        LAUNCH(cudaStreamWaitEvent(as, pp->fork, 0));
+        LAUNCH(lfps::launch_stats(cg, as));
+        LAUNCH(lfps::launch_select(cg, m_max, as));
+        LAUNCH(cudaEventRecord(pp->stats[g], as));
+      } else if (!pre) {
         LAUNCH(cudaStreamWaitEvent(as, pp->fork, 0));
         LAUNCH(lfps::launch_stats(cg, as));
         LAUNCH(cudaEventRecord(pp->stats[g], as));
       }
       if (in_host) LAUNCH(cudaStreamWaitEvent(gs, pp->in_ready, 0));
       LAUNCH(lfps::launch_gate(cg, qb, gs));
-      if (!pre) {
+      if (ahead) {
+        LAUNCH(cudaStreamWaitEvent(gs, pp->stats[g], 0));
+      } else if (!pre) {
         LAUNCH(cudaStreamWaitEvent(gs, pp->stats[g], 0));
         LAUNCH(lfps::launch_select(cg, m_max, gs));
       }
@@ -761,6 +780,7 @@ static int decode_impl(const lfps_dims* dims, const lfps_params* p, const lfps_s
     if (!pp->pre_epoch)
       return fail(LFPS_E_INVALID, "LFPS_FLAG_PREFETCHED without a preceding lfps_decode_prefetch");
     c.epoch = pp->pre_epoch;
+    c.prefetch = 1;
     pp->pre_epoch = 0;
     return enqueue_step(c, pp, sm, q, k_new, v_new, out_host, in_host, m_max);
   }
