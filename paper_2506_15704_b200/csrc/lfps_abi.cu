@@ -302,6 +302,10 @@ constexpr int kSplitMin = LFPS_SPLIT_MIN;         // sessions below which the sp
 #define LFPS_SELECT_AHEAD 1
 #endif
 constexpr bool kSelectAhead = LFPS_SELECT_AHEAD != 0;   // select beside the gate, not after it
+#ifndef LFPS_GATE_SIDE
+#define LFPS_GATE_SIDE 1
+#endif
+constexpr bool kGateSide = LFPS_GATE_SIDE != 0;   // the gate on the side stream (with select ahead)
 // Internal streams and events of one workspace (one BatchedSession): the
 // fork/join events of a step are re-recorded by every call, so they must not
 // be shared between sessions that different host threads step concurrently
@@ -674,7 +678,17 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
     if (!g_prof_on) {
       cudaStream_t as = pp->aux[g];
       if (split) LAUNCH(cudaStreamWaitEvent(gs, pp->fork, 0));
-      if (ahead) {
+      if (ahead && kGateSide) {
+        // the gate (after the input copy) on the side stream; stats ->
+        // select -> finish stay one programmatic-launch chain on the group's
+        LAUNCH(cudaStreamWaitEvent(as, pp->fork, 0));
+        if (in_host) LAUNCH(cudaStreamWaitEvent(as, pp->in_ready, 0));
+        LAUNCH(lfps::launch_gate(cg, qb, as));
+        LAUNCH(cudaEventRecord(pp->stats[g], as));
+        LAUNCH(lfps::launch_stats(cg, gs));
+        LAUNCH(lfps::launch_select(cg, m_max, gs));
+        LAUNCH(cudaStreamWaitEvent(gs, pp->stats[g], 0));
+      } else if (ahead) {
         // the sets are built beside the gate (and the input copy): select
         // follows stats on the side stream, the finish joins both
         LAUNCH(cudaStreamWaitEvent(as, pp->fork, 0));
@@ -686,10 +700,12 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
         LAUNCH(lfps::launch_stats(cg, as));
         LAUNCH(cudaEventRecord(pp->stats[g], as));
       }
-      if (in_host) LAUNCH(cudaStreamWaitEvent(gs, pp->in_ready, 0));
-      LAUNCH(lfps::launch_gate(cg, qb, gs));
+      if (!(ahead && kGateSide)) {
+        if (in_host) LAUNCH(cudaStreamWaitEvent(gs, pp->in_ready, 0));
+        LAUNCH(lfps::launch_gate(cg, qb, gs));
+      }
       if (ahead) {
-        LAUNCH(cudaStreamWaitEvent(gs, pp->stats[g], 0));
+        if (!kGateSide) LAUNCH(cudaStreamWaitEvent(gs, pp->stats[g], 0));
       } else if (!pre) {
         LAUNCH(cudaStreamWaitEvent(gs, pp->stats[g], 0));
         LAUNCH(lfps::launch_select(cg, m_max, gs));
