@@ -149,6 +149,13 @@ __device__ __forceinline__ void trace_at(const Ctx& c, int s, int slot, long lon
 __device__ __forceinline__ double* ver_row(const Ctx& c, int s) { return c.ver + (size_t)s * c.m_cap; }
 __device__ __forceinline__ double* sla_row(const Ctx& c, int s) { return c.sla + (size_t)s * c.sla_cap; }
 
+// LFPS_EARLY_TRIGGER: stats / select / finish let their dependents be
+// scheduled from their start (the dependents still wait in pdl_wait for the
+// whole grid), so the next kernel's CTAs fill the SMs during the last wave
+#ifndef LFPS_EARLY_TRIGGER
+#define LFPS_EARLY_TRIGGER 0
+#endif
+
 // ---- host-side launch wrappers (defined in the k_*.cu files) -------------
 // Launch with programmatic stream serialization (PDL): the kernel may be
 // scheduled while its predecessor in the stream drains; it calls pdl_wait()

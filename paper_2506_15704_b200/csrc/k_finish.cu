@@ -45,8 +45,9 @@ __global__ void __launch_bounds__(kThreads, kRowCtas) lfps_finish_kernel(Ctx c, 
   extern __shared__ __align__(128) uint8_t stages[];      // kStagesR x [K tile | V tile]
   __shared__ FinishShared sh;
   pdl_wait();                                             // the select kernel's lists
+  if (LFPS_EARLY_TRIGGER) pdl_trigger();
   finish_session<PQ, RM>(c, q, c.s_off + blockIdx.x, stages, sh);
-  pdl_trigger();
+  if (!LFPS_EARLY_TRIGGER) pdl_trigger();
 }
 
 template <int PQ, int RM>

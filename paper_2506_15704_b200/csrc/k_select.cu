@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(kStatsThreads, LFPS_STATS_CTAS) lfps_stats_ker
   __shared__ StatsShared sh;
   const int s = c.s_off + (blockIdx.x >> 1), t = blockIdx.x & 1;
   const int tid = threadIdx.x;
+  if (LFPS_EARLY_TRIGGER) pdl_trigger();
   if (c.exhaustive) return;
   const int b = s / c.Hq;
   const int dw = c.bw.dwords;
@@ -90,9 +91,10 @@ __global__ void __launch_bounds__(kStatsThreads, LFPS_STATS_CTAS) lfps_stats_ker
 __global__ void __launch_bounds__(kThreads, LFPS_SELECT_CTAS) lfps_select_kernel(Ctx c) {
   extern __shared__ __align__(16) uint32_t smem[];
   __shared__ SelectShared sh;
-  pdl_wait();                                  // the gate's bypass decisions
+  pdl_wait();                                  // the stats kernel's thresholds and C0 words
+  if (LFPS_EARLY_TRIGGER) pdl_trigger();
   select_session(c, c.s_off + blockIdx.x, smem, sh);
-  pdl_trigger();
+  if (!LFPS_EARLY_TRIGGER) pdl_trigger();
 }
 
 }  // namespace
