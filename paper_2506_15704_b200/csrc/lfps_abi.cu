@@ -628,12 +628,14 @@ int lfps_decode_step_host_io(const lfps_dims* dims, const lfps_params* p, const 
 // Enqueue one decode step on stream sm (the caller's, or the capture stream).
 // Stats and select do not depend on the gate (they serve every session, and
 // the finish treats gated sessions and kappa = 0 as after a prefetch), so
-// they run beside it: stats -> select on an internal stream forked from sm,
-// joined before the finish.  (Select after the gate, LFPS_SELECT_AHEAD=0,
-// measured the same on the device and 10 us slower end to end at C1/C2:
-// the gate waits for the input copy.)  LFPS_FLAG_SPLIT additionally runs
-// kSplitGroups session groups, each [gate | stats -> select] -> finish, on their own
-// streams; the update (commit) joins them on sm.  Under lfps_profile_enable
+// the gate runs on an internal stream forked from sm and stats -> select ->
+// finish stay one PDL chain on sm, the finish joining the gate.  (Select
+// after the gate, LFPS_SELECT_AHEAD=0, measured the same on the device and
+// 10 us slower end to end at C1/C2: the gate waits for the input copy.)
+// LFPS_FLAG_SPLIT (>= kSplitMin sessions) instead runs kSplitGroups session
+// groups, each [gate | stats] -> select -> finish, on their own streams
+// (stats on an internal stream, joined before select); the update (commit)
+// joins them on sm.  Under lfps_profile_enable
 // everything runs serially on sm so each kernel is timed alone.  Host
 // inputs (lfps_decode_step_host_io): q | k_new | v_new are contiguous from q
 // on; the copy starts with the step on its own stream (after the caller's
@@ -649,7 +651,10 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
   if (in_host && g_prof_on)
     LAUNCH(cudaMemcpyAsync(const_cast<void*>(q), in_host, in_bytes, cudaMemcpyHostToDevice, sm));
   const bool pre = (c.flags & LFPS_FLAG_PREFETCHED) != 0;   // stats + select already ran
-  const bool ahead = !pre && kSelectAhead;   // select beside the gate
+  // select beside the gate: unsplit steps only (with the split groups the
+  // finish's cross-stream join on the gate costs more than it hides)
+  const bool split = (c.flags & LFPS_FLAG_SPLIT) && !g_prof_on && c.NS >= kSplitMin;
+  const bool ahead = !pre && kSelectAhead && !((c.flags & LFPS_FLAG_SPLIT) && c.NS >= kSplitMin);
   if (g_prof_on) {
     lfps::Ctx cf = c;
     cf.prefetch = ahead;
@@ -666,7 +671,6 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
       LAUNCH(cudaEventRecord(pp->in_ready, pp->in));
     }
   }
-  const bool split = (c.flags & LFPS_FLAG_SPLIT) && !g_prof_on && c.NS >= kSplitMin;
   const int groups = split ? kSplitGroups : 1;
   const int per = (c.NS / groups + 31) / 32 * 32;
   for (int g = 0; g < groups; ++g) {
