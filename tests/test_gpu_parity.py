@@ -286,6 +286,28 @@ def test_decode_step_host_io_small_and_rejects():
                               out_host=torch.empty(3, dtype=torch.float32))
 
 
+def test_decode_step_host_io_reused_buffers():
+    """A decode loop's pattern: the same pinned input and output buffers every
+    step with new contents (decode_step_host caches their checks per tensor),
+    bit-exact against the oracle through graph replays; a buffer of the
+    wrong size at a cached tensor's address is still rejected."""
+    pair, K, V, Q = _gqa_pair(batch=2, kv_heads=2, n0=900, steps=5, seed=41)
+    pair.host_io = True
+    pair.reuse_host = True
+    pair.sess.graph = True
+    n0 = pair.n0
+    for t in range(5):
+        res, outs = pair.step(Q[:, :, :, t], K[:, :, n0 + t], V[:, :, n0 + t], 0.05)
+        pair.compare_step(res, outs)
+    sess = pair.sess
+    inp, out = pair._host_bufs
+    with pytest.raises(ValueError):       # a view of the cached input buffer, the wrong size
+        sess.decode_step_host(inp[:-1], 0.05, out_host=out)
+    with pytest.raises(ValueError):       # the cached output tensor, resized in place
+        out.resize_(out.numel() - 1)
+        sess.decode_step_host(inp, 0.05, out_host=out)
+
+
 def test_paged_kv_pool_bit_exact_across_a_page():
     """N4 paged-KV caller: K/V in a KvPool (virtual [B, Hkv, n_max, d], 2 MiB
     pages mapped as contexts grow).  The prefill ends 3 rows before the first

@@ -50,6 +50,27 @@ def main():
                 enq.append((t1 - t0) * 1e6)
         enq.sort()
         print("decode_step_host (%s): median enqueue %.1f us" % (name, enq[len(enq) // 2]))
+    lib = sess.lib
+    print("ctypes abi_version %.2f us" % per_call(lambda: lib.lfps_abi_version()))
+    # the C-ABI step call alone (prepared arguments; same buffers every call)
+    from paper_2506_15704_b200 import _lib
+    n_host = (C.c_int32 * sess.B)(*sess.n_host)
+    args = (C.byref(sess.dims), C.byref(sess._params(0.05, True, False)), C.byref(sess.state),
+            C.byref(sess.ws), C.c_void_p(inp.data_ptr()), C.c_void_p(sess._in_dev.data_ptr()
+            if sess._in_dev is not None else 0), n_host, C.c_void_p(out.data_ptr()), sess._stream())
+    if sess._in_dev is not None:
+        ts = []
+        for t in range(300):
+            n_host[0] = sess.n_host[0]
+            t0 = time.perf_counter()
+            _lib.check(lib.lfps_decode_step_host_io(*args), "step")
+            t1 = time.perf_counter()
+            lib.lfps_wait_output(C.byref(sess.ws))
+            sess.n_host = [n + 1 for n in sess.n_host]
+            if t >= 20:
+                ts.append((t1 - t0) * 1e6)
+        ts.sort()
+        print("C-ABI step call alone: median %.1f us" % ts[len(ts) // 2])
     torch.cuda.synchronize()
 
 
