@@ -295,7 +295,7 @@ int next_epoch() {
 #endif
 constexpr int kSplitGroups = LFPS_SPLIT_GROUPS;   // session groups of LFPS_FLAG_SPLIT
 #ifndef LFPS_SPLIT_MIN
-#define LFPS_SPLIT_MIN 256
+#define LFPS_SPLIT_MIN 1024
 #endif
 constexpr int kSplitMin = LFPS_SPLIT_MIN;         // sessions below which the split is off
 #ifndef LFPS_SELECT_AHEAD

@@ -174,14 +174,16 @@ def test_long_trajectory_crosses_slash_blocks():
                                                  (True, 24, False), (True, 12, True),
                                                  (False, 4, True)])
 def test_split_streams_bit_exact(split, steps, host_io):
-    """256 sessions (8 requests x 8 KV heads x 4): LFPS_FLAG_SPLIT runs two
+    """LFPS_FLAG_SPLIT at 1024 sessions (32 requests x 8 KV heads x 4): two
     session groups on internal streams, each with its stats kernel beside its
-    gate, and PDL between the later kernels; results are identical to the
-    oracle over many steps (no cross-step or cross-stream races).  host_io:
-    every step through lfps_decode_step_host_io (the input copy on its own
-    stream beside the stats kernels, the output copied back to pinned host
-    memory, bit-identical to the device output)."""
-    pair, K, V, Q = _gqa_pair(batch=8, kv_heads=8, group=4, d=64, n0=700, steps=steps, seed=41)
+    gate, and PDL between the later kernels; without the flag (256 sessions)
+    the gate runs on an internal stream beside the stats -> select -> finish
+    chain.  Results are identical to the oracle over many steps (no
+    cross-step or cross-stream races).  host_io: every step through
+    lfps_decode_step_host_io (the input copy on its own stream, the output
+    copied back to pinned host memory, bit-identical to the device output)."""
+    pair, K, V, Q = _gqa_pair(batch=32 if split else 8, kv_heads=8, group=4, d=64, n0=700,
+                              steps=steps, seed=41)
     pair.sess.split = split
     pair.host_io = host_io
     n0 = pair.n0
@@ -374,8 +376,9 @@ def test_paged_kv_pool_bit_exact_across_a_page():
 def test_two_threads_two_sessions_bit_exact():
     """Reentrancy across distinct sessions (SURVEY §8(b) threading): two host
     threads step two sessions concurrently, each on its own CUDA stream, with
-    the two-stream split on (256 sessions each, so both use their internal
-    streams and fork/join events).  Each session's trajectory is identical
+    LFPS_FLAG_SPLIT set (256 sessions each: below the split threshold, so
+    each runs its gate on its own workspace's internal stream, joined by
+    event before the finish).  Each session's trajectory is identical
     to the oracle's, as if it had run alone."""
     import threading
     import gpu_drive
@@ -492,7 +495,7 @@ def test_graph_replay_bit_exact(host_io, split):
     then a failing step (non-finite query) raises and commits nothing, and
     the following replays commit again."""
     import gpu_drive
-    B, Hkv, G, d = (8, 8, 4, 64) if split else (2, 2, 4, 128)
+    B, Hkv, G, d = (32, 8, 4, 64) if split else (2, 2, 4, 128)
     pair, K, V, Q = _gqa_pair(batch=B, kv_heads=Hkv, group=G, d=d, n0=900, steps=8, seed=83)
     sess = pair.sess
     sess.graph = sess.graph_device = True
@@ -550,8 +553,8 @@ def test_prefetched_steps_bit_exact(epsilon, host_io, split, frac):
     counts (bypassed sessions report none), tables and outputs against the
     oracle -- with gated sessions (epsilon), the stream split, host I/O and
     Top-k cuts (1%)."""
-    pair, K, V, Q = _gqa_pair(batch=8, kv_heads=8, group=4, d=64, n0=900, steps=6, seed=7,
-                              epsilon=epsilon)
+    pair, K, V, Q = _gqa_pair(batch=32 if split else 8, kv_heads=8, group=4, d=64, n0=900,
+                              steps=6, seed=7, epsilon=epsilon)
     pair.sess.split = split
     pair.host_io = host_io
     pair.prefetch = True
