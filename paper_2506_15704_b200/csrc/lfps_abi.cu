@@ -302,6 +302,9 @@ constexpr int kSplitMin = LFPS_SPLIT_MIN;         // sessions below which the sp
 #define LFPS_SELECT_AHEAD 1
 #endif
 constexpr bool kSelectAhead = LFPS_SELECT_AHEAD != 0;   // select beside the gate, not after it
+#ifndef LFPS_AHEAD_SPLIT
+#define LFPS_AHEAD_SPLIT 0       // select beside the gate in split steps too
+#endif
 #ifndef LFPS_GATE_SIDE
 #define LFPS_GATE_SIDE 1
 #endif
@@ -654,7 +657,8 @@ static int enqueue_step(const lfps::Ctx& c, Pipe* pp, cudaStream_t sm, const voi
   // select beside the gate: unsplit steps only (with the split groups the
   // finish's cross-stream join on the gate costs more than it hides)
   const bool split = (c.flags & LFPS_FLAG_SPLIT) && !g_prof_on && c.NS >= kSplitMin;
-  const bool ahead = !pre && kSelectAhead && !((c.flags & LFPS_FLAG_SPLIT) && c.NS >= kSplitMin);
+  const bool ahead = !pre && kSelectAhead &&
+                     (LFPS_AHEAD_SPLIT || !((c.flags & LFPS_FLAG_SPLIT) && c.NS >= kSplitMin));
   if (g_prof_on) {
     lfps::Ctx cf = c;
     cf.prefetch = ahead;
