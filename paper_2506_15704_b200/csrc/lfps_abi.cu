@@ -291,7 +291,7 @@ int next_epoch() {
 }
 
 #ifndef LFPS_SPLIT_GROUPS
-#define LFPS_SPLIT_GROUPS 2
+#define LFPS_SPLIT_GROUPS 4
 #endif
 constexpr int kSplitGroups = LFPS_SPLIT_GROUPS;   // session groups of LFPS_FLAG_SPLIT
 #ifndef LFPS_SPLIT_MIN

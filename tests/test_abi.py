@@ -39,7 +39,7 @@ def test_library_exports_every_declared_symbol():
     assert lib.lfps_abi_version() == _lib.ABI_VERSION
     assert lib.lfps_decode_launches(None, 0) == 5 and lib.lfps_exact_launches() > 0
     big = _lib.Dims(64, 8, 4, 128, 4096, 4096)
-    assert lib.lfps_decode_launches(C.byref(big), _lib.FLAG_SPLIT) == 9
+    assert lib.lfps_decode_launches(C.byref(big), _lib.FLAG_SPLIT) == 17   # 4 groups x 4 + commit
     assert lib.lfps_step_input_bytes(C.byref(big)) == (64 * 8 * 4 + 2 * 64 * 8) * 128 * 2
     assert lib.lfps_step_input_bytes(C.byref(_lib.Dims(0, 8, 4, 128, 4096, 4096))) < 0
 
