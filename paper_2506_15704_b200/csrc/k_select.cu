@@ -32,7 +32,7 @@
 //      probe = C1 | local tail, compacted into a sorted absolute index list.
 //
 // A, B and C are fp64 latency chains per table: running them per (session,
-// table) in 128-thread CTAs (8 per SM) doubles the sessions in flight over
+// table) in 128-thread CTAs (7 per SM) nearly doubles the sessions in flight over
 // one 256-thread CTA per session doing both tables.
 //
 // All comparisons are exact fp64 (on bit patterns: phys values are +0 or
@@ -51,7 +51,7 @@ using namespace tbl;
 using namespace sel;
 
 #ifndef LFPS_STATS_CTAS
-#define LFPS_STATS_CTAS 8
+#define LFPS_STATS_CTAS 7
 #endif
 #ifndef LFPS_SELECT_CTAS
 #define LFPS_SELECT_CTAS 5
